@@ -1,0 +1,350 @@
+"""bench.py -- DTS-Gate MoE layer forward+backward throughput on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One "step" = one pass of the whole hot path over one batch of synthetic tokens:
+moe_dts_gate -> moe_dispatch -> moe_expert_ffn -> moe_combine -> moe_combine_bwd ->
+moe_expert_ffn_bwd -> moe_dts_gate_bwd -> moe_dispatch_bwd (all through the C ABI).
+The spawn runs once before timing (it is an initialisation step, Alg. 1 lines 4-5).
+
+Workload: BASELINE.json configs[1] (C2, GPT-small-shaped, T=8192 tokens per GPU,
+d=768, d_ff=3072, E=16, tau=2.0, c=0.001), synthetic seeded data (harness/inputs.py).
+Under torchrun (N > 1) each rank runs its own T tokens (weak scaling).
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the
+launching stream, with an L2 flush (write of a 256 MiB buffer) between steps outside
+the events; barrier + synchronize on both sides; the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from harness import configs, inputs  # noqa: E402
+
+METRIC = "MoE-layer fwd+bwd tokens/sec at 1/2/4/8 B200; % bf16 tensor peak"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def oracle_sample(cfg, T_sub: int, step: int = 0):
+    """Time the fp64 oracle (as it stands) on T_sub tokens of the workload, fwd+bwd."""
+    from oracle import dts_moe as O
+    li = inputs.make_inputs(cfg, T=T_sub, step=step)
+    ex = O.spawn(inputs.to_f64(li.W1s), inputs.to_f64(li.b1s), inputs.to_f64(li.W2s), inputs.to_f64(li.b2s),
+                 inputs.bits_u32(li.M1bits), inputs.bits_u32(li.M2bits))
+    x, Wg, u, dy = (inputs.to_f64(t) for t in (li.x, li.Wg, li.u, li.dy))
+    t0 = time.perf_counter()
+    fw = O.forward(x, Wg, u, float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)), ex, top1=cfg.top1)
+    O.backward(fw, dy)
+    dt = time.perf_counter() - t0
+    return dt
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world):
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.layer import DTSMoELayer
+
+    cfg = configs.get(args.config)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    li = inputs.make_inputs(cfg, rank=rank)
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
+    tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
+    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    # --- instrumented step: same call sequence as DTSMoELayer.forward/backward, with events
+    # around the expert GEMM calls (on the launching stream).
+    def full_step(timed: bool):
+        ev_ffn = (ev(), ev())
+        ev_bwd = (ev(), ev())
+        layer.forward(x, u, tau, c, events=ev_ffn if timed else None)
+        layer.backward(dy, events=ev_bwd if timed else None)
+        return ev_ffn, ev_bwd
+
+    for _ in range(args.warmup):
+        full_step(False)
+    torch.cuda.synchronize()
+    layer.check()
+    R = int(layer.state.offsets[-1].item())
+    counts = layer.state.counts.cpu().numpy()
+    n_launch0 = L.moe_kernel_launch_count()
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    step_ms, ffn_ms, bwd_ms = [], [], []
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        flush.fill_(1)                       # L2 flush outside the timed events
+        s0, s1 = ev(), ev()
+        s0.record(stream)
+        e_f, e_b = full_step(True)
+        s1.record(stream)
+        s1.synchronize()
+        step_ms.append(s0.elapsed_time(s1))
+        ffn_ms.append(e_f[0].elapsed_time(e_f[1]))
+        bwd_ms.append(e_b[0].elapsed_time(e_b[1]))
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    launches = (L.moe_kernel_launch_count() - n_launch0) // max(1, args.steps)
+    layer.check()
+
+    ms_step = max_over_ranks(sum(step_ms) / len(step_ms), world)
+    tokens = cfg.T * world
+    value = tokens / (ms_step / 1e3)
+
+    # roofline: expert GEMMs (12 R d d_ff FLOPs per step: 2 fwd + 4 bwd GEMMs)
+    peaks, peak_src = _peaks()
+    flops = 12.0 * R * cfg.d_model * cfg.d_ff
+    gemm_ms = (sum(ffn_ms) + sum(bwd_ms)) / len(ffn_ms)
+    achieved = flops / (gemm_ms / 1e3) / 1e12
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    step_flops = flops + 6.0 * cfg.T * cfg.d_model * cfg.E
+
+    # e2e through the public API with host buffers
+    e2e = run_e2e(args, layer, li, tau, c, world) if args.e2e else None
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
+        "data": "synthetic (seeded N(0,1) tokens, N(0,1/d) gate, N(0,0.02) shared expert, Bernoulli(0.8) masks)",
+        "config": {"workload": f"{cfg.name}: T={cfg.T}/GPU d_model={cfg.d_model} d_ff={cfg.d_ff} E={cfg.E} "
+                               f"tau={cfg.tau} c={cfg.threshold}",
+                   "tokens_per_gpu": cfg.T, "global_tokens": tokens, "rows_R": R,
+                   "mean_experts_per_token": R / cfg.T if cfg.T else 0.0,
+                   "max_over_mean_load": float(counts.max() / max(1e-9, counts.mean())),
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed between steps (256 MiB write, outside the events)",
+                   "wall_s_timed_region": wall},
+        "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained",
+                     "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
+                     "gemm_ms_per_step": gemm_ms, "flops_per_step": flops, "traffic": None},
+        "step_tflops": step_flops / (ms_step / 1e3) / 1e12,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if e2e:
+        out["e2e"] = e2e
+    if rank == 0 and world == 1 and args.cpu_baseline:
+        T_sub = args.cpu_tokens
+        dt_cpu = oracle_sample(cfg, T_sub)
+        out["cpu_baseline"] = {"value": T_sub / dt_cpu, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                               "sample": f"{T_sub} tokens of {cfg.name} (same d/d_ff/E/tau/c), fwd+bwd, fp64 NumPy, "
+                                         f"{dt_cpu:.2f} s"}
+    return out
+
+
+def run_e2e(args, layer, li, tau, c, world):
+    """Same metric through the public API, with host (pinned) buffers: every step copies
+    x, u, dy host->device and reads y and dx back device->host."""
+    dev = layer.device
+    hx, hu, hdy = (t.pin_memory() for t in (li.x, li.u, li.dy))
+    hy = torch.empty_like(li.x).pin_memory()
+    hdx = torch.empty_like(li.x).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        x = hx.to(dev, non_blocking=True)
+        u = hu.to(dev, non_blocking=True)
+        dy = hdy.to(dev, non_blocking=True)
+        y = layer.forward(x, u, tau, c)
+        g = layer.backward(dy)
+        hy.copy_(y, non_blocking=True)
+        hdx.copy_(g["dx"], non_blocking=True)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    e1.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    bi = sum(t.numel() * t.element_size() for t in (hx, hu, hdy))
+    bo = sum(t.numel() * t.element_size() for t in (hy, hdx))
+    return {"value": layer.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cfg = configs.get(args.config)
+    T_sub = args.ref_tokens
+    for _ in range(args.warmup):
+        oracle_sample(cfg, T_sub)
+    times = [oracle_sample(cfg, T_sub) for _ in range(args.steps)]
+    ms = 1e3 * sum(times) / len(times)
+    value = T_sub / (ms / 1e3)
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: T={cfg.T}/GPU d_model={cfg.d_model} d_ff={cfg.d_ff} E={cfg.E} "
+                               f"tau={cfg.tau} c={cfg.threshold}", "sample_tokens_per_step": T_sub},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                         "sample": f"{T_sub} tokens of {cfg.name} per step, fwd+bwd, fp64 NumPy oracle"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-tokens", type=int, default=1024)
+    ap.add_argument("--ref-tokens", type=int, default=256)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out))
+        return 0
+    rank, world, local = dist_setup(args.gpus)
+    out = run_ours(args, rank, world)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

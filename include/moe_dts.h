@@ -1,0 +1,191 @@
+/*
+ * moe_dts.h -- C ABI of the B200-native DTS-Gate MoE layer (EvoMoE, arXiv 2112.14397).
+ *
+ * One MoE FFN layer under the Dense-to-Sparse gate: forward and backward, plus the
+ * expert-diversify spawn.  Citations are PAPER.md line numbers (P:n) with the
+ * equation / algorithm they fall in; readings R1..R21 are listed in DESIGN.md.
+ *
+ * Conventions (all calls)
+ *  - Every tensor pointer is a DEVICE pointer owned by the caller (allocated with
+ *    torch or cudaMalloc).  The library never allocates or frees caller memory; the
+ *    only memory it uses besides the caller's tensors is the caller-provided
+ *    workspace (moe_set_workspace).
+ *  - Layouts are row-major, element strides implied by the dims stored in the ctx.
+ *    "D" is the activation/weight storage dtype chosen at moe_create (MOE_F32 or
+ *    MOE_BF16); gate probabilities, combine weights and weight gradients are fp32.
+ *  - Every compute call enqueues asynchronously on `stream` (a cudaStream_t, may be
+ *    NULL for the legacy default stream) and returns a moe_status.  Host-side
+ *    validation is synchronous: MOE_EINVAL for a bad scalar or a NULL required
+ *    pointer, MOE_ESHAPE for bad dims.  moe_last_error() returns a thread-local
+ *    message for the last failing call.  No C++ exception crosses the ABI.
+ *  - Device-detected faults (non-finite gate logits -> MOE_ENONFINITE, row capacity
+ *    exceeded -> MOE_ECAPACITY) set a flag in the workspace; they are returned by
+ *    moe_check(), which synchronises `stream`.
+ *  - Expert-major permuted ("row") layout: rows of expert e occupy
+ *    [offsets[e], offsets[e] + counts[e]) in ascending token order (stable), followed
+ *    by zero pad rows up to offsets[e+1]; offsets[e] is a multiple of 128
+ *    (MOE_ROW_ALIGN).  R_pad = offsets[E].  Buffers in row layout have R_cap rows,
+ *    R_cap >= R_pad (the caller sizes them, e.g. from counts copied to the host).
+ */
+#ifndef MOE_DTS_H
+#define MOE_DTS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_ABI_VERSION 1
+#define MOE_ROW_ALIGN 128
+
+typedef enum {
+  MOE_OK = 0,
+  MOE_EINVAL = 1,      /* bad scalar argument (tau <= 0 or non-finite, c not in [0,1)), NULL pointer */
+  MOE_ESHAPE = 2,      /* bad dims: E < 1, E % world != 0, d or d_ff not a multiple of 64 (bf16) / 4 (f32) */
+  MOE_EDTYPE = 3,      /* unknown dtype */
+  MOE_ECUDA = 4,       /* a CUDA runtime call failed (message has the CUDA error string) */
+  MOE_ENCCL = 5,       /* an NCCL call failed */
+  MOE_ENONFINITE = 6,  /* device: a gate logit was NaN/Inf ("NaN is an error state") */
+  MOE_ECAPACITY = 7,   /* device: R_pad > R_cap; rows beyond R_cap were not written */
+  MOE_EWORKSPACE = 8   /* workspace missing or too small */
+} moe_status;
+
+typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype;
+
+typedef struct moe_ctx moe_ctx;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Create a layer context.  T = tokens on this rank, E = global number of experts,
+ * world = expert-parallel group size (E_local = E / world experts live on `rank`).
+ * nccl_comm: an ncclComm_t (borrowed, never destroyed) or NULL when world == 1.
+ * Returns MOE_ESHAPE / MOE_EDTYPE / MOE_EINVAL on bad arguments. */
+int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype,
+               void* nccl_comm, int rank, int world);
+int moe_destroy(moe_ctx* ctx);
+
+/* Thread-local message describing the last error returned on this thread. */
+const char* moe_last_error(void);
+int moe_abi_version(void);
+
+/* Process-wide count of CUDA kernels this library has launched (all contexts).  Used
+ * by bench.py to report the number of library kernels inside the timed region. */
+uint64_t moe_kernel_launch_count(void);
+
+/* Workspace: device scratch owned by the caller, >= moe_workspace_bytes(ctx) bytes,
+ * 256-byte aligned.  Holds per-block expert counts, the fp64-refine queue, split-K
+ * partials and the device error flag. */
+size_t moe_workspace_bytes(const moe_ctx* ctx);
+int moe_set_workspace(moe_ctx* ctx, void* dev_ptr, size_t bytes);
+
+/* Synchronise `stream`, read and clear the device error flag; returns MOE_OK,
+ * MOE_ENONFINITE or MOE_ECAPACITY. */
+int moe_check(moe_ctx* ctx, void* stream);
+
+/* ---------------------------------------------------------------- forward */
+
+/* Expert-diversify spawn (Alg. 1 lines 4-5; Fig. P:241-247).
+ * For each LOCAL expert j (global id e = rank*E_local + j):
+ *   W1[j] = W1s (.) M1_e,  W2[j] = W2s (.) M2_e,  b1[j] = b1s,  b2[j] = b2s  (R10).
+ * W1s [d_ff, d], b1s [d_ff], W2s [d, d_ff], b2s [d]  (D, shared expert, nn.Linear [out,in]).
+ * M1bits [E][ceil(d_ff*d/32)], M2bits [E][ceil(d*d_ff/32)] uint32 words, GLOBAL expert
+ * index; bit (j % 32) of word j / 32 keeps flat element j (1 = keep).
+ * Outputs W1 [E_local, d_ff, d], b1 [E_local, d_ff], W2 [E_local, d, d_ff], b2 [E_local, d].
+ * One-time initialisation: there is no spawn backward (the paper defines none). */
+int moe_dts_spawn(moe_ctx* ctx, const void* W1s, const void* b1s, const void* W2s, const void* b2s,
+                  const uint32_t* M1bits, const uint32_t* M2bits,
+                  void* W1, void* b1, void* W2, void* b2, void* stream);
+
+/* DTS gate, steps 1-3 (Alg. 2; Eq. 6; Eq. 8; Eq. 9).
+ *   L = x W_g;  zeta = -log(-log u);  p = softmax_E((L + zeta)/tau)        (R1, R2)
+ *   dense (top1 == 0): m_i = [p_i > c] (strict, R3), argmax kept if none passes (R5)
+ *   top1 (top1 != 0):  m = onehot(argmax p)   (Alg. 2 else-branch)
+ *   G = p (.) m, NOT renormalised (R4).
+ * x [T, d] D; Wg [d, E] D; u [T, E] fp32 in (0,1) or NULL (no noise).
+ * Outputs: probs [T, E] fp32 (g'); slot [T, E] int32 (>= 0 selected, -1 not; the
+ * row index is filled in by moe_dispatch); counts [E] int32 (this rank's tokens per
+ * GLOBAL expert); near_band [1] int32 = #tokens with some |p - c| < 1e-6 (or, for
+ * argmax-decided tokens, top-2 gap < 1e-6) -- the band reported by the tests (R18).
+ * Entries within 5e-5 of the decision boundary are recomputed in fp64 before the
+ * decision.  Errors: MOE_EINVAL if tau <= 0 or not
+ * finite, c not in [0,1), or a required pointer is NULL. */
+int moe_dts_gate(moe_ctx* ctx, const void* x, const void* Wg, const float* u, float tau,
+                 float threshold, int top1, float* probs, int32_t* slot, int32_t* counts,
+                 int32_t* near_band, void* stream);
+
+/* Dispatch, step 4 (Alg. 1 lines 9-12 P:299-304; EP P:227).  Uses the per-block
+ * counts left in the workspace by the preceding moe_dts_gate on the same stream.
+ * Writes offsets [E+1] int32 (128-aligned exclusive prefix of counts), fills
+ * slot[t,e] with the row index, row_token [R_cap] int32 (-1 on pad rows),
+ * row_gate [R_cap] fp32 (= probs[t,e]; 0 on pads), x_perm [R_cap, d] D (copy of x_t;
+ * 0 on pads) and R_out [1] int32 = offsets[E].  Rows >= R_cap are not written and
+ * raise MOE_ECAPACITY at the next moe_check. */
+int moe_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot,
+                 void* x_perm, int32_t* row_token, float* row_gate, int32_t* offsets,
+                 int64_t R_cap, int32_t* R_out, void* stream);
+
+/* Grouped expert FFN, step 5 (Eq. 3 P:169-172 with GELU erf form P:472, R8).
+ * For every row r of expert e (rows [offsets[e], offsets[e+1])):
+ *   a[r] = W1[e] x_perm[r] + b1[e];  h[r] = GELU(a[r]);  e_out[r] = W2[e] h[r] + b2[e].
+ * a_saved, h_saved [R_cap, d_ff] D; e_out [R_cap, d] D.  W1..b2 are LOCAL experts
+ * (moe_dts_spawn layout).  bf16: tcgen05 tensor cores, fp32 accumulation; f32: fp32
+ * CUDA-core FMA. */
+int moe_expert_ffn(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int64_t R_cap,
+                   const void* W1, const void* b1, const void* W2, const void* b2,
+                   void* a_saved, void* h_saved, void* e_out, void* stream);
+
+/* Combine + un-permute, step 6 (Eq. 4, Eq. 7, Alg. 1 line 11):
+ *   y[t] = sum over selected e in ASCENDING e of row_gate[slot[t,e]] * e_out[slot[t,e]]
+ * accumulated in fp32 (R14), stored as D.  y [T, d]. */
+int moe_combine(moe_ctx* ctx, const void* e_out, const float* row_gate, const int32_t* slot,
+                void* y, void* stream);
+
+/* ---------------------------------------------------------------- backward */
+
+/* Combine backward (chain rule of Eq. 7).  For every row r < offsets[E]:
+ *   t = row_token[r];  d_eout[r] = row_gate[r] * dy[t];  dG_row[r] = <dy[t], e_out[r]>
+ * (0 for pad rows).  dy [T, d] D; d_eout [R_cap, d] D; dG_row [R_cap] fp32. */
+int moe_combine_bwd(moe_ctx* ctx, const void* dy, const void* e_out, const float* row_gate,
+                    const int32_t* row_token, const int32_t* offsets, int64_t R_cap,
+                    void* d_eout, float* dG_row, void* stream);
+
+/* Expert FFN backward (chain rule of Eq. 3).  Per expert e over its rows:
+ *   dh = d_eout W2[e];  da = dh (.) GELU'(a),  GELU'(a) = Phi(a) + a phi(a)
+ *   dW2[e] = d_eout^T h;  db2[e] = colsum(d_eout);  dW1[e] = da^T x_perm;  db1[e] = colsum(da)
+ *   dx_perm = da W1[e]
+ * da [R_cap, d_ff] D may ALIAS a_saved (overwritten in place).  dW1 [E_local, d_ff, d],
+ * db1 [E_local, d_ff], dW2 [E_local, d, d_ff], db2 [E_local, d] fp32 (overwritten). */
+int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, const void* a_saved,
+                       const void* h_saved, const int32_t* offsets, int64_t R_cap,
+                       const void* W1, const void* W2, void* da, void* dx_perm,
+                       float* dW1, float* db1, float* dW2, float* db2, void* stream);
+
+/* Gate backward (softmax Jacobian; mask, u and tau are constants).  Per token:
+ *   dp_e = m_e dG[slot[t,e]] (+ balance term alpha N count_e / B^2 if balance_alpha > 0,
+ *          Eq. 10, counts = global counts, B = global batch size)
+ *   dz = p (.) (dp - <p, dp>);  dlogits = dz / tau;   dWg = x^T dlogits  (fp32, [d, E])
+ * dlogits [T, E] fp32 is an output consumed by moe_dispatch_bwd (which adds
+ * dlogits W_g^T to dx).  counts may be NULL when balance_alpha == 0. */
+int moe_dts_gate_bwd(moe_ctx* ctx, const float* dG_row, const int32_t* slot, const float* probs,
+                     const void* x, float tau, float balance_alpha, const int32_t* counts,
+                     int64_t B_total, float* dWg, float* dlogits, void* stream);
+
+/* Dispatch backward (inverse of step 4) fused with the gate's input gradient:
+ *   dx[t] = sum over selected e in ASCENDING e of dx_perm[slot[t,e]]  +  dlogits[t] W_g^T
+ * dx [T, d] D (overwritten).  dlogits may be NULL (then Wg is unused). */
+int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, const float* dlogits,
+                     const void* Wg, void* dx, void* stream);
+
+/* ---------------------------------------------------------------- NEXT #1 */
+
+/* Balance loss, Eq. 10: loss = alpha N sum_i (counts_i / B^2) sum_s p[s,i]
+ * over this rank's probs (the caller all-reduces across ranks).  loss [1] fp32. */
+int moe_balance_loss(moe_ctx* ctx, const float* probs, const int32_t* counts, float alpha,
+                     int64_t B_total, float* loss, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MOE_DTS_H */

@@ -1,0 +1,183 @@
+"""ctypes binding of libmoe_dts.so -- argument marshalling only.
+
+Function names match include/moe_dts.h.  Tensors are passed as raw device pointers
+(`tensor.data_ptr()`), streams as `torch.cuda.current_stream().cuda_stream`.  Every
+non-zero status raises MoEError with moe_last_error().  There is NO fallback: if the
+shared library is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("MOE_DTS_LIB", os.path.join(_PKG, "lib", "libmoe_dts.so"))
+
+STATUS = {0: "MOE_OK", 1: "MOE_EINVAL", 2: "MOE_ESHAPE", 3: "MOE_EDTYPE", 4: "MOE_ECUDA", 5: "MOE_ENCCL",
+          6: "MOE_ENONFINITE", 7: "MOE_ECAPACITY", 8: "MOE_EWORKSPACE"}
+MOE_F32, MOE_BF16 = 0, 1
+ROW_ALIGN = 128
+
+# name -> (restype, argtypes)
+_P, _I, _F, _L, _S = C.c_void_p, C.c_int, C.c_float, C.c_int64, C.c_size_t
+SIGNATURES = {
+    "moe_create": (_I, [C.POINTER(_P), _I, _I, _I, _I, _I, _P, _I, _I]),
+    "moe_destroy": (_I, [_P]),
+    "moe_last_error": (C.c_char_p, []),
+    "moe_abi_version": (_I, []),
+    "moe_kernel_launch_count": (C.c_uint64, []),
+    "moe_workspace_bytes": (_S, [_P]),
+    "moe_set_workspace": (_I, [_P, _P, _S]),
+    "moe_check": (_I, [_P, _P]),
+    "moe_dts_spawn": (_I, [_P] + [_P] * 10 + [_P]),
+    "moe_dts_gate": (_I, [_P, _P, _P, _P, _F, _F, _I, _P, _P, _P, _P, _P]),
+    "moe_dispatch": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _P, _P]),
+    "moe_expert_ffn": (_I, [_P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "moe_combine": (_I, [_P, _P, _P, _P, _P, _P]),
+    "moe_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
+    "moe_expert_ffn_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "moe_dts_gate_bwd": (_I, [_P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P]),
+    "moe_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "moe_balance_loss": (_I, [_P, _P, _P, _F, _L, _P, _P]),
+}
+
+
+class MoEError(RuntimeError):
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} -> {STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"libmoe_dts.so not built at {path}; run `python -m paper_2112_14397_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_lib: Optional[C.CDLL] = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load()
+    return _lib
+
+
+def last_error() -> str:
+    return (lib().moe_last_error() or b"").decode()
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _call(name: str, *args):
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        raise MoEError(name, rc, last_error())
+    return rc
+
+
+# ---------------------------------------------------------------- same names as the C ABI
+def moe_create(T: int, d_model: int, d_ff: int, E: int, dtype: int, nccl_comm: int = 0, rank: int = 0,
+               world: int = 1) -> int:
+    h = C.c_void_p()
+    _call("moe_create", C.byref(h), T, d_model, d_ff, E, dtype, nccl_comm or None, rank, world)
+    return h.value
+
+
+def moe_destroy(ctx: int) -> None:
+    _call("moe_destroy", ctx)
+
+
+def moe_abi_version() -> int:
+    return lib().moe_abi_version()
+
+
+def moe_kernel_launch_count() -> int:
+    return int(lib().moe_kernel_launch_count())
+
+
+def moe_workspace_bytes(ctx: int) -> int:
+    return lib().moe_workspace_bytes(ctx)
+
+
+def moe_set_workspace(ctx: int, ws) -> None:
+    _call("moe_set_workspace", ctx, _ptr(ws), ws.numel() * ws.element_size())
+
+
+def moe_check(ctx: int, stream=None) -> None:
+    _call("moe_check", ctx, _stream(stream))
+
+
+def moe_dts_spawn(ctx, W1s, b1s, W2s, b2s, M1bits, M2bits, W1, b1, W2, b2, stream=None):
+    _call("moe_dts_spawn", ctx, *[_ptr(t) for t in (W1s, b1s, W2s, b2s, M1bits, M2bits, W1, b1, W2, b2)],
+          _stream(stream))
+
+
+def moe_dts_gate(ctx, x, Wg, u, tau, threshold, top1, probs, slot, counts, near_band, stream=None):
+    _call("moe_dts_gate", ctx, _ptr(x), _ptr(Wg), _ptr(u), float(tau), float(threshold), int(top1),
+          _ptr(probs), _ptr(slot), _ptr(counts), _ptr(near_band), _stream(stream))
+
+
+def moe_dispatch(ctx, x, probs, slot, x_perm, row_token, row_gate, offsets, R_cap, R_out, stream=None):
+    _call("moe_dispatch", ctx, _ptr(x), _ptr(probs), _ptr(slot), _ptr(x_perm), _ptr(row_token),
+          _ptr(row_gate), _ptr(offsets), int(R_cap), _ptr(R_out), _stream(stream))
+
+
+def moe_expert_ffn(ctx, x_perm, offsets, R_cap, W1, b1, W2, b2, a_saved, h_saved, e_out, stream=None):
+    _call("moe_expert_ffn", ctx, _ptr(x_perm), _ptr(offsets), int(R_cap), _ptr(W1), _ptr(b1), _ptr(W2),
+          _ptr(b2), _ptr(a_saved), _ptr(h_saved), _ptr(e_out), _stream(stream))
+
+
+def moe_combine(ctx, e_out, row_gate, slot, y, stream=None):
+    _call("moe_combine", ctx, _ptr(e_out), _ptr(row_gate), _ptr(slot), _ptr(y), _stream(stream))
+
+
+def moe_combine_bwd(ctx, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, stream=None):
+    _call("moe_combine_bwd", ctx, _ptr(dy), _ptr(e_out), _ptr(row_gate), _ptr(row_token), _ptr(offsets),
+          int(R_cap), _ptr(d_eout), _ptr(dG_row), _stream(stream))
+
+
+def moe_expert_ffn_bwd(ctx, d_eout, x_perm, a_saved, h_saved, offsets, R_cap, W1, W2, da, dx_perm,
+                       dW1, db1, dW2, db2, stream=None):
+    _call("moe_expert_ffn_bwd", ctx, _ptr(d_eout), _ptr(x_perm), _ptr(a_saved), _ptr(h_saved),
+          _ptr(offsets), int(R_cap), _ptr(W1), _ptr(W2), _ptr(da), _ptr(dx_perm), _ptr(dW1), _ptr(db1),
+          _ptr(dW2), _ptr(db2), _stream(stream))
+
+
+def moe_dts_gate_bwd(ctx, dG_row, slot, probs, x, tau, balance_alpha, counts, B_total, dWg, dlogits,
+                     stream=None):
+    _call("moe_dts_gate_bwd", ctx, _ptr(dG_row), _ptr(slot), _ptr(probs), _ptr(x), float(tau),
+          float(balance_alpha), _ptr(counts), int(B_total), _ptr(dWg), _ptr(dlogits), _stream(stream))
+
+
+def moe_dispatch_bwd(ctx, dx_perm, slot, dlogits, Wg, dx, stream=None):
+    _call("moe_dispatch_bwd", ctx, _ptr(dx_perm), _ptr(slot), _ptr(dlogits), _ptr(Wg), _ptr(dx),
+          _stream(stream))
+
+
+def moe_balance_loss(ctx, probs, counts, alpha, B_total, loss, stream=None):
+    _call("moe_balance_loss", ctx, _ptr(probs), _ptr(counts), float(alpha), int(B_total), _ptr(loss),
+          _stream(stream))

@@ -1,0 +1,329 @@
+// gate.cu -- DTS gate forward (steps 1-3) and backward (B1-3), balance loss (NEXT #1).
+//
+// Step 1  L = x W_g                                  Eq. 6
+// Step 2  p = softmax_E((L + zeta)/tau), zeta = -log(-log u)     Eq. 8, P:330-333 (R1, R2)
+// Step 3  m = [p > c] (strict), argmax guard; or top-1           Eq. 9, Alg. 2
+//
+// Routing precision: logits are accumulated in fp32.
+// Any token with an entry |p - c| < kRefine (dense branch), or whose decision is
+// argmax-based with a top-2 gap < kRefine, is recomputed entirely in fp64 from the
+// same inputs before deciding, so the selection equals the fp64 definition except
+// for entries within ~1e-7 of c.
+#include "common.cuh"
+#include "internal.h"
+
+namespace moe {
+
+namespace {
+
+constexpr float kRefine = 5e-5f;
+constexpr float kBand = 1e-6f;
+constexpr int kMaxEPL = 4;          // experts per lane (E <= 128)
+
+__device__ __forceinline__ void warp_argmax(float& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+  }
+}
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+  }
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_maxd(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Second largest value given the argmax index (for the top-2 gap).
+__device__ __forceinline__ float warp_second(const float* p, int E, int lane, int am) {
+  float s = -1.f;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    if (e < E && e != am) s = fmaxf(s, p[i]);
+  }
+  return warp_max(s);
+}
+
+// One warp per token.  Block = 8 warps handles kGateBT tokens (16 per warp).
+template <typename T>
+__global__ void __launch_bounds__(256) gate_softmax_kernel(
+    const float* __restrict__ logits, const T* __restrict__ x, const T* __restrict__ Wg,
+    const float* __restrict__ u, int T_, int d, int E, float tau, float thr, int top1,
+    float* __restrict__ probs, int* __restrict__ slot, int* __restrict__ counts,
+    int* __restrict__ blk_cnt, int* __restrict__ near_band, int* __restrict__ flags) {
+  __shared__ int s_cnt[128];
+  __shared__ int s_band;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
+  if (threadIdx.x == 0) s_band = 0;
+  __syncthreads();
+  const int tpw = kGateBT / 8;
+  for (int j = 0; j < tpw; ++j) {
+    const int t = blockIdx.x * kGateBT + warp * tpw + j;
+    if (t >= T_) break;
+    float z[kMaxEPL], p[kMaxEPL];
+    bool bad = false;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      int e = lane + 32 * i;
+      z[i] = -INFINITY;
+      if (e < E) {
+        float L = logits[(long long)t * E + e];
+        if (!isfinite(L)) bad = true;
+        float zeta = u ? -logf(-logf(u[(long long)t * E + e])) : 0.f;
+        z[i] = (L + zeta) / tau;
+      }
+    }
+    if (__any_sync(0xffffffffu, bad)) {
+      if (lane == 0 && atomicOr(&flags[0], kFlagNonFinite) == 0) flags[1] = t;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) mx = fmaxf(mx, z[i]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      p[i] = (lane + 32 * i < E) ? expf(z[i] - mx) : 0.f;
+      sum += p[i];
+    }
+    sum = warp_sum(sum);
+    const float inv = 1.0f / sum;
+    bool any_pass = false, near = false;
+    float pmax = -1.f;
+    int am = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      int e = lane + 32 * i;
+      if (e < E) {
+        p[i] = p[i] * inv;
+        if (p[i] > thr) any_pass = true;
+        if (fabsf(p[i] - thr) < kRefine) near = true;
+        if (p[i] > pmax) { pmax = p[i]; am = e; }
+      }
+    }
+    warp_argmax(pmax, am);
+    any_pass = __any_sync(0xffffffffu, any_pass);
+    bool argmax_decided = top1 || !any_pass;
+    near = __any_sync(0xffffffffu, near) && !top1;
+    if (argmax_decided) {
+      float second = warp_second(p, E, lane, am);
+      if (pmax - second < kRefine) near = true;
+    }
+    if (near) {
+      // ---- fp64 refinement: recompute logits, noise and softmax exactly from the inputs
+      double z64[kMaxEPL];
+#pragma unroll
+      for (int i = 0; i < kMaxEPL; ++i) {
+        int e = lane + 32 * i;
+        z64[i] = -INFINITY;
+        if (e < E) {
+          double acc = 0.0;
+          const T* xr = x + (long long)t * d;
+          for (int k = 0; k < d; ++k) acc = fma((double)to_f32(xr[k]), (double)to_f32(Wg[(long long)k * E + e]), acc);
+          double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
+          z64[i] = (acc + zeta) / (double)tau;
+        }
+      }
+      double mx64 = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < kMaxEPL; ++i) mx64 = fmax(mx64, z64[i]);
+      mx64 = warp_maxd(mx64);
+      double s64 = 0.0, p64[kMaxEPL];
+#pragma unroll
+      for (int i = 0; i < kMaxEPL; ++i) {
+        p64[i] = (lane + 32 * i < E) ? exp(z64[i] - mx64) : 0.0;
+        s64 += p64[i];
+      }
+      s64 = warp_sum(s64);
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      any_pass = false;
+#pragma unroll
+      for (int i = 0; i < kMaxEPL; ++i) {
+        int e = lane + 32 * i;
+        if (e < E) {
+          p64[i] /= s64;
+          p[i] = (float)p64[i];
+          if (p[i] > thr) any_pass = true;
+          if (p64[i] > best) { best = p64[i]; bi = e; }
+        }
+      }
+      warp_argmax(best, bi);
+      am = bi;
+      pmax = (float)best;
+      any_pass = __any_sync(0xffffffffu, any_pass);
+      argmax_decided = top1 || !any_pass;
+    }
+    // ---- decision + band
+    bool in_band = false;
+    if (!argmax_decided) {
+#pragma unroll
+      for (int i = 0; i < kMaxEPL; ++i)
+        if (lane + 32 * i < E && fabsf(p[i] - thr) < kBand) in_band = true;
+      in_band = __any_sync(0xffffffffu, in_band);
+    } else {
+      float second = warp_second(p, E, lane, am);
+      in_band = (pmax - second) < kBand;
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      int e = lane + 32 * i;
+      if (e < E) {
+        bool sel = argmax_decided ? (e == am) : (p[i] > thr);
+        probs[(long long)t * E + e] = p[i];
+        slot[(long long)t * E + e] = sel ? 0 : -1;
+        if (sel) atomicAdd(&s_cnt[e], 1);
+      }
+    }
+    if (lane == 0 && in_band) atomicAdd(&s_band, 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int c = s_cnt[e];
+    blk_cnt[(long long)blockIdx.x * E + e] = c;
+    if (c) atomicAdd(&counts[e], c);
+  }
+  if (threadIdx.x == 0 && s_band) atomicAdd(near_band, s_band);
+}
+
+// ------------------------------------------------------------------ gate backward
+// One warp per token: dp = m dG (+ balance), dz = p (dp - <p,dp>), dlogits = dz / tau.
+__global__ void __launch_bounds__(256) gate_bwd_token_kernel(
+    const float* __restrict__ dG_row, const int* __restrict__ slot, const float* __restrict__ probs,
+    int T_, int E, float tau, float alpha, const int* __restrict__ counts, double bal_scale,
+    float* __restrict__ dlogits) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  float p[kMaxEPL], dp[kMaxEPL];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    p[i] = 0.f; dp[i] = 0.f;
+    if (e < E) {
+      p[i] = probs[(long long)t * E + e];
+      int r = slot[(long long)t * E + e];
+      dp[i] = r >= 0 ? dG_row[r] : 0.f;
+      if (alpha > 0.f) dp[i] += (float)(bal_scale * (double)counts[e]);
+      s += p[i] * dp[i];
+    }
+  }
+  s = warp_sum(s);
+  const float inv_tau = 1.0f / tau;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    if (e < E) dlogits[(long long)t * E + e] = p[i] * (dp[i] - s) * inv_tau;
+  }
+}
+
+// out[i] = sum_z part[z][i], fixed order
+__global__ void reduce_splits_kernel(const float* __restrict__ part, int splits, long long n,
+                                     float* __restrict__ out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc = 0.f;
+  for (int z = 0; z < splits; ++z) acc += part[(long long)z * n + i];
+  out[i] = acc;
+}
+
+// ------------------------------------------------------------------ balance loss
+__global__ void colsum_probs_kernel(const float* __restrict__ probs, int T_, int E, float* __restrict__ out) {
+  const int e = blockIdx.x;
+  __shared__ float red[256];
+  float acc = 0.f;
+  for (int t = threadIdx.x; t < T_; t += blockDim.x) acc += probs[(long long)t * E + e];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[e] = red[0];
+}
+
+__global__ void balance_loss_kernel(const float* __restrict__ colsum, const int* __restrict__ counts, int E,
+                                    float alpha, double B, float* __restrict__ loss) {
+  if (threadIdx.x != 0) return;
+  double acc = 0.0;
+  for (int e = 0; e < E; ++e) acc += (double)counts[e] / (B * B) * (double)colsum[e];
+  *loss = (float)(alpha * E * acc);
+}
+
+}  // namespace
+
+cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const float* u, float tau, float thr,
+                        int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
+                        cudaStream_t s) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(counts, 0, sizeof(int) * c->E, s)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(near_band, 0, sizeof(int), s)) != cudaSuccess) return e;
+  if (c->T == 0) return cudaSuccess;
+  // Step 1: logits [T, E] fp32 = x [T, d] . Wg [d, E]
+  SimtGemm g{};
+  g.A = x; g.sAm = c->d; g.sAk = 1;
+  g.B = Wg; g.sBk = c->E; g.sBn = 1;
+  g.C = c->logits; g.sCm = c->E;
+  g.M = c->T; g.N = c->E; g.K = c->d; g.G = 1; g.k_split = 1;
+  if ((e = launch_simt_gemm(g, c->dtype, c->dtype, 0, EPI_F32, s)) != cudaSuccess) return e;
+  // Steps 2-3
+  if (c->dtype == 1)
+    gate_softmax_kernel<bf16><<<c->nblk, 256, 0, s>>>(c->logits, (const bf16*)x, (const bf16*)Wg, u, c->T, c->d,
+                                                      c->E, tau, thr, top1, probs, slot, counts, c->blk_cnt,
+                                                      near_band, c->flags), count_launch();
+  else
+    gate_softmax_kernel<float><<<c->nblk, 256, 0, s>>>(c->logits, (const float*)x, (const float*)Wg, u, c->T,
+                                                       c->d, c->E, tau, thr, top1, probs, slot, counts,
+                                                       c->blk_cnt, near_band, c->flags), count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t* slot, const float* probs,
+                            const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
+                            float* dWg, float* dlogits, cudaStream_t s) {
+  if (c->T == 0) return cudaMemsetAsync(dWg, 0, sizeof(float) * c->d * c->E, s);
+  double bal = alpha > 0.f ? (double)alpha * c->E / ((double)B_total * (double)B_total) : 0.0;
+  gate_bwd_token_kernel<<<(c->T + 7) / 8, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts, bal,
+                                                        dlogits), count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // dWg [d, E] = x^T [d, T] . dlogits [T, E]  (split-K, deterministic reduction)
+  SimtGemm g{};
+  g.A = x; g.sAm = 1; g.sAk = c->d;
+  g.B = dlogits; g.sBk = c->E; g.sBn = 1;
+  g.M = c->d; g.N = c->E; g.K = c->T; g.G = 1;
+  g.k_split = c->dwg_splits;
+  g.sCm = c->E; g.gC = (long long)c->d * c->E;
+  g.C = c->dwg_splits > 1 ? (void*)c->part : (void*)dWg;
+  if ((e = launch_simt_gemm(g, c->dtype, 0, 0, EPI_F32, s)) != cudaSuccess) return e;
+  if (c->dwg_splits > 1) {
+    long long n = (long long)c->d * c->E;
+    reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->part, c->dwg_splits, n, dWg), count_launch();
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_balance_loss(const moe_ctx* c, const float* probs, const int32_t* counts, float alpha,
+                                int64_t B_total, float* loss, cudaStream_t s) {
+  colsum_probs_kernel<<<c->E, 256, 0, s>>>(probs, c->T, c->E, c->colsum), count_launch();
+  balance_loss_kernel<<<1, 32, 0, s>>>(c->colsum, counts, c->E, alpha, (double)B_total, loss), count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,188 @@
+// gemm_simt.cu -- CUDA-core (FFMA) grouped GEMM with fp32 accumulation.
+//
+// Used for the fp32 configuration (C1), where tf32 tensor cores would miss the
+// 1e-4 tolerance (SURVEY §2.3 note), and for the small gate contractions until their
+// tensor-core versions land.  64x64 output tile, BK = 16, 256 threads, 4x4 per thread.
+#include "common.cuh"
+#include "internal.h"
+
+namespace moe {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <typename TX> __device__ __forceinline__ float ldf(const TX* p, long long i) { return to_f32(p[i]); }
+
+template <typename TA, typename TB, typename TO, int EPI>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(SimtGemm g) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int n0 = blockIdx.x * BN;
+  long long m0 = (long long)blockIdx.y * BM;
+  int grp = 0;
+  long long k_begin = 0, k_end = g.K;
+  long long m_end = g.M;
+  if (g.m_off) {
+    const long long R = g.m_off[g.G];
+    if (m0 >= R) return;
+    // tile lies inside one 128-aligned segment: find it
+    int lo = 0, hi = g.G - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (g.m_off[mid] <= m0) lo = mid; else hi = mid - 1;
+    }
+    grp = lo;
+    m_end = g.m_off[grp + 1];
+  } else if (g.k_off) {
+    grp = blockIdx.z;
+    k_begin = g.k_off[grp];
+    k_end = g.k_off[grp + 1];
+  } else if (g.k_split > 1) {
+    long long chunk = ((g.K + g.k_split - 1) / g.k_split + BK - 1) / BK * BK;
+    k_begin = (long long)blockIdx.z * chunk;
+    k_end = min((long long)g.K, k_begin + chunk);
+    grp = blockIdx.z;
+  }
+  const TA* A = reinterpret_cast<const TA*>(g.A);
+  const TB* B = reinterpret_cast<const TB*>(g.B) + (long long)grp * g.gB;
+  const bool a_mcontig = (g.sAm == 1);
+  const bool b_ncontig = (g.sBn == 1);
+
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (long long k0 = k_begin; k0 < k_end; k0 += BK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int idx = tid + i * 256;
+      int r, kk;
+      if (a_mcontig) { r = idx % BM; kk = idx / BM; } else { r = idx / BK; kk = idx % BK; }
+      long long m = m0 + r, k = k0 + kk;
+      As[kk][r] = (m < m_end && k < k_end) ? ldf(A, m * g.sAm + k * g.sAk) : 0.f;
+      int c, kb;
+      if (b_ncontig) { c = idx % BN; kb = idx / BN; } else { c = idx / BK; kb = idx % BK; }
+      long long n = n0 + c, k2 = k0 + kb;
+      Bs[kb][c] = (n < g.N && k2 < k_end) ? ldf(B, k2 * g.sBk + n * g.sBn) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+
+  long long cbase = 0;
+  if (g.k_off || (!g.m_off && g.k_split > 1)) cbase = (long long)grp * g.gC;
+  const TO* bias = reinterpret_cast<const TO*>(g.bias);
+  if (bias) bias += (long long)grp * g.gBias;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    long long m = m0 + ty * 4 + i;
+    if (m >= m_end) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n >= g.N) continue;
+      long long ci = cbase + m * g.sCm + n;
+      float v = acc[i][j];
+      if (EPI == EPI_F32) {
+        reinterpret_cast<float*>(g.C)[ci] = v;
+      } else if (EPI == EPI_T) {
+        reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(v);
+      } else if (EPI == EPI_BIAS_T) {
+        reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(v + to_f32(bias[n]));
+      } else if (EPI == EPI_BIAS_GELU) {
+        float a = v + to_f32(bias[n]);
+        TO a_t = from_f32<TO>(a);
+        reinterpret_cast<TO*>(g.C)[ci] = a_t;
+        // h is GELU of the exact fp32 pre-activation, then rounded (R16)
+        reinterpret_cast<TO*>(g.C2)[ci] = from_f32<TO>(gelu_f(a));
+      } else if (EPI == EPI_GELU_BWD) {
+        float a = to_f32(reinterpret_cast<const TO*>(g.aux)[ci]);
+        reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(v * gelu_prime_f(a));
+      }
+    }
+  }
+}
+
+template <typename TA, typename TB, typename TO>
+cudaError_t launch_typed(const SimtGemm& g, int epi, cudaStream_t s) {
+  dim3 grid((g.N + BN - 1) / BN, 1, 1);
+  if (g.m_off) {
+    grid.y = (unsigned)g.m_tiles;
+  } else {
+    grid.y = (g.M + BM - 1) / BM;
+    if (g.k_off) grid.z = g.G;
+    else if (g.k_split > 1) grid.z = g.k_split;
+  }
+  if (grid.y == 0 || grid.x == 0) return cudaSuccess;
+  switch (epi) {
+    case EPI_F32: simt_gemm_kernel<TA, TB, TO, EPI_F32><<<grid, 256, 0, s>>>(g), count_launch(); break;
+    case EPI_T: simt_gemm_kernel<TA, TB, TO, EPI_T><<<grid, 256, 0, s>>>(g), count_launch(); break;
+    case EPI_BIAS_T: simt_gemm_kernel<TA, TB, TO, EPI_BIAS_T><<<grid, 256, 0, s>>>(g), count_launch(); break;
+    case EPI_BIAS_GELU: simt_gemm_kernel<TA, TB, TO, EPI_BIAS_GELU><<<grid, 256, 0, s>>>(g), count_launch(); break;
+    case EPI_GELU_BWD: simt_gemm_kernel<TA, TB, TO, EPI_GELU_BWD><<<grid, 256, 0, s>>>(g), count_launch(); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// out[g][n] = sum_{r in group g} X[r][n], one thread per column, fixed row order.
+template <typename TI>
+__global__ void colsum_grouped_kernel(const TI* __restrict__ X, int N, const int* __restrict__ m_off,
+                                      float* __restrict__ out) {
+  const int gi = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int r0 = m_off[gi], r1 = m_off[gi + 1];
+  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+  int r = r0;
+  for (; r + 3 < r1; r += 4) {
+    acc0 += to_f32(X[(long long)r * N + n]);
+    acc1 += to_f32(X[(long long)(r + 1) * N + n]);
+    acc2 += to_f32(X[(long long)(r + 2) * N + n]);
+    acc3 += to_f32(X[(long long)(r + 3) * N + n]);
+  }
+  for (; r < r1; ++r) acc0 += to_f32(X[(long long)r * N + n]);
+  out[(long long)gi * N + n] = (acc0 + acc1) + (acc2 + acc3);
+}
+
+}  // namespace
+
+cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int epi, cudaStream_t s) {
+  if (ta == 0 && tb == 0) return launch_typed<float, float, float>(g, epi, s);
+  if (ta == 1 && tb == 1) {
+    if (tout == 1) return launch_typed<bf16, bf16, bf16>(g, epi, s);
+    return launch_typed<bf16, bf16, float>(g, EPI_F32, s);
+  }
+  if (ta == 1 && tb == 0) return launch_typed<bf16, float, float>(g, EPI_F32, s);
+  return launch_typed<float, bf16, float>(g, EPI_F32, s);
+}
+
+cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_off, int G, float* out,
+                                  cudaStream_t s) {
+  dim3 grid((N + 255) / 256, G);
+  if (G == 0 || N == 0) return cudaSuccess;
+  if (tin == 0)
+    colsum_grouped_kernel<float><<<grid, 256, 0, s>>>(reinterpret_cast<const float*>(X), N, m_off, out), count_launch();
+  else
+    colsum_grouped_kernel<bf16><<<grid, 256, 0, s>>>(reinterpret_cast<const bf16*>(X), N, m_off, out), count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,110 @@
+// internal.h -- context, workspace carve-up and kernel launchers (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+
+struct moe_ctx {
+  int T, d, f, E, E_local, dtype, rank, world;
+  void* comm;          // borrowed ncclComm_t (world > 1)
+  int sm_count;
+  int nblk;            // gate/dispatch token blocks = ceil(T / kGateBT)
+  int dwg_splits;      // split-K factor for dW_g
+  // workspace (caller owned)
+  uint8_t* ws;
+  size_t ws_bytes;
+  int* flags;          // [4] device error flags
+  int* blk_cnt;        // [nblk, E]
+  int* blk_base;       // [nblk, E]
+  float* logits;       // [T, E] fp32 gate logits
+  float* part;         // [dwg_splits, d, E] split-K partials of dW_g
+  float* dxg;          // [T, d] fp32  dlogits W_g^T  (v1 path)
+  float* colsum;       // [E] balance-loss column sums
+  int* tot;            // [E] per-expert totals written by the dispatch scan
+};
+
+namespace moe {
+
+constexpr int kGateBT = 128;   // tokens per gate/dispatch block
+
+size_t workspace_bytes(const moe_ctx* c);
+void carve_workspace(moe_ctx* c);
+
+// ---------------------------------------------------------------- launchers
+// All return cudaGetLastError() of the launch.
+cudaError_t launch_spawn(const moe_ctx* c, const void* W1s, const void* b1s, const void* W2s,
+                         const void* b2s, const uint32_t* M1, const uint32_t* M2, void* W1,
+                         void* b1, void* W2, void* b2, cudaStream_t s);
+
+cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const float* u, float tau,
+                        float thr, int top1, float* probs, int32_t* slot, int32_t* counts,
+                        int32_t* near_band, cudaStream_t s);
+
+cudaError_t launch_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot,
+                            const int32_t* counts, void* x_perm, int32_t* row_token, float* row_gate,
+                            int32_t* offsets, int64_t R_cap, int32_t* R_out, cudaStream_t s);
+
+cudaError_t launch_combine(const moe_ctx* c, const void* e_out, const float* row_gate,
+                           const int32_t* slot, void* y, cudaStream_t s);
+
+cudaError_t launch_combine_bwd(const moe_ctx* c, const void* dy, const void* e_out,
+                               const float* row_gate, const int32_t* row_token,
+                               const int32_t* offsets, int64_t R_cap, void* d_eout, float* dG_row,
+                               cudaStream_t s);
+
+cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot,
+                                const float* dlogits, const void* Wg, void* dx, cudaStream_t s);
+
+cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t* slot,
+                            const float* probs, const void* x, float tau, float alpha,
+                            const int32_t* counts, int64_t B_total, float* dWg, float* dlogits,
+                            cudaStream_t s);
+
+cudaError_t launch_balance_loss(const moe_ctx* c, const float* probs, const int32_t* counts,
+                                float alpha, int64_t B_total, float* loss, cudaStream_t s);
+
+cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets,
+                              int64_t R_cap, const void* W1, const void* b1, const void* W2,
+                              const void* b2, void* a, void* h, void* e_out, cudaStream_t s);
+
+cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm,
+                                  const void* a, const void* h, const int32_t* offsets,
+                                  int64_t R_cap, const void* W1, const void* W2, void* da,
+                                  void* dx_perm, float* dW1, float* db1, float* dW2, float* db2,
+                                  cudaStream_t s);
+
+// ---------------------------------------------------------------- SIMT grouped GEMM
+enum SimtEpi { EPI_F32 = 0, EPI_T = 1, EPI_BIAS_T = 2, EPI_BIAS_GELU = 3, EPI_GELU_BWD = 4 };
+
+struct SimtGemm {
+  const void* A; long long sAm, sAk, gA;   // A(m,k) = A[m*sAm + k*sAk] (+ g*gA)
+  const void* B; long long sBk, sBn, gB;   // B(k,n) = B[k*sBk + n*sBn] (+ g*gB)
+  void* C; long long sCm, gC;              // C(m,n) = C[m*sCm + n]     (+ g*gC / split*gC)
+  int M, N, K;
+  const int* m_off;   // row-grouped: group of a 64-row tile found in m_off[0..G]; rows global
+  const int* k_off;   // K-grouped: group g = blockIdx.z, K range [k_off[g], k_off[g+1])
+  int G;
+  int k_split;        // single problem split-K (C + z*gC), 1 = none
+  int64_t m_tiles;    // grid.y upper bound for row-grouped problems
+  const void* bias; long long gBias;        // bias[n] (+ g*gBias)
+  const void* aux;    // GELU' input, same layout as C
+  void* C2;           // second output (h) for EPI_BIAS_GELU, same layout as C
+};
+
+// ta/tb: element types of A and B (0 f32, 1 bf16); tout: type of C for EPI_T/BIAS/GELU epilogues.
+// Mixed-type combinations always use the fp32-output epilogue.
+cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int epi, cudaStream_t s);
+
+// out[g][n] = sum over rows of group g of X[r][n]  (fp32 out, deterministic)
+cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_off, int G, float* out,
+                                  cudaStream_t s);
+
+}  // namespace moe
+
+namespace moe {
+// Count of kernels this library has launched (moe_kernel_launch_count): every launch
+// site calls count_launch() right after its <<<>>> so the number is a direct tally.
+void count_launch(int n = 1);
+}  // namespace moe

@@ -1,0 +1,310 @@
+// moe_api.cu -- the extern "C" boundary (include/moe_dts.h): validation, workspace,
+// error reporting.  Every compute call forwards to a kernel launcher in namespace moe.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+
+#include "../../include/moe_dts.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return MOE_OK;
+  return fail(MOE_ECUDA, "%s: CUDA error %s (%s)", where, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define REQUIRE(p)                                                              \
+  do {                                                                          \
+    if ((p) == nullptr) return fail(MOE_EINVAL, "%s: argument '%s' is NULL", __func__, #p); \
+  } while (0)
+
+// token-sized arrays may be NULL when the rank holds no tokens (T == 0)
+#define REQUIRE_T(p)                                                            \
+  do {                                                                          \
+    if ((p) == nullptr && ctx->T > 0)                                           \
+      return fail(MOE_EINVAL, "%s: argument '%s' is NULL", __func__, #p);      \
+  } while (0)
+// row-sized arrays may be NULL when R_cap == 0
+#define REQUIRE_R(p)                                                            \
+  do {                                                                          \
+    if ((p) == nullptr && R_cap > 0)                                            \
+      return fail(MOE_EINVAL, "%s: argument '%s' is NULL", __func__, #p);      \
+  } while (0)
+
+int check_ctx(const moe_ctx* c, const char* fn) {
+  if (!c) return fail(MOE_EINVAL, "%s: ctx is NULL", fn);
+  if (!c->ws) return fail(MOE_EWORKSPACE, "%s: no workspace set (moe_set_workspace)", fn);
+  return MOE_OK;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+}  // namespace
+
+namespace moe {
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Carve {
+  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, total;
+};
+
+static Carve carve(const moe_ctx* c) {
+  Carve k;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  k.flags = take(16 * sizeof(int));
+  k.blk_cnt = take(sizeof(int) * (size_t)c->nblk * c->E);
+  k.blk_base = take(sizeof(int) * (size_t)c->nblk * c->E);
+  k.logits = take(sizeof(float) * (size_t)c->T * c->E);
+  k.part = take(sizeof(float) * (size_t)c->dwg_splits * c->d * c->E);
+  k.dxg = take(sizeof(float) * (size_t)c->T * c->d);
+  k.colsum = take(sizeof(float) * (size_t)c->E);
+  k.tot = take(sizeof(int) * (size_t)c->E);
+  k.total = o;
+  return k;
+}
+
+size_t workspace_bytes(const moe_ctx* c) { return carve(c).total; }
+
+void carve_workspace(moe_ctx* c) {
+  Carve k = carve(c);
+  c->flags = reinterpret_cast<int*>(c->ws + k.flags);
+  c->blk_cnt = reinterpret_cast<int*>(c->ws + k.blk_cnt);
+  c->blk_base = reinterpret_cast<int*>(c->ws + k.blk_base);
+  c->logits = reinterpret_cast<float*>(c->ws + k.logits);
+  c->part = reinterpret_cast<float*>(c->ws + k.part);
+  c->dxg = reinterpret_cast<float*>(c->ws + k.dxg);
+  c->colsum = reinterpret_cast<float*>(c->ws + k.colsum);
+  c->tot = reinterpret_cast<int*>(c->ws + k.tot);
+}
+
+}  // namespace moe
+
+extern "C" {
+
+const char* moe_last_error(void) { return g_err.c_str(); }
+int moe_abi_version(void) { return MOE_ABI_VERSION; }
+
+int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype, void* nccl_comm,
+               int rank, int world) {
+  if (!out) return fail(MOE_EINVAL, "moe_create: out is NULL");
+  *out = nullptr;
+  if (dtype != MOE_F32 && dtype != MOE_BF16) return fail(MOE_EDTYPE, "moe_create: unknown dtype %d", dtype);
+  const int q = dtype == MOE_BF16 ? 64 : 4;
+  if (T < 0 || E < 1 || d_model < 1 || d_ff < 1 || world < 1 || rank < 0 || rank >= world)
+    return fail(MOE_ESHAPE, "moe_create: bad dims T=%d E=%d d_model=%d d_ff=%d rank=%d world=%d", T, E,
+                d_model, d_ff, rank, world);
+  if (E % world != 0)
+    return fail(MOE_ESHAPE, "moe_create: E=%d not divisible by world=%d", E, world);
+  if (d_model % q != 0 || d_ff % q != 0)
+    return fail(MOE_ESHAPE, "moe_create: d_model=%d and d_ff=%d must be multiples of %d for %s", d_model,
+                d_ff, q, dtype == MOE_BF16 ? "bf16" : "f32");
+  if (E > 128) return fail(MOE_ESHAPE, "moe_create: E=%d > 128 is not supported", E);
+  if (world > 1 && !nccl_comm) return fail(MOE_EINVAL, "moe_create: world=%d needs an NCCL comm", world);
+  moe_ctx* c = new (std::nothrow) moe_ctx();
+  if (!c) return fail(MOE_EINVAL, "moe_create: out of host memory");
+  c->T = T; c->d = d_model; c->f = d_ff; c->E = E; c->E_local = E / world; c->dtype = dtype;
+  c->rank = rank; c->world = world; c->comm = nccl_comm;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  c->sm_count = sms > 0 ? sms : 148;
+  c->nblk = (T + moe::kGateBT - 1) / moe::kGateBT;
+  c->dwg_splits = T >= 4096 ? 32 : 1;
+  *out = c;
+  return MOE_OK;
+}
+
+int moe_destroy(moe_ctx* ctx) {
+  delete ctx;
+  return MOE_OK;
+}
+
+size_t moe_workspace_bytes(const moe_ctx* ctx) { return ctx ? moe::workspace_bytes(ctx) : 0; }
+
+int moe_set_workspace(moe_ctx* ctx, void* dev_ptr, size_t bytes) {
+  if (!ctx) return fail(MOE_EINVAL, "moe_set_workspace: ctx is NULL");
+  if (!dev_ptr) return fail(MOE_EINVAL, "moe_set_workspace: dev_ptr is NULL");
+  if (reinterpret_cast<uintptr_t>(dev_ptr) % 256 != 0)
+    return fail(MOE_EINVAL, "moe_set_workspace: workspace must be 256-byte aligned");
+  size_t need = moe::workspace_bytes(ctx);
+  if (bytes < need)
+    return fail(MOE_EWORKSPACE, "moe_set_workspace: %zu bytes given, %zu needed", bytes, need);
+  ctx->ws = reinterpret_cast<uint8_t*>(dev_ptr);
+  ctx->ws_bytes = bytes;
+  moe::carve_workspace(ctx);
+  return cuda_status(cudaMemset(ctx->flags, 0, 16 * sizeof(int)), "moe_set_workspace");
+}
+
+int moe_check(moe_ctx* ctx, void* stream) {
+  int rc = check_ctx(ctx, "moe_check");
+  if (rc) return rc;
+  int h[4] = {0, 0, 0, 0};
+  cudaError_t e = cudaMemcpyAsync(h, ctx->flags, sizeof(h), cudaMemcpyDeviceToHost, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  if (e != cudaSuccess) return cuda_status(e, "moe_check");
+  e = cudaMemsetAsync(ctx->flags, 0, 16 * sizeof(int), S(stream));
+  if (e != cudaSuccess) return cuda_status(e, "moe_check");
+  if (h[0] & moe::kFlagNonFinite)
+    return fail(MOE_ENONFINITE, "moe_check: non-finite gate logit detected (first token %d)", h[1]);
+  if (h[0] & moe::kFlagCapacity)
+    return fail(MOE_ECAPACITY, "moe_check: R_pad=%d exceeds R_cap; rows beyond R_cap were dropped", h[2]);
+  return MOE_OK;
+}
+
+int moe_dts_spawn(moe_ctx* ctx, const void* W1s, const void* b1s, const void* W2s, const void* b2s,
+                  const uint32_t* M1bits, const uint32_t* M2bits, void* W1, void* b1, void* W2,
+                  void* b2, void* stream) {
+  if (!ctx) return fail(MOE_EINVAL, "moe_dts_spawn: ctx is NULL");
+  REQUIRE(W1s); REQUIRE(b1s); REQUIRE(W2s); REQUIRE(b2s); REQUIRE(M1bits); REQUIRE(M2bits);
+  REQUIRE(W1); REQUIRE(b1); REQUIRE(W2); REQUIRE(b2);
+  return cuda_status(moe::launch_spawn(ctx, W1s, b1s, W2s, b2s, M1bits, M2bits, W1, b1, W2, b2, S(stream)),
+                     "moe_dts_spawn");
+}
+
+int moe_dts_gate(moe_ctx* ctx, const void* x, const void* Wg, const float* u, float tau, float threshold,
+                 int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
+                 void* stream) {
+  int rc = check_ctx(ctx, "moe_dts_gate");
+  if (rc) return rc;
+  REQUIRE_T(x); REQUIRE(Wg); REQUIRE_T(probs); REQUIRE_T(slot); REQUIRE(counts); REQUIRE(near_band);
+  if (!(tau > 0.0f) || !isfinite(tau)) return fail(MOE_EINVAL, "moe_dts_gate: tau=%g must be finite and > 0", tau);
+  if (!(threshold >= 0.0f && threshold < 1.0f))
+    return fail(MOE_EINVAL, "moe_dts_gate: threshold=%g must be in [0, 1)", threshold);
+  return cuda_status(moe::launch_gate(ctx, x, Wg, u, tau, threshold, top1, probs, slot, counts, near_band,
+                                      S(stream)),
+                     "moe_dts_gate");
+}
+
+int moe_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, void* x_perm,
+                 int32_t* row_token, float* row_gate, int32_t* offsets, int64_t R_cap, int32_t* R_out,
+                 void* stream) {
+  int rc = check_ctx(ctx, "moe_dispatch");
+  if (rc) return rc;
+  REQUIRE_T(x); REQUIRE_T(probs); REQUIRE_T(slot); REQUIRE_R(x_perm); REQUIRE_R(row_token); REQUIRE_R(row_gate);
+  REQUIRE(offsets); REQUIRE(R_out);
+  if (R_cap < 0 || R_cap > (int64_t)INT32_MAX) return fail(MOE_EINVAL, "moe_dispatch: bad R_cap %lld", (long long)R_cap);
+  return cuda_status(moe::launch_dispatch(ctx, x, probs, slot, nullptr, x_perm, row_token, row_gate,
+                                          offsets, R_cap, R_out, S(stream)),
+                     "moe_dispatch");
+}
+
+int moe_expert_ffn(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int64_t R_cap, const void* W1,
+                   const void* b1, const void* W2, const void* b2, void* a_saved, void* h_saved,
+                   void* e_out, void* stream) {
+  int rc = check_ctx(ctx, "moe_expert_ffn");
+  if (rc) return rc;
+  REQUIRE_R(x_perm); REQUIRE(offsets); REQUIRE(W1); REQUIRE(b1); REQUIRE(W2); REQUIRE(b2);
+  REQUIRE_R(a_saved); REQUIRE_R(h_saved); REQUIRE_R(e_out);
+  if (R_cap < 0 || R_cap % moe::kRowAlign != 0)
+    return fail(MOE_EINVAL, "moe_expert_ffn: R_cap=%lld must be a non-negative multiple of %d",
+                (long long)R_cap, moe::kRowAlign);
+  return cuda_status(moe::launch_expert_ffn(ctx, x_perm, offsets, R_cap, W1, b1, W2, b2, a_saved, h_saved,
+                                            e_out, S(stream)),
+                     "moe_expert_ffn");
+}
+
+int moe_combine(moe_ctx* ctx, const void* e_out, const float* row_gate, const int32_t* slot, void* y,
+                void* stream) {
+  int rc = check_ctx(ctx, "moe_combine");
+  if (rc) return rc;
+  if (ctx->T == 0) return MOE_OK;
+  REQUIRE(e_out); REQUIRE(row_gate); REQUIRE(slot); REQUIRE(y);
+  return cuda_status(moe::launch_combine(ctx, e_out, row_gate, slot, y, S(stream)), "moe_combine");
+}
+
+int moe_combine_bwd(moe_ctx* ctx, const void* dy, const void* e_out, const float* row_gate,
+                    const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
+                    float* dG_row, void* stream) {
+  int rc = check_ctx(ctx, "moe_combine_bwd");
+  if (rc) return rc;
+  REQUIRE_T(dy); REQUIRE_R(e_out); REQUIRE_R(row_gate); REQUIRE_R(row_token); REQUIRE(offsets); REQUIRE_R(d_eout);
+  REQUIRE_R(dG_row);
+  if (R_cap < 0) return fail(MOE_EINVAL, "moe_combine_bwd: bad R_cap");
+  return cuda_status(moe::launch_combine_bwd(ctx, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout,
+                                             dG_row, S(stream)),
+                     "moe_combine_bwd");
+}
+
+int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, const void* a_saved,
+                       const void* h_saved, const int32_t* offsets, int64_t R_cap, const void* W1,
+                       const void* W2, void* da, void* dx_perm, float* dW1, float* db1, float* dW2,
+                       float* db2, void* stream) {
+  int rc = check_ctx(ctx, "moe_expert_ffn_bwd");
+  if (rc) return rc;
+  REQUIRE_R(d_eout); REQUIRE_R(x_perm); REQUIRE_R(a_saved); REQUIRE_R(h_saved); REQUIRE(offsets); REQUIRE(W1);
+  REQUIRE(W2); REQUIRE_R(da); REQUIRE_R(dx_perm); REQUIRE(dW1); REQUIRE(db1); REQUIRE(dW2); REQUIRE(db2);
+  if (R_cap < 0 || R_cap % moe::kRowAlign != 0)
+    return fail(MOE_EINVAL, "moe_expert_ffn_bwd: R_cap=%lld must be a non-negative multiple of %d",
+                (long long)R_cap, moe::kRowAlign);
+  return cuda_status(moe::launch_expert_ffn_bwd(ctx, d_eout, x_perm, a_saved, h_saved, offsets, R_cap, W1,
+                                                W2, da, dx_perm, dW1, db1, dW2, db2, S(stream)),
+                     "moe_expert_ffn_bwd");
+}
+
+int moe_dts_gate_bwd(moe_ctx* ctx, const float* dG_row, const int32_t* slot, const float* probs,
+                     const void* x, float tau, float balance_alpha, const int32_t* counts, int64_t B_total,
+                     float* dWg, float* dlogits, void* stream) {
+  int rc = check_ctx(ctx, "moe_dts_gate_bwd");
+  if (rc) return rc;
+  REQUIRE(dG_row); REQUIRE_T(slot); REQUIRE_T(probs); REQUIRE_T(x); REQUIRE(dWg); REQUIRE_T(dlogits);
+  if (!(tau > 0.0f) || !isfinite(tau)) return fail(MOE_EINVAL, "moe_dts_gate_bwd: tau=%g must be finite and > 0", tau);
+  if (!(balance_alpha >= 0.0f) || !isfinite(balance_alpha))
+    return fail(MOE_EINVAL, "moe_dts_gate_bwd: balance_alpha=%g must be finite and >= 0", balance_alpha);
+  if (balance_alpha > 0.0f && (!counts || B_total <= 0))
+    return fail(MOE_EINVAL, "moe_dts_gate_bwd: balance term needs counts and B_total > 0");
+  return cuda_status(moe::launch_gate_bwd(ctx, dG_row, slot, probs, x, tau, balance_alpha, counts, B_total,
+                                          dWg, dlogits, S(stream)),
+                     "moe_dts_gate_bwd");
+}
+
+int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, const float* dlogits,
+                     const void* Wg, void* dx, void* stream) {
+  int rc = check_ctx(ctx, "moe_dispatch_bwd");
+  if (rc) return rc;
+  REQUIRE(dx_perm); REQUIRE_T(slot); REQUIRE_T(dx);
+  if (dlogits && !Wg) return fail(MOE_EINVAL, "moe_dispatch_bwd: dlogits given without Wg");
+  return cuda_status(moe::launch_dispatch_bwd(ctx, dx_perm, slot, dlogits, Wg, dx, S(stream)),
+                     "moe_dispatch_bwd");
+}
+
+int moe_balance_loss(moe_ctx* ctx, const float* probs, const int32_t* counts, float alpha, int64_t B_total,
+                     float* loss, void* stream) {
+  int rc = check_ctx(ctx, "moe_balance_loss");
+  if (rc) return rc;
+  REQUIRE_T(probs); REQUIRE(counts); REQUIRE(loss);
+  if (B_total <= 0) return fail(MOE_EINVAL, "moe_balance_loss: B_total must be > 0");
+  return cuda_status(moe::launch_balance_loss(ctx, probs, counts, alpha, B_total, loss, S(stream)),
+                     "moe_balance_loss");
+}
+
+}  // extern "C"
+
+#include <atomic>
+namespace moe {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+}  // namespace moe
+
+extern "C" uint64_t moe_kernel_launch_count(void) { return moe::g_launches.load(); }

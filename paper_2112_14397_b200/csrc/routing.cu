@@ -1,0 +1,389 @@
+// routing.cu -- step 4 (dispatch: scan + stable permute), step 6 (combine), their
+// backward passes (combine_bwd, dispatch_bwd) and step 6b (expert-diversify spawn).
+// All HBM-bound: 16-byte vector loads/stores, fp32 accumulation, fixed summation order.
+#include "common.cuh"
+#include "internal.h"
+
+namespace moe {
+
+namespace {
+
+// ------------------------------------------------------------------ scan
+// Single CTA of 1024 threads.  Per expert: exclusive prefix of the per-block counts
+// over blocks (blk_base), totals -> tot[], then 128-aligned exclusive prefix of the
+// totals -> offsets[E+1].  Deterministic (integer arithmetic only).
+__global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restrict__ blk_cnt, int nblk, int E,
+                                                            int* __restrict__ blk_base, int* __restrict__ tot,
+                                                            int* __restrict__ offsets, int* __restrict__ R_out,
+                                                            long long R_cap, int* __restrict__ flags) {
+  __shared__ int s_tot[128];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int e = warp; e < E; e += nw) {
+    int carry = 0;
+    for (int b0 = 0; b0 < nblk; b0 += 32) {
+      int b = b0 + lane;
+      int v = b < nblk ? blk_cnt[(long long)b * E + e] : 0;
+      int inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int n = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += n;
+      }
+      if (b < nblk) blk_base[(long long)b * E + e] = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) s_tot[e] = carry;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long off = 0;
+    for (int e = 0; e < E; ++e) {
+      offsets[e] = (int)off;
+      tot[e] = s_tot[e];
+      off += (long long)(s_tot[e] + kRowAlign - 1) / kRowAlign * kRowAlign;
+    }
+    offsets[E] = (int)off;
+    *R_out = (int)off;
+    if (off > R_cap) {
+      atomicOr(&flags[0], kFlagCapacity);
+      flags[2] = (int)off;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ permute
+// One CTA per gate block of kGateBT tokens, thread = token for the ranking phase.
+template <typename T>
+__global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
+    const T* __restrict__ x, const float* __restrict__ probs, int* __restrict__ slot, int T_, int d, int E,
+    const int* __restrict__ blk_base, const int* __restrict__ offsets, const int* __restrict__ tot,
+    T* __restrict__ x_perm, int* __restrict__ row_token, float* __restrict__ row_gate, long long R_cap) {
+  extern __shared__ int s_rows[];              // [kGateBT][E]
+  __shared__ int s_wsum[2][kGateBT / 32];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int t = blockIdx.x * kGateBT + tid;
+  const bool valid = t < T_;
+  for (int e = 0; e < E; ++e) {
+    const bool sel = valid && slot[(long long)t * E + e] >= 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    const int pre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_wsum[e & 1][warp] = __popc(bal);
+    __syncthreads();
+    int wpre = 0;
+#pragma unroll
+    for (int w = 0; w < kGateBT / 32; ++w) wpre += (w < warp) ? s_wsum[e & 1][w] : 0;
+    int row = -1;
+    if (sel) {
+      row = offsets[e] + blk_base[(long long)blockIdx.x * E + e] + wpre + pre;
+      if (row < R_cap) {
+        slot[(long long)t * E + e] = row;
+        row_token[row] = t;
+        row_gate[row] = probs[(long long)t * E + e];
+      } else {
+        slot[(long long)t * E + e] = -1;   // dropped (MOE_ECAPACITY raised by the scan)
+        row = -1;
+      }
+    }
+    s_rows[tid * E + e] = row;
+  }
+  __syncthreads();
+  // copy phase: each warp copies whole tokens, x_t read once, written to each selected row
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  for (int i = warp; i < kGateBT; i += kGateBT / 32) {
+    const int tok = blockIdx.x * kGateBT + i;
+    if (tok >= T_) break;
+    const T* src = x + (long long)tok * d;
+    for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+      uint4 buf[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int v = v0 + q * 32 + lane;
+        if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
+      }
+      for (int e = 0; e < E; ++e) {
+        const int row = s_rows[i * E + e];
+        if (row < 0) continue;
+        T* dst = x_perm + (long long)row * d;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          int v = v0 + q * 32 + lane;
+          if (v < nvec) st_v4(dst + (long long)v * V, buf[q]);
+        }
+      }
+    }
+  }
+  // pad rows of experts e = blockIdx.x, blockIdx.x + gridDim.x, ...: zero
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    const long long r0 = (long long)offsets[e] + tot[e], r1 = offsets[e + 1];
+    for (long long r = r0 + warp; r < r1 && r < R_cap; r += kGateBT / 32) {
+      if (lane == 0) { row_token[r] = -1; row_gate[r] = 0.f; }
+      T* dst = x_perm + r * d;
+      for (int v = lane; v < nvec; v += 32) st_v4(dst + (long long)v * V, make_uint4(0, 0, 0, 0));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ combine
+// One warp per token: y[t] = sum_{e asc} row_gate[r] * e_out[r], r = slot[t,e].
+template <typename T>
+__global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ e_out, const float* __restrict__ row_gate,
+                                                      const int* __restrict__ slot, int T_, int d, int E,
+                                                      T* __restrict__ y) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  int my_slot[4];
+  float my_g[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int e = lane + 32 * i;
+    my_slot[i] = e < E ? slot[(long long)t * E + e] : -1;
+    my_g[i] = my_slot[i] >= 0 ? row_gate[my_slot[i]] : 0.f;
+  }
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  for (int v = lane; v - lane < nvec; v += 32) {
+    float acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.f;
+    for (int e = 0; e < E; ++e) {
+      const int r = __shfl_sync(0xffffffffu, my_slot[e >> 5], e & 31);
+      if (r < 0) continue;
+      const float gw = __shfl_sync(0xffffffffu, my_g[e >> 5], e & 31);
+      if (v < nvec) {
+        float o[V];
+        unpack16(ld_nc_v4(e_out + (long long)r * d + (long long)v * V), o, T());
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = fmaf(gw, o[k], acc[k]);
+      }
+    }
+    if (v < nvec) st_v4(y + (long long)t * d + (long long)v * V, pack16(acc, T()));
+  }
+}
+
+// ------------------------------------------------------------------ combine backward
+// One warp per row r < offsets[E]: d_eout[r] = g dy[t]; dG_row[r] = <dy[t], e_out[r]>.
+template <typename T>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ e_out,
+                                                          const float* __restrict__ row_gate,
+                                                          const int* __restrict__ row_token,
+                                                          const int* __restrict__ offsets, int E, int d,
+                                                          long long R_cap, T* __restrict__ d_eout,
+                                                          float* __restrict__ dG_row) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long r = (long long)blockIdx.x * 8 + warp;
+  const long long R = min((long long)offsets[E], R_cap);
+  if (r >= R) return;
+  const int t = row_token[r];
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  T* dst = d_eout + r * d;
+  if (t < 0) {
+    for (int v = lane; v < nvec; v += 32) st_v4(dst + (long long)v * V, make_uint4(0, 0, 0, 0));
+    if (lane == 0) dG_row[r] = 0.f;
+    return;
+  }
+  const float gw = row_gate[r];
+  float dot = 0.f;
+  for (int v = lane; v < nvec; v += 32) {
+    float a[V], b[V], o[V];
+    unpack16(ld_nc_v4(dy + (long long)t * d + (long long)v * V), a, T());
+    unpack16(ld_nc_v4(e_out + r * d + (long long)v * V), b, T());
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      dot = fmaf(a[k], b[k], dot);
+      o[k] = gw * a[k];
+    }
+    st_v4(dst + (long long)v * V, pack16(o, T()));
+  }
+  dot = warp_sum(dot);
+  if (lane == 0) dG_row[r] = dot;
+}
+
+// ------------------------------------------------------------------ dispatch backward
+// One warp per token: dx[t] = sum_{e asc} dx_perm[slot[t,e]] + dxg[t] (fp32, may be NULL).
+template <typename T>
+__global__ void __launch_bounds__(256) dispatch_bwd_kernel(const T* __restrict__ dx_perm, const int* __restrict__ slot,
+                                                           const float* __restrict__ dxg, int T_, int d, int E,
+                                                           T* __restrict__ dx) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  int my_slot[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int e = lane + 32 * i;
+    my_slot[i] = e < E ? slot[(long long)t * E + e] : -1;
+  }
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  for (int v = lane; v - lane < nvec; v += 32) {
+    float acc[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] = 0.f;
+    for (int e = 0; e < E; ++e) {
+      const int r = __shfl_sync(0xffffffffu, my_slot[e >> 5], e & 31);
+      if (r < 0) continue;
+      if (v < nvec) {
+        float o[V];
+        unpack16(ld_nc_v4(dx_perm + (long long)r * d + (long long)v * V), o, T());
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] += o[k];
+      }
+    }
+    if (v < nvec) {
+      if (dxg) {
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] += dxg[(long long)t * d + (long long)v * V + k];
+      }
+      st_v4(dx + (long long)t * d + (long long)v * V, pack16(acc, T()));
+    }
+  }
+}
+
+// ------------------------------------------------------------------ spawn (step 6b)
+// Thread per 32-element mask word: read W_s once, write E_local masked copies.
+template <typename T>
+__global__ void __launch_bounds__(256) spawn_kernel(const T* __restrict__ Ws, const uint32_t* __restrict__ M,
+                                                    long long n, long long words, int e0, int E_local,
+                                                    T* __restrict__ W) {
+  const long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= words) return;
+  constexpr int V = Vec16<T>::N;
+  const long long base = w * 32;
+  if (base + 32 <= n) {
+    uint4 src[32 / V];
+#pragma unroll
+    for (int q = 0; q < 32 / V; ++q) src[q] = ld_nc_v4(Ws + base + q * V);
+    for (int j = 0; j < E_local; ++j) {
+      const uint32_t bits = M[(long long)(e0 + j) * words + w];
+      T* dst = W + (long long)j * n + base;
+#pragma unroll
+      for (int q = 0; q < 32 / V; ++q) {
+        uint4 v = src[q];
+        uint32_t* pv = reinterpret_cast<uint32_t*>(&v);
+        if (V == 4) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (!((bits >> (q * 4 + k)) & 1u)) pv[k] = 0u;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint32_t lo = (bits >> (q * 8 + 2 * k)) & 1u, hi = (bits >> (q * 8 + 2 * k + 1)) & 1u;
+            pv[k] &= (lo ? 0x0000ffffu : 0u) | (hi ? 0xffff0000u : 0u);
+          }
+        }
+        st_v4(dst + q * V, v);
+      }
+    }
+  } else {
+    for (int j = 0; j < E_local; ++j) {
+      const uint32_t bits = M[(long long)(e0 + j) * words + w];
+      for (long long i = base; i < n; ++i)
+        W[(long long)j * n + i] = ((bits >> (i - base)) & 1u) ? Ws[i] : from_f32<T>(0.f);
+    }
+  }
+}
+
+template <typename T>
+__global__ void copy_bias_kernel(const T* __restrict__ b, int n, int E_local, T* __restrict__ out) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)n * E_local) return;
+  out[i] = b[i % n];
+}
+
+template <typename T>
+cudaError_t spawn_typed(const moe_ctx* c, const void* W1s, const void* b1s, const void* W2s, const void* b2s,
+                        const uint32_t* M1, const uint32_t* M2, void* W1, void* b1, void* W2, void* b2,
+                        cudaStream_t s) {
+  const long long n = (long long)c->f * c->d;
+  const long long words = (n + 31) / 32;
+  const int e0 = c->rank * c->E_local;
+  spawn_kernel<T><<<(unsigned)((words + 255) / 256), 256, 0, s>>>((const T*)W1s, M1, n, words, e0, c->E_local, (T*)W1), count_launch();
+  spawn_kernel<T><<<(unsigned)((words + 255) / 256), 256, 0, s>>>((const T*)W2s, M2, n, words, e0, c->E_local, (T*)W2), count_launch();
+  copy_bias_kernel<T><<<(c->f * c->E_local + 255) / 256, 256, 0, s>>>((const T*)b1s, c->f, c->E_local, (T*)b1), count_launch();
+  copy_bias_kernel<T><<<(c->d * c->E_local + 255) / 256, 256, 0, s>>>((const T*)b2s, c->d, c->E_local, (T*)b2), count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_spawn(const moe_ctx* c, const void* W1s, const void* b1s, const void* W2s, const void* b2s,
+                         const uint32_t* M1, const uint32_t* M2, void* W1, void* b1, void* W2, void* b2,
+                         cudaStream_t s) {
+  if (c->dtype == 1) return spawn_typed<bf16>(c, W1s, b1s, W2s, b2s, M1, M2, W1, b1, W2, b2, s);
+  return spawn_typed<float>(c, W1s, b1s, W2s, b2s, M1, M2, W1, b1, W2, b2, s);
+}
+
+cudaError_t launch_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot,
+                            const int32_t* /*counts*/, void* x_perm, int32_t* row_token, float* row_gate,
+                            int32_t* offsets, int64_t R_cap, int32_t* R_out, cudaStream_t s) {
+  dispatch_scan_kernel<<<1, 1024, 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot, offsets, R_out, R_cap,
+                                          c->flags), count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || c->nblk == 0) return e;
+  const size_t smem = sizeof(int) * kGateBT * c->E;
+  if (c->dtype == 1) {
+    cudaFuncSetAttribute(dispatch_permute_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dispatch_permute_kernel<bf16><<<c->nblk, kGateBT, smem, s>>>((const bf16*)x, probs, slot, c->T, c->d, c->E,
+                                                                 c->blk_base, offsets, c->tot, (bf16*)x_perm,
+                                                                 row_token, row_gate, R_cap), count_launch();
+  } else {
+    cudaFuncSetAttribute(dispatch_permute_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dispatch_permute_kernel<float><<<c->nblk, kGateBT, smem, s>>>((const float*)x, probs, slot, c->T, c->d, c->E,
+                                                                  c->blk_base, offsets, c->tot, (float*)x_perm,
+                                                                  row_token, row_gate, R_cap), count_launch();
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine(const moe_ctx* c, const void* e_out, const float* row_gate, const int32_t* slot,
+                           void* y, cudaStream_t s) {
+  if (c->T == 0) return cudaSuccess;
+  const unsigned grid = (c->T + 7) / 8;
+  if (c->dtype == 1)
+    combine_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)e_out, row_gate, slot, c->T, c->d, c->E, (bf16*)y), count_launch();
+  else
+    combine_kernel<float><<<grid, 256, 0, s>>>((const float*)e_out, row_gate, slot, c->T, c->d, c->E, (float*)y), count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_bwd(const moe_ctx* c, const void* dy, const void* e_out, const float* row_gate,
+                               const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
+                               float* dG_row, cudaStream_t s) {
+  if (R_cap == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((R_cap + 7) / 8);
+  if (c->dtype == 1)
+    combine_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)e_out, row_gate, row_token, offsets,
+                                                  c->E, c->d, R_cap, (bf16*)d_eout, dG_row), count_launch();
+  else
+    combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)e_out, row_gate, row_token,
+                                                   offsets, c->E, c->d, R_cap, (float*)d_eout, dG_row), count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot, const float* dlogits,
+                                const void* Wg, void* dx, cudaStream_t s) {
+  if (c->T == 0) return cudaSuccess;
+  const float* dxg = nullptr;
+  if (dlogits) {
+    // dxg [T, d] fp32 = dlogits [T, E] . Wg^T  (Wg [d, E] -> B(k=e, n=dd) = Wg[dd*E + e])
+    SimtGemm g{};
+    g.A = dlogits; g.sAm = c->E; g.sAk = 1;
+    g.B = Wg; g.sBk = 1; g.sBn = c->E;
+    g.C = c->dxg; g.sCm = c->d;
+    g.M = c->T; g.N = c->d; g.K = c->E; g.G = 1; g.k_split = 1;
+    cudaError_t e = launch_simt_gemm(g, 0, c->dtype, 0, EPI_F32, s);
+    if (e != cudaSuccess) return e;
+    dxg = c->dxg;
+  }
+  const unsigned grid = (c->T + 7) / 8;
+  if (c->dtype == 1)
+    dispatch_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, dxg, c->T, c->d, c->E, (bf16*)dx), count_launch();
+  else
+    dispatch_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dx_perm, slot, dxg, c->T, c->d, c->E, (float*)dx), count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace moe

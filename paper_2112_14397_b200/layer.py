@@ -1,0 +1,181 @@
+"""DTSMoELayer: the public Python entry point -- runs the C-ABI call sequence of one
+DTS-Gate MoE layer forward + backward.  Marshalling and buffer management only: every
+step of the path runs in libmoe_dts.so kernels (see include/moe_dts.h).
+
+Forward  : moe_dts_gate -> moe_dispatch -> moe_expert_ffn -> moe_combine
+Backward : moe_combine_bwd -> moe_expert_ffn_bwd -> moe_dts_gate_bwd -> moe_dispatch_bwd
+
+PyTorch provides device memory and streams only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib as L
+
+DTYPES = {torch.float32: L.MOE_F32, torch.bfloat16: L.MOE_BF16}
+
+
+def padded_rows(counts_host, align: int = L.ROW_ALIGN) -> int:
+    return int(sum((int(c) + align - 1) // align * align for c in counts_host))
+
+
+@dataclass
+class ForwardState:
+    tau: float
+    threshold: float
+    top1: bool
+    x: torch.Tensor
+    probs: torch.Tensor
+    slot: torch.Tensor
+    counts: torch.Tensor
+    near_band: torch.Tensor
+    offsets: torch.Tensor
+    R_cap: int
+    y: torch.Tensor
+
+
+class DTSMoELayer:
+    """One MoE FFN layer under the DTS gate on the current CUDA device (one rank)."""
+
+    def __init__(self, T: int, d_model: int, d_ff: int, E: int, dtype: torch.dtype = torch.bfloat16,
+                 device: Optional[torch.device] = None, rank: int = 0, world: int = 1, nccl_comm: int = 0):
+        if dtype not in DTYPES:
+            raise ValueError(f"dtype must be one of {list(DTYPES)}")
+        self.T, self.d, self.f, self.E = T, d_model, d_ff, E
+        self.E_local = E // world
+        self.dtype = dtype
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.ctx = L.moe_create(T, d_model, d_ff, E, DTYPES[dtype], nccl_comm, rank, world)
+        nbytes = L.moe_workspace_bytes(self.ctx)
+        self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        L.moe_set_workspace(self.ctx, self.ws)
+        self._rows = None      # row-layout buffers, grown on demand
+        self._counts_host = torch.empty(E, dtype=torch.int32, pin_memory=True)
+        self.Wg = None
+        self.W1 = self.b1 = self.W2 = self.b2 = None
+        self.state: Optional[ForwardState] = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                L.moe_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ parameters
+    def spawn(self, W1s, b1s, W2s, b2s, M1bits, M2bits, stream=None):
+        """Expert-diversify (Alg. 1 lines 4-5): local experts from the shared expert + masks."""
+        El, d, f = self.E_local, self.d, self.f
+        kw = dict(dtype=self.dtype, device=self.device)
+        self.W1 = torch.empty(El, f, d, **kw)
+        self.b1 = torch.empty(El, f, **kw)
+        self.W2 = torch.empty(El, d, f, **kw)
+        self.b2 = torch.empty(El, d, **kw)
+        L.moe_dts_spawn(self.ctx, W1s, b1s, W2s, b2s, M1bits, M2bits, self.W1, self.b1, self.W2, self.b2, stream)
+
+    def set_gate(self, Wg: torch.Tensor):
+        self.Wg = Wg
+
+    # ------------------------------------------------------------ buffers
+    def _ensure_rows(self, R_cap: int):
+        if self._rows is not None and self._rows["R_cap"] >= R_cap:
+            return self._rows
+        R_cap = max(R_cap, L.ROW_ALIGN)
+        kw = dict(dtype=self.dtype, device=self.device)
+        d, f = self.d, self.f
+        self._rows = dict(
+            R_cap=R_cap,
+            x_perm=torch.empty(R_cap, d, **kw),
+            row_token=torch.empty(R_cap, dtype=torch.int32, device=self.device),
+            row_gate=torch.empty(R_cap, dtype=torch.float32, device=self.device),
+            a=torch.empty(R_cap, f, **kw),
+            h=torch.empty(R_cap, f, **kw),
+            e_out=torch.empty(R_cap, d, **kw),
+            d_eout=torch.empty(R_cap, d, **kw),
+            dG_row=torch.empty(R_cap, dtype=torch.float32, device=self.device),
+            dx_perm=torch.empty(R_cap, d, **kw),
+        )
+        return self._rows
+
+    # ------------------------------------------------------------ forward
+    def forward(self, x: torch.Tensor, u: Optional[torch.Tensor], tau: float, threshold: float,
+                top1: bool = False, R_cap: Optional[int] = None, stream=None, events=None) -> torch.Tensor:
+        """events: optional (start, end) torch.cuda.Event pair recorded around moe_expert_ffn
+        on the current stream (bench roofline timing)."""
+        T, E = self.T, self.E
+        dev = self.device
+        probs = torch.empty(T, E, dtype=torch.float32, device=dev)
+        slot = torch.empty(T, E, dtype=torch.int32, device=dev)
+        counts = torch.empty(E, dtype=torch.int32, device=dev)
+        near = torch.empty(1, dtype=torch.int32, device=dev)
+        L.moe_dts_gate(self.ctx, x, self.Wg, u, tau, threshold, top1, probs, slot, counts, near, stream)
+        if R_cap is None:
+            # size the row buffers from the routing result (one small D2H copy)
+            self._counts_host.copy_(counts, non_blocking=True)
+            torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+            R_cap = padded_rows(self._counts_host.tolist())
+        R_cap = max(L.ROW_ALIGN, (R_cap + L.ROW_ALIGN - 1) // L.ROW_ALIGN * L.ROW_ALIGN)
+        rb = self._ensure_rows(R_cap)
+        R_cap = rb["R_cap"]
+        offsets = torch.empty(E + 1, dtype=torch.int32, device=dev)
+        R_out = torch.empty(1, dtype=torch.int32, device=dev)
+        L.moe_dispatch(self.ctx, x, probs, slot, rb["x_perm"], rb["row_token"], rb["row_gate"], offsets, R_cap,
+                       R_out, stream)
+        if events:
+            events[0].record()
+        L.moe_expert_ffn(self.ctx, rb["x_perm"], offsets, R_cap, self.W1, self.b1, self.W2, self.b2, rb["a"],
+                         rb["h"], rb["e_out"], stream)
+        if events:
+            events[1].record()
+        y = torch.empty(T, self.d, dtype=self.dtype, device=dev)
+        L.moe_combine(self.ctx, rb["e_out"], rb["row_gate"], slot, y, stream)
+        self.state = ForwardState(tau, threshold, top1, x, probs, slot, counts, near, offsets, R_cap, y)
+        return y
+
+    # ------------------------------------------------------------ backward
+    def backward(self, dy: torch.Tensor, balance_alpha: float = 0.0, B_total: Optional[int] = None,
+                 inplace_da: bool = True, stream=None, events=None):
+        st = self.state
+        if st is None:
+            raise RuntimeError("backward() before forward()")
+        rb = self._rows
+        El, d, f, dev = self.E_local, self.d, self.f, self.device
+        L.moe_combine_bwd(self.ctx, dy, rb["e_out"], rb["row_gate"], rb["row_token"], st.offsets, st.R_cap,
+                          rb["d_eout"], rb["dG_row"], stream)
+        grads = dict(
+            dW1=torch.empty(El, f, d, dtype=torch.float32, device=dev),
+            db1=torch.empty(El, f, dtype=torch.float32, device=dev),
+            dW2=torch.empty(El, d, f, dtype=torch.float32, device=dev),
+            db2=torch.empty(El, d, dtype=torch.float32, device=dev),
+            dWg=torch.empty(d, self.E, dtype=torch.float32, device=dev),
+        )
+        da = rb["a"] if inplace_da else torch.empty_like(rb["a"])
+        if events:
+            events[0].record()
+        L.moe_expert_ffn_bwd(self.ctx, rb["d_eout"], rb["x_perm"], rb["a"], rb["h"], st.offsets, st.R_cap,
+                             self.W1, self.W2, da, rb["dx_perm"], grads["dW1"], grads["db1"], grads["dW2"],
+                             grads["db2"], stream)
+        if events:
+            events[1].record()
+        dlogits = torch.empty(self.T, self.E, dtype=torch.float32, device=dev)
+        B = self.T if B_total is None else B_total
+        L.moe_dts_gate_bwd(self.ctx, rb["dG_row"], st.slot, st.probs, st.x, st.tau, balance_alpha,
+                           st.counts if balance_alpha > 0 else None, B, grads["dWg"], dlogits, stream)
+        dx = torch.empty(self.T, d, dtype=self.dtype, device=dev)
+        L.moe_dispatch_bwd(self.ctx, rb["dx_perm"], st.slot, dlogits, self.Wg, dx, stream)
+        grads["dx"] = dx
+        grads["dlogits"] = dlogits
+        grads["da"] = da
+        return grads
+
+    def check(self, stream=None):
+        L.moe_check(self.ctx, stream)
+
+    @property
+    def rows(self):
+        return self._rows

@@ -1,0 +1,165 @@
+"""Shared helpers for the GPU parity tests: run the CUDA path through the C ABI
+(via DTSMoELayer) and the fp64 oracle on identical seeded inputs, then compare with
+the band procedure of SURVEY.md §8c.  Test infrastructure only."""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, Optional
+
+import numpy as np
+import torch
+
+from harness import inputs
+from harness.configs import MoEConfig
+from oracle import dts_moe as O
+
+BAND = 1e-6
+
+
+def rel_err(got: np.ndarray, ref: np.ndarray) -> float:
+    """Norm-wise relative error ||got - ref|| / ||ref|| (reading R17)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    den = np.linalg.norm(ref)
+    num = np.linalg.norm(got - ref)
+    if den == 0.0:
+        return float(num)
+    return float(num / den)
+
+
+def tol_for(cfg: MoEConfig) -> float:
+    return 1e-4 if cfg.dtype == "f32" else 2e-2
+
+
+def f32(v: float) -> float:
+    return float(np.float32(v))
+
+
+def band_tokens(p32: np.ndarray, m_gpu: np.ndarray, c: float, top1: bool) -> np.ndarray:
+    """Tokens excluded from the bit-exact mask check (R18): any |p - c| < 1e-6 in the
+    dense branch; top-2 gap < 1e-6 where the decision is argmax-based (guard / top-1)."""
+    c32 = np.float32(c)
+    dense_band = np.any(np.abs(p32 - c32) < np.float32(BAND), axis=1)
+    srt = np.sort(p32, axis=1)
+    gap = srt[:, -1] - srt[:, -2] if p32.shape[1] > 1 else np.full(p32.shape[0], np.inf, np.float32)
+    argmax_decided = np.full(p32.shape[0], True) if top1 else ~np.any(p32 > c32, axis=1)
+    return np.where(argmax_decided, gap < BAND, dense_band)
+
+
+@dataclass
+class GpuRun:
+    layer: object
+    y: np.ndarray
+    probs: np.ndarray
+    slot: np.ndarray
+    counts: np.ndarray
+    near_band: int
+    offsets: np.ndarray
+    rows: Dict[str, np.ndarray]
+    W: Dict[str, np.ndarray]
+    grads: Optional[Dict[str, np.ndarray]]
+
+
+def _np(t: torch.Tensor) -> np.ndarray:
+    if t.dtype == torch.bfloat16:
+        t = t.float()
+    return t.detach().cpu().numpy()
+
+
+def run_gpu(cfg: MoEConfig, li: inputs.LayerInputs, backward: bool = True) -> GpuRun:
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    dev = torch.device("cuda", 0)
+    T = li.x.shape[0]
+    layer = DTSMoELayer(T, cfg.d_model, cfg.d_ff, cfg.E, dtype=li.x.dtype, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    u = li.u.to(dev) if li.u is not None else None
+    y = layer.forward(li.x.to(dev), u, f32(cfg.tau), f32(cfg.threshold), top1=cfg.top1)
+    torch.cuda.synchronize()
+    layer.check()
+    st = layer.state
+    rb = layer.rows
+    R = int(st.offsets[-1].item())
+    rows = {k: _np(rb[k][:R]) for k in ("x_perm", "row_token", "row_gate", "a", "h", "e_out")}
+    W = {k: _np(getattr(layer, k)) for k in ("W1", "b1", "W2", "b2")}
+    run = GpuRun(layer, _np(y), _np(st.probs), _np(st.slot), _np(st.counts), int(st.near_band.item()),
+                 _np(st.offsets), rows, W, None)
+    if backward:
+        g = layer.backward(li.dy.to(dev), inplace_da=False)
+        torch.cuda.synchronize()
+        layer.check()
+        run.grads = {k: _np(v) for k, v in g.items() if k not in ("da",)}
+        run.grads["da"] = _np(g["da"][:R])
+        for k in ("d_eout", "dG_row", "dx_perm"):
+            run.rows[k] = _np(rb[k][:R])
+    return run
+
+
+def run_oracle(cfg: MoEConfig, li: inputs.LayerInputs, mask_override=None, backward=True):
+    ex = O.spawn(inputs.to_f64(li.W1s), inputs.to_f64(li.b1s), inputs.to_f64(li.W2s), inputs.to_f64(li.b2s),
+                 inputs.bits_u32(li.M1bits), inputs.bits_u32(li.M2bits))
+    fw = O.forward(inputs.to_f64(li.x), inputs.to_f64(li.Wg), inputs.to_f64(li.u), f32(cfg.tau),
+                   f32(cfg.threshold), ex, top1=cfg.top1, mask_override=mask_override)
+    bw = O.backward(fw, inputs.to_f64(li.dy)) if backward else None
+    return ex, fw, bw
+
+
+def compare(cfg: MoEConfig, li: inputs.LayerInputs, g: GpuRun, backward: bool = True) -> Dict[str, float]:
+    """Full per-call comparison; asserts and returns the error report."""
+    tol = tol_for(cfg)
+    rep: Dict[str, float] = {}
+    m_gpu = g.slot >= 0
+    band = band_tokens(g.probs, m_gpu, cfg.threshold, cfg.top1)
+    ex, fw, bw = run_oracle(cfg, li, backward=backward)
+    flips = np.any(fw.m != m_gpu, axis=1)
+    rep["band_tokens"] = int(band.sum())
+    rep["mask_flips"] = int(flips.sum())
+    assert not np.any(flips & ~band), f"routing mismatch outside the band on tokens {np.nonzero(flips & ~band)[0][:10]}"
+    assert g.near_band == int(band.sum()), (g.near_band, int(band.sum()))
+    if flips.any():
+        ex, fw, bw = run_oracle(cfg, li, mask_override=m_gpu, backward=backward)
+    # spawn: bit-exact
+    for k in ("W1", "b1", "W2", "b2"):
+        assert np.array_equal(g.W[k], ex[k]), f"spawn {k} not bit-exact"
+    # gate probabilities (1e-5 abs, BJ:5)
+    rep["probs_maxabs"] = float(np.max(np.abs(g.probs - fw.p)))
+    assert rep["probs_maxabs"] <= 1e-5, rep
+    # counts / dispatch layout: bit-exact vs the stable rule on the GPU's mask
+    counts, offsets, slot, row_token = O.dispatch_layout(m_gpu)
+    assert np.array_equal(g.counts, counts)
+    assert np.array_equal(g.offsets, offsets)
+    assert np.array_equal(g.slot, slot)
+    assert np.array_equal(g.rows["row_token"], row_token)
+    valid = row_token >= 0
+    x64 = inputs.to_f64(li.x)
+    assert np.array_equal(g.rows["x_perm"][valid], x64[row_token[valid]]), "x_perm not a bit-exact copy"
+    assert not np.any(g.rows["x_perm"][~valid]), "pad rows not zero"
+    toks, es = np.nonzero(m_gpu)
+    assert np.array_equal(g.rows["row_gate"][slot[toks, es]], g.probs[toks, es]), "row_gate provenance"
+    # expert FFN intermediates and output
+    a_ref = O.to_rows(fw.a, offsets, cfg.d_ff)
+    e_ref = O.to_rows(fw.o, offsets, cfg.d_model)
+    rep["a"] = rel_err(g.rows["a"][valid], a_ref[valid])
+    rep["e_out"] = rel_err(g.rows["e_out"][valid], e_ref[valid])
+    rep["y"] = rel_err(g.y, fw.y)
+    if backward:
+        do_ref = O.to_rows(bw.do, offsets, cfg.d_model)
+        dxe_ref = O.to_rows(bw.dxe, offsets, cfg.d_model)
+        rep["d_eout"] = rel_err(g.rows["d_eout"][valid], do_ref[valid])
+        assert not np.any(g.rows["d_eout"][~valid]), "d_eout pad rows not zero"
+        rep["dG_row"] = rel_err(g.rows["dG_row"][slot[toks, es]], bw.dG[toks, es])
+        rep["dx_perm"] = rel_err(g.rows["dx_perm"][valid], dxe_ref[valid])
+        rep["dx"] = rel_err(g.grads["dx"], bw.dx)
+        rep["dWg"] = rel_err(g.grads["dWg"], bw.dWg)
+        rep["dlogits"] = rel_err(g.grads["dlogits"], bw.dlogits)
+        for k, ref in (("dW1", bw.dW1), ("db1", bw.db1), ("dW2", bw.dW2), ("db2", bw.db2)):
+            per = [rel_err(g.grads[k][e], ref[e]) for e in range(cfg.E) if fw.counts[e] > 0]
+            rep[k] = max(per) if per else 0.0
+            for e in range(cfg.E):
+                if fw.counts[e] == 0:
+                    assert not np.any(g.grads[k][e]), f"{k}[{e}] must be zero for an empty expert"
+    for k, v in rep.items():
+        if k in ("band_tokens", "mask_flips", "probs_maxabs"):
+            continue
+        assert v <= tol, f"{k}: rel err {v:.3e} > {tol} ({rep})"
+    return rep

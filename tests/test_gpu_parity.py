@@ -1,0 +1,145 @@
+"""GPU parity of the CUDA path (through the C ABI) against the fp64 oracle.
+
+Sizes: C1 in full; C2-C5 at reduced T (same d, d_ff, E, tau, c -- several tiles and a
+ragged tail), plus edge cases (ragged T, T=1, c=0, no noise, top-1, the guard).
+Tolerances (BJ:5): probs 1e-5 abs; masks/counts/layout bit-exact outside the 1e-6
+band; values 1e-4 (fp32) / 2e-2 (bf16) norm-wise relative.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from harness import configs, inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2112_14397_b200 import build
+    build.build()
+
+
+def _run(cfg, T=None, step=0, with_noise=True, backward=True):
+    from _parity import compare, run_gpu
+    li = inputs.make_inputs(cfg, step=step, with_noise=with_noise, T=T)
+    g = run_gpu(cfg, li, backward=backward)
+    rep = compare(cfg, li, g, backward=backward)
+    print(cfg.name, T, rep)
+    return rep, g
+
+
+def test_c1_full():
+    _run(configs.C1)
+
+
+def test_c1_ragged_tail():
+    _run(configs.C1, T=200)
+
+
+def test_c1_single_token():
+    _run(configs.C1, T=1)
+
+
+def test_c1_threshold_zero_all_selected():
+    cfg = dataclasses.replace(configs.C1, threshold=0.0)
+    rep, g = _run(cfg)
+    assert np.all(g.slot >= 0)
+
+
+def test_c1_guard_fires():
+    # c >= 1/E makes empty selections possible; a low tau makes them common
+    cfg = dataclasses.replace(configs.C1, threshold=0.6, tau=4.0)
+    rep, g = _run(cfg)
+    assert np.all((g.slot >= 0).sum(1) >= 1)
+
+
+def test_c1_top1():
+    cfg = dataclasses.replace(configs.C1, top1=True)
+    rep, g = _run(cfg)
+    assert np.all((g.slot >= 0).sum(1) == 1)
+
+
+def test_c2_reduced_dense():
+    _run(configs.C2, T=1024)
+
+
+def test_c2_reduced_no_noise():
+    _run(configs.C2, T=384, with_noise=False)
+
+
+def test_c3_reduced():
+    _run(configs.C3, T=1000)
+
+
+def test_c3_reduced_top1():
+    _run(dataclasses.replace(configs.C3, top1=True), T=512)
+
+
+def test_c4_reduced():
+    _run(configs.C4, T=640)
+
+
+@pytest.mark.parametrize("s", [0, 2, 9, 19])
+def test_c5_schedule_steps(s):
+    _run(configs.C5.at_step(s), T=512, step=s)
+
+
+def test_deterministic_rerun():
+    from _parity import run_gpu
+    cfg = configs.C3
+    li = inputs.make_inputs(cfg, T=777)
+    a = run_gpu(cfg, li)
+    b = run_gpu(cfg, li)
+    assert np.array_equal(a.y, b.y) and np.array_equal(a.slot, b.slot)
+    for k in a.grads:
+        assert np.array_equal(a.grads[k], b.grads[k]), k
+
+
+def test_nonfinite_input_flagged():
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.C1
+    li = inputs.make_inputs(cfg)
+    dev = torch.device("cuda", 0)
+    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=torch.float32, device=dev)
+    x = li.x.clone()
+    x[5, 3] = float("nan")
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    layer.forward(x.to(dev), li.u.to(dev), 1.0, 0.1)
+    with pytest.raises(L.MoEError) as e:
+        layer.check()
+    assert e.value.code == 6
+
+
+def test_capacity_overflow_flagged():
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.C1
+    li = inputs.make_inputs(cfg)
+    dev = torch.device("cuda", 0)
+    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=torch.float32, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    layer.forward(li.x.to(dev), li.u.to(dev), 1.0, 0.1, R_cap=128)
+    with pytest.raises(L.MoEError) as e:
+        layer.check()
+    assert e.value.code == 7
+
+
+def test_invalid_scalars_rejected():
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.C1
+    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=torch.float32)
+    li = inputs.make_inputs(cfg)
+    layer.set_gate(li.Wg.cuda())
+    for tau, c in ((0.0, 0.1), (float("nan"), 0.1), (1.0, 1.0), (1.0, -0.1)):
+        with pytest.raises(L.MoEError) as e:
+            layer.forward(li.x.cuda(), li.u.cuda(), tau, c)
+        assert e.value.code == 1
