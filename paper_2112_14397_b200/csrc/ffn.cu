@@ -22,6 +22,7 @@ cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_
                               void* e_out, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local, dt = c->dtype;
   cudaError_t e;
+  if (c->use_tc) return tc_expert_ffn(c, x_perm, offsets, R_cap, W1, b1, W2, b2, a, h, e_out, s);
   // GEMM1: a = x_perm W1_e^T + b1_e, h = GELU(a)
   SimtGemm g1 = base_rows(offsets, El, R_cap);
   g1.A = x_perm; g1.sAm = d; g1.sAk = 1;
@@ -46,6 +47,13 @@ cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const vo
                                   float* db2, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local, dt = c->dtype;
   cudaError_t e;
+  if (c->use_tc) {
+    if ((e = tc_expert_ffn_bwd(c, d_eout, x_perm, a, h, offsets, R_cap, W1, W2, da, dx_perm, dW1, dW2, s)) !=
+        cudaSuccess)
+      return e;
+    if ((e = launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, s)) != cudaSuccess) return e;
+    return launch_colsum_grouped(da, dt, f, offsets, El, db1, s);
+  }
   // dgrad2 + GELU': da = (d_eout W2_e) (.) GELU'(a)      (da may alias a)
   SimtGemm g = base_rows(offsets, El, R_cap);
   g.A = d_eout; g.sAm = d; g.sAk = 1;

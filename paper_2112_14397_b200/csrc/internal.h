@@ -12,6 +12,7 @@ struct moe_ctx {
   int sm_count;
   int nblk;            // gate/dispatch token blocks = ceil(T / kGateBT)
   int dwg_splits;      // split-K factor for dW_g
+  int use_tc;          // bf16 expert GEMMs on tcgen05 (1) or CUDA cores (0, MOE_GEMM=simt debug)
   // workspace (caller owned)
   uint8_t* ws;
   size_t ws_bytes;
@@ -74,6 +75,15 @@ cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const vo
                                   int64_t R_cap, const void* W1, const void* W2, void* da,
                                   void* dx_perm, float* dW1, float* db1, float* dW2, float* db2,
                                   cudaStream_t s);
+
+// ---------------------------------------------------------------- tcgen05 grouped GEMM (bf16)
+bool tc_available();
+cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
+                          const void* W1, const void* b1, const void* W2, const void* b2, void* a, void* h,
+                          void* e_out, cudaStream_t s);
+cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* a,
+                              const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
+                              const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, cudaStream_t s);
 
 // ---------------------------------------------------------------- SIMT grouped GEMM
 enum SimtEpi { EPI_F32 = 0, EPI_T = 1, EPI_BIAS_T = 2, EPI_BIAS_GELU = 3, EPI_GELU_BWD = 4 };

@@ -1,6 +1,7 @@
 // moe_api.cu -- the extern "C" boundary (include/moe_dts.h): validation, workspace,
 // error reporting.  Every compute call forwards to a kernel launcher in namespace moe.
 #include <math.h>
+#include <stdlib.h>
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
@@ -132,6 +133,10 @@ int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype, vo
   c->sm_count = sms > 0 ? sms : 148;
   c->nblk = (T + moe::kGateBT - 1) / moe::kGateBT;
   c->dwg_splits = T >= 4096 ? 32 : 1;
+  {
+    const char* g = getenv("MOE_GEMM");
+    c->use_tc = (dtype == MOE_BF16) && !(g && strcmp(g, "simt") == 0);
+  }
   *out = c;
   return MOE_OK;
 }
