@@ -19,9 +19,12 @@ import sysconfig
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "build")
+# Experiment builds: MOE_NVCC_EXTRA="-DFOO" MOE_LIB_OUT=.../libx.so (separate object dir)
+EXTRA = os.environ.get("MOE_NVCC_EXTRA", "").split()
+_tag = ("_" + "".join(c if c.isalnum() else "_" for c in "".join(EXTRA))) if EXTRA else ""
+BUILD = os.path.join(PKG, "build" + _tag)
 LIB_DIR = os.path.join(PKG, "lib")
-LIB = os.path.join(LIB_DIR, "libmoe_dts.so")
+LIB = os.environ.get("MOE_LIB_OUT", os.path.join(LIB_DIR, "libmoe_dts.so"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -53,7 +56,7 @@ def _newest_header() -> float:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    os.makedirs(LIB_DIR, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nd = nccl_dir()
     inc = [os.path.join(nd, "include")] if nd else []
     defs = ["-DMOE_HAVE_NCCL=1"] if nd else []
@@ -67,7 +70,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def comp(so):
         s, o = so
-        cmd = [NVCC] + _flags(inc) + defs + ["-c", s, "-o", o]
+        cmd = [NVCC] + _flags(inc) + defs + EXTRA + ["-c", s, "-o", o]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)

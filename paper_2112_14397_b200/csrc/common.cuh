@@ -75,4 +75,39 @@ __device__ __forceinline__ float gelu_prime_f(float a) {
          a * 0.39894228040143268f * __expf(-0.5f * a * a);
 }
 
+// Epilogue-grade Phi(a) = (1 + erf(a/sqrt2))/2 from Abramowitz & Stegun 7.1.26
+// (|erf error| <= 1.5e-7, far below the bf16 rounding of a and h): for x = |a|/sqrt2,
+// erfc(x) = t*(a1 + t*(a2 + ... a5)) * exp(-x^2), t = 1/(1 + p x).  The 1/2 of Phi is folded
+// into the coefficients; exp(-x^2) = exp(-a^2/2) is returned for phi(a) = exp(-a^2/2)/sqrt(2 pi).
+// One MUFU.RCP + one MUFU.EX2 per element.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float phi_cdf_as(float a, float& e) {
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(a), 1.0f));
+  const float poly = t * fmaf(fmaf(fmaf(fmaf(0.5f * 1.061405429f, t, 0.5f * -1.453152027f), t, 0.5f * 1.421413741f), t,
+                                   0.5f * -0.284496736f),
+                              t, 0.5f * 0.254829592f);
+  e = ex2_approx(a * (a * (-0.5f * 1.4426950408889634f)));   // exp(-a^2/2)
+  const float q = poly * e;                                  // erfc(|a|/sqrt2) / 2 = Phi(-|a|)
+  return a >= 0.0f ? 1.0f - q : q;
+}
+__device__ __forceinline__ float gelu_fast(float a) {
+  float e;
+  return a * phi_cdf_as(a, e);
+}
+// GELU'(a) = Phi(a) + a phi(a)
+__device__ __forceinline__ float gelu_prime_fast(float a) {
+  float e;
+  const float ph = phi_cdf_as(a, e);
+  return fmaf(a * 0.39894228040143268f, e, ph);
+}
+
 }  // namespace moe

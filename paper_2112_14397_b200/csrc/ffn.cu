@@ -51,8 +51,8 @@ cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const vo
     if ((e = tc_expert_ffn_bwd(c, d_eout, x_perm, a, h, offsets, R_cap, W1, W2, da, dx_perm, dW1, dW2, s)) !=
         cudaSuccess)
       return e;
-    if ((e = launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, s)) != cudaSuccess) return e;
-    return launch_colsum_grouped(da, dt, f, offsets, El, db1, s);
+    if ((e = launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, c->colpart, s)) != cudaSuccess) return e;
+    return launch_colsum_grouped(da, dt, f, offsets, El, db1, c->colpart, s);
   }
   // dgrad2 + GELU': da = (d_eout W2_e) (.) GELU'(a)      (da may alias a)
   SimtGemm g = base_rows(offsets, El, R_cap);
@@ -83,8 +83,8 @@ cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const vo
   g1.N = d; g1.K = f;
   if ((e = launch_simt_gemm(g1, dt, dt, dt, EPI_T, s)) != cudaSuccess) return e;
   // bias gradients: column sums per expert (pad rows are zero)
-  if ((e = launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, s)) != cudaSuccess) return e;
-  return launch_colsum_grouped(da, dt, f, offsets, El, db1, s);
+  if ((e = launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, c->colpart, s)) != cudaSuccess) return e;
+  return launch_colsum_grouped(da, dt, f, offsets, El, db1, c->colpart, s);
 }
 
 }  // namespace moe

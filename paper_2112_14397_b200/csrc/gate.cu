@@ -60,7 +60,7 @@ __device__ __forceinline__ float warp_second(const float* p, int E, int lane, in
 
 // One warp per token.  Block = 8 warps handles kGateBT tokens (16 per warp).
 template <typename T>
-__global__ void __launch_bounds__(256) gate_softmax_kernel(
+__global__ void __launch_bounds__(1024) gate_softmax_kernel(
     const float* __restrict__ logits, const T* __restrict__ x, const T* __restrict__ Wg,
     const float* __restrict__ u, int T_, int d, int E, float tau, float thr, int top1,
     float* __restrict__ probs, int* __restrict__ slot, int* __restrict__ counts,
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) gate_softmax_kernel(
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
   if (threadIdx.x == 0) s_band = 0;
   __syncthreads();
-  const int tpw = kGateBT / 8;
+  const int tpw = kGateBT / 32;
   for (int j = 0; j < tpw; ++j) {
     const int t = blockIdx.x * kGateBT + warp * tpw + j;
     if (t >= T_) break;
@@ -284,11 +284,11 @@ cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const f
   if ((e = launch_simt_gemm(g, c->dtype, c->dtype, 0, EPI_F32, s)) != cudaSuccess) return e;
   // Steps 2-3
   if (c->dtype == 1)
-    gate_softmax_kernel<bf16><<<c->nblk, 256, 0, s>>>(c->logits, (const bf16*)x, (const bf16*)Wg, u, c->T, c->d,
+    gate_softmax_kernel<bf16><<<c->nblk, 1024, 0, s>>>(c->logits, (const bf16*)x, (const bf16*)Wg, u, c->T, c->d,
                                                       c->E, tau, thr, top1, probs, slot, counts, c->blk_cnt,
                                                       near_band, c->flags), count_launch();
   else
-    gate_softmax_kernel<float><<<c->nblk, 256, 0, s>>>(c->logits, (const float*)x, (const float*)Wg, u, c->T,
+    gate_softmax_kernel<float><<<c->nblk, 1024, 0, s>>>(c->logits, (const float*)x, (const float*)Wg, u, c->T,
                                                        c->d, c->E, tau, thr, top1, probs, slot, counts,
                                                        c->blk_cnt, near_band, c->flags), count_launch();
   return cudaGetLastError();

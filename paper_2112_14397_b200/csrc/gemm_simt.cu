@@ -142,24 +142,64 @@ cudaError_t launch_typed(const SimtGemm& g, int epi, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// out[g][n] = sum_{r in group g} X[r][n], one thread per column, fixed row order.
+// Per-group column sums (bias gradients), deterministic two-phase reduction.
+// Phase 1: block (column block of 256, split s, group g); lane = 8 columns (16-byte loads),
+// warp w sums rows r0 + w, r0 + w + 8, ... of its split; warps combined in fixed order.
 template <typename TI>
-__global__ void colsum_grouped_kernel(const TI* __restrict__ X, int N, const int* __restrict__ m_off,
-                                      float* __restrict__ out) {
-  const int gi = blockIdx.y;
+__global__ void __launch_bounds__(256) colsum_part_kernel(const TI* __restrict__ X, int N, const int* __restrict__ m_off,
+                                                         int S, float* __restrict__ part) {
+  constexpr int V = Vec16<TI>::N;                 // elements per 16-byte vector
+  constexpr int COLS = 32 * V;                     // columns per block
+  __shared__ float red[8][COLS];
+  const int g = blockIdx.z, s = blockIdx.y;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n0 = blockIdx.x * COLS + lane * V;
+  const int off0 = m_off[g], len = m_off[g + 1] - off0;
+  const int per = (len + S - 1) / S;
+  const int r0 = off0 + s * per, r1 = min(off0 + len, r0 + per);
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  if (n0 < N) {
+    int r = r0 + warp;
+    for (; r + 24 < r1; r += 32) {
+      uint4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q[u] = ld_nc_v4(X + (long long)(r + 8 * u) * N + n0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float f[V];
+        unpack16(q[u], f, TI());
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] += f[k];
+      }
+    }
+    for (; r < r1; r += 8) {
+      float f[V];
+      unpack16(ld_nc_v4(X + (long long)r * N + n0), f, TI());
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[k] += f[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k) red[warp][lane * V + k] = acc[k];
+  __syncthreads();
+  for (int c = threadIdx.x; c < COLS; c += 256) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][c];
+    const int n = blockIdx.x * COLS + c;
+    if (n < N) part[((long long)g * S + s) * N + n] = t;
+  }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ part, int N, int S, float* __restrict__ out) {
+  const int g = blockIdx.y;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
-  const int r0 = m_off[gi], r1 = m_off[gi + 1];
-  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
-  int r = r0;
-  for (; r + 3 < r1; r += 4) {
-    acc0 += to_f32(X[(long long)r * N + n]);
-    acc1 += to_f32(X[(long long)(r + 1) * N + n]);
-    acc2 += to_f32(X[(long long)(r + 2) * N + n]);
-    acc3 += to_f32(X[(long long)(r + 3) * N + n]);
-  }
-  for (; r < r1; ++r) acc0 += to_f32(X[(long long)r * N + n]);
-  out[(long long)gi * N + n] = (acc0 + acc1) + (acc2 + acc3);
+  float t = 0.f;
+  for (int s = 0; s < S; ++s) t += part[((long long)g * S + s) * N + n];
+  out[(long long)g * N + n] = t;
 }
 
 }  // namespace
@@ -175,13 +215,16 @@ cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int ep
 }
 
 cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_off, int G, float* out,
-                                  cudaStream_t s) {
-  dim3 grid((N + 255) / 256, G);
+                                  float* part, cudaStream_t s) {
   if (G == 0 || N == 0) return cudaSuccess;
+  const int S = kColsumSplits;
+  const int cols = tin == 0 ? 128 : 256;
+  dim3 g1((N + cols - 1) / cols, S, G);
   if (tin == 0)
-    colsum_grouped_kernel<float><<<grid, 256, 0, s>>>(reinterpret_cast<const float*>(X), N, m_off, out), count_launch();
+    colsum_part_kernel<float><<<g1, 256, 0, s>>>(reinterpret_cast<const float*>(X), N, m_off, S, part), count_launch();
   else
-    colsum_grouped_kernel<bf16><<<grid, 256, 0, s>>>(reinterpret_cast<const bf16*>(X), N, m_off, out), count_launch();
+    colsum_part_kernel<bf16><<<g1, 256, 0, s>>>(reinterpret_cast<const bf16*>(X), N, m_off, S, part), count_launch();
+  colsum_final_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, S, out), count_launch();
   return cudaGetLastError();
 }
 

@@ -1,16 +1,23 @@
 // gemm_tc.cu -- persistent, warp-specialised tcgen05 grouped GEMM for the expert FFN
-// (step 5 and B5).  bf16 operands staged by TMA (128-byte swizzle) into a 4-stage
-// shared-memory ring, tcgen05.mma (M=128, N=256, K=16) accumulating in TMEM (two
-// 256-column accumulators so the epilogue of tile i overlaps the mainloop of tile i+1),
-// tcgen05.ld epilogue with the fused bias / GELU / GELU' / fp32-store variants.
+// (step 5 and B5), run as CTA PAIRS (cluster of 2, tcgen05 cta_group::2).
 //
-// Roles (192 threads):  warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
-//                       warps 2..5 = epilogue (thread = accumulator row).
-// Scheduling: static round-robin over tiles; every role walks the same tile sequence.
-//   ROWS mode  (ragged M): tiles = (offsets[G]/128) x ceil(N/256); group found from the
-//              device offsets[] (segments are 128-row aligned, so a tile never straddles).
-//   KGRP mode  (ragged K, weight gradients): tiles = G x ceil(M/128) x ceil(N/256);
-//              K range of group g = [offsets[g], offsets[g+1]); empty groups store zeros.
+// One pair computes a 256 x 256 fp32 tile: each CTA holds 128 rows of A and 128 rows
+// (N-columns) of B per 64-deep K stage (32 KB / stage / CTA), the pair leader issues
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16) and each CTA's TMEM receives its own
+// 128 accumulator rows.  Two 256-column TMEM accumulators let the epilogue of tile i
+// overlap the mainloop of tile i+1.  Operands arrive by TMA (128-byte swizzle) into a
+// 5-7 stage ring; the epilogue (8 warps, thread = accumulator row, 128 columns per warp)
+// reads TMEM with tcgen05.ld, applies the fused bias / GELU / GELU' / fp32 variants and
+// writes bf16 results through shared memory with TMA bulk-tensor stores.  The GELU'
+// operand a is TMA-loaded into the same staging buffers two chunks ahead.
+//
+// Roles (320 threads / CTA): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+//   issuer (leader CTA only), warps 2..9 = epilogue.
+// Scheduling (static, per pair): ROWS mode (ragged M): a tile is a pair of 128-row blocks
+//   of ONE expert (segments are 128-aligned; an odd last block leaves the second CTA's
+//   half idle) x one 256-wide N block; the expert comes from the device offsets[].
+//   KGRP mode (ragged K, weight gradients): tiles = G x ceil(M/256) x ceil(N/256), K range
+//   of group g = [offsets[g], offsets[g+1]); empty groups store zeros.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -22,58 +29,78 @@ namespace moe {
 
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;          // 16 KB
-constexpr int B_BYTES = BN * BK * 2;          // 32 KB
+constexpr int BM = 128;                      // rows per CTA (pair tile: 256)
+constexpr int BN = 256;                      // pair tile width; each CTA stages BNH rows of B
+constexpr int BNH = 128;
+constexpr int BK = 64;
+constexpr int A_BYTES = BM * BK * 2;         // 16 KB
+constexpr int B_BYTES = BNH * BK * 2;        // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 512;                // 2 accumulators x 256 fp32 columns
-constexpr int NUM_THREADS = 192;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, offsets*/;
+constexpr int TMEM_COLS = 512;               // 2 accumulators x 256 fp32 columns
+constexpr int EPI_WARPS = 8;                 // 2 per TMEM lane quarter, each owns 128 of the 256 columns
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int CHUNK_BYTES = 32 * 32 * 2;     // one 32x32 bf16 sub-tile (TMA box, 64-byte swizzle)
 constexpr int MAX_G = 128;
+constexpr int SMEM_LIMIT = 232448;
+
+#ifdef MOE_EXP_NOAUX
+#define AUX_LOAD(p) make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u)
+#else
+#define AUX_LOAD(p) ld_nc_v4(p)
+#endif
 
 enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 3, TEPI_F32 = 4 };
 
+template <int EPI> struct EpiCfg {
+  static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
+  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4 : 2;                            // staging buffers per warp
+  static constexpr int STAGING = NOUT * EPI_WARPS * NBUF * CHUNK_BYTES;
+  static constexpr int BAR_BYTES = 2048;
+  static constexpr int STAGES = (SMEM_LIMIT - 1024 - BAR_BYTES - STAGING) / STAGE_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 + BAR_BYTES;
+};
+
 struct TcParams {
-  int kgrp;               // 0 = ragged M (ROWS), 1 = ragged K (KGRP)
   int G;
   const int* offsets;     // [G+1]
   int M, N, K;            // ROWS: N, K used; KGRP: M, N used
-  int m_tiles_cap;        // ROWS: R_cap / 128
+  int rows_cap;           // ROWS: R_cap (rows of every row-layout buffer)
   int b_group_rows;       // ROWS: B tensor-map row offset of group g = g * b_group_rows
-  void* out;              // row-major, pitch ldo elements
+  float* out;             // KGRP fp32 output, row-major pitch ldo (+ g * out_g)
   long long ldo;
-  long long out_g;        // KGRP: out + g * out_g
-  void* out2;             // TEPI_BIAS_GELU: h
-  const void* bias;       // + g * bias_g
+  long long out_g;
+  const bf16* bias;       // + g * bias_g
   long long bias_g;
-  const void* aux;        // TEPI_GELU_BWD: a (pitch ldo)
 };
 
 struct Tile {
-  int g, m0, n0, kb0, nkb;
+  int g, m_own, n0, kb0, nkb, row_end;
 };
 
 template <bool KGRP>
-__device__ __forceinline__ bool decode_tile(const TcParams& p, const int* s_off, int t, int n_tiles, Tile& tl) {
+__device__ __forceinline__ bool decode_tile(const TcParams& p, const int* s_off, const int* s_pair, int t,
+                                            int n_tiles, uint32_t rank, Tile& tl) {
   if (!KGRP) {
-    const int mt = t / n_tiles, nt = t - mt * n_tiles;
-    tl.m0 = mt * BM;
-    tl.n0 = nt * BN;
+    const int P = t / n_tiles, nt = t - P * n_tiles;
     int lo = 0, hi = p.G - 1;
     while (lo < hi) {
       int mid = (lo + hi + 1) >> 1;
-      if (s_off[mid] <= tl.m0) lo = mid; else hi = mid - 1;
+      if (s_pair[mid] <= P) lo = mid; else hi = mid - 1;
     }
     tl.g = lo;
+    tl.m_own = s_off[lo] + 256 * (P - s_pair[lo]) + 128 * (int)rank;
+    tl.row_end = min(s_off[lo + 1], p.rows_cap);
+    tl.n0 = nt * BN;
     tl.kb0 = 0;
     tl.nkb = (p.K + BK - 1) / BK;
   } else {
-    const int m_tiles = (p.M + BM - 1) / BM;
+    const int m_tiles = (p.M + 255) / 256;
     const int per_g = m_tiles * n_tiles;
     tl.g = t / per_g;
     const int r = t - tl.g * per_g;
     const int mt = r / n_tiles, nt = r - mt * n_tiles;
-    tl.m0 = mt * BM;
+    tl.m_own = mt * 256 + 128 * (int)rank;
+    tl.row_end = p.M;
     tl.n0 = nt * BN;
     tl.kb0 = s_off[tl.g] / BK;
     tl.nkb = (s_off[tl.g + 1] - s_off[tl.g]) / BK;
@@ -82,98 +109,117 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, const int* s_off,
 }
 
 template <int EPI, bool A_MN, bool B_MN, bool KGRP>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmO1, const __grid_constant__ CUtensorMap tmO2,
+                   const __grid_constant__ CUtensorMap tmX, TcParams p) {
+  using Cfg = EpiCfg<EPI>;
+  constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
-  // 1024-byte aligned ring (SWIZZLE_128B atoms)
   const uint32_t raw_u32 = tc::smem_u32(smem_raw);
-  uint8_t* smem = smem_raw + ((1024 - (raw_u32 & 1023)) & 1023);
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* smem = smem_raw + ((1024 - (raw_u32 & 1023)) & 1023);   // 1024-aligned (SWIZZLE_128B atoms)
+  uint8_t* staging = smem + STAGES * STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + Cfg::STAGING);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* aux_bar = tempty_bar + 2;                               // [EPI_WARPS][4] (GELU' operand loads)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(aux_bar + EPI_WARPS * 4);
   int* s_off = reinterpret_cast<int*>(s_tmem + 4);
+  int* s_pair = s_off + (MAX_G + 1);
 
+  const uint32_t rank = tc::cluster_rank();
+  const bool leader = rank == 0;
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
   for (int i = threadIdx.x; i <= p.G && i <= MAX_G; i += NUM_THREADS) s_off[i] = p.offsets[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int g = 0; g < p.G; ++g) {
+      s_pair[g] = acc;
+      acc += (s_off[g + 1] - s_off[g] + 255) / 256;
+    }
+    s_pair[p.G] = acc;
+  }
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
+    if (Cfg::NOUT >= 1) tc::tma_prefetch(&tmO1);
+    if (Cfg::NOUT >= 2) tc::tma_prefetch(&tmO2);
+    if (EPI == TEPI_GELU_BWD) tc::tma_prefetch(&tmX);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full_bar[s], 1);
       tc::mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&tfull_bar[a], 1);
-      tc::mbar_init(&tempty_bar[a], 4);
+      tc::mbar_init(&tempty_bar[a], 2 * EPI_WARPS);
     }
+    for (int i = 0; i < EPI_WARPS * 4; ++i) tc::mbar_init(&aux_bar[i], 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) {
-    tc::tmem_alloc(s_tmem, TMEM_COLS);
-    tc::tmem_relinquish();
+    tc::tmem_alloc_pair(s_tmem, TMEM_COLS);
+    tc::tmem_relinquish_pair();
   }
   tc::tc_fence_before();
   __syncthreads();
+  tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
 
   const int n_tiles = (p.N + BN - 1) / BN;
-  int total;
-  if (!KGRP) {
-    int R = s_off[p.G];
-    const int cap = p.m_tiles_cap * BM;
-    if (R > cap) R = cap;
-    total = (R / BM) * n_tiles;
-  } else {
-    total = p.G * ((p.M + BM - 1) / BM) * n_tiles;
-  }
+  const int total = KGRP ? p.G * ((p.M + 255) / 256) * n_tiles : s_pair[p.G] * n_tiles;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const uint32_t smem_base = tc::smem_u32(smem);
+      const uint32_t full_leader = tc::mapa(tc::smem_u32(full_bar), 0);
+      for (int t = cid; t < total; t += ncl) {
         Tile tl;
-        if (!decode_tile<KGRP>(p, s_off, t, n_tiles, tl)) continue;
+        if (!decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tl)) continue;
+        const int n_own = tl.n0 + BNH * (int)rank;
+        const int brow = KGRP ? 0 : tl.g * p.b_group_rows;
         for (int kb = 0; kb < tl.nkb; ++kb) {
           tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          tc::mbar_arrive_expect_tx(&full_bar[stage], STAGE_BYTES);
+          if (leader) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
+          const uint32_t bar = full_leader + stage * 8;
+          const uint32_t sa = smem_base + stage * STAGE_BYTES;
+          const uint32_t sb = sa + A_BYTES;
           const int k = (tl.kb0 + kb) * BK;
           if (!A_MN) {
-            tc::tma_load_2d(sa, &tmA, &full_bar[stage], k, tl.m0);
+            tc::tma_load_2d_pair(sa, &tmA, bar, k, tl.m_own);
           } else {
-#pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tc::tma_load_2d(sa + c * 8192, &tmA, &full_bar[stage], tl.m0 + c * 64, k);
+            tc::tma_load_2d_pair(sa, &tmA, bar, tl.m_own, k);
+            tc::tma_load_2d_pair(sa + 8192, &tmA, bar, tl.m_own + 64, k);
           }
-          const int brow = KGRP ? 0 : tl.g * p.b_group_rows;
           if (!B_MN) {
-            tc::tma_load_2d(sb, &tmB, &full_bar[stage], k, brow + tl.n0);
+            tc::tma_load_2d_pair(sb, &tmB, bar, k, brow + n_own);
           } else {
-#pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              tc::tma_load_2d(sb + c * 8192, &tmB, &full_bar[stage], tl.n0 + c * 64, brow + k);
+            tc::tma_load_2d_pair(sb, &tmB, bar, n_own, brow + k);
+            tc::tma_load_2d_pair(sb + 8192, &tmB, bar, n_own + 64, brow + k);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    // ------------------------------------------------------------ MMA issuer (pair leader)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_bf16(256, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       const uint32_t smem_base = tc::smem_u32(smem);
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = cid; t < total; t += ncl) {
         Tile tl;
-        if (!decode_tile<KGRP>(p, s_off, t, n_tiles, tl)) continue;
+        if (!decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tl)) continue;
         tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -185,64 +231,105 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // K-major SW128: +32 B per K=16 step, SBO = 1024 (8 rows x 128 B)
-            // MN-major SW128: +2048 B per K=16 step (16 rows x 128 B), LBO = 8 KB (64-wide MN chunk), SBO = 1024
+            // MN-major SW128: +2048 B per K=16 step, LBO = 8 KB (64-wide MN chunk), SBO = 1024
             const uint64_t ad = A_MN ? tc::smem_desc_sw128(sa + k * 2048, 8192, 1024)
                                      : tc::smem_desc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? tc::smem_desc_sw128(sb + k * 2048, 8192, 1024)
                                      : tc::smem_desc_sw128(sb + k * 32, 16, 1024);
-            tc::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            tc::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          tc::mma_commit(&empty_bar[stage]);           // frees the smem slot when these MMAs finish
+          tc::mma_commit_pair_mc(tc::smem_u32(&empty_bar[stage]), 0x3);   // frees the slot in both CTAs
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc::mma_commit(&tfull_bar[acc]);                // accumulator ready for the epilogue
+        tc::mma_commit_pair_mc(tc::smem_u32(&tfull_bar[acc]), 0x3);       // accumulators ready in both CTAs
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------------------ epilogue (warps 2..9)
+    const int ew = warp - 2;
     const int sub = warp & 3;                          // TMEM lane quarter this warp may access
+    const int half = ew >> 2;                          // column half: [half*128, half*128 + 128)
     const int row_in_tile = sub * 32 + lane;
+    const uint32_t stage_base = tc::smem_u32(staging) + ew * (Cfg::NBUF * Cfg::NOUT * CHUNK_BYTES);
+    const uint32_t swz = (uint32_t)((lane >> 1) & 3);  // SWIZZLE_64B: 16-byte chunk q -> q ^ ((row >> 1) & 3)
+    const uint32_t tempty_leader = tc::mapa(tc::smem_u32(tempty_bar), 0);
+    const uint32_t auxb = tc::smem_u32(aux_bar + ew * 4);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    uint32_t seq = 0;                                   // chunk sequence number (4 per tile)
+
+    // GELU' operand: TMA-load a[rows, 32 cols] two chunks ahead into the staging buffers
+    auto aux_issue = [&](uint32_t s) {
+      const int t = cid + (int)(s >> 2) * ncl;
+      if (t >= total) return;
+      Tile tn;
+      decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tn);
+      const int col = tn.n0 + half * 128 + (int)(s & 3) * 32;
+      const uint32_t b = s % Cfg::NBUF;
+      tc::mbar_arrive_expect_tx_u32(auxb + b * 8, CHUNK_BYTES);
+      tc::tma_load_2d_u32(stage_base + b * CHUNK_BYTES, &tmX, auxb + b * 8, col, tn.m_own + sub * 32);
+    };
+    if (EPI == TEPI_GELU_BWD && lane == 0) {
+      aux_issue(0);
+      aux_issue(1);
+    }
+
+    for (int t = cid; t < total; t += ncl) {
       Tile tl;
-      const bool nonempty = decode_tile<KGRP>(p, s_off, t, n_tiles, tl);
-      const long long row = (long long)tl.m0 + row_in_tile;
-      const bool row_ok = KGRP ? (row < p.M) : true;
-      if (!nonempty) {
-        // KGRP only: empty expert -> zero gradient tile
-        if (row_ok) {
-          float* o = reinterpret_cast<float*>(p.out) + (long long)tl.g * p.out_g + row * p.ldo;
-          for (int c = 0; c < BN; c += 4)
+      const bool nonempty = decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tl);
+      const long long row = (long long)tl.m_own + row_in_tile;
+      if (KGRP && !nonempty) {
+        // empty expert -> zero gradient tile
+        if (row < p.M) {
+          float* o = p.out + (long long)tl.g * p.out_g + row * p.ldo;
+          for (int c = half * 128; c < half * 128 + 128; c += 4)
             if (tl.n0 + c < p.N) *reinterpret_cast<float4*>(o + tl.n0 + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         continue;
       }
+      const bool warp_rows_ok = tl.m_own + sub * 32 < tl.row_end;   // warp-uniform for ROWS tiles
       tc::mbar_wait(&tfull_bar[acc], acc_phase);
       tc::tc_fence_after();
-      const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16);
+      const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16) + half * 128;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int cc = 0; cc < 4; ++cc, ++seq) {
+        const int n = tl.n0 + half * 128 + cc * 32;
         uint32_t r[32];
-        tc::tmem_ld32(t_row + c, r);
+        tc::tmem_ld32(t_row + cc * 32, r);
         tc::tmem_ld_wait();
-        const int n = tl.n0 + c;
-        if (n >= p.N || !row_ok) continue;
         if (EPI == TEPI_F32) {
-          float* o = reinterpret_cast<float*>(p.out) + (long long)tl.g * p.out_g + row * p.ldo + n;
+          if (row < p.M && n < p.N) {
+            float* o = p.out + (long long)tl.g * p.out_g + row * p.ldo + n;
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                            __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                              __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          }
+          continue;
+        }
+        const bool store = warp_rows_ok && n < p.N;
+        const uint32_t buf = stage_base + (seq % Cfg::NBUF) * (Cfg::NOUT * CHUNK_BYTES);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        if (EPI == TEPI_GELU_BWD) {
+          tc::mbar_wait_u32(auxb + (seq % Cfg::NBUF) * 8, (seq / Cfg::NBUF) & 1);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float a[8];
+            unpack16(tc::ld_shared_v4(buf + lane * 64 + ((q ^ swz) << 4)), a, bf16());
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[q * 8 + j] *= gelu_prime_fast(a[j]);
+          }
         } else {
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          bf16* o = reinterpret_cast<bf16*>(p.out) + row * p.ldo + n;
-          if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) {
-            const bf16* bp = reinterpret_cast<const bf16*>(p.bias) + (long long)tl.g * p.bias_g + n;
+          if (seq >= 2) {                                 // the group that last used this buffer must be read
+            if (lane == 0) tc::bulk_wait_read<1>();
+            __syncwarp();
+          }
+          if ((EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) && n < p.N) {
+            const bf16* bp = p.bias + (long long)tl.g * p.bias_g + n;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float b[8];
@@ -251,48 +338,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 8; ++j) v[q * 8 + j] += b[j];
             }
           }
-          if (EPI == TEPI_BIAS_GELU) {
-            bf16* o2 = reinterpret_cast<bf16*>(p.out2) + row * p.ldo + n;
+        }
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              st_v4(o + q * 8, pack16(v + q * 8, bf16()));
-              float hq[8];
+        for (int q = 0; q < 4; ++q)
+          tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(v + q * 8, bf16()));
+        if (EPI == TEPI_BIAS_GELU) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) hq[j] = gelu_f(v[q * 8 + j]);
-              st_v4(o2 + q * 8, pack16(hq, bf16()));
-            }
-          } else if (EPI == TEPI_GELU_BWD) {
-            const bf16* ap = reinterpret_cast<const bf16*>(p.aux) + row * p.ldo + n;
-            uint4 araw[4];
+          for (int q = 0; q < 4; ++q) {
+            float hq[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) araw[q] = ld_v4(ap + q * 8);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float a[8];
-              unpack16(araw[q], a, bf16());
-#pragma unroll
-              for (int j = 0; j < 8; ++j) v[q * 8 + j] *= gelu_prime_f(a[j]);
-              st_v4(o + q * 8, pack16(v + q * 8, bf16()));
-            }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) st_v4(o + q * 8, pack16(v + q * 8, bf16()));
+            for (int j = 0; j < 8; ++j) hq[j] = gelu_fast(v[q * 8 + j]);
+            tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), pack16(hq, bf16()));
           }
         }
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          if (store) {
+            const int row0 = tl.m_own + sub * 32;
+            tc::tma_store_2d(&tmO1, buf, n, row0);
+            if (Cfg::NOUT == 2) tc::tma_store_2d(&tmO2, buf + CHUNK_BYTES, n, row0);
+          }
+          tc::bulk_commit();                              // one (possibly empty) group per chunk
+          if (EPI == TEPI_GELU_BWD) {
+            tc::bulk_wait_read<2>();                      // buffer (seq+2)%4 was last stored at seq-2
+            aux_issue(seq + 2);
+          }
+        }
+        __syncwarp();
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) tc::mbar_arrive_cluster(tempty_leader + acc * 8);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (Cfg::NOUT > 0 && lane == 0) tc::bulk_wait<0>();
   }
   tc::tc_fence_before();
   __syncthreads();
+  tc::cluster_sync();
   if (warp == 1) {
     __syncwarp();
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem_base, TMEM_COLS);
+    tc::tmem_dealloc_pair(tmem_base, TMEM_COLS);
   }
 }
 
@@ -314,34 +403,40 @@ EncodeTiledFn encode_fn() {
 }
 
 // 2D bf16 tensor map over a row-major [rows, cols] matrix with row pitch `pitch` elements;
-// box = {box_cols (inner), box_rows}, 128-byte swizzle (box_cols * 2 must be 128).
+// box = {box_cols (inner), box_rows}; swizzle 128B for MMA operands (box_cols * 2 == 128),
+// 64B for the 32x32 epilogue store boxes (box_cols * 2 == 64).
 bool make_map(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long pitch, int box_cols,
-              int box_rows) {
+              int box_rows, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn f = encode_fn();
-  if (!f) return false;
+  if (!f || !ptr) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)pitch * 2};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+bool make_store_map(CUtensorMap* m, const void* ptr, long long rows, long long cols) {
+  return make_map(m, ptr, rows, cols, cols, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+}
 
 template <int EPI, bool A_MN, bool B_MN, bool KGRP>
-cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int tiles_upper, int sms,
-                      cudaStream_t s) {
+cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o1, const CUtensorMap& o2,
+                      const CUtensorMap& x, const TcParams& p, long long tiles_upper, int sms, cudaStream_t s) {
   auto k = tc_gemm_kernel<EPI, A_MN, B_MN, KGRP>;
+  constexpr int smem = EpiCfg<EPI>::SMEM;
+  static_assert(smem <= SMEM_LIMIT, "shared memory budget");
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  int grid = tiles_upper < sms ? tiles_upper : sms;
-  if (grid <= 0) return cudaSuccess;
-  k<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(a, b, p), count_launch();
+  long long pairs = tiles_upper < sms / 2 ? tiles_upper : sms / 2;
+  if (pairs <= 0) return cudaSuccess;
+  k<<<(unsigned)(2 * pairs), NUM_THREADS, smem, s>>>(a, b, o1, o2, x, p), count_launch();
   return cudaGetLastError();
 }
 
@@ -349,73 +444,84 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const TcParams
 
 bool tc_available() { return encode_fn() != nullptr; }
 
+// Upper bound on ROWS pair-tiles: every expert may add one half-used pair.
+static long long rows_pairs_upper(int64_t R_cap, int El) { return R_cap / 256 + El; }
+
 // ---------------------------------------------------------------- step 5 / B5 on tensor cores
 cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
                           const void* W1, const void* b1, const void* W2, const void* b2, void* a, void* h,
                           void* e_out, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local;
   if (R_cap == 0) return cudaSuccess;
-  CUtensorMap mA, mB;
+  CUtensorMap mA, mB, mO1, mO2;
   TcParams p{};
-  p.kgrp = 0; p.G = El; p.offsets = offsets; p.m_tiles_cap = (int)(R_cap / BM);
+  p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
   // GEMM1: a = x_perm W1^T + b1, h = GELU(a)      A [R, d] K-major, B = W1 [El*f, d] K-major
-  if (!make_map(&mA, x_perm, R_cap, d, d, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, BN))
+  if (!make_map(&mA, x_perm, R_cap, d, d, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, BNH) ||
+      !make_store_map(&mO1, a, R_cap, f) || !make_store_map(&mO2, h, R_cap, f))
     return cudaErrorInvalidValue;
   p.N = f; p.K = d; p.b_group_rows = f;
-  p.out = a; p.out2 = h; p.ldo = f; p.bias = b1; p.bias_g = f;
-  cudaError_t e = launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, p, p.m_tiles_cap * ((f + BN - 1) / BN),
-                                                                  c->sm_count, s);
+  p.bias = reinterpret_cast<const bf16*>(b1); p.bias_g = f;
+  const long long up = rows_pairs_upper(R_cap, El);
+  cudaError_t e = launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p,
+                                                                  up * ((f + BN - 1) / BN), c->sm_count, s);
   if (e != cudaSuccess) return e;
   // GEMM2: e_out = h W2^T + b2                     A [R, f] K-major, B = W2 [El*d, f] K-major
-  if (!make_map(&mA, h, R_cap, f, f, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, BN))
+  if (!make_map(&mA, h, R_cap, f, f, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, BNH) ||
+      !make_store_map(&mO1, e_out, R_cap, d))
     return cudaErrorInvalidValue;
   p.N = d; p.K = f; p.b_group_rows = d;
-  p.out = e_out; p.out2 = nullptr; p.ldo = d; p.bias = b2; p.bias_g = d;
-  return launch_tc<TEPI_BIAS, false, false, false>(mA, mB, p, p.m_tiles_cap * ((d + BN - 1) / BN), c->sm_count, s);
+  p.bias = reinterpret_cast<const bf16*>(b2); p.bias_g = d;
+  return launch_tc<TEPI_BIAS, false, false, false>(mA, mB, mO1, mO1, mO1, p, up * ((d + BN - 1) / BN),
+                                                   c->sm_count, s);
 }
 
 cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* a,
                               const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
                               const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local;
-  CUtensorMap mA, mB;
+  CUtensorMap mA, mB, mO, mX;
   cudaError_t e;
   if (R_cap == 0) {   // no rows at all: every expert gradient is zero
     if ((e = cudaMemsetAsync(dW1, 0, sizeof(float) * El * f * d, s)) != cudaSuccess) return e;
     return cudaMemsetAsync(dW2, 0, sizeof(float) * El * d * f, s);
   }
+  const long long up = rows_pairs_upper(R_cap, El);
   {
     TcParams p{};
-    p.kgrp = 0; p.G = El; p.offsets = offsets; p.m_tiles_cap = (int)(R_cap / BM);
+    p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
     // dgrad2: da = (d_eout W2_e) (.) GELU'(a)   A = d_eout [R, d] K-major; B(k=d, n=f) = W2 [El*d, f] MN-major
-    if (!make_map(&mA, d_eout, R_cap, d, d, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, 64))
+    if (!make_map(&mA, d_eout, R_cap, d, d, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, 64) ||
+        !make_store_map(&mO, da, R_cap, f) || !make_store_map(&mX, a, R_cap, f))
       return cudaErrorInvalidValue;
     p.N = f; p.K = d; p.b_group_rows = d;
-    p.out = da; p.ldo = f; p.aux = a;
-    e = launch_tc<TEPI_GELU_BWD, false, true, false>(mA, mB, p, p.m_tiles_cap * ((f + BN - 1) / BN), c->sm_count, s);
+    e = launch_tc<TEPI_GELU_BWD, false, true, false>(mA, mB, mO, mO, mX, p, up * ((f + BN - 1) / BN),
+                                                     c->sm_count, s);
     if (e != cudaSuccess) return e;
     // dgrad1: dx_perm = da W1_e                 A = da [R, f] K-major; B(k=f, n=d) = W1 [El*f, d] MN-major
-    if (!make_map(&mA, da, R_cap, f, f, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, 64))
+    if (!make_map(&mA, da, R_cap, f, f, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, 64) ||
+        !make_store_map(&mO, dx_perm, R_cap, d))
       return cudaErrorInvalidValue;
     p.N = d; p.K = f; p.b_group_rows = f;
-    p.out = dx_perm; p.ldo = d; p.aux = nullptr;
-    e = launch_tc<TEPI_STORE, false, true, false>(mA, mB, p, p.m_tiles_cap * ((d + BN - 1) / BN), c->sm_count, s);
+    e = launch_tc<TEPI_STORE, false, true, false>(mA, mB, mO, mO, mO, p, up * ((d + BN - 1) / BN), c->sm_count, s);
     if (e != cudaSuccess) return e;
   }
   // wgrad2: dW2_e [d, f] = d_eout_e^T h_e       A(m=d, k=row) = d_eout MN-major; B(k=row, n=f) = h MN-major
-  const long long rows = R_cap;
   TcParams q{};
-  q.kgrp = 1; q.G = El; q.offsets = offsets;
-  if (!make_map(&mA, d_eout, rows, d, d, 64, 64) || !make_map(&mB, h, rows, f, f, 64, 64))
+  q.G = El; q.offsets = offsets; q.rows_cap = (int)R_cap;
+  if (!make_map(&mA, d_eout, R_cap, d, d, 64, 64) || !make_map(&mB, h, R_cap, f, f, 64, 64))
     return cudaErrorInvalidValue;
   q.M = d; q.N = f; q.out = dW2; q.ldo = f; q.out_g = (long long)d * f;
-  e = launch_tc<TEPI_F32, true, true, true>(mA, mB, q, El * ((d + BM - 1) / BM) * ((f + BN - 1) / BN), c->sm_count, s);
+  e = launch_tc<TEPI_F32, true, true, true>(mA, mB, mA, mA, mA, q,
+                                            (long long)El * ((d + 255) / 256) * ((f + BN - 1) / BN), c->sm_count, s);
   if (e != cudaSuccess) return e;
   // wgrad1: dW1_e [f, d] = da_e^T x_perm_e      A(m=f, k=row) = da MN-major; B(k=row, n=d) = x_perm MN-major
-  if (!make_map(&mA, da, rows, f, f, 64, 64) || !make_map(&mB, x_perm, rows, d, d, 64, 64))
+  if (!make_map(&mA, da, R_cap, f, f, 64, 64) || !make_map(&mB, x_perm, R_cap, d, d, 64, 64))
     return cudaErrorInvalidValue;
   q.M = f; q.N = d; q.out = dW1; q.ldo = d; q.out_g = (long long)f * d;
-  return launch_tc<TEPI_F32, true, true, true>(mA, mB, q, El * ((f + BM - 1) / BM) * ((d + BN - 1) / BN), c->sm_count, s);
+  return launch_tc<TEPI_F32, true, true, true>(mA, mB, mA, mA, mA, q,
+                                               (long long)El * ((f + 255) / 256) * ((d + BN - 1) / BN), c->sm_count,
+                                               s);
 }
 
 }  // namespace moe

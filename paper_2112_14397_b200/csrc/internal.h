@@ -24,6 +24,7 @@ struct moe_ctx {
   float* dxg;          // [T, d] fp32  dlogits W_g^T  (v1 path)
   float* colsum;       // [E] balance-loss column sums
   int* tot;            // [E] per-expert totals written by the dispatch scan
+  float* colpart;      // [E_local, kColsumSplits, max(d, f)] bias-gradient partials
 };
 
 namespace moe {
@@ -107,9 +108,11 @@ struct SimtGemm {
 // Mixed-type combinations always use the fp32-output epilogue.
 cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int epi, cudaStream_t s);
 
-// out[g][n] = sum over rows of group g of X[r][n]  (fp32 out, deterministic)
+// out[g][n] = sum over rows of group g of X[r][n]  (fp32 out, deterministic two-phase;
+// `part` = workspace [G, kColsumSplits, N] fp32)
+constexpr int kColsumSplits = 8;
 cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_off, int G, float* out,
-                                  cudaStream_t s);
+                                  float* part, cudaStream_t s);
 
 }  // namespace moe
 

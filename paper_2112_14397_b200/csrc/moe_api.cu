@@ -63,7 +63,7 @@ namespace moe {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carve {
-  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, total;
+  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, total;
 };
 
 static Carve carve(const moe_ctx* c) {
@@ -82,6 +82,7 @@ static Carve carve(const moe_ctx* c) {
   k.dxg = take(sizeof(float) * (size_t)c->T * c->d);
   k.colsum = take(sizeof(float) * (size_t)c->E);
   k.tot = take(sizeof(int) * (size_t)c->E);
+  k.colpart = take(sizeof(float) * (size_t)c->E_local * kColsumSplits * (size_t)(c->d > c->f ? c->d : c->f));
   k.total = o;
   return k;
 }
@@ -98,6 +99,7 @@ void carve_workspace(moe_ctx* c) {
   c->dxg = reinterpret_cast<float*>(c->ws + k.dxg);
   c->colsum = reinterpret_cast<float*>(c->ws + k.colsum);
   c->tot = reinterpret_cast<int*>(c->ws + k.tot);
+  c->colpart = reinterpret_cast<float*>(c->ws + k.colpart);
 }
 
 }  // namespace moe
