@@ -290,6 +290,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         continue;
       }
       const bool warp_rows_ok = tl.m_own + sub * 32 < tl.row_end;   // warp-uniform for ROWS tiles
+      uint4 bq[4];                                                   // bias of the current chunk
+      const bf16* bias_t = nullptr;
+      if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) {
+        bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0 + half * 128;
+        if (tl.n0 + half * 128 < p.N) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + q * 8);
+        }
+      }
       tc::mbar_wait(&tfull_bar[acc], acc_phase);
       tc::tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16) + half * 128;
@@ -328,14 +337,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) tc::bulk_wait_read<1>();
             __syncwarp();
           }
-          if ((EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) && n < p.N) {
-            const bf16* bp = p.bias + (long long)tl.g * p.bias_g + n;
+          if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float b[8];
-              unpack16(ld_v4(bp + q * 8), b, bf16());
+              unpack16(bq[q], b, bf16());
 #pragma unroll
               for (int j = 0; j < 8; ++j) v[q * 8 + j] += b[j];
+            }
+            if (cc < 3 && n + 32 < p.N) {                 // prefetch the next chunk's bias
+#pragma unroll
+              for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + (cc + 1) * 32 + q * 8);
             }
           }
         }
