@@ -58,147 +58,264 @@ __device__ __forceinline__ float warp_second(const float* p, int E, int lane, in
   return warp_max(s);
 }
 
-// One warp per token.  Block = 8 warps handles kGateBT tokens (16 per warp).
+// Steps 2-3 for one token, executed by one warp.  L points at the token's E fp32 logits.
 template <typename T>
-__global__ void __launch_bounds__(1024) gate_softmax_kernel(
-    const float* __restrict__ logits, const T* __restrict__ x, const T* __restrict__ Wg,
-    const float* __restrict__ u, int T_, int d, int E, float tau, float thr, int top1,
-    float* __restrict__ probs, int* __restrict__ slot, int* __restrict__ counts,
+__device__ __forceinline__ void gate_token(const float* L, int t, const T* __restrict__ x, const T* __restrict__ Wg,
+                                           const float* __restrict__ u, int d, int E, float tau, float thr, int top1,
+                                           float* __restrict__ probs, int* __restrict__ slot, int* s_cnt, int* s_band,
+                                           int* __restrict__ flags, int lane) {
+  float z[kMaxEPL], p[kMaxEPL];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    z[i] = -INFINITY;
+    if (e < E) {
+      float Lv = L[e];
+      if (!isfinite(Lv)) bad = true;
+      float zeta = u ? -logf(-logf(u[(long long)t * E + e])) : 0.f;
+      z[i] = (Lv + zeta) / tau;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0 && atomicOr(&flags[0], kFlagNonFinite) == 0) flags[1] = t;
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) mx = fmaxf(mx, z[i]);
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    p[i] = (lane + 32 * i < E) ? expf(z[i] - mx) : 0.f;
+    sum += p[i];
+  }
+  sum = warp_sum(sum);
+  const float inv = 1.0f / sum;
+  bool any_pass = false, near = false;
+  float pmax = -1.f;
+  int am = 0x7fffffff;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    if (e < E) {
+      p[i] = p[i] * inv;
+      if (p[i] > thr) any_pass = true;
+      if (fabsf(p[i] - thr) < kRefine) near = true;
+      if (p[i] > pmax) { pmax = p[i]; am = e; }
+    }
+  }
+  warp_argmax(pmax, am);
+  any_pass = __any_sync(0xffffffffu, any_pass);
+  bool argmax_decided = top1 || !any_pass;
+  near = __any_sync(0xffffffffu, near) && !top1;
+  if (argmax_decided) {
+    float second = warp_second(p, E, lane, am);
+    if (pmax - second < kRefine) near = true;
+  }
+  if (near) {
+    // ---- fp64 refinement: recompute logits, noise and softmax exactly from the inputs
+    double z64[kMaxEPL];
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      int e = lane + 32 * i;
+      z64[i] = -INFINITY;
+      if (e < E) {
+        double acc = 0.0;
+        const T* xr = x + (long long)t * d;
+        for (int k = 0; k < d; ++k) acc = fma((double)to_f32(xr[k]), (double)to_f32(Wg[(long long)k * E + e]), acc);
+        double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
+        z64[i] = (acc + zeta) / (double)tau;
+      }
+    }
+    double mx64 = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) mx64 = fmax(mx64, z64[i]);
+    mx64 = warp_maxd(mx64);
+    double s64 = 0.0, p64[kMaxEPL];
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      p64[i] = (lane + 32 * i < E) ? exp(z64[i] - mx64) : 0.0;
+      s64 += p64[i];
+    }
+    s64 = warp_sum(s64);
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    any_pass = false;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      int e = lane + 32 * i;
+      if (e < E) {
+        p64[i] /= s64;
+        p[i] = (float)p64[i];
+        if (p[i] > thr) any_pass = true;
+        if (p64[i] > best) { best = p64[i]; bi = e; }
+      }
+    }
+    warp_argmax(best, bi);
+    am = bi;
+    pmax = (float)best;
+    any_pass = __any_sync(0xffffffffu, any_pass);
+    argmax_decided = top1 || !any_pass;
+  }
+  // ---- decision + band
+  bool in_band = false;
+  if (!argmax_decided) {
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i)
+      if (lane + 32 * i < E && fabsf(p[i] - thr) < kBand) in_band = true;
+    in_band = __any_sync(0xffffffffu, in_band);
+  } else {
+    float second = warp_second(p, E, lane, am);
+    in_band = (pmax - second) < kBand;
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    if (e < E) {
+      bool sel = argmax_decided ? (e == am) : (p[i] > thr);
+      probs[(long long)t * E + e] = p[i];
+      slot[(long long)t * E + e] = sel ? 0 : -1;
+      if (sel) atomicAdd(&s_cnt[e], 1);
+    }
+  }
+  if (lane == 0 && in_band) atomicAdd(s_band, 1);
+}
+
+// Fused gate: one CTA per kGateBT (128) tokens, 256 threads.
+//   Step 1 on CUDA cores: thread = TPT tokens x 4 experts; K in chunks of KC = 32 staged in
+//   smem as fp32; chunk partial sums are added with TwoSum (error-free transformation), so
+//   the fp32 logits carry ~1 ulp of error instead of the ~sqrt(d) ulp of a plain running
+//   sum (the 1e-5 probs tolerance at tau = 0.05..0.1 needs it).
+//   Steps 2-3: warp per token on the smem logits (gate_token).
+constexpr int kKC = 32;
+template <typename T, int TPT>
+__global__ void __launch_bounds__(256) gate_fused_kernel(
+    const T* __restrict__ x, const T* __restrict__ Wg, const float* __restrict__ u, int T_, int d, int E, float tau,
+    float thr, int top1, float* __restrict__ probs, int* __restrict__ slot, int* __restrict__ counts,
     int* __restrict__ blk_cnt, int* __restrict__ near_band, int* __restrict__ flags) {
+  extern __shared__ float sm[];
   __shared__ int s_cnt[128];
   __shared__ int s_band;
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < E; i += blockDim.x) s_cnt[i] = 0;
-  if (threadIdx.x == 0) s_band = 0;
-  __syncthreads();
-  const int tpw = kGateBT / 32;
-  for (int j = 0; j < tpw; ++j) {
-    const int t = blockIdx.x * kGateBT + warp * tpw + j;
-    if (t >= T_) break;
-    float z[kMaxEPL], p[kMaxEPL];
-    bool bad = false;
+  const int EG = (E + 3) / 4;
+  const int Ep = EG * 4;
+  float* xs = sm;                          // [kKC][kGateBT + 4]
+  float* ws = xs + kKC * (kGateBT + 4);    // [kKC][Ep]
+  float* ls = ws + kKC * Ep;               // [kGateBT][E + 1]
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int t0 = blockIdx.x * kGateBT;
+  for (int i = tid; i < E; i += 256) s_cnt[i] = 0;
+  if (tid == 0) s_band = 0;
+  const int eg = tid % EG, tg = tid / EG;
+  const bool active = tg * TPT < kGateBT;
+  float sum[TPT][4], comp[TPT][4];
 #pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      int e = lane + 32 * i;
-      z[i] = -INFINITY;
-      if (e < E) {
-        float L = logits[(long long)t * E + e];
-        if (!isfinite(L)) bad = true;
-        float zeta = u ? -logf(-logf(u[(long long)t * E + e])) : 0.f;
-        z[i] = (L + zeta) / tau;
+  for (int i = 0; i < TPT; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sum[i][j] = comp[i][j] = 0.f;
+  constexpr int V = Vec16<T>::N;
+  for (int k0 = 0; k0 < d; k0 += kKC) {
+    // x chunk: kGateBT tokens x kKC, 16-byte vectors
+    for (int v = tid; v < kGateBT * (kKC / V); v += 256) {
+      const int tok = v / (kKC / V), part = v % (kKC / V);
+      const int kk = part * V;
+      float f[V];
+      if (t0 + tok < T_ && k0 + kk < d) {
+        unpack16(ld_nc_v4(x + (long long)(t0 + tok) * d + k0 + kk), f, T());
+      } else {
+#pragma unroll
+        for (int q = 0; q < V; ++q) f[q] = 0.f;
       }
-    }
-    if (__any_sync(0xffffffffu, bad)) {
-      if (lane == 0 && atomicOr(&flags[0], kFlagNonFinite) == 0) flags[1] = t;
-    }
-    float mx = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) mx = fmaxf(mx, z[i]);
-    mx = warp_max(mx);
-    float sum = 0.f;
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      p[i] = (lane + 32 * i < E) ? expf(z[i] - mx) : 0.f;
-      sum += p[i];
+      for (int q = 0; q < V; ++q) xs[(kk + q) * (kGateBT + 4) + tok] = f[q];
     }
-    sum = warp_sum(sum);
-    const float inv = 1.0f / sum;
-    bool any_pass = false, near = false;
-    float pmax = -1.f;
-    int am = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      int e = lane + 32 * i;
-      if (e < E) {
-        p[i] = p[i] * inv;
-        if (p[i] > thr) any_pass = true;
-        if (fabsf(p[i] - thr) < kRefine) near = true;
-        if (p[i] > pmax) { pmax = p[i]; am = e; }
-      }
+    for (int i = tid; i < kKC * Ep; i += 256) {
+      const int kk = i / Ep, e = i % Ep;
+      ws[i] = (k0 + kk < d && e < E) ? to_f32(Wg[(long long)(k0 + kk) * E + e]) : 0.f;
     }
-    warp_argmax(pmax, am);
-    any_pass = __any_sync(0xffffffffu, any_pass);
-    bool argmax_decided = top1 || !any_pass;
-    near = __any_sync(0xffffffffu, near) && !top1;
-    if (argmax_decided) {
-      float second = warp_second(p, E, lane, am);
-      if (pmax - second < kRefine) near = true;
-    }
-    if (near) {
-      // ---- fp64 refinement: recompute logits, noise and softmax exactly from the inputs
-      double z64[kMaxEPL];
+    __syncthreads();
+    if (active) {
+      float c[TPT][4];
 #pragma unroll
-      for (int i = 0; i < kMaxEPL; ++i) {
-        int e = lane + 32 * i;
-        z64[i] = -INFINITY;
-        if (e < E) {
-          double acc = 0.0;
-          const T* xr = x + (long long)t * d;
-          for (int k = 0; k < d; ++k) acc = fma((double)to_f32(xr[k]), (double)to_f32(Wg[(long long)k * E + e]), acc);
-          double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
-          z64[i] = (acc + zeta) / (double)tau;
+      for (int i = 0; i < TPT; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[i][j] = 0.f;
+#pragma unroll 8
+      for (int kk = 0; kk < kKC; ++kk) {
+        const float4 b = *reinterpret_cast<const float4*>(&ws[kk * Ep + eg * 4]);
+        float a[TPT];
+#pragma unroll
+        for (int i = 0; i < TPT; ++i) a[i] = xs[kk * (kGateBT + 4) + tg * TPT + i];
+#pragma unroll
+        for (int i = 0; i < TPT; ++i) {
+          c[i][0] = fmaf(a[i], b.x, c[i][0]);
+          c[i][1] = fmaf(a[i], b.y, c[i][1]);
+          c[i][2] = fmaf(a[i], b.z, c[i][2]);
+          c[i][3] = fmaf(a[i], b.w, c[i][3]);
         }
       }
-      double mx64 = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < kMaxEPL; ++i) mx64 = fmax(mx64, z64[i]);
-      mx64 = warp_maxd(mx64);
-      double s64 = 0.0, p64[kMaxEPL];
+      for (int i = 0; i < TPT; ++i)
 #pragma unroll
-      for (int i = 0; i < kMaxEPL; ++i) {
-        p64[i] = (lane + 32 * i < E) ? exp(z64[i] - mx64) : 0.0;
-        s64 += p64[i];
-      }
-      s64 = warp_sum(s64);
-      double best = -1.0;
-      int bi = 0x7fffffff;
-      any_pass = false;
-#pragma unroll
-      for (int i = 0; i < kMaxEPL; ++i) {
-        int e = lane + 32 * i;
-        if (e < E) {
-          p64[i] /= s64;
-          p[i] = (float)p64[i];
-          if (p[i] > thr) any_pass = true;
-          if (p64[i] > best) { best = p64[i]; bi = e; }
+        for (int j = 0; j < 4; ++j) {   // TwoSum(sum, c) -> (sum, err)
+          const float s1 = sum[i][j] + c[i][j];
+          const float bp = s1 - sum[i][j];
+          const float err = (sum[i][j] - (s1 - bp)) + (c[i][j] - bp);
+          sum[i][j] = s1;
+          comp[i][j] += err;
         }
-      }
-      warp_argmax(best, bi);
-      am = bi;
-      pmax = (float)best;
-      any_pass = __any_sync(0xffffffffu, any_pass);
-      argmax_decided = top1 || !any_pass;
     }
-    // ---- decision + band
-    bool in_band = false;
-    if (!argmax_decided) {
+    __syncthreads();
+  }
+  if (active) {
 #pragma unroll
-      for (int i = 0; i < kMaxEPL; ++i)
-        if (lane + 32 * i < E && fabsf(p[i] - thr) < kBand) in_band = true;
-      in_band = __any_sync(0xffffffffu, in_band);
-    } else {
-      float second = warp_second(p, E, lane, am);
-      in_band = (pmax - second) < kBand;
-    }
+    for (int i = 0; i < TPT; ++i)
 #pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      int e = lane + 32 * i;
-      if (e < E) {
-        bool sel = argmax_decided ? (e == am) : (p[i] > thr);
-        probs[(long long)t * E + e] = p[i];
-        slot[(long long)t * E + e] = sel ? 0 : -1;
-        if (sel) atomicAdd(&s_cnt[e], 1);
+      for (int j = 0; j < 4; ++j) {
+        const int e = eg * 4 + j;
+        if (e < E) ls[(tg * TPT + i) * (E + 1) + e] = sum[i][j] + comp[i][j];
       }
-    }
-    if (lane == 0 && in_band) atomicAdd(&s_band, 1);
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+  for (int i = warp; i < kGateBT; i += 8) {
+    const int t = t0 + i;
+    if (t >= T_) break;
+    gate_token<T>(&ls[i * (E + 1)], t, x, Wg, u, d, E, tau, thr, top1, probs, slot, s_cnt, &s_band, flags, lane);
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += 256) {
     int c = s_cnt[e];
     blk_cnt[(long long)blockIdx.x * E + e] = c;
     if (c) atomicAdd(&counts[e], c);
   }
-  if (threadIdx.x == 0 && s_band) atomicAdd(near_band, s_band);
+  if (tid == 0 && s_band) atomicAdd(near_band, s_band);
+}
+
+template <typename T, int TPT>
+cudaError_t launch_gate_fused(const moe_ctx* c, const void* x, const void* Wg, const float* u, float tau, float thr,
+                              int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
+                              cudaStream_t s) {
+  const int Ep = (c->E + 3) / 4 * 4;
+  const size_t smem = sizeof(float) * (kKC * (kGateBT + 4) + kKC * Ep + kGateBT * (c->E + 1));
+  cudaError_t e = cudaFuncSetAttribute(gate_fused_kernel<T, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  gate_fused_kernel<T, TPT><<<c->nblk, 256, smem, s>>>((const T*)x, (const T*)Wg, u, c->T, c->d, c->E, tau, thr,
+                                                       top1, probs, slot, counts, c->blk_cnt, near_band, c->flags),
+      count_launch();
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_gate_typed(const moe_ctx* c, const void* x, const void* Wg, const float* u, float tau, float thr,
+                              int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
+                              cudaStream_t s) {
+  const int EG = (c->E + 3) / 4;   // TPT >= EG / 2 so that EG * (128 / TPT) <= 256 threads
+  if (EG <= 2) return launch_gate_fused<T, 1>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
+  if (EG <= 4) return launch_gate_fused<T, 2>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
+  if (EG <= 8) return launch_gate_fused<T, 4>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
+  if (EG <= 16) return launch_gate_fused<T, 8>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
+  return launch_gate_fused<T, 16>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
 }
 
 // ------------------------------------------------------------------ gate backward
@@ -275,23 +392,8 @@ cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const f
   if ((e = cudaMemsetAsync(counts, 0, sizeof(int) * c->E, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(near_band, 0, sizeof(int), s)) != cudaSuccess) return e;
   if (c->T == 0) return cudaSuccess;
-  // Step 1: logits [T, E] fp32 = x [T, d] . Wg [d, E]
-  SimtGemm g{};
-  g.A = x; g.sAm = c->d; g.sAk = 1;
-  g.B = Wg; g.sBk = c->E; g.sBn = 1;
-  g.C = c->logits; g.sCm = c->E;
-  g.M = c->T; g.N = c->E; g.K = c->d; g.G = 1; g.k_split = 1;
-  if ((e = launch_simt_gemm(g, c->dtype, c->dtype, 0, EPI_F32, s)) != cudaSuccess) return e;
-  // Steps 2-3
-  if (c->dtype == 1)
-    gate_softmax_kernel<bf16><<<c->nblk, 1024, 0, s>>>(c->logits, (const bf16*)x, (const bf16*)Wg, u, c->T, c->d,
-                                                      c->E, tau, thr, top1, probs, slot, counts, c->blk_cnt,
-                                                      near_band, c->flags), count_launch();
-  else
-    gate_softmax_kernel<float><<<c->nblk, 1024, 0, s>>>(c->logits, (const float*)x, (const float*)Wg, u, c->T,
-                                                       c->d, c->E, tau, thr, top1, probs, slot, counts,
-                                                       c->blk_cnt, near_band, c->flags), count_launch();
-  return cudaGetLastError();
+  if (c->dtype == 1) return launch_gate_typed<bf16>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
+  return launch_gate_typed<float>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
 }
 
 cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t* slot, const float* probs,
