@@ -160,7 +160,12 @@ def run_ours(args, rank, world):
     li = inputs.make_inputs(cfg, rank=rank)
     dt = inputs.TORCH_DTYPE[cfg.dtype]
     tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
-    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev)
+    comm = 0
+    if world > 1:
+        from paper_2112_14397_b200.layer import make_nccl_comm
+        comm = make_nccl_comm(rank, world)
+    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev, rank=rank, world=world,
+                        nccl_comm=comm)
     layer.set_gate(li.Wg.to(dev))
     layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
     x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
@@ -234,7 +239,8 @@ def run_ours(args, rank, world):
                    "tokens_per_gpu": cfg.T, "global_tokens": tokens, "rows_R": R,
                    "mean_experts_per_token": R / cfg.T if cfg.T else 0.0,
                    "max_over_mean_load": float(counts.max() / max(1e-9, counts.mean())),
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": f"ep{world} (E/{world} experts per GPU, NCCL all-to-all-v over NVLink)"
+                   if world > 1 else "single",
                    "l2": "flushed between steps (256 MiB write, outside the events)",
                    "wall_s_timed_region": wall},
         "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",

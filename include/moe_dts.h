@@ -178,6 +178,51 @@ int moe_dts_gate_bwd(moe_ctx* ctx, const float* dG_row, const int32_t* slot, con
 int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, const float* dlogits,
                      const void* Wg, void* dx, void* stream);
 
+/* ---------------------------------------------------------------- expert parallelism */
+/* EP (GShard-style): E/world experts per rank (global ids rank*E_local ...),
+ * tokens data-parallel.  Per layer pass: moe_dts_gate -> moe_ep_exchange_counts ->
+ * moe_ep_plan -> moe_ep_upload -> moe_dispatch (token side, "send" layout over all E
+ * experts) -> moe_ep_dispatch (send -> expert side "recv" layout) -> moe_expert_ffn on the
+ * recv layout -> moe_ep_combine (recv -> send) -> moe_combine.  Backward mirrors it:
+ * combine_bwd -> moe_ep_dispatch(d_eout) -> expert_ffn_bwd -> moe_ep_combine(dx_perm) ->
+ * gate_bwd -> moe_ep_allreduce(dWg) -> dispatch_bwd.
+ * Recv layout: local expert j occupies [offsets_recv[j], offsets_recv[j+1]) (128-aligned);
+ * inside it the rows of source rank 0, 1, ... in order (ascending global token index);
+ * pad rows are zeroed by moe_ep_dispatch.  Messages: one ncclSend/ncclRecv per
+ * (peer, local expert) segment inside one NCCL group, written in place (no re-layout). */
+
+/* NCCL bootstrap helpers (the id is broadcast by the caller, e.g. with torch.distributed). */
+int moe_nccl_unique_id(void* id_out, size_t bytes);   /* bytes >= 128 */
+int moe_nccl_comm_init(void** comm_out, const void* id, int world, int rank);
+int moe_nccl_comm_destroy(void* comm);
+
+/* All-gather this rank's counts [E] (device) into counts_all_host [world][E] (host);
+ * synchronises `stream` (the plan needs the counts on the host). */
+int moe_ep_exchange_counts(moe_ctx* ctx, const int32_t* counts, int32_t* counts_all_host, void* stream);
+
+/* Host-only: build the exchange plan from counts_all [world][E] (host) and return the
+ * token-side offsets_send [E+1], expert-side offsets_recv [E_local+1] (either may be
+ * NULL) and the row totals R_send, R_recv.  Needs no GPU.  MOE_EINVAL on counts < 0 or > T. */
+int moe_ep_plan(moe_ctx* ctx, const int32_t* counts_all, int32_t* offsets_send, int32_t* offsets_recv,
+                int64_t* R_send, int64_t* R_recv);
+
+/* Host-only accessor for tests: which = 0 -> this rank's sends (peer, send-layout row, rows),
+ * which = 1 -> its receives (peer, recv-layout row, rows), in NCCL posting order. */
+int moe_ep_plan_chunks(moe_ctx* ctx, int which, int32_t* peer, int64_t* row, int32_t* nrows, int max_chunks,
+                       int* n_out);
+
+/* Copy the plan's offsets_recv to a device buffer (and the library's pad table); syncs. */
+int moe_ep_upload(moe_ctx* ctx, int32_t* offsets_recv_dev, void* stream);
+
+/* Row exchange of `width`-element D rows: send layout -> recv layout (zeroing recv pads),
+ * and the reverse.  MOE_ECAPACITY if R_recv_cap < the plan's R_recv; MOE_ENCCL on NCCL errors. */
+int moe_ep_dispatch(moe_ctx* ctx, const void* send_rows, void* recv_rows, int width, int64_t R_recv_cap,
+                    void* stream);
+int moe_ep_combine(moe_ctx* ctx, const void* recv_rows, void* send_rows, int width, void* stream);
+
+/* In-place sum all-reduce over the EP group: fp32 (dW_g, C6) or int32 (global counts, C7). */
+int moe_ep_allreduce(moe_ctx* ctx, void* buf, int64_t n, int is_int32, void* stream);
+
 /* ---------------------------------------------------------------- NEXT #1 */
 
 /* Balance loss, Eq. 10: loss = alpha N sum_i (counts_i / B^2) sum_s p[s,i]

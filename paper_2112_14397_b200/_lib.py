@@ -40,6 +40,16 @@ SIGNATURES = {
     "moe_dts_gate_bwd": (_I, [_P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P]),
     "moe_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "moe_balance_loss": (_I, [_P, _P, _P, _F, _L, _P, _P]),
+    "moe_nccl_unique_id": (_I, [_P, _S]),
+    "moe_nccl_comm_init": (_I, [C.POINTER(_P), _P, _I, _I]),
+    "moe_nccl_comm_destroy": (_I, [_P]),
+    "moe_ep_exchange_counts": (_I, [_P, _P, _P, _P]),
+    "moe_ep_plan": (_I, [_P, _P, _P, _P, C.POINTER(_L), C.POINTER(_L)]),
+    "moe_ep_plan_chunks": (_I, [_P, _I, _P, _P, _P, _I, C.POINTER(_I)]),
+    "moe_ep_upload": (_I, [_P, _P, _P]),
+    "moe_ep_dispatch": (_I, [_P, _P, _P, _I, _L, _P]),
+    "moe_ep_combine": (_I, [_P, _P, _P, _I, _P]),
+    "moe_ep_allreduce": (_I, [_P, _P, _L, _I, _P]),
 }
 
 
@@ -181,3 +191,73 @@ def moe_dispatch_bwd(ctx, dx_perm, slot, dlogits, Wg, dx, stream=None):
 def moe_balance_loss(ctx, probs, counts, alpha, B_total, loss, stream=None):
     _call("moe_balance_loss", ctx, _ptr(probs), _ptr(counts), float(alpha), int(B_total), _ptr(loss),
           _stream(stream))
+
+
+# ---------------------------------------------------------------- expert parallelism
+def moe_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _call("moe_nccl_unique_id", C.cast(buf, C.c_void_p), 128)
+    return buf.raw
+
+
+def moe_nccl_comm_init(uid: bytes, world: int, rank: int) -> int:
+    h = C.c_void_p()
+    buf = C.create_string_buffer(uid, 128)
+    _call("moe_nccl_comm_init", C.byref(h), C.cast(buf, C.c_void_p), world, rank)
+    return h.value
+
+
+def moe_nccl_comm_destroy(comm: int) -> None:
+    _call("moe_nccl_comm_destroy", comm)
+
+
+def _np_i32(a):
+    import numpy as np
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return a, a.ctypes.data
+
+
+def moe_ep_exchange_counts(ctx, counts, world: int, E: int, stream=None):
+    import numpy as np
+    out = np.zeros((world, E), dtype=np.int32)
+    _call("moe_ep_exchange_counts", ctx, _ptr(counts), out.ctypes.data, _stream(stream))
+    return out
+
+
+def moe_ep_plan(ctx, counts_all, E: int, E_local: int):
+    """Host-only.  Returns (offsets_send [E+1], offsets_recv [E_local+1], R_send, R_recv)."""
+    import numpy as np
+    ca, ca_p = _np_i32(counts_all)
+    os_ = np.zeros(E + 1, dtype=np.int32)
+    or_ = np.zeros(E_local + 1, dtype=np.int32)
+    rs, rr = C.c_int64(), C.c_int64()
+    _call("moe_ep_plan", ctx, ca_p, os_.ctypes.data, or_.ctypes.data, C.byref(rs), C.byref(rr))
+    return os_, or_, rs.value, rr.value
+
+
+def moe_ep_plan_chunks(ctx, which: int):
+    """Host-only: list of (peer, row, nrows) in NCCL posting order (0 = sends, 1 = recvs)."""
+    import numpy as np
+    n = C.c_int()
+    _call("moe_ep_plan_chunks", ctx, which, None, None, None, 0, C.byref(n))
+    peer = np.zeros(max(1, n.value), np.int32)
+    row = np.zeros(max(1, n.value), np.int64)
+    nr = np.zeros(max(1, n.value), np.int32)
+    _call("moe_ep_plan_chunks", ctx, which, peer.ctypes.data, row.ctypes.data, nr.ctypes.data, n.value, C.byref(n))
+    return [(int(peer[i]), int(row[i]), int(nr[i])) for i in range(n.value)]
+
+
+def moe_ep_upload(ctx, offsets_recv_dev, stream=None):
+    _call("moe_ep_upload", ctx, _ptr(offsets_recv_dev), _stream(stream))
+
+
+def moe_ep_dispatch(ctx, send_rows, recv_rows, width: int, R_recv_cap: int, stream=None):
+    _call("moe_ep_dispatch", ctx, _ptr(send_rows), _ptr(recv_rows), int(width), int(R_recv_cap), _stream(stream))
+
+
+def moe_ep_combine(ctx, recv_rows, send_rows, width: int, stream=None):
+    _call("moe_ep_combine", ctx, _ptr(recv_rows), _ptr(send_rows), int(width), _stream(stream))
+
+
+def moe_ep_allreduce(ctx, buf, n: int, is_int32: bool = False, stream=None):
+    _call("moe_ep_allreduce", ctx, _ptr(buf), int(n), int(is_int32), _stream(stream))

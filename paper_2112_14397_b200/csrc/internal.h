@@ -6,6 +6,7 @@
 
 #include <string>
 
+namespace moe { struct EpPlan; }
 struct moe_ctx {
   int T, d, f, E, E_local, dtype, rank, world;
   void* comm;          // borrowed ncclComm_t (world > 1)
@@ -25,9 +26,17 @@ struct moe_ctx {
   float* colsum;       // [E] balance-loss column sums
   int* tot;            // [E] per-expert totals written by the dispatch scan
   float* colpart;      // [E_local, kColsumSplits, max(d, f)] bias-gradient partials
+  int* ep_counts;      // [world, E] gathered counts (EP)
+  int* ep_off;         // [E_local + 1] recv-layout offsets (EP)
+  int* ep_tot;         // [E_local] recv-layout rows per local expert (EP)
+  moe::EpPlan* ep;     // host exchange plan (EP), owned by the ctx
 };
 
 namespace moe {
+struct EpPlan;
+void ep_build_plan(EpPlan& P, const int* counts_all, int W, int E, int rank);
+cudaError_t launch_zero_pads(const moe_ctx* c, void* buf, const int* offsets_dev, const int* tot_dev, int width,
+                             cudaStream_t s);
 
 constexpr int kGateBT = 128;   // tokens per gate/dispatch block
 

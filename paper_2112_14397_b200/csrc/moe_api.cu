@@ -12,6 +12,7 @@
 #include "../../include/moe_dts.h"
 #include "common.cuh"
 #include "internal.h"
+#include "ep.h"
 
 namespace {
 thread_local std::string g_err;
@@ -63,7 +64,7 @@ namespace moe {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carve {
-  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, total;
+  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, total;
 };
 
 static Carve carve(const moe_ctx* c) {
@@ -83,6 +84,9 @@ static Carve carve(const moe_ctx* c) {
   k.colsum = take(sizeof(float) * (size_t)c->E);
   k.tot = take(sizeof(int) * (size_t)c->E);
   k.colpart = take(sizeof(float) * (size_t)c->E_local * kColsumSplits * (size_t)(c->d > c->f ? c->d : c->f));
+  k.ep_counts = take(sizeof(int) * (size_t)c->world * c->E);
+  k.ep_off = take(sizeof(int) * (size_t)(c->E_local + 1));
+  k.ep_tot = take(sizeof(int) * (size_t)c->E_local);
   k.total = o;
   return k;
 }
@@ -100,6 +104,9 @@ void carve_workspace(moe_ctx* c) {
   c->colsum = reinterpret_cast<float*>(c->ws + k.colsum);
   c->tot = reinterpret_cast<int*>(c->ws + k.tot);
   c->colpart = reinterpret_cast<float*>(c->ws + k.colpart);
+  c->ep_counts = reinterpret_cast<int*>(c->ws + k.ep_counts);
+  c->ep_off = reinterpret_cast<int*>(c->ws + k.ep_off);
+  c->ep_tot = reinterpret_cast<int*>(c->ws + k.ep_tot);
 }
 
 }  // namespace moe
@@ -125,6 +132,7 @@ int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype, vo
                 d_ff, q, dtype == MOE_BF16 ? "bf16" : "f32");
   if (E > 128) return fail(MOE_ESHAPE, "moe_create: E=%d > 128 is not supported", E);
   if (world > 1 && !nccl_comm) return fail(MOE_EINVAL, "moe_create: world=%d needs an NCCL comm", world);
+  // (world == 1 with a comm enables the EP exchange path against itself: used by the tests)
   moe_ctx* c = new (std::nothrow) moe_ctx();
   if (!c) return fail(MOE_EINVAL, "moe_create: out of host memory");
   c->T = T; c->d = d_model; c->f = d_ff; c->E = E; c->E_local = E / world; c->dtype = dtype;
@@ -144,6 +152,7 @@ int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype, vo
 }
 
 int moe_destroy(moe_ctx* ctx) {
+  if (ctx) delete ctx->ep;
   delete ctx;
   return MOE_OK;
 }
@@ -315,3 +324,169 @@ void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memo
 }  // namespace moe
 
 extern "C" uint64_t moe_kernel_launch_count(void) { return moe::g_launches.load(); }
+
+// ====================================================================== expert parallelism
+namespace {
+#ifdef MOE_HAVE_NCCL
+int nccl_status(ncclResult_t r, const char* where) {
+  if (r == ncclSuccess) return MOE_OK;
+  return fail(MOE_ENCCL, "%s: NCCL error %d (%s)", where, (int)r, ncclGetErrorString(r));
+}
+#endif
+int check_ep(moe_ctx* c, const char* fn, bool need_plan) {
+  if (!c) return fail(MOE_EINVAL, "%s: ctx is NULL", fn);
+  if (!c->comm) return fail(MOE_EINVAL, "%s: ctx has no NCCL communicator (expert parallelism disabled)", fn);
+  if (need_plan && !c->ep) return fail(MOE_EINVAL, "%s: no exchange plan (call moe_ep_plan first)", fn);
+  return MOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int moe_nccl_unique_id(void* id_out, size_t bytes) {
+#ifdef MOE_HAVE_NCCL
+  if (!id_out || bytes < sizeof(ncclUniqueId)) return fail(MOE_EINVAL, "moe_nccl_unique_id: need %zu bytes", sizeof(ncclUniqueId));
+  return nccl_status(ncclGetUniqueId(reinterpret_cast<ncclUniqueId*>(id_out)), "moe_nccl_unique_id");
+#else
+  return fail(MOE_ENCCL, "moe_nccl_unique_id: built without NCCL");
+#endif
+}
+
+int moe_nccl_comm_init(void** comm_out, const void* id, int world, int rank) {
+#ifdef MOE_HAVE_NCCL
+  if (!comm_out || !id) return fail(MOE_EINVAL, "moe_nccl_comm_init: NULL argument");
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm = nullptr;
+  int rc = nccl_status(ncclCommInitRank(&comm, world, uid, rank), "moe_nccl_comm_init");
+  *comm_out = comm;
+  return rc;
+#else
+  return fail(MOE_ENCCL, "moe_nccl_comm_init: built without NCCL");
+#endif
+}
+
+int moe_nccl_comm_destroy(void* comm) {
+#ifdef MOE_HAVE_NCCL
+  if (!comm) return MOE_OK;
+  return nccl_status(ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)), "moe_nccl_comm_destroy");
+#else
+  return fail(MOE_ENCCL, "moe_nccl_comm_destroy: built without NCCL");
+#endif
+}
+
+int moe_ep_plan(moe_ctx* ctx, const int32_t* counts_all, int32_t* offsets_send, int32_t* offsets_recv, int64_t* R_send,
+                int64_t* R_recv) {
+  if (!ctx) return fail(MOE_EINVAL, "moe_ep_plan: ctx is NULL");
+  REQUIRE(counts_all);
+  for (long long i = 0; i < (long long)ctx->world * ctx->E; ++i)
+    if (counts_all[i] < 0 || counts_all[i] > ctx->T)
+      return fail(MOE_EINVAL, "moe_ep_plan: counts_all[%lld]=%d outside [0, T=%d]", i, counts_all[i], ctx->T);
+  if (!ctx->ep) ctx->ep = new (std::nothrow) moe::EpPlan();
+  if (!ctx->ep) return fail(MOE_EINVAL, "moe_ep_plan: out of host memory");
+  moe::ep_build_plan(*ctx->ep, counts_all, ctx->world, ctx->E, ctx->rank);
+  const moe::EpPlan& P = *ctx->ep;
+  if (offsets_send) memcpy(offsets_send, P.offsets_send.data(), sizeof(int) * (ctx->E + 1));
+  if (offsets_recv) memcpy(offsets_recv, P.offsets_recv.data(), sizeof(int) * (ctx->E_local + 1));
+  if (R_send) *R_send = P.R_send;
+  if (R_recv) *R_recv = P.R_recv;
+  return MOE_OK;
+}
+
+int moe_ep_plan_chunks(moe_ctx* ctx, int which, int32_t* peer, int64_t* row, int32_t* nrows, int max_chunks,
+                       int* n_out) {
+  if (!ctx || !ctx->ep) return fail(MOE_EINVAL, "moe_ep_plan_chunks: no plan");
+  REQUIRE(n_out);
+  const moe::EpPlan& P = *ctx->ep;
+  const std::vector<int>& pe = which == 0 ? P.s_peer : P.r_peer;
+  const std::vector<int>& nr = which == 0 ? P.s_rows : P.r_rows;
+  const std::vector<long long>& ro = which == 0 ? P.s_src : P.r_dst;
+  *n_out = (int)pe.size();
+  for (int i = 0; i < (int)pe.size() && i < max_chunks; ++i) {
+    if (peer) peer[i] = pe[i];
+    if (row) row[i] = ro[i];
+    if (nrows) nrows[i] = nr[i];
+  }
+  return MOE_OK;
+}
+
+int moe_ep_exchange_counts(moe_ctx* ctx, const int32_t* counts, int32_t* counts_all_host, void* stream) {
+  int rc = check_ctx(ctx, "moe_ep_exchange_counts");
+  if (rc) return rc;
+  if ((rc = check_ep(ctx, "moe_ep_exchange_counts", false))) return rc;
+  REQUIRE(counts); REQUIRE(counts_all_host);
+#ifdef MOE_HAVE_NCCL
+  rc = nccl_status(ncclAllGather(counts, ctx->ep_counts, ctx->E, ncclInt32, reinterpret_cast<ncclComm_t>(ctx->comm),
+                                 S(stream)),
+                   "moe_ep_exchange_counts");
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(counts_all_host, ctx->ep_counts, sizeof(int) * ctx->world * ctx->E,
+                                  cudaMemcpyDeviceToHost, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  return cuda_status(e, "moe_ep_exchange_counts");
+#else
+  return fail(MOE_ENCCL, "moe_ep_exchange_counts: built without NCCL");
+#endif
+}
+
+int moe_ep_upload(moe_ctx* ctx, int32_t* offsets_recv_dev, void* stream) {
+  int rc = check_ctx(ctx, "moe_ep_upload");
+  if (rc) return rc;
+  if ((rc = check_ep(ctx, "moe_ep_upload", true))) return rc;
+  REQUIRE(offsets_recv_dev);
+  const moe::EpPlan& P = *ctx->ep;
+  cudaError_t e = cudaMemcpyAsync(offsets_recv_dev, P.offsets_recv.data(), sizeof(int) * (ctx->E_local + 1),
+                                  cudaMemcpyHostToDevice, S(stream));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ctx->ep_off, P.offsets_recv.data(), sizeof(int) * (ctx->E_local + 1), cudaMemcpyHostToDevice,
+                        S(stream));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(ctx->ep_tot, P.recv_tot.data(), sizeof(int) * ctx->E_local, cudaMemcpyHostToDevice, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));   // host vectors are pageable
+  return cuda_status(e, "moe_ep_upload");
+}
+
+int moe_ep_dispatch(moe_ctx* ctx, const void* send_rows, void* recv_rows, int width, int64_t R_recv_cap, void* stream) {
+  int rc = check_ctx(ctx, "moe_ep_dispatch");
+  if (rc) return rc;
+  if ((rc = check_ep(ctx, "moe_ep_dispatch", true))) return rc;
+  if (width <= 0 || width % 8 != 0) return fail(MOE_ESHAPE, "moe_ep_dispatch: width=%d must be a positive multiple of 8", width);
+  if (R_recv_cap < ctx->ep->R_recv)
+    return fail(MOE_ECAPACITY, "moe_ep_dispatch: R_recv_cap=%lld < plan R_recv=%lld", (long long)R_recv_cap,
+                (long long)ctx->ep->R_recv);
+#ifdef MOE_HAVE_NCCL
+  rc = nccl_status(moe::ep_exchange(ctx, *ctx->ep, send_rows, recv_rows, width, 0, S(stream)), "moe_ep_dispatch");
+  if (rc) return rc;
+  return cuda_status(moe::launch_zero_pads(ctx, recv_rows, ctx->ep_off, ctx->ep_tot, width, S(stream)), "moe_ep_dispatch");
+#else
+  return fail(MOE_ENCCL, "moe_ep_dispatch: built without NCCL");
+#endif
+}
+
+int moe_ep_combine(moe_ctx* ctx, const void* recv_rows, void* send_rows, int width, void* stream) {
+  int rc = check_ctx(ctx, "moe_ep_combine");
+  if (rc) return rc;
+  if ((rc = check_ep(ctx, "moe_ep_combine", true))) return rc;
+  if (width <= 0 || width % 8 != 0) return fail(MOE_ESHAPE, "moe_ep_combine: width=%d must be a positive multiple of 8", width);
+#ifdef MOE_HAVE_NCCL
+  return nccl_status(moe::ep_exchange(ctx, *ctx->ep, recv_rows, send_rows, width, 1, S(stream)), "moe_ep_combine");
+#else
+  return fail(MOE_ENCCL, "moe_ep_combine: built without NCCL");
+#endif
+}
+
+int moe_ep_allreduce(moe_ctx* ctx, void* buf, int64_t n, int is_int32, void* stream) {
+  int rc = check_ctx(ctx, "moe_ep_allreduce");
+  if (rc) return rc;
+  if ((rc = check_ep(ctx, "moe_ep_allreduce", false))) return rc;
+  REQUIRE(buf);
+#ifdef MOE_HAVE_NCCL
+  return nccl_status(ncclAllReduce(buf, buf, (size_t)n, is_int32 ? ncclInt32 : ncclFloat32, ncclSum,
+                                   reinterpret_cast<ncclComm_t>(ctx->comm), S(stream)),
+                     "moe_ep_allreduce");
+#else
+  return fail(MOE_ENCCL, "moe_ep_allreduce: built without NCCL");
+#endif
+}
+
+}  // extern "C"

@@ -23,6 +23,23 @@ def padded_rows(counts_host, align: int = L.ROW_ALIGN) -> int:
     return int(sum((int(c) + align - 1) // align * align for c in counts_host))
 
 
+def make_nccl_comm(rank: int, world: int) -> int:
+    """Create the library's own NCCL communicator over the ranks of the default
+    torch.distributed process group (the 128-byte unique id is broadcast through it)."""
+    import torch.distributed as dist
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        uid = torch.frombuffer(bytearray(L.moe_nccl_unique_id()), dtype=torch.uint8).clone()
+    if world > 1:
+        if dist.get_backend() == "nccl":
+            t = uid.cuda()
+            dist.broadcast(t, 0)
+            uid = t.cpu()
+        else:
+            dist.broadcast(uid, 0)
+    return L.moe_nccl_comm_init(bytes(uid.numpy().tobytes()), world, rank)
+
+
 @dataclass
 class ForwardState:
     tau: float
@@ -49,11 +66,16 @@ class DTSMoELayer:
         self.E_local = E // world
         self.dtype = dtype
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.rank, self.world = rank, world
+        self.ep = bool(nccl_comm)          # expert-parallel exchange (world > 1, or world == 1 self-exchange)
+        if world > 1 and not self.ep:
+            raise ValueError("world > 1 needs an NCCL communicator (see make_nccl_comm)")
         self.ctx = L.moe_create(T, d_model, d_ff, E, DTYPES[dtype], nccl_comm, rank, world)
         nbytes = L.moe_workspace_bytes(self.ctx)
         self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         L.moe_set_workspace(self.ctx, self.ws)
         self._rows = None      # row-layout buffers, grown on demand
+        self._buf = {}
         self._counts_host = torch.empty(E, dtype=torch.int32, pin_memory=True)
         self.Wg = None
         self.W1 = self.b1 = self.W2 = self.b2 = None
@@ -82,25 +104,44 @@ class DTSMoELayer:
         self.Wg = Wg
 
     # ------------------------------------------------------------ buffers
-    def _ensure_rows(self, R_cap: int):
-        if self._rows is not None and self._rows["R_cap"] >= R_cap:
-            return self._rows
-        R_cap = max(R_cap, L.ROW_ALIGN)
-        kw = dict(dtype=self.dtype, device=self.device)
-        d, f = self.d, self.f
-        self._rows = dict(
-            R_cap=R_cap,
-            x_perm=torch.empty(R_cap, d, **kw),
-            row_token=torch.empty(R_cap, dtype=torch.int32, device=self.device),
-            row_gate=torch.empty(R_cap, dtype=torch.float32, device=self.device),
-            a=torch.empty(R_cap, f, **kw),
-            h=torch.empty(R_cap, f, **kw),
-            e_out=torch.empty(R_cap, d, **kw),
-            d_eout=torch.empty(R_cap, d, **kw),
-            dG_row=torch.empty(R_cap, dtype=torch.float32, device=self.device),
-            dx_perm=torch.empty(R_cap, d, **kw),
-        )
-        return self._rows
+    def _grow(self, name, rows, width, dtype):
+        t = self._buf.get(name)
+        if t is None or t.shape[0] < rows:
+            t = torch.empty((max(rows, L.ROW_ALIGN),) + ((width,) if width else ()), dtype=dtype, device=self.device)
+            self._buf[name] = t
+        return t
+
+    def _ensure_rows(self, R_send: int, R_recv: int):
+        """Token-side ("send") and expert-side ("recv") row-layout buffers; without EP they
+        are the same buffers."""
+        d, f, D = self.d, self.f, self.dtype
+        b = {}
+        b["x_perm"] = self._grow("x_perm", R_send, d, D)
+        b["row_token"] = self._grow("row_token", R_send, 0, torch.int32)
+        b["row_gate"] = self._grow("row_gate", R_send, 0, torch.float32)
+        b["e_out"] = self._grow("e_out", R_send, d, D)
+        b["d_eout"] = self._grow("d_eout", R_send, d, D)
+        b["dG_row"] = self._grow("dG_row", R_send, 0, torch.float32)
+        b["dx_perm"] = self._grow("dx_perm", R_send, d, D)
+        b["a"] = self._grow("a", R_recv, f, D)
+        b["h"] = self._grow("h", R_recv, f, D)
+        if self.ep:
+            b["x_recv"] = self._grow("x_recv", R_recv, d, D)
+            b["e_out_recv"] = self._grow("e_out_recv", R_recv, d, D)
+            b["d_eout_recv"] = self._grow("d_eout_recv", R_recv, d, D)
+            b["dx_perm_recv"] = self._grow("dx_perm_recv", R_recv, d, D)
+        else:
+            b["x_recv"], b["e_out_recv"] = b["x_perm"], b["e_out"]
+            b["d_eout_recv"], b["dx_perm_recv"] = b["d_eout"], b["dx_perm"]
+        b["R_send_cap"] = b["x_perm"].shape[0]
+        b["R_recv_cap"] = min(b["a"].shape[0], b["h"].shape[0], b["x_recv"].shape[0], b["e_out_recv"].shape[0],
+                              b["d_eout_recv"].shape[0], b["dx_perm_recv"].shape[0])
+        b["R_send_cap"] = min(b["R_send_cap"], b["row_token"].shape[0], b["row_gate"].shape[0], b["e_out"].shape[0],
+                              b["d_eout"].shape[0], b["dG_row"].shape[0], b["dx_perm"].shape[0])
+        if not self.ep:
+            b["R_recv_cap"] = b["R_send_cap"] = min(b["R_send_cap"], b["R_recv_cap"])
+        self._rows = b
+        return b
 
     # ------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor, u: Optional[torch.Tensor], tau: float, threshold: float,
@@ -114,27 +155,41 @@ class DTSMoELayer:
         counts = torch.empty(E, dtype=torch.int32, device=dev)
         near = torch.empty(1, dtype=torch.int32, device=dev)
         L.moe_dts_gate(self.ctx, x, self.Wg, u, tau, threshold, top1, probs, slot, counts, near, stream)
-        if R_cap is None:
-            # size the row buffers from the routing result (one small D2H copy)
-            self._counts_host.copy_(counts, non_blocking=True)
-            torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
-            R_cap = padded_rows(self._counts_host.tolist())
-        R_cap = max(L.ROW_ALIGN, (R_cap + L.ROW_ALIGN - 1) // L.ROW_ALIGN * L.ROW_ALIGN)
-        rb = self._ensure_rows(R_cap)
-        R_cap = rb["R_cap"]
         offsets = torch.empty(E + 1, dtype=torch.int32, device=dev)
+        if self.ep:
+            counts_all = L.moe_ep_exchange_counts(self.ctx, counts, self.world, E, stream)
+            _, _, R_send, R_recv = L.moe_ep_plan(self.ctx, counts_all, E, self.E_local)
+            rb = self._ensure_rows(R_send, R_recv)
+            offsets_recv = torch.empty(self.E_local + 1, dtype=torch.int32, device=dev)
+            L.moe_ep_upload(self.ctx, offsets_recv, stream)
+        else:
+            if R_cap is None:
+                # size the row buffers from the routing result (one small D2H copy)
+                self._counts_host.copy_(counts, non_blocking=True)
+                torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+                R_cap = padded_rows(self._counts_host.tolist())
+            R_cap = max(L.ROW_ALIGN, (R_cap + L.ROW_ALIGN - 1) // L.ROW_ALIGN * L.ROW_ALIGN)
+            rb = self._ensure_rows(R_cap, R_cap)
+            offsets_recv = offsets
+        R_send_cap, R_recv_cap = rb["R_send_cap"], rb["R_recv_cap"]
         R_out = torch.empty(1, dtype=torch.int32, device=dev)
-        L.moe_dispatch(self.ctx, x, probs, slot, rb["x_perm"], rb["row_token"], rb["row_gate"], offsets, R_cap,
+        L.moe_dispatch(self.ctx, x, probs, slot, rb["x_perm"], rb["row_token"], rb["row_gate"], offsets, R_send_cap,
                        R_out, stream)
+        if self.ep:
+            L.moe_ep_dispatch(self.ctx, rb["x_perm"], rb["x_recv"], self.d, R_recv_cap, stream)
         if events:
             events[0].record()
-        L.moe_expert_ffn(self.ctx, rb["x_perm"], offsets, R_cap, self.W1, self.b1, self.W2, self.b2, rb["a"],
-                         rb["h"], rb["e_out"], stream)
+        L.moe_expert_ffn(self.ctx, rb["x_recv"], offsets_recv, R_recv_cap, self.W1, self.b1, self.W2, self.b2,
+                         rb["a"], rb["h"], rb["e_out_recv"], stream)
         if events:
             events[1].record()
+        if self.ep:
+            L.moe_ep_combine(self.ctx, rb["e_out_recv"], rb["e_out"], self.d, stream)
         y = torch.empty(T, self.d, dtype=self.dtype, device=dev)
         L.moe_combine(self.ctx, rb["e_out"], rb["row_gate"], slot, y, stream)
-        self.state = ForwardState(tau, threshold, top1, x, probs, slot, counts, near, offsets, R_cap, y)
+        self.state = ForwardState(tau, threshold, top1, x, probs, slot, counts, near, offsets, R_send_cap, y)
+        self.state.offsets_recv = offsets_recv
+        self.state.R_recv_cap = R_recv_cap
         return y
 
     # ------------------------------------------------------------ backward
@@ -147,6 +202,8 @@ class DTSMoELayer:
         El, d, f, dev = self.E_local, self.d, self.f, self.device
         L.moe_combine_bwd(self.ctx, dy, rb["e_out"], rb["row_gate"], rb["row_token"], st.offsets, st.R_cap,
                           rb["d_eout"], rb["dG_row"], stream)
+        if self.ep:
+            L.moe_ep_dispatch(self.ctx, rb["d_eout"], rb["d_eout_recv"], d, st.R_recv_cap, stream)
         grads = dict(
             dW1=torch.empty(El, f, d, dtype=torch.float32, device=dev),
             db1=torch.empty(El, f, dtype=torch.float32, device=dev),
@@ -157,15 +214,23 @@ class DTSMoELayer:
         da = rb["a"] if inplace_da else torch.empty_like(rb["a"])
         if events:
             events[0].record()
-        L.moe_expert_ffn_bwd(self.ctx, rb["d_eout"], rb["x_perm"], rb["a"], rb["h"], st.offsets, st.R_cap,
-                             self.W1, self.W2, da, rb["dx_perm"], grads["dW1"], grads["db1"], grads["dW2"],
-                             grads["db2"], stream)
+        L.moe_expert_ffn_bwd(self.ctx, rb["d_eout_recv"], rb["x_recv"], rb["a"], rb["h"], st.offsets_recv,
+                             st.R_recv_cap, self.W1, self.W2, da, rb["dx_perm_recv"], grads["dW1"], grads["db1"],
+                             grads["dW2"], grads["db2"], stream)
         if events:
             events[1].record()
+        if self.ep:
+            L.moe_ep_combine(self.ctx, rb["dx_perm_recv"], rb["dx_perm"], d, stream)
         dlogits = torch.empty(self.T, self.E, dtype=torch.float32, device=dev)
-        B = self.T if B_total is None else B_total
+        B = self.T * self.world if B_total is None else B_total
+        counts = st.counts
+        if balance_alpha > 0 and self.ep:
+            counts = st.counts.clone()
+            L.moe_ep_allreduce(self.ctx, counts, self.E, is_int32=True, stream=stream)
         L.moe_dts_gate_bwd(self.ctx, rb["dG_row"], st.slot, st.probs, st.x, st.tau, balance_alpha,
-                           st.counts if balance_alpha > 0 else None, B, grads["dWg"], dlogits, stream)
+                           counts if balance_alpha > 0 else None, B, grads["dWg"], dlogits, stream)
+        if self.ep:
+            L.moe_ep_allreduce(self.ctx, grads["dWg"], d * self.E, stream=stream)
         dx = torch.empty(self.T, d, dtype=self.dtype, device=dev)
         L.moe_dispatch_bwd(self.ctx, rb["dx_perm"], st.slot, dlogits, self.Wg, dx, stream)
         grads["dx"] = dx

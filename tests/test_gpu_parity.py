@@ -143,3 +143,30 @@ def test_invalid_scalars_rejected():
         with pytest.raises(L.MoEError) as e:
             layer.forward(li.x.cuda(), li.u.cuda(), tau, c)
         assert e.value.code == 1
+
+
+def test_ep_self_exchange_matches_single_rank():
+    """The EP code path (NCCL counts all-gather, plan, grouped send/recv row exchange with
+    pad zeroing, dW_g all-reduce) on a world-1 communicator must reproduce the non-EP
+    layer bit for bit (C3 reduced, bf16)."""
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.C3
+    li = inputs.make_inputs(cfg, T=700)
+    dev = torch.device("cuda", 0)
+    comm = L.moe_nccl_comm_init(L.moe_nccl_unique_id(), 1, 0)
+    outs = []
+    for c in (0, comm):
+        layer = DTSMoELayer(700, cfg.d_model, cfg.d_ff, cfg.E, dtype=torch.bfloat16, device=dev, nccl_comm=c)
+        layer.set_gate(li.Wg.to(dev))
+        layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+        y = layer.forward(li.x.to(dev), li.u.to(dev), float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)))
+        g = layer.backward(li.dy.to(dev), inplace_da=False)
+        torch.cuda.synchronize()
+        layer.check()
+        outs.append((y.float().cpu(), {k: v.float().cpu() for k, v in g.items() if k != "da"}))
+        del layer
+    assert torch.equal(outs[0][0], outs[1][0])
+    for k in outs[0][1]:
+        assert torch.equal(outs[0][1][k], outs[1][1][k]), k
+    L.moe_nccl_comm_destroy(comm)
