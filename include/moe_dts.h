@@ -128,13 +128,15 @@ int moe_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot,
 
 /* Grouped expert FFN, step 5 (Eq. 3 P:169-172 with GELU erf form P:472, R8).
  * For every row r of expert e (rows [offsets[e], offsets[e+1])):
- *   a[r] = W1[e] x_perm[r] + b1[e];  h[r] = GELU(a[r]);  e_out[r] = W2[e] h[r] + b2[e].
- * a_saved, h_saved [R_cap, d_ff] D; e_out [R_cap, d] D.  W1..b2 are LOCAL experts
+ *   a = W1[e] x_perm[r] + b1[e];  h[r] = GELU(a) = a Phi(a);  e_out[r] = W2[e] h[r] + b2[e]
+ * and, for the backward, gp[r] = GELU'(a) = Phi(a) + a phi(a), computed in the same
+ * epilogue from the same Phi(a) and exp(-a^2/2) (the pre-activation a itself is not kept).
+ * gp_saved, h_saved [R_cap, d_ff] D; e_out [R_cap, d] D.  W1..b2 are LOCAL experts
  * (moe_dts_spawn layout).  bf16: tcgen05 tensor cores, fp32 accumulation; f32: fp32
  * CUDA-core FMA. */
 int moe_expert_ffn(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int64_t R_cap,
                    const void* W1, const void* b1, const void* W2, const void* b2,
-                   void* a_saved, void* h_saved, void* e_out, void* stream);
+                   void* gp_saved, void* h_saved, void* e_out, void* stream);
 
 /* Combine + un-permute, step 6 (Eq. 4, Eq. 7, Alg. 1 line 11):
  *   y[t] = sum over selected e in ASCENDING e of row_gate[slot[t,e]] * e_out[slot[t,e]]
@@ -152,12 +154,12 @@ int moe_combine_bwd(moe_ctx* ctx, const void* dy, const void* e_out, const float
                     void* d_eout, float* dG_row, void* stream);
 
 /* Expert FFN backward (chain rule of Eq. 3).  Per expert e over its rows:
- *   dh = d_eout W2[e];  da = dh (.) GELU'(a),  GELU'(a) = Phi(a) + a phi(a)
+ *   dh = d_eout W2[e];  da = dh (.) gp   (gp = GELU'(a) saved by moe_expert_ffn)
  *   dW2[e] = d_eout^T h;  db2[e] = colsum(d_eout);  dW1[e] = da^T x_perm;  db1[e] = colsum(da)
  *   dx_perm = da W1[e]
- * da [R_cap, d_ff] D may ALIAS a_saved (overwritten in place).  dW1 [E_local, d_ff, d],
+ * da [R_cap, d_ff] D may ALIAS gp_saved (overwritten in place).  dW1 [E_local, d_ff, d],
  * db1 [E_local, d_ff], dW2 [E_local, d, d_ff], db2 [E_local, d] fp32 (overwritten). */
-int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, const void* a_saved,
+int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, const void* gp_saved,
                        const void* h_saved, const int32_t* offsets, int64_t R_cap,
                        const void* W1, const void* W2, void* da, void* dx_perm,
                        float* dW1, float* db1, float* dW2, float* db2, void* stream);

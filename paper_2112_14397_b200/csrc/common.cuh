@@ -109,5 +109,12 @@ __device__ __forceinline__ float gelu_prime_fast(float a) {
   const float ph = phi_cdf_as(a, e);
   return fmaf(a * 0.39894228040143268f, e, ph);
 }
+// Both at once from one Phi(a) / exp(-a^2/2): h = GELU(a), gp = GELU'(a).
+__device__ __forceinline__ void gelu_and_prime_fast(float a, float& h, float& gp) {
+  float e;
+  const float ph = phi_cdf_as(a, e);
+  h = a * ph;
+  gp = fmaf(a * 0.39894228040143268f, e, ph);
+}
 
 }  // namespace moe

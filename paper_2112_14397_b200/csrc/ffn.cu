@@ -18,16 +18,16 @@ static SimtGemm base_rows(const int32_t* offsets, int G, int64_t R_cap) {
 }
 
 cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
-                              const void* W1, const void* b1, const void* W2, const void* b2, void* a, void* h,
+                              const void* W1, const void* b1, const void* W2, const void* b2, void* gp, void* h,
                               void* e_out, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local, dt = c->dtype;
   cudaError_t e;
-  if (c->use_tc) return tc_expert_ffn(c, x_perm, offsets, R_cap, W1, b1, W2, b2, a, h, e_out, s);
+  if (c->use_tc) return tc_expert_ffn(c, x_perm, offsets, R_cap, W1, b1, W2, b2, gp, h, e_out, s);
   // GEMM1: a = x_perm W1_e^T + b1_e, h = GELU(a)
   SimtGemm g1 = base_rows(offsets, El, R_cap);
   g1.A = x_perm; g1.sAm = d; g1.sAk = 1;
   g1.B = W1; g1.sBk = 1; g1.sBn = d; g1.gB = (long long)f * d;
-  g1.C = a; g1.sCm = f; g1.C2 = h;
+  g1.C = gp; g1.sCm = f; g1.C2 = h;
   g1.bias = b1; g1.gBias = f;
   g1.M = 0; g1.N = f; g1.K = d;
   if ((e = launch_simt_gemm(g1, dt, dt, dt, EPI_BIAS_GELU, s)) != cudaSuccess) return e;
@@ -41,14 +41,14 @@ cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_
   return launch_simt_gemm(g2, dt, dt, dt, EPI_BIAS_T, s);
 }
 
-cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* a,
+cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                                   const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
                                   const void* W2, void* da, void* dx_perm, float* dW1, float* db1, float* dW2,
                                   float* db2, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local, dt = c->dtype;
   cudaError_t e;
   if (c->use_tc) {
-    if ((e = tc_expert_ffn_bwd(c, d_eout, x_perm, a, h, offsets, R_cap, W1, W2, da, dx_perm, dW1, dW2, s)) !=
+    if ((e = tc_expert_ffn_bwd(c, d_eout, x_perm, gp, h, offsets, R_cap, W1, W2, da, dx_perm, dW1, dW2, s)) !=
         cudaSuccess)
       return e;
     if ((e = launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, c->colpart, s)) != cudaSuccess) return e;
@@ -58,7 +58,7 @@ cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const vo
   SimtGemm g = base_rows(offsets, El, R_cap);
   g.A = d_eout; g.sAm = d; g.sAk = 1;
   g.B = W2; g.sBk = f; g.sBn = 1; g.gB = (long long)d * f;
-  g.C = da; g.sCm = f; g.aux = a;
+  g.C = da; g.sCm = f; g.aux = gp;
   g.N = f; g.K = d;
   if ((e = launch_simt_gemm(g, dt, dt, dt, EPI_GELU_BWD, s)) != cudaSuccess) return e;
   // wgrad2: dW2_e [d, f] = d_eout_e^T h_e   (ragged K = rows of e)

@@ -189,8 +189,8 @@ __device__ __forceinline__ void gate_token(const float* L, int t, const T* __res
 //   sum (the 1e-5 probs tolerance at tau = 0.05..0.1 needs it).
 //   Steps 2-3: warp per token on the smem logits (gate_token).
 constexpr int kKC = 32;
-template <typename T, int TPT>
-__global__ void __launch_bounds__(256) gate_fused_kernel(
+template <typename T, int TPT, int kGateThreads>   // kGateThreads / 256 k-groups
+__global__ void __launch_bounds__(kGateThreads) gate_fused_kernel(
     const T* __restrict__ x, const T* __restrict__ Wg, const float* __restrict__ u, int T_, int d, int E, float tau,
     float thr, int top1, float* __restrict__ probs, int* __restrict__ slot, int* __restrict__ counts,
     int* __restrict__ blk_cnt, int* __restrict__ near_band, int* __restrict__ flags) {
@@ -201,12 +201,16 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(
   const int Ep = EG * 4;
   float* xs = sm;                          // [kKC][kGateBT + 4]
   float* ws = xs + kKC * (kGateBT + 4);    // [kKC][Ep]
-  float* ls = ws + kKC * Ep;               // [kGateBT][E + 1]
+  float* ls = ws + kKC * Ep;               // [kGateBT][E + 1]   logits (sum part)
+  float* lc = ls + kGateBT * (E + 1);      // [kGateBT][E + 1]   compensation part
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t0 = blockIdx.x * kGateBT;
-  for (int i = tid; i < E; i += 256) s_cnt[i] = 0;
+  for (int i = tid; i < E; i += kGateThreads) s_cnt[i] = 0;
   if (tid == 0) s_band = 0;
-  const int eg = tid % EG, tg = tid / EG;
+  // thread = (k-group ks, token group tg, expert group eg): ks owns k-steps [ks*KG, ks*KG + KG) of each chunk
+  constexpr int KS = kGateThreads / 256, KG = kKC / KS;
+  const int ks = tid / 256, tl = tid % 256;
+  const int eg = tl % EG, tg = tl / EG;
   const bool active = tg * TPT < kGateBT;
   float sum[TPT][4], comp[TPT][4];
 #pragma unroll
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(
   constexpr int V = Vec16<T>::N;
   for (int k0 = 0; k0 < d; k0 += kKC) {
     // x chunk: kGateBT tokens x kKC, 16-byte vectors
-    for (int v = tid; v < kGateBT * (kKC / V); v += 256) {
+    for (int v = tid; v < kGateBT * (kKC / V); v += kGateThreads) {
       const int tok = v / (kKC / V), part = v % (kKC / V);
       const int kk = part * V;
       float f[V];
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(
 #pragma unroll
       for (int q = 0; q < V; ++q) xs[(kk + q) * (kGateBT + 4) + tok] = f[q];
     }
-    for (int i = tid; i < kKC * Ep; i += 256) {
+    for (int i = tid; i < kKC * Ep; i += kGateThreads) {
       const int kk = i / Ep, e = i % Ep;
       ws[i] = (k0 + kk < d && e < E) ? to_f32(Wg[(long long)(k0 + kk) * E + e]) : 0.f;
     }
@@ -240,8 +244,9 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(
       for (int i = 0; i < TPT; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) c[i][j] = 0.f;
-#pragma unroll 8
-      for (int kk = 0; kk < kKC; ++kk) {
+#pragma unroll
+      for (int k2 = 0; k2 < KG; ++k2) {
+        const int kk = ks * KG + k2;
         const float4 b = *reinterpret_cast<const float4*>(&ws[kk * Ep + eg * 4]);
         float a[TPT];
 #pragma unroll
@@ -267,25 +272,42 @@ __global__ void __launch_bounds__(256) gate_fused_kernel(
     }
     __syncthreads();
   }
-  if (active) {
+  // combine the KS partial (sum, comp) pairs in fixed order ks = 0, 1, ... with TwoSum
+  for (int g = 0; g < KS; ++g) {
+    if (ks == g && active) {
 #pragma unroll
-    for (int i = 0; i < TPT; ++i)
+      for (int i = 0; i < TPT; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int e = eg * 4 + j;
-        if (e < E) ls[(tg * TPT + i) * (E + 1) + e] = sum[i][j] + comp[i][j];
-      }
+        for (int j = 0; j < 4; ++j) {
+          const int e = eg * 4 + j;
+          if (e >= E) continue;
+          const int at = (tg * TPT + i) * (E + 1) + e;
+          if (g == 0) {
+            ls[at] = sum[i][j];
+            lc[at] = comp[i][j];
+          } else {
+            const float s0 = ls[at];
+            const float s1 = s0 + sum[i][j];
+            const float bp = s1 - s0;
+            const float err = (s0 - (s1 - bp)) + (sum[i][j] - bp);
+            ls[at] = s1;
+            lc[at] += err + comp[i][j];
+          }
+        }
+    }
+    __syncthreads();
   }
+  for (int i = tid; i < kGateBT * (E + 1); i += kGateThreads) ls[i] += lc[i];
   __syncthreads();
-  for (int i = warp; i < kGateBT; i += 8) {
+  for (int i = warp; i < kGateBT; i += kGateThreads / 32) {
     const int t = t0 + i;
     if (t >= T_) break;
     gate_token<T>(&ls[i * (E + 1)], t, x, Wg, u, d, E, tau, thr, top1, probs, slot, s_cnt, &s_band, flags, lane);
   }
   __syncthreads();
-  for (int e = tid; e < E; e += 256) {
+  for (int e = tid; e < E; e += kGateThreads) {
     int c = s_cnt[e];
-    blk_cnt[(long long)blockIdx.x * E + e] = c;
+    blk_cnt[(long long)e * gridDim.x + blockIdx.x] = c;   // expert-major [E][nblk]
     if (c) atomicAdd(&counts[e], c);
   }
   if (tid == 0 && s_band) atomicAdd(near_band, s_band);
@@ -296,11 +318,13 @@ cudaError_t launch_gate_fused(const moe_ctx* c, const void* x, const void* Wg, c
                               int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
                               cudaStream_t s) {
   const int Ep = (c->E + 3) / 4 * 4;
-  const size_t smem = sizeof(float) * (kKC * (kGateBT + 4) + kKC * Ep + kGateBT * (c->E + 1));
-  cudaError_t e = cudaFuncSetAttribute(gate_fused_kernel<T, TPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  // more k-groups (threads) when the per-thread tile is small; 64/128 registers budget otherwise
+  constexpr int kGateThreads = TPT <= 4 ? 1024 : (TPT <= 8 ? 512 : 256);
+  const size_t smem = sizeof(float) * (kKC * (kGateBT + 4) + kKC * Ep + 2 * kGateBT * (c->E + 1));
+  cudaError_t e = cudaFuncSetAttribute(gate_fused_kernel<T, TPT, kGateThreads>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  gate_fused_kernel<T, TPT><<<c->nblk, 256, smem, s>>>((const T*)x, (const T*)Wg, u, c->T, c->d, c->E, tau, thr,
+  gate_fused_kernel<T, TPT, kGateThreads><<<c->nblk, kGateThreads, smem, s>>>((const T*)x, (const T*)Wg, u, c->T, c->d, c->E, tau, thr,
                                                        top1, probs, slot, counts, c->blk_cnt, near_band, c->flags),
       count_launch();
   return cudaGetLastError();

@@ -107,14 +107,13 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SimtGemm g) {
       } else if (EPI == EPI_BIAS_T) {
         reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(v + to_f32(bias[n]));
       } else if (EPI == EPI_BIAS_GELU) {
-        float a = v + to_f32(bias[n]);
-        TO a_t = from_f32<TO>(a);
-        reinterpret_cast<TO*>(g.C)[ci] = a_t;
-        // h is GELU of the exact fp32 pre-activation, then rounded (R16)
+        // pre-activation a in fp32; store gp = GELU'(a) (for the backward) and h = GELU(a)
+        const float a = v + to_f32(bias[n]);
+        reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(gelu_prime_f(a));
         reinterpret_cast<TO*>(g.C2)[ci] = from_f32<TO>(gelu_f(a));
       } else if (EPI == EPI_GELU_BWD) {
-        float a = to_f32(reinterpret_cast<const TO*>(g.aux)[ci]);
-        reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(v * gelu_prime_f(a));
+        const float gp = to_f32(reinterpret_cast<const TO*>(g.aux)[ci]);   // saved GELU'(a)
+        reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(v * gp);
       }
     }
   }

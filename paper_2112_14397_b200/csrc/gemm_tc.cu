@@ -37,7 +37,12 @@ constexpr int A_BYTES = BM * BK * 2;         // 16 KB
 constexpr int B_BYTES = BNH * BK * 2;        // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;               // 2 accumulators x 256 fp32 columns
-constexpr int EPI_WARPS = 8;                 // 2 per TMEM lane quarter, each owns 128 of the 256 columns
+#ifndef MOE_EPI_PER_Q
+#define MOE_EPI_PER_Q 3
+#endif
+constexpr int EPI_PER_Q = MOE_EPI_PER_Q;                 // epilogue warps per TMEM lane quarter
+constexpr int EPI_WARPS = 4 * EPI_PER_Q;     // thread = accumulator row; a warp owns every 3rd 32-column chunk
+constexpr int CHUNKS = 256 / 32;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int CHUNK_BYTES = 32 * 32 * 2;     // one 32x32 bf16 sub-tile (TMA box, 64-byte swizzle)
 constexpr int MAX_G = 128;
@@ -71,6 +76,9 @@ struct TcParams {
   long long out_g;
   const bf16* bias;       // + g * bias_g
   long long bias_g;
+  bf16* o1;               // bf16 outputs (ROWS), pitch ldo_b -- used by the LSU store variant
+  bf16* o2;
+  long long ldo_b;
 };
 
 struct Tile {
@@ -250,7 +258,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     // ------------------------------------------------------------ epilogue (warps 2..9)
     const int ew = warp - 2;
     const int sub = warp & 3;                          // TMEM lane quarter this warp may access
-    const int half = ew >> 2;                          // column half: [half*128, half*128 + 128)
+    const int part = ew >> 2;                          // chunks part, part + 3, part + 6 (< 8) of the 8 x 32 columns
+    const int nch = (CHUNKS - part + EPI_PER_Q - 1) / EPI_PER_Q;
     const int row_in_tile = sub * 32 + lane;
     const uint32_t stage_base = tc::smem_u32(staging) + ew * (Cfg::NBUF * Cfg::NOUT * CHUNK_BYTES);
     const uint32_t swz = (uint32_t)((lane >> 1) & 3);  // SWIZZLE_64B: 16-byte chunk q -> q ^ ((row >> 1) & 3)
@@ -258,15 +267,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const uint32_t auxb = tc::smem_u32(aux_bar + ew * 4);
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t seq = 0;                                   // chunk sequence number (4 per tile)
+    uint32_t seq = 0;                                   // this warp's chunk sequence number (nch per tile)
 
     // GELU' operand: TMA-load a[rows, 32 cols] two chunks ahead into the staging buffers
     auto aux_issue = [&](uint32_t s) {
-      const int t = cid + (int)(s >> 2) * ncl;
+      const int t = cid + (int)(s / nch) * ncl;
       if (t >= total) return;
       Tile tn;
       decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tn);
-      const int col = tn.n0 + half * 128 + (int)(s & 3) * 32;
+      const int col = tn.n0 + (part + EPI_PER_Q * (int)(s % nch)) * 32;
       const uint32_t b = s % Cfg::NBUF;
       tc::mbar_arrive_expect_tx_u32(auxb + b * 8, CHUNK_BYTES);
       tc::tma_load_2d_u32(stage_base + b * CHUNK_BYTES, &tmX, auxb + b * 8, col, tn.m_own + sub * 32);
@@ -284,8 +293,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         // empty expert -> zero gradient tile
         if (row < p.M) {
           float* o = p.out + (long long)tl.g * p.out_g + row * p.ldo;
-          for (int c = half * 128; c < half * 128 + 128; c += 4)
-            if (tl.n0 + c < p.N) *reinterpret_cast<float4*>(o + tl.n0 + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int k = 0; k < nch; ++k)
+            for (int c = (part + EPI_PER_Q * k) * 32; c < (part + EPI_PER_Q * k) * 32 + 32; c += 4)
+              if (tl.n0 + c < p.N) *reinterpret_cast<float4*>(o + tl.n0 + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         continue;
       }
@@ -293,20 +303,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint4 bq[4];                                                   // bias of the current chunk
       const bf16* bias_t = nullptr;
       if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) {
-        bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0 + half * 128;
-        if (tl.n0 + half * 128 < p.N) {
+        bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0;
+        if (tl.n0 + part * 32 < p.N) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + q * 8);
+          for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + part * 32 + q * 8);
         }
       }
       tc::mbar_wait(&tfull_bar[acc], acc_phase);
       tc::tc_fence_after();
-      const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16) + half * 128;
+      const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16);
+#ifdef MOE_EXP_NOEPI
+      if (!KGRP) seq += nch; else
+#endif
 #pragma unroll 1
-      for (int cc = 0; cc < 4; ++cc, ++seq) {
-        const int n = tl.n0 + half * 128 + cc * 32;
+      for (int k = 0; k < nch; ++k, ++seq) {
+        const int col = (part + EPI_PER_Q * k) * 32;
+        const int n = tl.n0 + col;
         uint32_t r[32];
-        tc::tmem_ld32(t_row + cc * 32, r);
+        tc::tmem_ld32(t_row + col, r);
         tc::tmem_ld_wait();
         if (EPI == TEPI_F32) {
           if (row < p.M && n < p.N) {
@@ -327,10 +341,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           tc::mbar_wait_u32(auxb + (seq % Cfg::NBUF) * 8, (seq / Cfg::NBUF) & 1);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            float a[8];
+            float a[8];                                            // gp = GELU'(a) saved by the forward
             unpack16(tc::ld_shared_v4(buf + lane * 64 + ((q ^ swz) << 4)), a, bf16());
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[q * 8 + j] *= gelu_prime_fast(a[j]);
+            for (int j = 0; j < 8; ++j) v[q * 8 + j] *= a[j];   // da = dh (.) GELU'(a)
           }
         } else {
           if (seq >= 2) {                                 // the group that last used this buffer must be read
@@ -345,28 +359,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
               for (int j = 0; j < 8; ++j) v[q * 8 + j] += b[j];
             }
-            if (cc < 3 && n + 32 < p.N) {                 // prefetch the next chunk's bias
+            if (k + 1 < nch && n + EPI_PER_Q * 32 < p.N) {   // prefetch the next chunk's bias
 #pragma unroll
-              for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + (cc + 1) * 32 + q * 8);
+              for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + col + EPI_PER_Q * 32 + q * 8);
             }
           }
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(v + q * 8, bf16()));
         if (EPI == TEPI_BIAS_GELU) {
+          // out1 = GELU'(a) (kept for the backward), out2 = h = GELU(a): one Phi / exp per element
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            float hq[8];
+            float hq[8], gq[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) hq[j] = gelu_fast(v[q * 8 + j]);
+            for (int j = 0; j < 8; ++j) gelu_and_prime_fast(v[q * 8 + j], hq[j], gq[j]);
+            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(gq, bf16()));
             tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), pack16(hq, bf16()));
           }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(v + q * 8, bf16()));
         }
         tc::fence_proxy_async();
         __syncwarp();
+#ifdef MOE_EXP_STG
+        if (store) {   // coalesced LSU stores from the swizzled smem sub-tile: 8 rows x 64 B per instruction
+          const int row0 = tl.m_own + sub * 32;
+#pragma unroll
+          for (int o = 0; o < Cfg::NOUT; ++o) {
+            bf16* dst = (o == 0 ? p.o1 : p.o2) + n + (lane & 3) * 8;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = (lane >> 2) + 8 * i;
+              const uint4 v4 = tc::ld_shared_v4(buf + o * CHUNK_BYTES + r * 64 + (((lane & 3) ^ ((r >> 1) & 3)) << 4));
+              st_v4(dst + (long long)(row0 + r) * p.ldo_b, v4);
+            }
+          }
+        }
+#endif
         if (lane == 0) {
+#if defined(MOE_EXP_NOSTORE) || defined(MOE_EXP_STG)
+          if (false) {
+#else
           if (store) {
+#endif
             const int row0 = tl.m_own + sub * 32;
             tc::tma_store_2d(&tmO1, buf, n, row0);
             if (Cfg::NOUT == 2) tc::tma_store_2d(&tmO2, buf + CHUNK_BYTES, n, row0);
@@ -461,7 +497,7 @@ static long long rows_pairs_upper(int64_t R_cap, int El) { return R_cap / 256 + 
 
 // ---------------------------------------------------------------- step 5 / B5 on tensor cores
 cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
-                          const void* W1, const void* b1, const void* W2, const void* b2, void* a, void* h,
+                          const void* W1, const void* b1, const void* W2, const void* b2, void* gp, void* h,
                           void* e_out, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local;
   if (R_cap == 0) return cudaSuccess;
@@ -470,10 +506,11 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
   p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
   // GEMM1: a = x_perm W1^T + b1, h = GELU(a)      A [R, d] K-major, B = W1 [El*f, d] K-major
   if (!make_map(&mA, x_perm, R_cap, d, d, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, BNH) ||
-      !make_store_map(&mO1, a, R_cap, f) || !make_store_map(&mO2, h, R_cap, f))
+      !make_store_map(&mO1, gp, R_cap, f) || !make_store_map(&mO2, h, R_cap, f))
     return cudaErrorInvalidValue;
   p.N = f; p.K = d; p.b_group_rows = f;
   p.bias = reinterpret_cast<const bf16*>(b1); p.bias_g = f;
+  p.o1 = reinterpret_cast<bf16*>(gp); p.o2 = reinterpret_cast<bf16*>(h); p.ldo_b = f;
   const long long up = rows_pairs_upper(R_cap, El);
   cudaError_t e = launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p,
                                                                   up * ((f + BN - 1) / BN), c->sm_count, s);
@@ -484,11 +521,12 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
     return cudaErrorInvalidValue;
   p.N = d; p.K = f; p.b_group_rows = d;
   p.bias = reinterpret_cast<const bf16*>(b2); p.bias_g = d;
+  p.o1 = reinterpret_cast<bf16*>(e_out); p.o2 = nullptr; p.ldo_b = d;
   return launch_tc<TEPI_BIAS, false, false, false>(mA, mB, mO1, mO1, mO1, p, up * ((d + BN - 1) / BN),
                                                    c->sm_count, s);
 }
 
-cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* a,
+cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                               const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
                               const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local;
@@ -504,9 +542,10 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
     p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
     // dgrad2: da = (d_eout W2_e) (.) GELU'(a)   A = d_eout [R, d] K-major; B(k=d, n=f) = W2 [El*d, f] MN-major
     if (!make_map(&mA, d_eout, R_cap, d, d, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, 64) ||
-        !make_store_map(&mO, da, R_cap, f) || !make_store_map(&mX, a, R_cap, f))
+        !make_store_map(&mO, da, R_cap, f) || !make_store_map(&mX, gp, R_cap, f))
       return cudaErrorInvalidValue;
     p.N = f; p.K = d; p.b_group_rows = d;
+    p.o1 = reinterpret_cast<bf16*>(da); p.ldo_b = f;
     e = launch_tc<TEPI_GELU_BWD, false, true, false>(mA, mB, mO, mO, mX, p, up * ((f + BN - 1) / BN),
                                                      c->sm_count, s);
     if (e != cudaSuccess) return e;
@@ -515,6 +554,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
         !make_store_map(&mO, dx_perm, R_cap, d))
       return cudaErrorInvalidValue;
     p.N = d; p.K = f; p.b_group_rows = f;
+    p.o1 = reinterpret_cast<bf16*>(dx_perm); p.ldo_b = d;
     e = launch_tc<TEPI_STORE, false, true, false>(mA, mB, mO, mO, mO, p, up * ((d + BN - 1) / BN), c->sm_count, s);
     if (e != cudaSuccess) return e;
   }

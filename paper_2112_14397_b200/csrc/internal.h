@@ -78,10 +78,10 @@ cudaError_t launch_balance_loss(const moe_ctx* c, const float* probs, const int3
 
 cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets,
                               int64_t R_cap, const void* W1, const void* b1, const void* W2,
-                              const void* b2, void* a, void* h, void* e_out, cudaStream_t s);
+                              const void* b2, void* gp, void* h, void* e_out, cudaStream_t s);
 
 cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm,
-                                  const void* a, const void* h, const int32_t* offsets,
+                                  const void* gp, const void* h, const int32_t* offsets,
                                   int64_t R_cap, const void* W1, const void* W2, void* da,
                                   void* dx_perm, float* dW1, float* db1, float* dW2, float* db2,
                                   cudaStream_t s);
@@ -89,9 +89,9 @@ cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const vo
 // ---------------------------------------------------------------- tcgen05 grouped GEMM (bf16)
 bool tc_available();
 cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
-                          const void* W1, const void* b1, const void* W2, const void* b2, void* a, void* h,
+                          const void* W1, const void* b1, const void* W2, const void* b2, void* gp, void* h,
                           void* e_out, cudaStream_t s);
-cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* a,
+cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                               const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
                               const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, cudaStream_t s);
 

@@ -227,16 +227,16 @@ int moe_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot,
 }
 
 int moe_expert_ffn(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int64_t R_cap, const void* W1,
-                   const void* b1, const void* W2, const void* b2, void* a_saved, void* h_saved,
+                   const void* b1, const void* W2, const void* b2, void* gp_saved, void* h_saved,
                    void* e_out, void* stream) {
   int rc = check_ctx(ctx, "moe_expert_ffn");
   if (rc) return rc;
   REQUIRE_R(x_perm); REQUIRE(offsets); REQUIRE(W1); REQUIRE(b1); REQUIRE(W2); REQUIRE(b2);
-  REQUIRE_R(a_saved); REQUIRE_R(h_saved); REQUIRE_R(e_out);
+  REQUIRE_R(gp_saved); REQUIRE_R(h_saved); REQUIRE_R(e_out);
   if (R_cap < 0 || R_cap % moe::kRowAlign != 0)
     return fail(MOE_EINVAL, "moe_expert_ffn: R_cap=%lld must be a non-negative multiple of %d",
                 (long long)R_cap, moe::kRowAlign);
-  return cuda_status(moe::launch_expert_ffn(ctx, x_perm, offsets, R_cap, W1, b1, W2, b2, a_saved, h_saved,
+  return cuda_status(moe::launch_expert_ffn(ctx, x_perm, offsets, R_cap, W1, b1, W2, b2, gp_saved, h_saved,
                                             e_out, S(stream)),
                      "moe_expert_ffn");
 }
@@ -263,18 +263,18 @@ int moe_combine_bwd(moe_ctx* ctx, const void* dy, const void* e_out, const float
                      "moe_combine_bwd");
 }
 
-int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, const void* a_saved,
+int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, const void* gp_saved,
                        const void* h_saved, const int32_t* offsets, int64_t R_cap, const void* W1,
                        const void* W2, void* da, void* dx_perm, float* dW1, float* db1, float* dW2,
                        float* db2, void* stream) {
   int rc = check_ctx(ctx, "moe_expert_ffn_bwd");
   if (rc) return rc;
-  REQUIRE_R(d_eout); REQUIRE_R(x_perm); REQUIRE_R(a_saved); REQUIRE_R(h_saved); REQUIRE(offsets); REQUIRE(W1);
+  REQUIRE_R(d_eout); REQUIRE_R(x_perm); REQUIRE_R(gp_saved); REQUIRE_R(h_saved); REQUIRE(offsets); REQUIRE(W1);
   REQUIRE(W2); REQUIRE_R(da); REQUIRE_R(dx_perm); REQUIRE(dW1); REQUIRE(db1); REQUIRE(dW2); REQUIRE(db2);
   if (R_cap < 0 || R_cap % moe::kRowAlign != 0)
     return fail(MOE_EINVAL, "moe_expert_ffn_bwd: R_cap=%lld must be a non-negative multiple of %d",
                 (long long)R_cap, moe::kRowAlign);
-  return cuda_status(moe::launch_expert_ffn_bwd(ctx, d_eout, x_perm, a_saved, h_saved, offsets, R_cap, W1,
+  return cuda_status(moe::launch_expert_ffn_bwd(ctx, d_eout, x_perm, gp_saved, h_saved, offsets, R_cap, W1,
                                                 W2, da, dx_perm, dW1, db1, dW2, db2, S(stream)),
                      "moe_expert_ffn_bwd");
 }

@@ -9,9 +9,10 @@ namespace moe {
 namespace {
 
 // ------------------------------------------------------------------ scan
-// Single CTA of 1024 threads.  Per expert: exclusive prefix of the per-block counts
-// over blocks (blk_base), totals -> tot[], then 128-aligned exclusive prefix of the
-// totals -> offsets[E+1].  Deterministic (integer arithmetic only).
+// Single CTA of 1024 threads over the expert-major per-block counts blk_cnt[E][nblk]:
+// warp per expert, each lane 4 consecutive blocks per 128-block step (coalesced), warp
+// scan of lane totals -> exclusive per-block bases blk_base[E][nblk]; then the 128-aligned
+// exclusive prefix of the totals -> offsets[E+1].  Integer arithmetic only (deterministic).
 __global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restrict__ blk_cnt, int nblk, int E,
                                                             int* __restrict__ blk_base, int* __restrict__ tot,
                                                             int* __restrict__ offsets, int* __restrict__ R_out,
@@ -19,17 +20,27 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restri
   __shared__ int s_tot[128];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   for (int e = warp; e < E; e += nw) {
+    const int* src = blk_cnt + (long long)e * nblk;
+    int* dst = blk_base + (long long)e * nblk;
     int carry = 0;
-    for (int b0 = 0; b0 < nblk; b0 += 32) {
-      int b = b0 + lane;
-      int v = b < nblk ? blk_cnt[(long long)b * E + e] : 0;
-      int inc = v;
+    for (int b0 = 0; b0 < nblk; b0 += 128) {
+      const int b = b0 + lane * 4;
+      int v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (b + q < nblk) ? src[b + q] : 0;
+      const int lsum = v[0] + v[1] + v[2] + v[3];
+      int inc = lsum;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         int n = __shfl_up_sync(0xffffffffu, inc, o);
         if (lane >= o) inc += n;
       }
-      if (b < nblk) blk_base[(long long)b * E + e] = carry + inc - v;
+      int run = carry + inc - lsum;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (b + q < nblk) dst[b + q] = run;
+        run += v[q];
+      }
       carry += __shfl_sync(0xffffffffu, inc, 31);
     }
     if (lane == 0) s_tot[e] = carry;
@@ -58,8 +69,10 @@ __global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
     const T* __restrict__ x, const float* __restrict__ probs, int* __restrict__ slot, int T_, int d, int E,
     const int* __restrict__ blk_base, const int* __restrict__ offsets, const int* __restrict__ tot,
     T* __restrict__ x_perm, int* __restrict__ row_token, float* __restrict__ row_gate, long long R_cap) {
-  extern __shared__ int s_rows[];              // [kGateBT][E]
+  extern __shared__ int s_rows[];              // [kGateBT][E]: each token's selected rows, compacted
   __shared__ int s_wsum[2][kGateBT / 32];
+  __shared__ int s_n[kGateBT];
+  int nsel = 0;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
@@ -74,7 +87,7 @@ __global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
     for (int w = 0; w < kGateBT / 32; ++w) wpre += (w < warp) ? s_wsum[e & 1][w] : 0;
     int row = -1;
     if (sel) {
-      row = offsets[e] + blk_base[(long long)blockIdx.x * E + e] + wpre + pre;
+      row = offsets[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre + pre;
       if (row < R_cap) {
         slot[(long long)t * E + e] = row;
         row_token[row] = t;
@@ -84,8 +97,9 @@ __global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
         row = -1;
       }
     }
-    s_rows[tid * E + e] = row;
+    if (row >= 0) s_rows[tid * E + nsel++] = row;
   }
+  s_n[tid] = nsel;
   __syncthreads();
   // copy phase: each warp copies whole tokens, x_t read once, written to each selected row
   constexpr int V = Vec16<T>::N;
@@ -101,9 +115,9 @@ __global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
         int v = v0 + q * 32 + lane;
         if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
       }
-      for (int e = 0; e < E; ++e) {
-        const int row = s_rows[i * E + e];
-        if (row < 0) continue;
+      const int n = s_n[i];
+      for (int k = 0; k < n; ++k) {
+        const int row = s_rows[i * E + k];
         T* dst = x_perm + (long long)row * d;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -125,7 +139,62 @@ __global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
 }
 
 // ------------------------------------------------------------------ combine
-// One warp per token: y[t] = sum_{e asc} row_gate[r] * e_out[r], r = slot[t,e].
+// One warp per token.  The token's selected rows are found with ballots over its slot row
+// (ascending expert order is the bit order), so the work is O(selected), not O(E).
+// Columns are processed 4 x 16-byte vectors per lane at a time (independent loads in flight).
+template <typename T, bool WEIGHTED>
+__device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src, const float* __restrict__ row_gate,
+                                                 const int* __restrict__ slot_row, int d, int E,
+                                                 const float* __restrict__ extra, T* __restrict__ out, int lane) {
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+    float acc[4][V];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc[q][k] = 0.f;
+    for (int g = 0; g < E; g += 32) {
+      const int sv = (g + lane < E) ? slot_row[g + lane] : -1;
+      unsigned bal = __ballot_sync(0xffffffffu, sv >= 0);
+      while (bal) {
+        const int b = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int r = __shfl_sync(0xffffffffu, sv, b);
+        const float gw = WEIGHTED ? row_gate[r] : 1.0f;
+        uint4 raw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = v0 + q * 32 + lane;
+          if (v < nvec) raw[q] = ld_nc_v4(rows_src + (long long)r * d + (long long)v * V);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = v0 + q * 32 + lane;
+          if (v < nvec) {
+            float o[V];
+            unpack16(raw[q], o, T());
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc[q][k] = WEIGHTED ? fmaf(gw, o[k], acc[q][k]) : acc[q][k] + o[k];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) {
+        if (extra) {
+#pragma unroll
+          for (int k = 0; k < V; ++k) acc[q][k] += extra[(long long)v * V + k];
+        }
+        st_v4(out + (long long)v * V, pack16(acc[q], T()));
+      }
+    }
+  }
+}
+
+// y[t] = sum_{e asc} row_gate[r] * e_out[r], r = slot[t,e]
 template <typename T>
 __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ e_out, const float* __restrict__ row_gate,
                                                       const int* __restrict__ slot, int T_, int d, int E,
@@ -133,33 +202,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ e_ou
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  int my_slot[4];
-  float my_g[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int e = lane + 32 * i;
-    my_slot[i] = e < E ? slot[(long long)t * E + e] : -1;
-    my_g[i] = my_slot[i] >= 0 ? row_gate[my_slot[i]] : 0.f;
-  }
-  constexpr int V = Vec16<T>::N;
-  const int nvec = d / V;
-  for (int v = lane; v - lane < nvec; v += 32) {
-    float acc[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) acc[k] = 0.f;
-    for (int e = 0; e < E; ++e) {
-      const int r = __shfl_sync(0xffffffffu, my_slot[e >> 5], e & 31);
-      if (r < 0) continue;
-      const float gw = __shfl_sync(0xffffffffu, my_g[e >> 5], e & 31);
-      if (v < nvec) {
-        float o[V];
-        unpack16(ld_nc_v4(e_out + (long long)r * d + (long long)v * V), o, T());
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] = fmaf(gw, o[k], acc[k]);
-      }
-    }
-    if (v < nvec) st_v4(y + (long long)t * d + (long long)v * V, pack16(acc, T()));
-  }
+  gather_sum_token<T, true>(e_out, row_gate, slot + (long long)t * E, d, E, nullptr, y + (long long)t * d, lane);
 }
 
 // ------------------------------------------------------------------ combine backward
@@ -210,36 +253,8 @@ __global__ void __launch_bounds__(256) dispatch_bwd_kernel(const T* __restrict__
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  int my_slot[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int e = lane + 32 * i;
-    my_slot[i] = e < E ? slot[(long long)t * E + e] : -1;
-  }
-  constexpr int V = Vec16<T>::N;
-  const int nvec = d / V;
-  for (int v = lane; v - lane < nvec; v += 32) {
-    float acc[V];
-#pragma unroll
-    for (int k = 0; k < V; ++k) acc[k] = 0.f;
-    for (int e = 0; e < E; ++e) {
-      const int r = __shfl_sync(0xffffffffu, my_slot[e >> 5], e & 31);
-      if (r < 0) continue;
-      if (v < nvec) {
-        float o[V];
-        unpack16(ld_nc_v4(dx_perm + (long long)r * d + (long long)v * V), o, T());
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] += o[k];
-      }
-    }
-    if (v < nvec) {
-      if (dxg) {
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[k] += dxg[(long long)t * d + (long long)v * V + k];
-      }
-      st_v4(dx + (long long)t * d + (long long)v * V, pack16(acc, T()));
-    }
-  }
+  gather_sum_token<T, false>(dx_perm, nullptr, slot + (long long)t * E, d, E, dxg ? dxg + (long long)t * d : nullptr,
+                             dx + (long long)t * d, lane);
 }
 
 // ------------------------------------------------------------------ spawn (step 6b)

@@ -123,7 +123,7 @@ class DTSMoELayer:
         b["d_eout"] = self._grow("d_eout", R_send, d, D)
         b["dG_row"] = self._grow("dG_row", R_send, 0, torch.float32)
         b["dx_perm"] = self._grow("dx_perm", R_send, d, D)
-        b["a"] = self._grow("a", R_recv, f, D)
+        b["gp"] = self._grow("gp", R_recv, f, D)
         b["h"] = self._grow("h", R_recv, f, D)
         if self.ep:
             b["x_recv"] = self._grow("x_recv", R_recv, d, D)
@@ -134,7 +134,7 @@ class DTSMoELayer:
             b["x_recv"], b["e_out_recv"] = b["x_perm"], b["e_out"]
             b["d_eout_recv"], b["dx_perm_recv"] = b["d_eout"], b["dx_perm"]
         b["R_send_cap"] = b["x_perm"].shape[0]
-        b["R_recv_cap"] = min(b["a"].shape[0], b["h"].shape[0], b["x_recv"].shape[0], b["e_out_recv"].shape[0],
+        b["R_recv_cap"] = min(b["gp"].shape[0], b["h"].shape[0], b["x_recv"].shape[0], b["e_out_recv"].shape[0],
                               b["d_eout_recv"].shape[0], b["dx_perm_recv"].shape[0])
         b["R_send_cap"] = min(b["R_send_cap"], b["row_token"].shape[0], b["row_gate"].shape[0], b["e_out"].shape[0],
                               b["d_eout"].shape[0], b["dG_row"].shape[0], b["dx_perm"].shape[0])
@@ -180,7 +180,7 @@ class DTSMoELayer:
         if events:
             events[0].record()
         L.moe_expert_ffn(self.ctx, rb["x_recv"], offsets_recv, R_recv_cap, self.W1, self.b1, self.W2, self.b2,
-                         rb["a"], rb["h"], rb["e_out_recv"], stream)
+                         rb["gp"], rb["h"], rb["e_out_recv"], stream)
         if events:
             events[1].record()
         if self.ep:
@@ -211,10 +211,10 @@ class DTSMoELayer:
             db2=torch.empty(El, d, dtype=torch.float32, device=dev),
             dWg=torch.empty(d, self.E, dtype=torch.float32, device=dev),
         )
-        da = rb["a"] if inplace_da else torch.empty_like(rb["a"])
+        da = rb["gp"] if inplace_da else torch.empty_like(rb["gp"])
         if events:
             events[0].record()
-        L.moe_expert_ffn_bwd(self.ctx, rb["d_eout_recv"], rb["x_recv"], rb["a"], rb["h"], st.offsets_recv,
+        L.moe_expert_ffn_bwd(self.ctx, rb["d_eout_recv"], rb["x_recv"], rb["gp"], rb["h"], st.offsets_recv,
                              st.R_recv_cap, self.W1, self.W2, da, rb["dx_perm_recv"], grads["dW1"], grads["db1"],
                              grads["dW2"], grads["db2"], stream)
         if events:

@@ -80,7 +80,7 @@ def run_gpu(cfg: MoEConfig, li: inputs.LayerInputs, backward: bool = True) -> Gp
     st = layer.state
     rb = layer.rows
     R = int(st.offsets[-1].item())
-    rows = {k: _np(rb[k][:R]) for k in ("x_perm", "row_token", "row_gate", "a", "h", "e_out")}
+    rows = {k: _np(rb[k][:R]) for k in ("x_perm", "row_token", "row_gate", "gp", "h", "e_out")}
     W = {k: _np(getattr(layer, k)) for k in ("W1", "b1", "W2", "b2")}
     run = GpuRun(layer, _np(y), _np(st.probs), _np(st.slot), _np(st.counts), int(st.near_band.item()),
                  _np(st.offsets), rows, W, None)
@@ -137,9 +137,11 @@ def compare(cfg: MoEConfig, li: inputs.LayerInputs, g: GpuRun, backward: bool = 
     toks, es = np.nonzero(m_gpu)
     assert np.array_equal(g.rows["row_gate"][slot[toks, es]], g.probs[toks, es]), "row_gate provenance"
     # expert FFN intermediates and output
-    a_ref = O.to_rows(fw.a, offsets, cfg.d_ff)
+    gp_ref = O.to_rows({e: O.gelu_prime(a) for e, a in fw.a.items()}, offsets, cfg.d_ff)
+    h_ref = O.to_rows(fw.h, offsets, cfg.d_ff)
     e_ref = O.to_rows(fw.o, offsets, cfg.d_model)
-    rep["a"] = rel_err(g.rows["a"][valid], a_ref[valid])
+    rep["gp"] = rel_err(g.rows["gp"][valid], gp_ref[valid])       # saved GELU'(a)
+    rep["h"] = rel_err(g.rows["h"][valid], h_ref[valid])
     rep["e_out"] = rel_err(g.rows["e_out"][valid], e_ref[valid])
     rep["y"] = rel_err(g.y, fw.y)
     if backward:
