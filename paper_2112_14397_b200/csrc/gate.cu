@@ -11,176 +11,11 @@
 // for entries within ~1e-7 of c.
 #include "common.cuh"
 #include "internal.h"
+#include "gate_token.cuh"
 
 namespace moe {
 
 namespace {
-
-constexpr float kRefine = 5e-5f;
-constexpr float kBand = 1e-6f;
-constexpr int kMaxEPL = 4;          // experts per lane (E <= 128)
-
-__device__ __forceinline__ void warp_argmax(float& v, int& i) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    float ov = __shfl_xor_sync(0xffffffffu, v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, i, o);
-    if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
-  }
-}
-__device__ __forceinline__ void warp_argmax(double& v, int& i) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, i, o);
-    if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
-  }
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-__device__ __forceinline__ double warp_maxd(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Second largest value given the argmax index (for the top-2 gap).
-__device__ __forceinline__ float warp_second(const float* p, int E, int lane, int am) {
-  float s = -1.f;
-#pragma unroll
-  for (int i = 0; i < kMaxEPL; ++i) {
-    int e = lane + 32 * i;
-    if (e < E && e != am) s = fmaxf(s, p[i]);
-  }
-  return warp_max(s);
-}
-
-// Steps 2-3 for one token, executed by one warp.  L points at the token's E fp32 logits.
-template <typename T>
-__device__ __forceinline__ void gate_token(const float* L, int t, const T* __restrict__ x, const T* __restrict__ Wg,
-                                           const float* __restrict__ u, int d, int E, float tau, float thr, int top1,
-                                           float* __restrict__ probs, int* __restrict__ slot, int* s_cnt, int* s_band,
-                                           int* __restrict__ flags, int lane) {
-  float z[kMaxEPL], p[kMaxEPL];
-  bool bad = false;
-#pragma unroll
-  for (int i = 0; i < kMaxEPL; ++i) {
-    int e = lane + 32 * i;
-    z[i] = -INFINITY;
-    if (e < E) {
-      float Lv = L[e];
-      if (!isfinite(Lv)) bad = true;
-      float zeta = u ? -logf(-logf(u[(long long)t * E + e])) : 0.f;
-      z[i] = (Lv + zeta) / tau;
-    }
-  }
-  if (__any_sync(0xffffffffu, bad)) {
-    if (lane == 0 && atomicOr(&flags[0], kFlagNonFinite) == 0) flags[1] = t;
-  }
-  float mx = -INFINITY;
-#pragma unroll
-  for (int i = 0; i < kMaxEPL; ++i) mx = fmaxf(mx, z[i]);
-  mx = warp_max(mx);
-  float sum = 0.f;
-#pragma unroll
-  for (int i = 0; i < kMaxEPL; ++i) {
-    p[i] = (lane + 32 * i < E) ? expf(z[i] - mx) : 0.f;
-    sum += p[i];
-  }
-  sum = warp_sum(sum);
-  const float inv = 1.0f / sum;
-  bool any_pass = false, near = false;
-  float pmax = -1.f;
-  int am = 0x7fffffff;
-#pragma unroll
-  for (int i = 0; i < kMaxEPL; ++i) {
-    int e = lane + 32 * i;
-    if (e < E) {
-      p[i] = p[i] * inv;
-      if (p[i] > thr) any_pass = true;
-      if (fabsf(p[i] - thr) < kRefine) near = true;
-      if (p[i] > pmax) { pmax = p[i]; am = e; }
-    }
-  }
-  warp_argmax(pmax, am);
-  any_pass = __any_sync(0xffffffffu, any_pass);
-  bool argmax_decided = top1 || !any_pass;
-  near = __any_sync(0xffffffffu, near) && !top1;
-  if (argmax_decided) {
-    float second = warp_second(p, E, lane, am);
-    if (pmax - second < kRefine) near = true;
-  }
-  if (near) {
-    // ---- fp64 refinement: recompute logits, noise and softmax exactly from the inputs
-    double z64[kMaxEPL];
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      int e = lane + 32 * i;
-      z64[i] = -INFINITY;
-      if (e < E) {
-        double acc = 0.0;
-        const T* xr = x + (long long)t * d;
-        for (int k = 0; k < d; ++k) acc = fma((double)to_f32(xr[k]), (double)to_f32(Wg[(long long)k * E + e]), acc);
-        double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
-        z64[i] = (acc + zeta) / (double)tau;
-      }
-    }
-    double mx64 = -INFINITY;
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) mx64 = fmax(mx64, z64[i]);
-    mx64 = warp_maxd(mx64);
-    double s64 = 0.0, p64[kMaxEPL];
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      p64[i] = (lane + 32 * i < E) ? exp(z64[i] - mx64) : 0.0;
-      s64 += p64[i];
-    }
-    s64 = warp_sum(s64);
-    double best = -1.0;
-    int bi = 0x7fffffff;
-    any_pass = false;
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      int e = lane + 32 * i;
-      if (e < E) {
-        p64[i] /= s64;
-        p[i] = (float)p64[i];
-        if (p[i] > thr) any_pass = true;
-        if (p64[i] > best) { best = p64[i]; bi = e; }
-      }
-    }
-    warp_argmax(best, bi);
-    am = bi;
-    pmax = (float)best;
-    any_pass = __any_sync(0xffffffffu, any_pass);
-    argmax_decided = top1 || !any_pass;
-  }
-  // ---- decision + band
-  bool in_band = false;
-  if (!argmax_decided) {
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i)
-      if (lane + 32 * i < E && fabsf(p[i] - thr) < kBand) in_band = true;
-    in_band = __any_sync(0xffffffffu, in_band);
-  } else {
-    float second = warp_second(p, E, lane, am);
-    in_band = (pmax - second) < kBand;
-  }
-#pragma unroll
-  for (int i = 0; i < kMaxEPL; ++i) {
-    int e = lane + 32 * i;
-    if (e < E) {
-      bool sel = argmax_decided ? (e == am) : (p[i] > thr);
-      probs[(long long)t * E + e] = p[i];
-      slot[(long long)t * E + e] = sel ? 0 : -1;
-      if (sel) atomicAdd(&s_cnt[e], 1);
-    }
-  }
-  if (lane == 0 && in_band) atomicAdd(s_band, 1);
-}
 
 // Fused gate: one CTA per kGateBT (128) tokens, 256 threads.
 //   Step 1 on CUDA cores: thread = TPT tokens x 4 experts; K in chunks of KC = 32 staged in
@@ -416,6 +251,7 @@ cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const f
   if ((e = cudaMemsetAsync(counts, 0, sizeof(int) * c->E, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(near_band, 0, sizeof(int), s)) != cudaSuccess) return e;
   if (c->T == 0) return cudaSuccess;
+  if (gate_tc_supported(c)) return gate_tc_forward(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
   if (c->dtype == 1) return launch_gate_typed<bf16>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
   return launch_gate_typed<float>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
 }
@@ -429,6 +265,7 @@ cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t
                                                         dlogits), count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (gate_tc_supported(c)) return gate_tc_dwg(c, x, dlogits, dWg, s);
   // dWg [d, E] = x^T [d, T] . dlogits [T, E]  (split-K, deterministic reduction)
   SimtGemm g{};
   g.A = x; g.sAm = 1; g.sAk = c->d;
@@ -442,6 +279,117 @@ cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t
     long long n = (long long)c->d * c->E;
     reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->part, c->dwg_splits, n, dWg), count_launch();
   }
+  return cudaGetLastError();
+}
+
+// Steps 2-3 from precomputed fp32 logits, thread per token (kGateBT tokens per block):
+// coalesced smem staging of the logits / noise blocks, Gumbel + tau-softmax + decision in one
+// thread, coalesced probs / slot writes, per-block expert counts.  Tokens within kRefine of a
+// decision boundary are queued for the fp64 gate_token_refine pass (which also counts them).
+__global__ void __launch_bounds__(kGateBT) gate_softmax_tpt_kernel(
+    const float* __restrict__ logits, const float* __restrict__ u, int T_, int E, float tau, float thr, int top1,
+    float* __restrict__ probs, int* __restrict__ slot, int* __restrict__ counts, int* __restrict__ blk_cnt,
+    int* __restrict__ near_band, int* __restrict__ flags, int* __restrict__ rq_count, int* __restrict__ rq_list) {
+  extern __shared__ float tsm[];
+  __shared__ int s_cnt[128];
+  __shared__ int s_band;
+  __shared__ unsigned s_bits[kGateBT][4];
+  const int LP = E + 1;
+  float* ls = tsm;                    // [kGateBT][E+1]
+  float* us = tsm + kGateBT * LP;     // [kGateBT][E+1]
+  const int tid = threadIdx.x;
+  const int t0 = blockIdx.x * kGateBT;
+  const int ntok = min(kGateBT, T_ - t0);
+  for (int i = tid; i < E; i += kGateBT) s_cnt[i] = 0;
+  if (tid == 0) s_band = 0;
+  for (int i = tid; i < ntok * E; i += kGateBT) {
+    ls[(i / E) * LP + (i % E)] = logits[(long long)t0 * E + i];
+    us[(i / E) * LP + (i % E)] = u ? u[(long long)t0 * E + i] : 0.5f;
+  }
+  __syncthreads();
+  if (tid < ntok) {
+    const int t = t0 + tid;
+    float* L = ls + tid * LP;
+    const float* uu = us + tid * LP;
+    float mx = -INFINITY;
+    bool bad = false;
+    for (int e = 0; e < E; ++e) {
+      const float Lv = L[e];
+      if (!isfinite(Lv)) bad = true;
+      const float zeta = u ? -logf(-logf(uu[e])) : 0.f;
+      const float z = (Lv + zeta) / tau;
+      L[e] = z;
+      mx = fmaxf(mx, z);
+    }
+    if (bad && atomicOr(&flags[0], kFlagNonFinite) == 0) flags[1] = t;
+    float sum = 0.f;
+    for (int e = 0; e < E; ++e) {
+      const float ex = expf(L[e] - mx);
+      L[e] = ex;
+      sum += ex;
+    }
+    const float inv = 1.0f / sum;
+    bool any_pass = false, near = false;
+    float best = -1.f, second = -1.f;
+    int am = 0;
+    for (int e = 0; e < E; ++e) {
+      const float pe = L[e] * inv;
+      L[e] = pe;
+      if (pe > thr) any_pass = true;
+      if (fabsf(pe - thr) < kRefine) near = true;
+      if (pe > best) { second = best; best = pe; am = e; }
+      else if (pe > second) second = pe;
+    }
+    const bool argmax_decided = top1 || !any_pass;
+    if (top1) near = false;
+    if (argmax_decided && best - second < kRefine) near = true;
+    unsigned b0 = 0u, b1 = 0u, b2 = 0u, b3 = 0u;
+    if (near) {
+      rq_list[atomicAdd(rq_count, 1)] = t;      // decided (and counted) by gate_refine_kernel
+    } else {
+      bool in_band = false;
+      for (int e = 0; e < E; ++e) {
+        const bool sel = argmax_decided ? (e == am) : (L[e] > thr);
+        if (sel) {
+          const unsigned bit = 1u << (e & 31);
+          if (e < 32) b0 |= bit; else if (e < 64) b1 |= bit; else if (e < 96) b2 |= bit; else b3 |= bit;
+          atomicAdd(&s_cnt[e], 1);
+        }
+        if (!argmax_decided && fabsf(L[e] - thr) < kBand) in_band = true;
+      }
+      if (argmax_decided) in_band = (best - second) < kBand;
+      if (in_band) atomicAdd(&s_band, 1);
+    }
+    s_bits[tid][0] = b0; s_bits[tid][1] = b1; s_bits[tid][2] = b2; s_bits[tid][3] = b3;
+  }
+  __syncthreads();
+  for (int i = tid; i < ntok * E; i += kGateBT) {
+    const int r = i / E, e = i % E;
+    probs[(long long)t0 * E + i] = ls[r * LP + e];
+    slot[(long long)t0 * E + i] = ((s_bits[r][e >> 5] >> (e & 31)) & 1u) ? 0 : -1;
+  }
+  for (int e = tid; e < E; e += kGateBT) {
+    const int c = s_cnt[e];
+    blk_cnt[(long long)e * gridDim.x + blockIdx.x] = c;
+    if (c) atomicAdd(&counts[e], c);
+  }
+  if (tid == 0 && s_band) atomicAdd(near_band, s_band);
+}
+
+cudaError_t launch_gate_softmax_tpt(const moe_ctx* c, const float* logits, const float* u, float tau, float thr,
+                                    int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
+                                    cudaStream_t s) {
+  const size_t smem = sizeof(float) * 2 * kGateBT * (c->E + 1);
+  cudaError_t e = cudaFuncSetAttribute(gate_softmax_tpt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  gate_softmax_tpt_kernel<<<c->nblk, kGateBT, smem, s>>>(logits, u, c->T, c->E, tau, thr, top1, probs, slot, counts,
+                                                         c->blk_cnt, near_band, c->flags, c->rq, c->rq + 1),
+      count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_splits(const float* part, int splits, long long n, float* out, cudaStream_t s) {
+  reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, splits, n, out), count_launch();
   return cudaGetLastError();
 }
 

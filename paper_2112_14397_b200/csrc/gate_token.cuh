@@ -1,0 +1,290 @@
+// gate_token.cuh -- steps 2-3 of the DTS gate for one token, executed by one warp
+// (lanes = experts): Gumbel noise, tau-softmax, threshold / guard / top-1 decision, fp64
+// refinement of near-boundary tokens, band count.  Shared by the SIMT and tcgen05 gates.
+#pragma once
+#include "common.cuh"
+
+namespace moe {
+namespace {
+
+constexpr float kRefine = 5e-5f;
+constexpr float kBand = 1e-6f;
+constexpr int kMaxEPL = 4;          // experts per lane (E <= 128)
+
+__device__ __forceinline__ void warp_argmax(float& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+  }
+}
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+  }
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_maxd(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Second largest value given the argmax index (for the top-2 gap).
+__device__ __forceinline__ float warp_second(const float* p, int E, int lane, int am) {
+  float s = -1.f;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    if (e < E && e != am) s = fmaxf(s, p[i]);
+  }
+  return warp_max(s);
+}
+
+// Steps 2-3 for one token, executed by one warp.  L points at the token's E fp32 logits.
+template <typename T>
+__device__ __forceinline__ void gate_token(const float* L, int t, const T* __restrict__ x, const T* __restrict__ Wg,
+                                           const float* __restrict__ u, int d, int E, float tau, float thr, int top1,
+                                           float* __restrict__ probs, int* __restrict__ slot, int* s_cnt, int* s_band,
+                                           int* __restrict__ flags, int lane) {
+  float z[kMaxEPL], p[kMaxEPL];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    z[i] = -INFINITY;
+    if (e < E) {
+      float Lv = L[e];
+      if (!isfinite(Lv)) bad = true;
+      float zeta = u ? -logf(-logf(u[(long long)t * E + e])) : 0.f;
+      z[i] = (Lv + zeta) / tau;
+    }
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    if (lane == 0 && atomicOr(&flags[0], kFlagNonFinite) == 0) flags[1] = t;
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) mx = fmaxf(mx, z[i]);
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    p[i] = (lane + 32 * i < E) ? expf(z[i] - mx) : 0.f;
+    sum += p[i];
+  }
+  sum = warp_sum(sum);
+  const float inv = 1.0f / sum;
+  bool any_pass = false, near = false;
+  float pmax = -1.f;
+  int am = 0x7fffffff;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    if (e < E) {
+      p[i] = p[i] * inv;
+      if (p[i] > thr) any_pass = true;
+      if (fabsf(p[i] - thr) < kRefine) near = true;
+      if (p[i] > pmax) { pmax = p[i]; am = e; }
+    }
+  }
+  warp_argmax(pmax, am);
+  any_pass = __any_sync(0xffffffffu, any_pass);
+  bool argmax_decided = top1 || !any_pass;
+  near = __any_sync(0xffffffffu, near) && !top1;
+  if (argmax_decided) {
+    float second = warp_second(p, E, lane, am);
+    if (pmax - second < kRefine) near = true;
+  }
+  if (near) {
+    // ---- fp64 refinement: recompute logits, noise and softmax exactly from the inputs
+    double z64[kMaxEPL];
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      int e = lane + 32 * i;
+      z64[i] = -INFINITY;
+      if (e < E) {
+        double acc = 0.0;
+        const T* xr = x + (long long)t * d;
+        for (int k = 0; k < d; ++k) acc = fma((double)to_f32(xr[k]), (double)to_f32(Wg[(long long)k * E + e]), acc);
+        double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
+        z64[i] = (acc + zeta) / (double)tau;
+      }
+    }
+    double mx64 = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) mx64 = fmax(mx64, z64[i]);
+    mx64 = warp_maxd(mx64);
+    double s64 = 0.0, p64[kMaxEPL];
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      p64[i] = (lane + 32 * i < E) ? exp(z64[i] - mx64) : 0.0;
+      s64 += p64[i];
+    }
+    s64 = warp_sum(s64);
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    any_pass = false;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      int e = lane + 32 * i;
+      if (e < E) {
+        p64[i] /= s64;
+        p[i] = (float)p64[i];
+        if (p[i] > thr) any_pass = true;
+        if (p64[i] > best) { best = p64[i]; bi = e; }
+      }
+    }
+    warp_argmax(best, bi);
+    am = bi;
+    pmax = (float)best;
+    any_pass = __any_sync(0xffffffffu, any_pass);
+    argmax_decided = top1 || !any_pass;
+  }
+  // ---- decision + band
+  bool in_band = false;
+  if (!argmax_decided) {
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i)
+      if (lane + 32 * i < E && fabsf(p[i] - thr) < kBand) in_band = true;
+    in_band = __any_sync(0xffffffffu, in_band);
+  } else {
+    float second = warp_second(p, E, lane, am);
+    in_band = (pmax - second) < kBand;
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    if (e < E) {
+      bool sel = argmax_decided ? (e == am) : (p[i] > thr);
+      probs[(long long)t * E + e] = p[i];
+      slot[(long long)t * E + e] = sel ? 0 : -1;
+      if (sel) atomicAdd(&s_cnt[e], 1);
+    }
+  }
+  if (lane == 0 && in_band) atomicAdd(s_band, 1);
+}
+
+
+
+// fp64 decision for one token deferred by the thread-per-token fast path (near the
+// threshold or an argmax tie), computed by a whole 256-thread block: warp w accumulates the
+// fp64 logits over K range w of 8 (lanes = experts, 8 independent loads in flight per lane),
+// partials are added in fixed order, then warp 0 applies noise / softmax / decision in fp64,
+// writes probs / slot and counts with global integer atomics.
+template <typename T>
+__device__ __forceinline__ void gate_token_refine_block(int t, const T* __restrict__ x, const T* __restrict__ Wg,
+                                                        const float* __restrict__ u, int d, int E, float tau,
+                                                        float thr, int top1, float* __restrict__ probs,
+                                                        int* __restrict__ slot, int* __restrict__ counts,
+                                                        int* __restrict__ blk_cnt, int nblk, int blk_tokens,
+                                                        int* __restrict__ near_band, double* s_part /*[8][128]*/) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kr = (d + 7) / 8;
+  const int k0 = warp * kr, k1 = min(d, k0 + kr);
+  const T* xr = x + (long long)t * d;
+#pragma unroll
+  for (int i = 0; i < kMaxEPL; ++i) {
+    const int e = lane + 32 * i;
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+    if (e < E) {
+      int k = k0;
+      for (; k + 7 < k1; k += 8) {
+        float w[8], xv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          w[j] = to_f32(Wg[(long long)(k + j) * E + e]);
+          xv[j] = to_f32(xr[k + j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = fma((double)xv[j], (double)w[j], acc[j]);
+      }
+      for (; k < k1; ++k) acc[0] = fma((double)to_f32(xr[k]), (double)to_f32(Wg[(long long)k * E + e]), acc[0]);
+    }
+    s_part[warp * 128 + (lane + 32 * i)] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double z64[kMaxEPL];
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      const int e = lane + 32 * i;
+      z64[i] = -INFINITY;
+      if (e < E) {
+        double acc = 0.0;
+        for (int w = 0; w < 8; ++w) acc += s_part[w * 128 + e];
+        const double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
+        z64[i] = (acc + zeta) / (double)tau;
+      }
+    }
+    double mx64 = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) mx64 = fmax(mx64, z64[i]);
+    mx64 = warp_maxd(mx64);
+    double s64 = 0.0, p64[kMaxEPL];
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      p64[i] = (lane + 32 * i < E) ? exp(z64[i] - mx64) : 0.0;
+      s64 += p64[i];
+    }
+    s64 = warp_sum(s64);
+    float p[kMaxEPL];
+    double best = -1.0;
+    int am = 0x7fffffff;
+    bool any_pass = false;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      const int e = lane + 32 * i;
+      p[i] = 0.f;
+      if (e < E) {
+        p64[i] /= s64;
+        p[i] = (float)p64[i];
+        if (p[i] > thr) any_pass = true;
+        if (p64[i] > best) { best = p64[i]; am = e; }
+      }
+    }
+    warp_argmax(best, am);
+    any_pass = __any_sync(0xffffffffu, any_pass);
+    const bool argmax_decided = top1 || !any_pass;
+    const float pmax = (float)best;
+    bool in_band = false;
+    if (!argmax_decided) {
+#pragma unroll
+      for (int i = 0; i < kMaxEPL; ++i)
+        if (lane + 32 * i < E && fabsf(p[i] - thr) < kBand) in_band = true;
+      in_band = __any_sync(0xffffffffu, in_band);
+    } else {
+      const float second = warp_second(p, E, lane, am);
+      in_band = (pmax - second) < kBand;
+    }
+    const int blk = t / blk_tokens;
+#pragma unroll
+    for (int i = 0; i < kMaxEPL; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E) {
+        const bool sel = argmax_decided ? (e == am) : (p[i] > thr);
+        probs[(long long)t * E + e] = p[i];
+        slot[(long long)t * E + e] = sel ? 0 : -1;
+        if (sel) {
+          atomicAdd(&counts[e], 1);
+          atomicAdd(&blk_cnt[(long long)e * nblk + blk], 1);
+        }
+      }
+    }
+    if (lane == 0 && in_band) atomicAdd(near_band, 1);
+  }
+  __syncthreads();
+}
+
+}  // namespace
+}  // namespace moe

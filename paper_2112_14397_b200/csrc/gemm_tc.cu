@@ -495,6 +495,25 @@ bool tc_available() { return encode_fn() != nullptr; }
 // Upper bound on ROWS pair-tiles: every expert may add one half-used pair.
 static long long rows_pairs_upper(int64_t R_cap, int El) { return R_cap / 256 + El; }
 
+// ---------------------------------------------------------------- dense helper (gate backward)
+// out [rows, N] bf16 = A [rows, K] . B [N, K]^T, both K-major bf16, one row segment
+// (offsets_dev = {0, rows_pad}, rows_pad = rows rounded up to 128).  Used for dL W_g^T.
+cudaError_t tc_dense_store(const moe_ctx* c, const void* A, long long rows, int K, const void* B, int N, void* out,
+                           const int* offsets_dev, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  const long long rows_pad = (rows + BM - 1) / BM * BM;
+  CUtensorMap mA, mB, mO;
+  if (!make_map(&mA, A, rows, K, K, 64, BM) || !make_map(&mB, B, N, K, K, 64, BNH) ||
+      !make_store_map(&mO, out, rows, N))
+    return cudaErrorInvalidValue;
+  TcParams p{};
+  p.G = 1; p.offsets = offsets_dev; p.rows_cap = (int)rows_pad;
+  p.N = N; p.K = K; p.b_group_rows = 0;
+  p.o1 = reinterpret_cast<bf16*>(out); p.ldo_b = N;
+  return launch_tc<TEPI_STORE, false, false, false>(mA, mB, mO, mO, mO, p,
+                                                    (rows_pad / 256 + 1) * ((N + BN - 1) / BN), c->sm_count, s);
+}
+
 // ---------------------------------------------------------------- step 5 / B5 on tensor cores
 cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
                           const void* W1, const void* b1, const void* W2, const void* b2, void* gp, void* h,

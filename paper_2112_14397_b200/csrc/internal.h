@@ -12,7 +12,8 @@ struct moe_ctx {
   void* comm;          // borrowed ncclComm_t (world > 1)
   int sm_count;
   int nblk;            // gate/dispatch token blocks = ceil(T / kGateBT)
-  int dwg_splits;      // split-K factor for dW_g
+  int dwg_splits;      // split-K factor for dW_g (SIMT path)
+  int dwg_splits_max;  // capacity of `part` in splits (tcgen05 path)
   int use_tc;          // bf16 expert GEMMs on tcgen05 (1) or CUDA cores (0, MOE_GEMM=simt debug)
   // workspace (caller owned)
   uint8_t* ws;
@@ -26,6 +27,9 @@ struct moe_ctx {
   float* colsum;       // [E] balance-loss column sums
   int* tot;            // [E] per-expert totals written by the dispatch scan
   float* colpart;      // [E_local, kColsumSplits, max(d, f)] bias-gradient partials
+  int* rq;             // [1 + T] fp64-refine queue of the tcgen05 gate (count, tokens)
+  int* tok_off;        // [2] = {0, roundup(T, 128)}: the token range as one row segment
+  void* gate_scratch;  // tcgen05 gate operands: W_g^T / [W_g|W_g] (bf16) and the hi|lo split of dL
   int* ep_counts;      // [world, E] gathered counts (EP)
   int* ep_off;         // [E_local + 1] recv-layout offsets (EP)
   int* ep_tot;         // [E_local] recv-layout rows per local expert (EP)
@@ -94,6 +98,20 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
 cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                               const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
                               const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, cudaStream_t s);
+
+// ---------------------------------------------------------------- tcgen05 gate contractions (bf16)
+bool gate_tc_supported(const moe_ctx* c);
+cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, const float* u, float tau, float thr,
+                            int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
+                            cudaStream_t s);
+cudaError_t gate_tc_dx(const moe_ctx* c, const float* dlogits, const void* Wg, void* dxg_bf16, cudaStream_t s);
+cudaError_t gate_tc_dwg(const moe_ctx* c, const void* x, const float* dlogits, float* dWg, cudaStream_t s);
+cudaError_t tc_dense_store(const moe_ctx* c, const void* A, long long rows, int K, const void* B, int N, void* out,
+                           const int* offsets_dev, cudaStream_t s);
+cudaError_t launch_gate_softmax_tpt(const moe_ctx* c, const float* logits, const float* u, float tau, float thr,
+                                    int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
+                                    cudaStream_t s);
+cudaError_t launch_reduce_splits(const float* part, int splits, long long n, float* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- SIMT grouped GEMM
 enum SimtEpi { EPI_F32 = 0, EPI_T = 1, EPI_BIAS_T = 2, EPI_BIAS_GELU = 3, EPI_GELU_BWD = 4 };

@@ -64,7 +64,7 @@ namespace moe {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carve {
-  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, total;
+  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, total;
 };
 
 static Carve carve(const moe_ctx* c) {
@@ -79,7 +79,8 @@ static Carve carve(const moe_ctx* c) {
   k.blk_cnt = take(sizeof(int) * (size_t)c->nblk * c->E);
   k.blk_base = take(sizeof(int) * (size_t)c->nblk * c->E);
   k.logits = take(sizeof(float) * (size_t)c->T * c->E);
-  k.part = take(sizeof(float) * (size_t)c->dwg_splits * c->d * c->E);
+  k.part = take(sizeof(float) * (size_t)(c->dwg_splits > c->dwg_splits_max ? c->dwg_splits : c->dwg_splits_max) *
+                c->d * c->E);
   k.dxg = take(sizeof(float) * (size_t)c->T * c->d);
   k.colsum = take(sizeof(float) * (size_t)c->E);
   k.tot = take(sizeof(int) * (size_t)c->E);
@@ -87,6 +88,13 @@ static Carve carve(const moe_ctx* c) {
   k.ep_counts = take(sizeof(int) * (size_t)c->world * c->E);
   k.ep_off = take(sizeof(int) * (size_t)(c->E_local + 1));
   k.ep_tot = take(sizeof(int) * (size_t)c->E_local);
+  {
+    const size_t Ep = (c->E + 15) / 16 * 16, Kp = (2 * Ep + 63) / 64 * 64;
+    const size_t a = Ep * c->d, b = Kp * (c->d + (size_t)c->T);
+    k.gate_scratch = take(2 * (a > b ? a : b));
+  }
+  k.rq = take(sizeof(int) * ((size_t)c->T + 1));
+  k.tok_off = take(sizeof(int) * 2);
   k.total = o;
   return k;
 }
@@ -107,6 +115,9 @@ void carve_workspace(moe_ctx* c) {
   c->ep_counts = reinterpret_cast<int*>(c->ws + k.ep_counts);
   c->ep_off = reinterpret_cast<int*>(c->ws + k.ep_off);
   c->ep_tot = reinterpret_cast<int*>(c->ws + k.ep_tot);
+  c->gate_scratch = c->ws + k.gate_scratch;
+  c->rq = reinterpret_cast<int*>(c->ws + k.rq);
+  c->tok_off = reinterpret_cast<int*>(c->ws + k.tok_off);
 }
 
 }  // namespace moe
@@ -143,6 +154,7 @@ int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype, vo
   c->sm_count = sms > 0 ? sms : 148;
   c->nblk = (T + moe::kGateBT - 1) / moe::kGateBT;
   c->dwg_splits = T >= 4096 ? 32 : 1;
+  c->dwg_splits_max = 64;
   {
     const char* g = getenv("MOE_GEMM");
     c->use_tc = (dtype == MOE_BF16) && !(g && strcmp(g, "simt") == 0);
@@ -170,7 +182,10 @@ int moe_set_workspace(moe_ctx* ctx, void* dev_ptr, size_t bytes) {
   ctx->ws = reinterpret_cast<uint8_t*>(dev_ptr);
   ctx->ws_bytes = bytes;
   moe::carve_workspace(ctx);
-  return cuda_status(cudaMemset(ctx->flags, 0, 16 * sizeof(int)), "moe_set_workspace");
+  const int tok_off[2] = {0, (ctx->T + moe::kRowAlign - 1) / moe::kRowAlign * moe::kRowAlign};
+  cudaError_t e = cudaMemcpy(ctx->tok_off, tok_off, sizeof(tok_off), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(ctx->flags, 0, 16 * sizeof(int));
+  return cuda_status(e, "moe_set_workspace");
 }
 
 int moe_check(moe_ctx* ctx, void* stream) {

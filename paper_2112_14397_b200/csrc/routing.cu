@@ -142,10 +142,10 @@ __global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
 // One warp per token.  The token's selected rows are found with ballots over its slot row
 // (ascending expert order is the bit order), so the work is O(selected), not O(E).
 // Columns are processed 4 x 16-byte vectors per lane at a time (independent loads in flight).
-template <typename T, bool WEIGHTED>
+template <typename T, bool WEIGHTED, typename TX = float>
 __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src, const float* __restrict__ row_gate,
                                                  const int* __restrict__ slot_row, int d, int E,
-                                                 const float* __restrict__ extra, T* __restrict__ out, int lane) {
+                                                 const TX* __restrict__ extra, T* __restrict__ out, int lane) {
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
   for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
@@ -186,7 +186,7 @@ __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src,
       if (v < nvec) {
         if (extra) {
 #pragma unroll
-          for (int k = 0; k < V; ++k) acc[q][k] += extra[(long long)v * V + k];
+          for (int k = 0; k < V; ++k) acc[q][k] += to_f32(extra[(long long)v * V + k]);
         }
         st_v4(out + (long long)v * V, pack16(acc[q], T()));
       }
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ e_ou
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  gather_sum_token<T, true>(e_out, row_gate, slot + (long long)t * E, d, E, nullptr, y + (long long)t * d, lane);
+  gather_sum_token<T, true, float>(e_out, row_gate, slot + (long long)t * E, d, E, nullptr, y + (long long)t * d, lane);
 }
 
 // ------------------------------------------------------------------ combine backward
@@ -246,15 +246,15 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
 
 // ------------------------------------------------------------------ dispatch backward
 // One warp per token: dx[t] = sum_{e asc} dx_perm[slot[t,e]] + dxg[t] (fp32, may be NULL).
-template <typename T>
+template <typename T, typename TX>
 __global__ void __launch_bounds__(256) dispatch_bwd_kernel(const T* __restrict__ dx_perm, const int* __restrict__ slot,
-                                                           const float* __restrict__ dxg, int T_, int d, int E,
+                                                           const TX* __restrict__ dxg, int T_, int d, int E,
                                                            T* __restrict__ dx) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  gather_sum_token<T, false>(dx_perm, nullptr, slot + (long long)t * E, d, E, dxg ? dxg + (long long)t * d : nullptr,
-                             dx + (long long)t * d, lane);
+  gather_sum_token<T, false, TX>(dx_perm, nullptr, slot + (long long)t * E, d, E,
+                                 dxg ? dxg + (long long)t * d : nullptr, dx + (long long)t * d, lane);
 }
 
 // ------------------------------------------------------------------ spawn (step 6b)
@@ -381,6 +381,15 @@ cudaError_t launch_combine_bwd(const moe_ctx* c, const void* dy, const void* e_o
 cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot, const float* dlogits,
                                 const void* Wg, void* dx, cudaStream_t s) {
   if (c->T == 0) return cudaSuccess;
+  const unsigned grid = (c->T + 7) / 8;
+  if (dlogits && gate_tc_supported(c)) {
+    // gate term dlogits W_g^T on tensor cores (bf16, hi|lo split of dlogits) -> added by the gather pass
+    cudaError_t e = gate_tc_dx(c, dlogits, Wg, c->dxg, s);
+    if (e != cudaSuccess) return e;
+    dispatch_bwd_kernel<bf16, bf16><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, (const bf16*)c->dxg, c->T,
+                                                         c->d, c->E, (bf16*)dx), count_launch();
+    return cudaGetLastError();
+  }
   const float* dxg = nullptr;
   if (dlogits) {
     // dxg [T, d] fp32 = dlogits [T, E] . Wg^T  (Wg [d, E] -> B(k=e, n=dd) = Wg[dd*E + e])
@@ -393,11 +402,12 @@ cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int
     if (e != cudaSuccess) return e;
     dxg = c->dxg;
   }
-  const unsigned grid = (c->T + 7) / 8;
   if (c->dtype == 1)
-    dispatch_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, dxg, c->T, c->d, c->E, (bf16*)dx), count_launch();
+    dispatch_bwd_kernel<bf16, float><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, dxg, c->T, c->d, c->E,
+                                                          (bf16*)dx), count_launch();
   else
-    dispatch_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dx_perm, slot, dxg, c->T, c->d, c->E, (float*)dx), count_launch();
+    dispatch_bwd_kernel<float, float><<<grid, 256, 0, s>>>((const float*)dx_perm, slot, dxg, c->T, c->d, c->E,
+                                                           (float*)dx), count_launch();
   return cudaGetLastError();
 }
 
