@@ -48,11 +48,10 @@ cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const vo
   const int d = c->d, f = c->f, El = c->E_local, dt = c->dtype;
   cudaError_t e;
   if (c->use_tc) {
-    if ((e = tc_expert_ffn_bwd(c, d_eout, x_perm, gp, h, offsets, R_cap, W1, W2, da, dx_perm, dW1, dW2, s)) !=
+    if ((e = tc_expert_ffn_bwd(c, d_eout, x_perm, gp, h, offsets, R_cap, W1, W2, da, dx_perm, dW1, dW2, db1, s)) !=
         cudaSuccess)
       return e;
-    if ((e = launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, c->colpart, s)) != cudaSuccess) return e;
-    return launch_colsum_grouped(da, dt, f, offsets, El, db1, c->colpart, s);
+    return launch_colsum_grouped(d_eout, dt, d, offsets, El, db2, c->colpart, s);
   }
   // dgrad2 + GELU': da = (d_eout W2_e) (.) GELU'(a)      (da may alias a)
   SimtGemm g = base_rows(offsets, El, R_cap);

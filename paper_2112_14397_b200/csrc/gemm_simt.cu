@@ -213,6 +213,30 @@ cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int ep
   return launch_typed<float, bf16, float>(g, EPI_F32, s);
 }
 
+__global__ void db1_reduce_kernel(const float* __restrict__ part, int N, const int* __restrict__ m_off,
+                                  float* __restrict__ out) {
+  const int g = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int rb0 = m_off[g] >> 5, rb1 = m_off[g + 1] >> 5;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  int rb = rb0;
+  for (; rb + 3 < rb1; rb += 4) {
+    a0 += part[(long long)rb * N + n];
+    a1 += part[(long long)(rb + 1) * N + n];
+    a2 += part[(long long)(rb + 2) * N + n];
+    a3 += part[(long long)(rb + 3) * N + n];
+  }
+  for (; rb < rb1; ++rb) a0 += part[(long long)rb * N + n];
+  out[(long long)g * N + n] = (a0 + a1) + (a2 + a3);
+}
+
+cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, cudaStream_t s) {
+  if (G == 0 || N == 0) return cudaSuccess;
+  db1_reduce_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, m_off, out), count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_off, int G, float* out,
                                   float* part, cudaStream_t s) {
   if (G == 0 || N == 0) return cudaSuccess;

@@ -79,6 +79,7 @@ struct TcParams {
   bf16* o1;               // bf16 outputs (ROWS), pitch ldo_b -- used by the LSU store variant
   bf16* o2;
   long long ldo_b;
+  float* colpart;         // TEPI_GELU_BWD: per-32-row column sums of da [R_cap/32][N] (bias gradient db1)
 };
 
 struct Tile {
@@ -382,6 +383,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         tc::fence_proxy_async();
         __syncwarp();
+        if (EPI == TEPI_GELU_BWD && p.colpart && store) {
+          // db1 partial: lane j sums column j of this warp's 32 x 32 bf16 da sub-tile (fixed row order)
+          float cs = 0.f;
+#pragma unroll 8
+          for (int r = 0; r < 32; ++r) {
+            const uint32_t addr = buf + r * 64 + ((((uint32_t)lane >> 3) ^ ((r >> 1) & 3)) << 4) + (lane & 7) * 2;
+            unsigned short hv;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hv) : "r"(addr));
+            cs += __uint_as_float((uint32_t)hv << 16);
+          }
+          p.colpart[(long long)((tl.m_own + sub * 32) >> 5) * p.N + n + lane] = cs;
+        }
 #ifdef MOE_EXP_STG
         if (store) {   // coalesced LSU stores from the swizzled smem sub-tile: 8 rows x 64 B per instruction
           const int row0 = tl.m_own + sub * 32;
@@ -547,11 +560,13 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
 
 cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                               const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
-                              const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, cudaStream_t s) {
+                              const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, float* db1,
+                              cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local;
   CUtensorMap mA, mB, mO, mX;
   cudaError_t e;
   if (R_cap == 0) {   // no rows at all: every expert gradient is zero
+    if ((e = cudaMemsetAsync(db1, 0, sizeof(float) * El * f, s)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(dW1, 0, sizeof(float) * El * f * d, s)) != cudaSuccess) return e;
     return cudaMemsetAsync(dW2, 0, sizeof(float) * El * d * f, s);
   }
@@ -565,9 +580,19 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
       return cudaErrorInvalidValue;
     p.N = f; p.K = d; p.b_group_rows = d;
     p.o1 = reinterpret_cast<bf16*>(da); p.ldo_b = f;
+    // db1 partials live in dx_perm's memory until dgrad1 overwrites it ([R_cap/32][f] fp32 <= R_cap x d bf16)
+    const bool fuse_db1 = db1 && (long long)f * 4 <= (long long)d * 2 * 32;
+    p.colpart = fuse_db1 ? reinterpret_cast<float*>(dx_perm) : nullptr;
     e = launch_tc<TEPI_GELU_BWD, false, true, false>(mA, mB, mO, mO, mX, p, up * ((f + BN - 1) / BN),
                                                      c->sm_count, s);
     if (e != cudaSuccess) return e;
+    if (fuse_db1) {
+      if ((e = launch_db1_reduce(reinterpret_cast<const float*>(dx_perm), f, offsets, El, db1, s)) != cudaSuccess)
+        return e;
+    } else if (db1) {
+      if ((e = launch_colsum_grouped(da, 1, f, offsets, El, db1, c->colpart, s)) != cudaSuccess) return e;
+    }
+    p.colpart = nullptr;
     // dgrad1: dx_perm = da W1_e                 A = da [R, f] K-major; B(k=f, n=d) = W1 [El*f, d] MN-major
     if (!make_map(&mA, da, R_cap, f, f, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, 64) ||
         !make_store_map(&mO, dx_perm, R_cap, d))

@@ -97,7 +97,10 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
                           void* e_out, cudaStream_t s);
 cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                               const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
-                              const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, cudaStream_t s);
+                              const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, float* db1,
+                              cudaStream_t s);
+// db1[g][n] = sum over the 32-row blocks of group g of part[rb][n]  (fixed order)
+cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 gate contractions (bf16)
 bool gate_tc_supported(const moe_ctx* c);
