@@ -62,7 +62,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -172,14 +172,14 @@ def run_ours(args, rank, world):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731  (usable inside graphs)
 
-    # --- instrumented step: same call sequence as DTSMoELayer.forward/backward, with events
-    # around the expert GEMM calls (on the launching stream).
-    def full_step(timed: bool):
+    # --- one step = the 8 C-ABI calls (DTSMoELayer.forward + backward), with events around the
+    # expert GEMM calls on the launching stream.
+    def full_step(timed: bool, R_cap=None):
         ev_ffn = (ev(), ev())
         ev_bwd = (ev(), ev())
-        layer.forward(x, u, tau, c, events=ev_ffn if timed else None)
+        layer.forward(x, u, tau, c, R_cap=R_cap, events=ev_ffn if timed else None)
         layer.backward(dy, events=ev_bwd if timed else None)
         return ev_ffn, ev_bwd
 
@@ -189,19 +189,46 @@ def run_ours(args, rank, world):
     layer.check()
     R = int(layer.state.offsets[-1].item())
     counts = layer.state.counts.cpu().numpy()
+
+    # --- CUDA graph of the whole step (single GPU): the row capacity is fixed to the routed
+    # rows seen in warm-up (static capacity; an overflow would raise MOE_ECAPACITY at the
+    # check after the timed region), so the step has no host synchronisation and is replayed
+    # as one graph launch.
+    graph = None
     n_launch0 = L.moe_kernel_launch_count()
+    launches = None
+    if args.graph and world == 1:
+        R_static = layer.state.R_cap
+        full_step(False, R_cap=R_static)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        g_ffn, g_bwd = (ev(), ev()), (ev(), ev())
+        n0 = L.moe_kernel_launch_count()
+        with torch.cuda.graph(graph):
+            layer.forward(x, u, tau, c, R_cap=R_static, events=g_ffn)
+            layer.backward(dy, events=g_bwd)
+        launches = L.moe_kernel_launch_count() - n0
+        for _ in range(max(1, args.warmup)):
+            graph.replay()
+        torch.cuda.synchronize()
+        layer.check()
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     barrier(world)
     torch.cuda.synchronize()
+    n_launch1 = L.moe_kernel_launch_count()
     step_ms, ffn_ms, bwd_ms = [], [], []
     t_wall = time.perf_counter()
     for _ in range(args.steps):
         flush.fill_(1)                       # L2 flush outside the timed events
         s0, s1 = ev(), ev()
         s0.record(stream)
-        e_f, e_b = full_step(True)
+        if graph is not None:
+            graph.replay()
+            e_f, e_b = g_ffn, g_bwd
+        else:
+            e_f, e_b = full_step(True)
         s1.record(stream)
         s1.synchronize()
         step_ms.append(s0.elapsed_time(s1))
@@ -211,7 +238,8 @@ def run_ours(args, rank, world):
     barrier(world)
     wall = time.perf_counter() - t_wall
     clk = clocks.stop()
-    launches = (L.moe_kernel_launch_count() - n_launch0) // max(1, args.steps)
+    if launches is None:
+        launches = (L.moe_kernel_launch_count() - n_launch1) // max(1, args.steps)
     layer.check()
 
     ms_step = max_over_ranks(sum(step_ms) / len(step_ms), world)
@@ -227,7 +255,8 @@ def run_ours(args, rank, world):
     step_flops = flops + 6.0 * cfg.T * cfg.d_model * cfg.E
 
     # e2e through the public API with host buffers
-    e2e = run_e2e(args, layer, li, tau, c, world) if args.e2e else None
+    e2e = run_e2e(args, layer, li, tau, c, world, (graph, x, u, dy) if graph is not None else None) \
+        if args.e2e else None
 
     out = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -242,6 +271,7 @@ def run_ours(args, rank, world):
                    "parallelism": f"ep{world} (E/{world} experts per GPU, NCCL all-to-all-v over NVLink)"
                    if world > 1 else "single",
                    "l2": "flushed between steps (256 MiB write, outside the events)",
+                   "launch": "cuda-graph replay, static row capacity" if graph is not None else "eager",
                    "wall_s_timed_region": wall},
         "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -263,39 +293,103 @@ def run_ours(args, rank, world):
     return out
 
 
-def run_e2e(args, layer, li, tau, c, world):
-    """Same metric through the public API, with host (pinned) buffers: every step copies
-    x, u, dy host->device and reads y and dx back device->host."""
+def run_e2e(args, layer, li, tau, c, world, graphed=None):
+    """Same metric through the public API with host (pinned) buffers: every step copies x, u,
+    dy host->device and reads y and dx back device->host.
+
+    Graph mode pipelines the copies with compute: two captured replicas of the step (each with
+    its own device input buffers) alternate; step i+1's H2D runs on a copy stream while step i
+    computes, step i's D2H runs on a third stream.  Every byte of every step is still copied
+    inside the timed region (first H2D start .. last D2H end)."""
     dev = layer.device
     hx, hu, hdy = (t.pin_memory() for t in (li.x, li.u, li.dy))
     hy = torch.empty_like(li.x).pin_memory()
     hdx = torch.empty_like(li.x).pin_memory()
-    stream = torch.cuda.current_stream()
-
-    def step():
-        x = hx.to(dev, non_blocking=True)
-        u = hu.to(dev, non_blocking=True)
-        dy = hdy.to(dev, non_blocking=True)
-        y = layer.forward(x, u, tau, c)
-        g = layer.backward(dy)
-        hy.copy_(y, non_blocking=True)
-        hdx.copy_(g["dx"], non_blocking=True)
-
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize()
-    barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    e1.synchronize()
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+    comp = torch.cuda.current_stream()
     bi = sum(t.numel() * t.element_size() for t in (hx, hu, hdy))
     bo = sum(t.numel() * t.element_size() for t in (hy, hdx))
+
+    if graphed is None:
+        def step():
+            x = hx.to(dev, non_blocking=True)
+            u = hu.to(dev, non_blocking=True)
+            dy = hdy.to(dev, non_blocking=True)
+            y = layer.forward(x, u, tau, c)
+            g = layer.backward(dy)
+            hy.copy_(y, non_blocking=True)
+            hdx.copy_(g["dx"], non_blocking=True)
+
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(comp)
+        for _ in range(args.steps):
+            step()
+        e1.record(comp)
+        e1.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        return {"value": layer.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": False}
+
+    # ---- two graph replicas with their own static inputs, copies overlapped with compute
+    R_static = layer.state.R_cap
+    reps = []
+    for k in range(2):
+        X = torch.empty_like(li.x, device=dev)
+        U = torch.empty_like(li.u, device=dev)
+        DY = torch.empty_like(li.dy, device=dev)
+        X.copy_(hx); U.copy_(hu); DY.copy_(hdy)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            Y = layer.forward(X, U, tau, c, R_cap=R_static)
+            DX = layer.backward(DY)["dx"]
+        reps.append((g, X, U, DY, Y, DX))
+    torch.cuda.synchronize()
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    in_free = [ev(), ev()]     # replica k finished reading its inputs (compute done)
+    h2d_done = [ev(), ev()]
+    comp_done = [ev(), ev()]
+    out_free = [ev(), ev()]    # replica k's outputs copied to the host
+    for k in range(2):
+        in_free[k].record(comp)
+        out_free[k].record(comp)
+
+    def run(n):
+        t0, t1 = ev(), ev()
+        t0.record(s_h2d)
+        for i in range(n):
+            k = i % 2
+            g, X, U, DY, Y, DX = reps[k]
+            with torch.cuda.stream(s_h2d):
+                s_h2d.wait_event(in_free[k])
+                X.copy_(hx, non_blocking=True)
+                U.copy_(hu, non_blocking=True)
+                DY.copy_(hdy, non_blocking=True)
+                h2d_done[k].record(s_h2d)
+            comp.wait_event(h2d_done[k])
+            comp.wait_event(out_free[k])
+            g.replay()
+            comp_done[k].record(comp)
+            in_free[k].record(comp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(comp_done[k])
+                hy.copy_(Y, non_blocking=True)
+                hdx.copy_(DX, non_blocking=True)
+                out_free[k].record(s_d2h)
+        t1.record(s_d2h)
+        t1.synchronize()
+        return t0.elapsed_time(t1)
+
+    run(4)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(run(args.steps) / args.steps, world)
+    layer.check()
     return {"value": layer.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo}
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": True}
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
@@ -324,7 +418,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -332,6 +426,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-tokens", type=int, default=1024)
     ap.add_argument("--ref-tokens", type=int, default=256)
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch the step eagerly instead of replaying a CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

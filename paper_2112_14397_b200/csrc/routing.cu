@@ -63,77 +63,88 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restri
 }
 
 // ------------------------------------------------------------------ permute
-// One CTA per gate block of kGateBT tokens, thread = token for the ranking phase.
+// Rank pass: one CTA per gate block of kGateBT tokens.  Each warp ballots every expert over
+// its 32 tokens (no block barrier per expert); one barrier; then a token's row for expert e is
+//   offsets[e] + blk_base[e][blk] + (selected tokens of e in lower warps) + (lower lanes).
+// Writes slot (row index), row_token, row_gate; zeroes the pad rows of expert blockIdx.x, ...
 template <typename T>
-__global__ void __launch_bounds__(kGateBT) dispatch_permute_kernel(
-    const T* __restrict__ x, const float* __restrict__ probs, int* __restrict__ slot, int T_, int d, int E,
-    const int* __restrict__ blk_base, const int* __restrict__ offsets, const int* __restrict__ tot,
-    T* __restrict__ x_perm, int* __restrict__ row_token, float* __restrict__ row_gate, long long R_cap) {
-  extern __shared__ int s_rows[];              // [kGateBT][E]: each token's selected rows, compacted
-  __shared__ int s_wsum[2][kGateBT / 32];
-  __shared__ int s_n[kGateBT];
-  int nsel = 0;
+__global__ void __launch_bounds__(kGateBT) dispatch_rank_kernel(
+    const float* __restrict__ probs, int* __restrict__ slot, int T_, int d, int E, const int* __restrict__ blk_base,
+    const int* __restrict__ offsets, const int* __restrict__ tot, T* __restrict__ x_perm, int* __restrict__ row_token,
+    float* __restrict__ row_gate, long long R_cap) {
+  __shared__ unsigned s_bal[kGateBT / 32][128];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
   for (int e = 0; e < E; ++e) {
     const bool sel = valid && slot[(long long)t * E + e] >= 0;
     const unsigned bal = __ballot_sync(0xffffffffu, sel);
-    const int pre = __popc(bal & ((1u << lane) - 1u));
-    if (lane == 0) s_wsum[e & 1][warp] = __popc(bal);
-    __syncthreads();
-    int wpre = 0;
-#pragma unroll
-    for (int w = 0; w < kGateBT / 32; ++w) wpre += (w < warp) ? s_wsum[e & 1][w] : 0;
-    int row = -1;
-    if (sel) {
-      row = offsets[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre + pre;
+    if (lane == 0) s_bal[warp][e] = bal;
+  }
+  __syncthreads();
+  if (valid) {
+    const unsigned lower = (1u << lane) - 1u;
+    for (int e = 0; e < E; ++e) {
+      const unsigned mine = s_bal[warp][e];
+      if (!((mine >> lane) & 1u)) continue;
+      int wpre = 0;
+      for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
+      const int row = offsets[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre + __popc(mine & lower);
       if (row < R_cap) {
         slot[(long long)t * E + e] = row;
         row_token[row] = t;
         row_gate[row] = probs[(long long)t * E + e];
       } else {
         slot[(long long)t * E + e] = -1;   // dropped (MOE_ECAPACITY raised by the scan)
-        row = -1;
-      }
-    }
-    if (row >= 0) s_rows[tid * E + nsel++] = row;
-  }
-  s_n[tid] = nsel;
-  __syncthreads();
-  // copy phase: each warp copies whole tokens, x_t read once, written to each selected row
-  constexpr int V = Vec16<T>::N;
-  const int nvec = d / V;
-  for (int i = warp; i < kGateBT; i += kGateBT / 32) {
-    const int tok = blockIdx.x * kGateBT + i;
-    if (tok >= T_) break;
-    const T* src = x + (long long)tok * d;
-    for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
-      uint4 buf[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int v = v0 + q * 32 + lane;
-        if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
-      }
-      const int n = s_n[i];
-      for (int k = 0; k < n; ++k) {
-        const int row = s_rows[i * E + k];
-        T* dst = x_perm + (long long)row * d;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          int v = v0 + q * 32 + lane;
-          if (v < nvec) st_v4(dst + (long long)v * V, buf[q]);
-        }
       }
     }
   }
   // pad rows of experts e = blockIdx.x, blockIdx.x + gridDim.x, ...: zero
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
   for (int e = blockIdx.x; e < E; e += gridDim.x) {
     const long long r0 = (long long)offsets[e] + tot[e], r1 = offsets[e + 1];
     for (long long r = r0 + warp; r < r1 && r < R_cap; r += kGateBT / 32) {
       if (lane == 0) { row_token[r] = -1; row_gate[r] = 0.f; }
       T* dst = x_perm + r * d;
       for (int v = lane; v < nvec; v += 32) st_v4(dst + (long long)v * V, make_uint4(0, 0, 0, 0));
+    }
+  }
+}
+
+// Copy pass: one warp per token; x_t is read once (4 x 16 B per lane in flight) and stored
+// to each of its selected rows (found with ballots over the final slot row).
+template <typename T>
+__global__ void __launch_bounds__(256) dispatch_copy_kernel(const T* __restrict__ x, const int* __restrict__ slot,
+                                                            int T_, int d, int E, T* __restrict__ x_perm) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  const T* src = x + (long long)t * d;
+  const int* srow = slot + (long long)t * E;
+  for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+    uint4 buf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
+    }
+    for (int g = 0; g < E; g += 32) {
+      const int sv = (g + lane < E) ? srow[g + lane] : -1;
+      unsigned bal = __ballot_sync(0xffffffffu, sv >= 0);
+      while (bal) {
+        const int b = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int row = __shfl_sync(0xffffffffu, sv, b);
+        T* dst = x_perm + (long long)row * d;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = v0 + q * 32 + lane;
+          if (v < nvec) st_v4(dst + (long long)v * V, buf[q]);
+        }
+      }
     }
   }
 }
@@ -338,17 +349,17 @@ cudaError_t launch_dispatch(const moe_ctx* c, const void* x, const float* probs,
                                           c->flags), count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || c->nblk == 0) return e;
-  const size_t smem = sizeof(int) * kGateBT * c->E;
   if (c->dtype == 1) {
-    cudaFuncSetAttribute(dispatch_permute_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dispatch_permute_kernel<bf16><<<c->nblk, kGateBT, smem, s>>>((const bf16*)x, probs, slot, c->T, c->d, c->E,
-                                                                 c->blk_base, offsets, c->tot, (bf16*)x_perm,
-                                                                 row_token, row_gate, R_cap), count_launch();
+    dispatch_rank_kernel<bf16><<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->d, c->E, c->blk_base, offsets, c->tot,
+                                                          (bf16*)x_perm, row_token, row_gate, R_cap), count_launch();
+    dispatch_copy_kernel<bf16><<<(c->T + 7) / 8, 256, 0, s>>>((const bf16*)x, slot, c->T, c->d, c->E, (bf16*)x_perm),
+        count_launch();
   } else {
-    cudaFuncSetAttribute(dispatch_permute_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dispatch_permute_kernel<float><<<c->nblk, kGateBT, smem, s>>>((const float*)x, probs, slot, c->T, c->d, c->E,
-                                                                  c->blk_base, offsets, c->tot, (float*)x_perm,
-                                                                  row_token, row_gate, R_cap), count_launch();
+    dispatch_rank_kernel<float><<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->d, c->E, c->blk_base, offsets,
+                                                           c->tot, (float*)x_perm, row_token, row_gate, R_cap),
+        count_launch();
+    dispatch_copy_kernel<float><<<(c->T + 7) / 8, 256, 0, s>>>((const float*)x, slot, c->T, c->d, c->E,
+                                                               (float*)x_perm), count_launch();
   }
   return cudaGetLastError();
 }

@@ -236,6 +236,7 @@ class DTSMoELayer:
         grads["dx"] = dx
         grads["dlogits"] = dlogits
         grads["da"] = da
+        self.last_grads = grads
         return grads
 
     def check(self, stream=None):
