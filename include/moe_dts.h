@@ -138,6 +138,15 @@ int moe_expert_ffn(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int
                    const void* W1, const void* b1, const void* W2, const void* b2,
                    void* gp_saved, void* h_saved, void* e_out, void* stream);
 
+/* NEXT #3, MoE-aware recomputation.  moe_expert_ffn may be called with
+ * gp_saved == NULL: GEMM1's epilogue then writes only h (a transient buffer the caller may
+ * reuse after the call), and nothing [R, d_ff]-sized is kept until the backward.  Before
+ * moe_expert_ffn_bwd, moe_expert_ffn_recompute re-runs GEMM1 + GELU from the kept x_perm
+ * (the expert-side input, which under EP is the received all-to-all buffer: no exchange is
+ * repeated) and writes gp_saved and h_saved.  Costs one extra GEMM1 (1/6 of the FLOPs). */
+int moe_expert_ffn_recompute(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int64_t R_cap,
+                             const void* W1, const void* b1, void* gp_saved, void* h_saved, void* stream);
+
 /* Combine + un-permute, step 6 (Eq. 4, Eq. 7, Alg. 1 line 11):
  *   y[t] = sum over selected e in ASCENDING e of row_gate[slot[t,e]] * e_out[slot[t,e]]
  * accumulated in fp32 (R14), stored as D.  y [T, d]. */

@@ -34,6 +34,7 @@ SIGNATURES = {
     "moe_dts_gate": (_I, [_P, _P, _P, _P, _F, _F, _I, _P, _P, _P, _P, _P]),
     "moe_dispatch": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _P, _P]),
     "moe_expert_ffn": (_I, [_P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "moe_expert_ffn_recompute": (_I, [_P, _P, _P, _L, _P, _P, _P, _P, _P]),
     "moe_combine": (_I, [_P, _P, _P, _P, _P, _P]),
     "moe_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
     "moe_expert_ffn_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
@@ -159,6 +160,11 @@ def moe_dispatch(ctx, x, probs, slot, x_perm, row_token, row_gate, offsets, R_ca
 def moe_expert_ffn(ctx, x_perm, offsets, R_cap, W1, b1, W2, b2, a_saved, h_saved, e_out, stream=None):
     _call("moe_expert_ffn", ctx, _ptr(x_perm), _ptr(offsets), int(R_cap), _ptr(W1), _ptr(b1), _ptr(W2),
           _ptr(b2), _ptr(a_saved), _ptr(h_saved), _ptr(e_out), _stream(stream))
+
+
+def moe_expert_ffn_recompute(ctx, x_perm, offsets, R_cap, W1, b1, gp_saved, h_saved, stream=None):
+    _call("moe_expert_ffn_recompute", ctx, _ptr(x_perm), _ptr(offsets), int(R_cap), _ptr(W1), _ptr(b1),
+          _ptr(gp_saved), _ptr(h_saved), _stream(stream))
 
 
 def moe_combine(ctx, e_out, row_gate, slot, y, stream=None):

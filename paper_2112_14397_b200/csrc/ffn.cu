@@ -31,6 +31,7 @@ cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_
   g1.bias = b1; g1.gBias = f;
   g1.M = 0; g1.N = f; g1.K = d;
   if ((e = launch_simt_gemm(g1, dt, dt, dt, EPI_BIAS_GELU, s)) != cudaSuccess) return e;
+  if (!W2) return cudaSuccess;          // recompute call: GEMM1 only
   // GEMM2: e_out = h W2_e^T + b2_e
   SimtGemm g2 = base_rows(offsets, El, R_cap);
   g2.A = h; g2.sAm = f; g2.sAk = 1;

@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(SimtGemm g) {
       } else if (EPI == EPI_BIAS_GELU) {
         // pre-activation a in fp32; store gp = GELU'(a) (for the backward) and h = GELU(a)
         const float a = v + to_f32(bias[n]);
-        reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(gelu_prime_f(a));
+        if (g.C) reinterpret_cast<TO*>(g.C)[ci] = from_f32<TO>(gelu_prime_f(a));
         reinterpret_cast<TO*>(g.C2)[ci] = from_f32<TO>(gelu_f(a));
       } else if (EPI == EPI_GELU_BWD) {
         const float gp = to_f32(reinterpret_cast<const TO*>(g.aux)[ci]);   // saved GELU'(a)

@@ -54,7 +54,8 @@ constexpr int SMEM_LIMIT = 232448;
 #define AUX_LOAD(p) ld_nc_v4(p)
 #endif
 
-enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 3, TEPI_F32 = 4 };
+// TEPI_BIAS_GELU writes (GELU'(a), GELU(a)); TEPI_BIAS_GELU_H writes GELU(a) only (recompute mode)
+enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 3, TEPI_F32 = 4, TEPI_BIAS_GELU_H = 5 };
 
 template <int EPI> struct EpiCfg {
   static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
@@ -303,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       const bool warp_rows_ok = tl.m_own + sub * 32 < tl.row_end;   // warp-uniform for ROWS tiles
       uint4 bq[4];                                                   // bias of the current chunk
       const bf16* bias_t = nullptr;
-      if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) {
+      if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
         bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0;
         if (tl.n0 + part * 32 < p.N) {
 #pragma unroll
@@ -352,7 +353,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) tc::bulk_wait_read<1>();
             __syncwarp();
           }
-          if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS) {
+          if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float b[8];
@@ -375,6 +376,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             for (int j = 0; j < 8; ++j) gelu_and_prime_fast(v[q * 8 + j], hq[j], gq[j]);
             tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(gq, bf16()));
             tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), pack16(hq, bf16()));
+          }
+        } else if (EPI == TEPI_BIAS_GELU_H) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float hq[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hq[j] = gelu_fast(v[q * 8 + j]);
+            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(hq, bf16()));
           }
         } else {
 #pragma unroll
@@ -538,15 +547,18 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
   p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
   // GEMM1: a = x_perm W1^T + b1, h = GELU(a)      A [R, d] K-major, B = W1 [El*f, d] K-major
   if (!make_map(&mA, x_perm, R_cap, d, d, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, BNH) ||
-      !make_store_map(&mO1, gp, R_cap, f) || !make_store_map(&mO2, h, R_cap, f))
+      (gp && !make_store_map(&mO1, gp, R_cap, f)) || !make_store_map(&mO2, h, R_cap, f))
     return cudaErrorInvalidValue;
   p.N = f; p.K = d; p.b_group_rows = f;
   p.bias = reinterpret_cast<const bf16*>(b1); p.bias_g = f;
-  p.o1 = reinterpret_cast<bf16*>(gp); p.o2 = reinterpret_cast<bf16*>(h); p.ldo_b = f;
+  p.o1 = reinterpret_cast<bf16*>(gp ? gp : h); p.o2 = reinterpret_cast<bf16*>(h); p.ldo_b = f;
   const long long up = rows_pairs_upper(R_cap, El);
-  cudaError_t e = launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p,
-                                                                  up * ((f + BN - 1) / BN), c->sm_count, s);
+  cudaError_t e = gp ? launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p,
+                                                                       up * ((f + BN - 1) / BN), c->sm_count, s)
+                      : launch_tc<TEPI_BIAS_GELU_H, false, false, false>(mA, mB, mO2, mO2, mO2, p,
+                                                                         up * ((f + BN - 1) / BN), c->sm_count, s);
   if (e != cudaSuccess) return e;
+  if (!W2) return cudaSuccess;          // recompute call: GEMM1 only
   // GEMM2: e_out = h W2^T + b2                     A [R, f] K-major, B = W2 [El*d, f] K-major
   if (!make_map(&mA, h, R_cap, f, f, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, BNH) ||
       !make_store_map(&mO1, e_out, R_cap, d))

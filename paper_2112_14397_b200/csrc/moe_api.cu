@@ -247,13 +247,26 @@ int moe_expert_ffn(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int
   int rc = check_ctx(ctx, "moe_expert_ffn");
   if (rc) return rc;
   REQUIRE_R(x_perm); REQUIRE(offsets); REQUIRE(W1); REQUIRE(b1); REQUIRE(W2); REQUIRE(b2);
-  REQUIRE_R(gp_saved); REQUIRE_R(h_saved); REQUIRE_R(e_out);
+  REQUIRE_R(h_saved); REQUIRE_R(e_out);      // gp_saved may be NULL (recompute mode)
   if (R_cap < 0 || R_cap % moe::kRowAlign != 0)
     return fail(MOE_EINVAL, "moe_expert_ffn: R_cap=%lld must be a non-negative multiple of %d",
                 (long long)R_cap, moe::kRowAlign);
   return cuda_status(moe::launch_expert_ffn(ctx, x_perm, offsets, R_cap, W1, b1, W2, b2, gp_saved, h_saved,
                                             e_out, S(stream)),
                      "moe_expert_ffn");
+}
+
+int moe_expert_ffn_recompute(moe_ctx* ctx, const void* x_perm, const int32_t* offsets, int64_t R_cap,
+                             const void* W1, const void* b1, void* gp_saved, void* h_saved, void* stream) {
+  int rc = check_ctx(ctx, "moe_expert_ffn_recompute");
+  if (rc) return rc;
+  REQUIRE_R(x_perm); REQUIRE(offsets); REQUIRE(W1); REQUIRE(b1); REQUIRE_R(gp_saved); REQUIRE_R(h_saved);
+  if (R_cap < 0 || R_cap % moe::kRowAlign != 0)
+    return fail(MOE_EINVAL, "moe_expert_ffn_recompute: R_cap=%lld must be a non-negative multiple of %d",
+                (long long)R_cap, moe::kRowAlign);
+  return cuda_status(moe::launch_expert_ffn(ctx, x_perm, offsets, R_cap, W1, b1, nullptr, nullptr, gp_saved, h_saved,
+                                            nullptr, S(stream)),
+                     "moe_expert_ffn_recompute");
 }
 
 int moe_combine(moe_ctx* ctx, const void* e_out, const float* row_gate, const int32_t* slot, void* y,

@@ -59,7 +59,8 @@ class DTSMoELayer:
     """One MoE FFN layer under the DTS gate on the current CUDA device (one rank)."""
 
     def __init__(self, T: int, d_model: int, d_ff: int, E: int, dtype: torch.dtype = torch.bfloat16,
-                 device: Optional[torch.device] = None, rank: int = 0, world: int = 1, nccl_comm: int = 0):
+                 device: Optional[torch.device] = None, rank: int = 0, world: int = 1, nccl_comm: int = 0,
+                 recompute: bool = False):
         if dtype not in DTYPES:
             raise ValueError(f"dtype must be one of {list(DTYPES)}")
         self.T, self.d, self.f, self.E = T, d_model, d_ff, E
@@ -67,6 +68,7 @@ class DTSMoELayer:
         self.dtype = dtype
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.rank, self.world = rank, world
+        self.recompute = recompute        # NEXT #3: keep only x_perm between forward and backward
         self.ep = bool(nccl_comm)          # expert-parallel exchange (world > 1, or world == 1 self-exchange)
         if world > 1 and not self.ep:
             raise ValueError("world > 1 needs an NCCL communicator (see make_nccl_comm)")
@@ -180,7 +182,7 @@ class DTSMoELayer:
         if events:
             events[0].record()
         L.moe_expert_ffn(self.ctx, rb["x_recv"], offsets_recv, R_recv_cap, self.W1, self.b1, self.W2, self.b2,
-                         rb["gp"], rb["h"], rb["e_out_recv"], stream)
+                         None if self.recompute else rb["gp"], rb["h"], rb["e_out_recv"], stream)
         if events:
             events[1].record()
         if self.ep:
@@ -211,6 +213,9 @@ class DTSMoELayer:
             db2=torch.empty(El, d, dtype=torch.float32, device=dev),
             dWg=torch.empty(d, self.E, dtype=torch.float32, device=dev),
         )
+        if self.recompute:
+            L.moe_expert_ffn_recompute(self.ctx, rb["x_recv"], st.offsets_recv, st.R_recv_cap, self.W1, self.b1,
+                                       rb["gp"], rb["h"], stream)
         da = rb["gp"] if inplace_da else torch.empty_like(rb["gp"])
         if events:
             events[0].record()

@@ -170,3 +170,64 @@ def test_ep_self_exchange_matches_single_rank():
     for k in outs[0][1]:
         assert torch.equal(outs[0][1][k], outs[1][1][k]), k
     L.moe_nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("cfg_name,T", [("C1", None), ("C3", 600)])
+def test_balance_loss_and_gradient(cfg_name, T):
+    """NEXT #1, Eq. 10: the loss value (moe_balance_loss) and its gradient folded
+    into the gate backward (balance_alpha) against the oracle."""
+    from _parity import f32, rel_err, run_oracle
+    from oracle import dts_moe as O
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.get(cfg_name)
+    li = inputs.make_inputs(cfg, T=T)
+    T_ = li.x.shape[0]
+    dev = torch.device("cuda", 0)
+    layer = DTSMoELayer(T_, cfg.d_model, cfg.d_ff, cfg.E, dtype=li.x.dtype, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    layer.forward(li.x.to(dev), li.u.to(dev), f32(cfg.tau), f32(cfg.threshold))
+    alpha = 0.1
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    L.moe_balance_loss(layer.ctx, layer.state.probs, layer.state.counts, alpha, T_, loss)
+    g = layer.backward(li.dy.to(dev), balance_alpha=alpha)
+    torch.cuda.synchronize()
+    layer.check()
+    m_gpu = (layer.state.slot >= 0).cpu().numpy()
+    ex, fw, _ = run_oracle(cfg, li, mask_override=m_gpu, backward=False)
+    ref_loss = O.balance_loss(fw.p, fw.m, alpha)
+    assert abs(loss.item() - ref_loss) <= 1e-5 * max(1.0, abs(ref_loss)), (loss.item(), ref_loss)
+    bw = O.backward(fw, inputs.to_f64(li.dy), balance_alpha=alpha)
+    tol = 1e-4 if cfg.dtype == "f32" else 2e-2
+    assert rel_err(g["dWg"].cpu().numpy(), bw.dWg) <= tol
+    assert rel_err(g["dx"].float().cpu().numpy(), bw.dx) <= tol
+
+
+@pytest.mark.parametrize("cfg_name,T", [("C1", None), ("C4", 512)])
+def test_recompute_mode_matches_saved_mode(cfg_name, T):
+    """NEXT #3: with recompute=True nothing [R, d_ff]-sized is kept between the
+    forward and the backward; GEMM1 + GELU are re-run from x_perm.  Results are bit-identical
+    to the saved-activation mode (same kernels, same inputs, same order)."""
+    from _parity import f32
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.get(cfg_name)
+    li = inputs.make_inputs(cfg, T=T)
+    T_ = li.x.shape[0]
+    dev = torch.device("cuda", 0)
+    outs = []
+    for rc in (False, True):
+        layer = DTSMoELayer(T_, cfg.d_model, cfg.d_ff, cfg.E, dtype=li.x.dtype, device=dev, recompute=rc)
+        layer.set_gate(li.Wg.to(dev))
+        layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+        y = layer.forward(li.x.to(dev), li.u.to(dev), f32(cfg.tau), f32(cfg.threshold))
+        if rc:
+            layer.rows["h"].fill_(float("nan"))      # the forward's h must not be needed any more
+            layer.rows["gp"].fill_(float("nan"))
+        g = layer.backward(li.dy.to(dev))
+        torch.cuda.synchronize()
+        layer.check()
+        outs.append((y.float().cpu(), {k: v.float().cpu() for k, v in g.items() if k not in ("da",)}))
+    assert torch.equal(outs[0][0], outs[1][0])
+    for k in outs[0][1]:
+        assert torch.equal(outs[0][1][k], outs[1][1][k]), k
