@@ -277,7 +277,10 @@ def run_ours(args, rank, world):
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": f"{peak_src} bf16_tflops_sustained",
                      "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
-                     "gemm_ms_per_step": gemm_ms, "flops_per_step": flops, "traffic": None},
+                     "gemm_ms_per_step": gemm_ms, "flops_per_step": flops,
+                     "algorithmic_bytes_per_step": R * (12 * cfg.d_model + 16 * cfg.d_ff) * (1 if cfg.dtype == "bf16" else 2)
+                     + cfg.E * cfg.d_model * cfg.d_ff * (4 * (2 if cfg.dtype == "bf16" else 4) + 2 * 4),
+                     **_traffic(cfg.name, world)},
         "step_tflops": step_flops / (ms_step / 1e3) / 1e12,
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -291,6 +294,22 @@ def run_ours(args, rank, world):
                                "sample": f"{T_sub} tokens of {cfg.name} (same d/d_ff/E/tau/c), fwd+bwd, fp64 NumPy, "
                                          f"{dt_cpu:.2f} s"}
     return out
+
+
+def _traffic(name, world):
+    """roofline.traffic: dram__bytes_read.sum + dram__bytes_write.sum of the expert GEMM set per
+    step (the six tc_gemm_kernel launches that `achieved` covers), from the committed
+    `ncu --set full` capture summary profiles/<round>/ncu_gemm_<workload>.json (null if none)."""
+    import glob
+    if world != 1:
+        return {"traffic": None}
+    hits = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_gemm_{name}.json")))
+    if not hits:
+        return {"traffic": None}
+    with open(hits[-1]) as f:
+        s = json.load(f)["expert_gemm_set"]
+    return {"traffic": s["dram_bytes"], "traffic_unit": "bytes per step (6 launches)",
+            "traffic_source": os.path.relpath(hits[-1], ROOT)}
 
 
 def run_e2e(args, layer, li, tau, c, world, graphed=None):

@@ -117,4 +117,69 @@ __device__ __forceinline__ void gelu_and_prime_fast(float a, float& h, float& gp
   gp = fmaf(a * 0.39894228040143268f, e, ph);
 }
 
+// ---- packed fp32x2 (sm_100a FFMA2/FMUL2/FADD2): two lanes of fp32 per instruction, each lane
+// rounded exactly like its scalar counterpart, so results are bit-identical to the scalar code.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2(float lo, float hi) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f32x2 f2(float v) { return f2(v, v); }
+__device__ __forceinline__ void f2_split(f32x2 v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// bf16x2 word -> fp32 pair (low half = first element)
+__device__ __forceinline__ f32x2 bf16x2_to_f2(uint32_t w) {
+  return f2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+__device__ __forceinline__ uint32_t f2_to_bf16x2(f32x2 v) {
+  float lo, hi;
+  f2_split(v, lo, hi);
+  return pack_bf16x2(lo, hi);
+}
+
+// gelu_and_prime_fast on two elements with the packed pipe.  Same operations and roundings as
+// the scalar form: with ns = -sign(a) (as +-1), -|a| = a*ns, t = rcp(1 + k|a|) = rcp(fma(-|a|, -k, 1)),
+// Phi = fma(ns, q, (1 - ns)/2), i.e. 1 - q for a >= 0 and q for a < 0 (the scalar select).
+__device__ __forceinline__ void gelu_and_prime_x2(f32x2 A, f32x2& H, f32x2& G, bool want_g = true) {
+  float a0, a1;
+  f2_split(A, a0, a1);
+  const uint32_t ns0 = (~__float_as_uint(a0) & 0x80000000u) | 0x3f800000u;
+  const uint32_t ns1 = (~__float_as_uint(a1) & 0x80000000u) | 0x3f800000u;
+  const f32x2 NS = f2(__uint_as_float(ns0), __uint_as_float(ns1));
+  const f32x2 X = fma2(mul2(A, NS), f2(-0.3275911f * 0.70710678118654752f), f2(1.0f));
+  float x0, x1;
+  f2_split(X, x0, x1);
+  const f32x2 T = f2(rcp_approx(x0), rcp_approx(x1));
+  f32x2 P = fma2(f2(0.5f * 1.061405429f), T, f2(0.5f * -1.453152027f));
+  P = fma2(P, T, f2(0.5f * 1.421413741f));
+  P = fma2(P, T, f2(0.5f * -0.284496736f));
+  P = fma2(P, T, f2(0.5f * 0.254829592f));
+  P = mul2(T, P);
+  const f32x2 S = mul2(A, mul2(A, f2(-0.5f * 1.4426950408889634f)));
+  float s0, s1;
+  f2_split(S, s0, s1);
+  const f32x2 E = f2(ex2_approx(s0), ex2_approx(s1));
+  const f32x2 Q = mul2(P, E);
+  const f32x2 PH = fma2(NS, Q, fma2(NS, f2(-0.5f), f2(0.5f)));
+  H = mul2(A, PH);
+  if (want_g) G = fma2(mul2(A, f2(0.39894228040143268f)), E, PH);
+}
+
 }  // namespace moe

@@ -311,7 +311,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + part * 32 + q * 8);
         }
       }
-      tc::mbar_wait(&tfull_bar[acc], acc_phase);
+      tc::mbar_wait_sleep(&tfull_bar[acc], acc_phase);
       tc::tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16);
 #ifdef MOE_EXP_NOEPI
@@ -336,17 +336,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
         const bool store = warp_rows_ok && n < p.N;
         const uint32_t buf = stage_base + (seq % Cfg::NBUF) * (Cfg::NOUT * CHUNK_BYTES);
-        float v[32];
+        f32x2 v[16];                                       // packed fp32 pairs (FFMA2/FMUL2/FADD2)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+        for (int j = 0; j < 16; ++j) v[j] = f2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
         if (EPI == TEPI_GELU_BWD) {
           tc::mbar_wait_u32(auxb + (seq % Cfg::NBUF) * 8, (seq / Cfg::NBUF) & 1);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float a[8];                                            // gp = GELU'(a) saved by the forward
-            unpack16(tc::ld_shared_v4(buf + lane * 64 + ((q ^ swz) << 4)), a, bf16());
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[q * 8 + j] *= a[j];   // da = dh (.) GELU'(a)
+          for (int q = 0; q < 4; ++q) {                        // gp = GELU'(a) saved by the forward
+            const uint4 g4 = tc::ld_shared_v4(buf + lane * 64 + ((q ^ swz) << 4));
+            v[q * 4 + 0] = mul2(v[q * 4 + 0], bf16x2_to_f2(g4.x));   // da = dh (.) GELU'(a)
+            v[q * 4 + 1] = mul2(v[q * 4 + 1], bf16x2_to_f2(g4.y));
+            v[q * 4 + 2] = mul2(v[q * 4 + 2], bf16x2_to_f2(g4.z));
+            v[q * 4 + 3] = mul2(v[q * 4 + 3], bf16x2_to_f2(g4.w));
           }
         } else {
           if (seq >= 2) {                                 // the group that last used this buffer must be read
@@ -356,10 +357,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              float b[8];
-              unpack16(bq[q], b, bf16());
-#pragma unroll
-              for (int j = 0; j < 8; ++j) v[q * 8 + j] += b[j];
+              v[q * 4 + 0] = add2(v[q * 4 + 0], bf16x2_to_f2(bq[q].x));
+              v[q * 4 + 1] = add2(v[q * 4 + 1], bf16x2_to_f2(bq[q].y));
+              v[q * 4 + 2] = add2(v[q * 4 + 2], bf16x2_to_f2(bq[q].z));
+              v[q * 4 + 3] = add2(v[q * 4 + 3], bf16x2_to_f2(bq[q].w));
             }
             if (k + 1 < nch && n + EPI_PER_Q * 32 < p.N) {   // prefetch the next chunk's bias
 #pragma unroll
@@ -371,38 +372,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           // out1 = GELU'(a) (kept for the backward), out2 = h = GELU(a): one Phi / exp per element
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            float hq[8], gq[8];
+            uint32_t hw[4], gw[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) gelu_and_prime_fast(v[q * 8 + j], hq[j], gq[j]);
-            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(gq, bf16()));
-            tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), pack16(hq, bf16()));
+            for (int j = 0; j < 4; ++j) {
+              f32x2 h2, g2;
+              gelu_and_prime_x2(v[q * 4 + j], h2, g2);
+              hw[j] = f2_to_bf16x2(h2);
+              gw[j] = f2_to_bf16x2(g2);
+            }
+            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), make_uint4(gw[0], gw[1], gw[2], gw[3]));
+            tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
           }
         } else if (EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            float hq[8];
+            uint32_t hw[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) hq[j] = gelu_fast(v[q * 8 + j]);
-            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(hq, bf16()));
+            for (int j = 0; j < 4; ++j) {
+              f32x2 h2, g2;
+              gelu_and_prime_x2(v[q * 4 + j], h2, g2, false);
+              hw[j] = f2_to_bf16x2(h2);
+            }
+            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
           }
         } else {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), pack16(v + q * 8, bf16()));
+            tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4),
+                             make_uint4(f2_to_bf16x2(v[q * 4]), f2_to_bf16x2(v[q * 4 + 1]), f2_to_bf16x2(v[q * 4 + 2]),
+                                        f2_to_bf16x2(v[q * 4 + 3])));
         }
         tc::fence_proxy_async();
         __syncwarp();
         if (EPI == TEPI_GELU_BWD && p.colpart && store) {
-          // db1 partial: lane j sums column j of this warp's 32 x 32 bf16 da sub-tile (fixed row order)
-          float cs = 0.f;
+          // db1 partial of this warp's 32 x 32 bf16 da sub-tile (fixed order): lane = (column pair
+          // cp = lane & 15, row parity rp = lane >> 4) sums rows rp, rp+2, ..., then the two parities
+          // are added.  Even/odd rows sit in opposite 64-byte bank halves: conflict-free.
+          const uint32_t cp = lane & 15, rp = lane >> 4;
+          f32x2 cs = f2(0.f);
 #pragma unroll 8
-          for (int r = 0; r < 32; ++r) {
-            const uint32_t addr = buf + r * 64 + ((((uint32_t)lane >> 3) ^ ((r >> 1) & 3)) << 4) + (lane & 7) * 2;
-            unsigned short hv;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(hv) : "r"(addr));
-            cs += __uint_as_float((uint32_t)hv << 16);
+          for (uint32_t i = 0; i < 16; ++i) {
+            const uint32_t r = 2 * i + rp;
+            const uint32_t addr = buf + r * 64 + (((cp >> 2) ^ ((r >> 1) & 3)) << 4) + (cp & 3) * 4;
+            uint32_t w;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(addr));
+            cs = add2(cs, bf16x2_to_f2(w));
           }
-          p.colpart[(long long)((tl.m_own + sub * 32) >> 5) * p.N + n + lane] = cs;
+          float c0, c1;
+          f2_split(cs, c0, c1);
+          c0 += __shfl_xor_sync(0xffffffffu, c0, 16);
+          c1 += __shfl_xor_sync(0xffffffffu, c1, 16);
+          if (rp == 0)
+            *reinterpret_cast<float2*>(p.colpart + (long long)((tl.m_own + sub * 32) >> 5) * p.N + n + 2 * cp) =
+                make_float2(c0, c1);
         }
 #ifdef MOE_EXP_STG
         if (store) {   // coalesced LSU stores from the swizzled smem sub-tile: 8 rows x 64 B per instruction
