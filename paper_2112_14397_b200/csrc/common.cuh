@@ -57,6 +57,11 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
+__device__ __forceinline__ float4 ld_nc_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint4 ld_v4(const void* p) {
   return *reinterpret_cast<const uint4*>(p);
 }
@@ -154,32 +159,43 @@ __device__ __forceinline__ uint32_t f2_to_bf16x2(f32x2 v) {
   return pack_bf16x2(lo, hi);
 }
 
-// gelu_and_prime_fast on two elements with the packed pipe.  Same operations and roundings as
-// the scalar form: with ns = -sign(a) (as +-1), -|a| = a*ns, t = rcp(1 + k|a|) = rcp(fma(-|a|, -k, 1)),
+// gelu_and_prime_fast on two elements with the packed pipe (same approximation; the constant
+// folding below changes the last-bit rounding, not the |erf error| <= 1.5e-7 bound): with
+// ns = -sign(a) (as +-1), -|a| = a*ns, t = rcp(1 + k|a|) = rcp(fma(-|a|, -k, 1)),
 // Phi = fma(ns, q, (1 - ns)/2), i.e. 1 - q for a >= 0 and q for a < 0 (the scalar select).
+// Instruction-lean form (GEMM1 epilogue): the sign word ns = (~a & 0x80000000) | 1.0f is one
+// LOP3 per element (1.0f held in a register), and 1/sqrt(2 pi) is folded into the exponent
+// (E' = exp(-a^2/2) / sqrt(2 pi) = ex2(-a^2 log2(e)/2 - log2(2 pi)/2) = phi(a)) and, inversely,
+// into the erfc polynomial, so q = P' E' is unchanged and GELU'(a) = Phi + a phi = fma(a, E', Phi).
+__device__ __forceinline__ uint32_t neg_sign_one(uint32_t a, uint32_t one) {
+  uint32_t d;   // (~a & 0x80000000) | one   (LUT 0xAE: f(a=F0, b=CC, c=AA) = (~a & b) | c)
+  asm("lop3.b32 %0, %1, %2, %3, 0xAE;" : "=r"(d) : "r"(a), "n"(0x80000000u), "r"(one));
+  return d;
+}
 __device__ __forceinline__ void gelu_and_prime_x2(f32x2 A, f32x2& H, f32x2& G, bool want_g = true) {
+  constexpr float kS2P = 2.5066282746310002f;   // sqrt(2 pi)
   float a0, a1;
   f2_split(A, a0, a1);
-  const uint32_t ns0 = (~__float_as_uint(a0) & 0x80000000u) | 0x3f800000u;
-  const uint32_t ns1 = (~__float_as_uint(a1) & 0x80000000u) | 0x3f800000u;
-  const f32x2 NS = f2(__uint_as_float(ns0), __uint_as_float(ns1));
+  const uint32_t one = 0x3f800000u;
+  const f32x2 NS = f2(__uint_as_float(neg_sign_one(__float_as_uint(a0), one)),
+                      __uint_as_float(neg_sign_one(__float_as_uint(a1), one)));
   const f32x2 X = fma2(mul2(A, NS), f2(-0.3275911f * 0.70710678118654752f), f2(1.0f));
   float x0, x1;
   f2_split(X, x0, x1);
   const f32x2 T = f2(rcp_approx(x0), rcp_approx(x1));
-  f32x2 P = fma2(f2(0.5f * 1.061405429f), T, f2(0.5f * -1.453152027f));
-  P = fma2(P, T, f2(0.5f * 1.421413741f));
-  P = fma2(P, T, f2(0.5f * -0.284496736f));
-  P = fma2(P, T, f2(0.5f * 0.254829592f));
+  f32x2 P = fma2(f2(0.5f * kS2P * 1.061405429f), T, f2(0.5f * kS2P * -1.453152027f));
+  P = fma2(P, T, f2(0.5f * kS2P * 1.421413741f));
+  P = fma2(P, T, f2(0.5f * kS2P * -0.284496736f));
+  P = fma2(P, T, f2(0.5f * kS2P * 0.254829592f));
   P = mul2(T, P);
-  const f32x2 S = mul2(A, mul2(A, f2(-0.5f * 1.4426950408889634f)));
+  const f32x2 S = fma2(A, mul2(A, f2(-0.5f * 1.4426950408889634f)), f2(-1.3257480647361595f));
   float s0, s1;
   f2_split(S, s0, s1);
-  const f32x2 E = f2(ex2_approx(s0), ex2_approx(s1));
-  const f32x2 Q = mul2(P, E);
+  const f32x2 E = f2(ex2_approx(s0), ex2_approx(s1));   // phi(a)
+  const f32x2 Q = mul2(P, E);                            // Phi(-|a|)
   const f32x2 PH = fma2(NS, Q, fma2(NS, f2(-0.5f), f2(0.5f)));
   H = mul2(A, PH);
-  if (want_g) G = fma2(mul2(A, f2(0.39894228040143268f)), E, PH);
+  if (want_g) G = fma2(A, E, PH);
 }
 
 }  // namespace moe

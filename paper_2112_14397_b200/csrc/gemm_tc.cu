@@ -24,6 +24,10 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
+#ifdef MOE_EXP_TRACE
+#include <cstdio>
+#include <cstdlib>
+#endif
 
 namespace moe {
 
@@ -59,7 +63,10 @@ enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 
 
 template <int EPI> struct EpiCfg {
   static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
-  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4 : 2;                            // staging buffers per warp
+#ifndef MOE_EPI_NBUF
+#define MOE_EPI_NBUF 2
+#endif
+  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4 : MOE_EPI_NBUF;                 // staging buffers per warp
   static constexpr int STAGING = NOUT * EPI_WARPS * NBUF * CHUNK_BYTES;
   static constexpr int BAR_BYTES = 2048;
   static constexpr int STAGES = (SMEM_LIMIT - 1024 - BAR_BYTES - STAGING) / STAGE_BYTES;
@@ -75,13 +82,27 @@ struct TcParams {
   float* out;             // KGRP fp32 output, row-major pitch ldo (+ g * out_g)
   long long ldo;
   long long out_g;
-  const bf16* bias;       // + g * bias_g
+  const float* bias;      // fp32 copy (c->biasf), rows padded to 256 columns: + g * bias_g
   long long bias_g;
   bf16* o1;               // bf16 outputs (ROWS), pitch ldo_b -- used by the LSU store variant
   bf16* o2;
   long long ldo_b;
   float* colpart;         // TEPI_GELU_BWD: per-32-row column sums of da [R_cap/32][N] (bias gradient db1)
+  unsigned long long* trace;   // MOE_EXP_TRACE builds only: per-warp event log of CTAs 0 and 1
 };
+
+#ifdef MOE_EXP_TRACE
+constexpr int kTraceN = 4096;
+#define TR(ev, tile)                                                                                        \
+  do {                                                                                                      \
+    if (p.trace && blockIdx.x < 2 && (threadIdx.x & 31) == 0 && tr_n < kTraceN)                             \
+      p.trace[((size_t)blockIdx.x * 16 + threadIdx.x / 32) * kTraceN + tr_n++] =                            \
+          ((unsigned long long)(ev) << 56) | ((unsigned long long)((tile) & 0xffff) << 40) |                \
+          ((unsigned long long)clock64() & 0xFFFFFFFFFFull);                                                \
+  } while (0)
+#else
+#define TR(ev, tile) do { } while (0)
+#endif
 
 struct Tile {
   int g, m_own, n0, kb0, nkb, row_end;
@@ -140,6 +161,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 
   const uint32_t rank = tc::cluster_rank();
   const bool leader = rank == 0;
+#ifdef MOE_EXP_TRACE
+  uint32_t tr_n = 0;
+#endif
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
@@ -196,7 +220,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int n_own = tl.n0 + BNH * (int)rank;
         const int brow = KGRP ? 0 : tl.g * p.b_group_rows;
         for (int kb = 0; kb < tl.nkb; ++kb) {
+          TR(1, t);
           tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          TR(2, t);
           if (leader) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
           const uint32_t bar = full_leader + stage * 8;
           const uint32_t sa = smem_base + stage * STAGE_BYTES;
@@ -230,11 +256,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int t = cid; t < total; t += ncl) {
         Tile tl;
         if (!decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tl)) continue;
+        TR(3, t);
         tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        TR(4, t);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < tl.nkb; ++kb) {
           tc::mbar_wait(&full_bar[stage], phase);
+          TR(5, t);
           tc::tc_fence_after();
           const uint32_t sa = smem_base + stage * STAGE_BYTES;
           const uint32_t sb = sa + A_BYTES;
@@ -302,16 +331,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         continue;
       }
       const bool warp_rows_ok = tl.m_own + sub * 32 < tl.row_end;   // warp-uniform for ROWS tiles
-      uint4 bq[4];                                                   // bias of the current chunk
-      const bf16* bias_t = nullptr;
-      if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
+      const float* bias_t = nullptr;                                 // padded fp32 bias row of this tile
+      if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H)
         bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0;
-        if (tl.n0 + part * 32 < p.N) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + part * 32 + q * 8);
-        }
-      }
+      TR(6, t);
       tc::mbar_wait_sleep(&tfull_bar[acc], acc_phase);
+      TR(7, t);
       tc::tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16);
 #ifdef MOE_EXP_NOEPI
@@ -322,8 +347,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         const int col = (part + EPI_PER_Q * k) * 32;
         const int n = tl.n0 + col;
         uint32_t r[32];
+        float4 bf[8];                                      // bias of this chunk (broadcast loads)
+        if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) bf[q] = ld_nc_f4(bias_t + col + 4 * q);
+        }
         tc::tmem_ld32(t_row + col, r);
         tc::tmem_ld_wait();
+        TR(8, t);
         if (EPI == TEPI_F32) {
           if (row < p.M && n < p.N) {
             float* o = p.out + (long long)tl.g * p.out_g + row * p.ldo + n;
@@ -350,21 +381,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             v[q * 4 + 3] = mul2(v[q * 4 + 3], bf16x2_to_f2(g4.w));
           }
         } else {
-          if (seq >= 2) {                                 // the group that last used this buffer must be read
-            if (lane == 0) tc::bulk_wait_read<1>();
+          if (seq >= (uint32_t)Cfg::NBUF) {               // the group that last used this buffer must be read
+            if (lane == 0) tc::bulk_wait_read<Cfg::NBUF - 1>();
             __syncwarp();
           }
           if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              v[q * 4 + 0] = add2(v[q * 4 + 0], bf16x2_to_f2(bq[q].x));
-              v[q * 4 + 1] = add2(v[q * 4 + 1], bf16x2_to_f2(bq[q].y));
-              v[q * 4 + 2] = add2(v[q * 4 + 2], bf16x2_to_f2(bq[q].z));
-              v[q * 4 + 3] = add2(v[q * 4 + 3], bf16x2_to_f2(bq[q].w));
-            }
-            if (k + 1 < nch && n + EPI_PER_Q * 32 < p.N) {   // prefetch the next chunk's bias
-#pragma unroll
-              for (int q = 0; q < 4; ++q) bq[q] = ld_v4(bias_t + col + EPI_PER_Q * 32 + q * 8);
+            for (int q = 0; q < 8; ++q) {
+              v[q * 2 + 0] = add2(v[q * 2 + 0], f2(bf[q].x, bf[q].y));
+              v[q * 2 + 1] = add2(v[q * 2 + 1], f2(bf[q].z, bf[q].w));
             }
           }
         }
@@ -380,8 +405,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
               hw[j] = f2_to_bf16x2(h2);
               gw[j] = f2_to_bf16x2(g2);
             }
+#ifdef MOE_EXP_DIRECT
+            if (store) {
+              st_v4(p.o1 + row * p.ldo_b + n + q * 8, make_uint4(gw[0], gw[1], gw[2], gw[3]));
+              st_v4(p.o2 + row * p.ldo_b + n + q * 8, make_uint4(hw[0], hw[1], hw[2], hw[3]));
+            }
+#else
             tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), make_uint4(gw[0], gw[1], gw[2], gw[3]));
             tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
+#endif
           }
         } else if (EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
@@ -402,8 +434,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                              make_uint4(f2_to_bf16x2(v[q * 4]), f2_to_bf16x2(v[q * 4 + 1]), f2_to_bf16x2(v[q * 4 + 2]),
                                         f2_to_bf16x2(v[q * 4 + 3])));
         }
+        TR(11, t);
         tc::fence_proxy_async();
         __syncwarp();
+        TR(12, t);
         if (EPI == TEPI_GELU_BWD && p.colpart && store) {
           // db1 partial of this warp's 32 x 32 bf16 da sub-tile (fixed order): lane = (column pair
           // cp = lane & 15, row parity rp = lane >> 4) sums rows rp, rp+2, ..., then the two parities
@@ -442,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         }
 #endif
         if (lane == 0) {
-#if defined(MOE_EXP_NOSTORE) || defined(MOE_EXP_STG)
+#if defined(MOE_EXP_NOSTORE) || defined(MOE_EXP_STG) || defined(MOE_EXP_DIRECT)
           if (false) {
 #else
           if (store) {
@@ -452,6 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (Cfg::NOUT == 2) tc::tma_store_2d(&tmO2, buf + CHUNK_BYTES, n, row0);
           }
           tc::bulk_commit();                              // one (possibly empty) group per chunk
+          TR(9, t);
           if (EPI == TEPI_GELU_BWD) {
             tc::bulk_wait_read<2>();                      // buffer (seq+2)%4 was last stored at seq-2
             aux_issue(seq + 2);
@@ -462,6 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_cluster(tempty_leader + acc * 8);
+      TR(10, t);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -528,8 +564,52 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
   }
   long long pairs = tiles_upper < sms / 2 ? tiles_upper : sms / 2;
   if (pairs <= 0) return cudaSuccess;
+#ifdef MOE_EXP_TRACE
+  // trace the 3rd launch of each ROWS epilogue kind; dumped to gpurun_out/trace_<EPI>.bin at exit
+  static int n_launch = 0;
+  static unsigned long long* buf = nullptr;
+  TcParams pt = p;
+  pt.trace = nullptr;
+  if (!KGRP && ++n_launch == 3) {
+    const size_t bytes = 2 * 16 * (size_t)kTraceN * 8;
+    cudaMallocManaged(&buf, bytes);
+    cudaMemset(buf, 0, bytes);
+    pt.trace = buf;
+    static unsigned long long* sbuf = nullptr;
+    sbuf = buf;
+    static char name[64];
+    snprintf(name, sizeof name, "gpurun_out/trace_%d.bin", EPI);
+    struct D { static void dump() {} };
+    std::atexit([] {
+      cudaDeviceSynchronize();
+      FILE* fp = fopen(name, "wb");
+      if (fp) { fwrite(sbuf, 8, 2 * 16 * (size_t)kTraceN, fp); fclose(fp); }
+    });
+  }
+  k<<<(unsigned)(2 * pairs), NUM_THREADS, smem, s>>>(a, b, o1, o2, x, pt), count_launch();
+#else
   k<<<(unsigned)(2 * pairs), NUM_THREADS, smem, s>>>(a, b, o1, o2, x, p), count_launch();
+#endif
   return cudaGetLastError();
+}
+
+// fp32, 256-column-padded copies of b1 and b2 for the epilogues (one launch per forward):
+// out = [El][fp] (b1, zero beyond f) then [El][dp] (b2, zero beyond d).
+__global__ void bias_f32_kernel(const bf16* __restrict__ b1, const bf16* __restrict__ b2, int El, int f, int d,
+                                int fp, int dp, float* __restrict__ out) {
+  const long long n1 = (long long)El * fp, n = n1 + (b2 ? (long long)El * dp : 0);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    if (i < n1) {
+      const int g = (int)(i / fp), c = (int)(i - (long long)g * fp);
+      if (c < f) v = __bfloat162float(b1[(long long)g * f + c]);
+    } else {
+      const long long j = i - n1;
+      const int g = (int)(j / dp), c = (int)(j - (long long)g * dp);
+      if (c < d) v = __bfloat162float(b2[(long long)g * d + c]);
+    }
+    out[i] = v;
+  }
 }
 
 }  // namespace
@@ -564,6 +644,15 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
                           void* e_out, cudaStream_t s) {
   const int d = c->d, f = c->f, El = c->E_local;
   if (R_cap == 0) return cudaSuccess;
+  const int fp = (f + 255) / 256 * 256, dp = (d + 255) / 256 * 256;
+  {
+    const long long n = (long long)El * (fp + (W2 ? dp : 0));
+    const int blocks = (int)((n + 255) / 256 < 4 * c->sm_count ? (n + 255) / 256 : 4 * c->sm_count);
+    bias_f32_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const bf16*>(b1), W2 ? reinterpret_cast<const bf16*>(b2) : nullptr,
+                                           El, f, d, fp, dp, c->biasf), count_launch();
+    cudaError_t e0 = cudaGetLastError();
+    if (e0 != cudaSuccess) return e0;
+  }
   CUtensorMap mA, mB, mO1, mO2;
   TcParams p{};
   p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
@@ -572,7 +661,7 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
       (gp && !make_store_map(&mO1, gp, R_cap, f)) || !make_store_map(&mO2, h, R_cap, f))
     return cudaErrorInvalidValue;
   p.N = f; p.K = d; p.b_group_rows = f;
-  p.bias = reinterpret_cast<const bf16*>(b1); p.bias_g = f;
+  p.bias = c->biasf; p.bias_g = fp;
   p.o1 = reinterpret_cast<bf16*>(gp ? gp : h); p.o2 = reinterpret_cast<bf16*>(h); p.ldo_b = f;
   const long long up = rows_pairs_upper(R_cap, El);
   cudaError_t e = gp ? launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p,
@@ -586,7 +675,7 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
       !make_store_map(&mO1, e_out, R_cap, d))
     return cudaErrorInvalidValue;
   p.N = d; p.K = f; p.b_group_rows = d;
-  p.bias = reinterpret_cast<const bf16*>(b2); p.bias_g = d;
+  p.bias = c->biasf + (long long)El * fp; p.bias_g = dp;
   p.o1 = reinterpret_cast<bf16*>(e_out); p.o2 = nullptr; p.ldo_b = d;
   return launch_tc<TEPI_BIAS, false, false, false>(mA, mB, mO1, mO1, mO1, p, up * ((d + BN - 1) / BN),
                                                    c->sm_count, s);

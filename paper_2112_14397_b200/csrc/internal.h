@@ -29,6 +29,7 @@ struct moe_ctx {
   float* colpart;      // [E_local, kColsumSplits, max(d, f)] bias-gradient partials
   int* rq;             // [1 + T] fp64-refine queue of the tcgen05 gate (count, tokens)
   int* tok_off;        // [2] = {0, roundup(T, 128)}: the token range as one row segment
+  float* biasf;        // [E_local, roundup(f,256)] b1 then [E_local, roundup(d,256)] b2 in fp32 (tcgen05 epilogues)
   void* gate_scratch;  // tcgen05 gate operands: W_g^T / [W_g|W_g] (bf16) and the hi|lo split of dL
   int* ep_counts;      // [world, E] gathered counts (EP)
   int* ep_off;         // [E_local + 1] recv-layout offsets (EP)

@@ -64,7 +64,7 @@ namespace moe {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carve {
-  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, total;
+  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, biasf, total;
 };
 
 static Carve carve(const moe_ctx* c) {
@@ -95,6 +95,8 @@ static Carve carve(const moe_ctx* c) {
   }
   k.rq = take(sizeof(int) * ((size_t)c->T + 1));
   k.tok_off = take(sizeof(int) * 2);
+  // fp32 copies of b1 / b2 for the tensor-core epilogues, rows padded to 256 columns
+  k.biasf = take(sizeof(float) * (size_t)c->E_local * (size_t)((c->f + 255) / 256 * 256 + (c->d + 255) / 256 * 256));
   k.total = o;
   return k;
 }
@@ -118,6 +120,7 @@ void carve_workspace(moe_ctx* c) {
   c->gate_scratch = c->ws + k.gate_scratch;
   c->rq = reinterpret_cast<int*>(c->ws + k.rq);
   c->tok_off = reinterpret_cast<int*>(c->ws + k.tok_off);
+  c->biasf = reinterpret_cast<float*>(c->ws + k.biasf);
 }
 
 }  // namespace moe
