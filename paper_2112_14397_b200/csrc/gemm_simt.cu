@@ -146,14 +146,14 @@ cudaError_t launch_typed(const SimtGemm& g, int epi, cudaStream_t s) {
 // warp w sums rows r0 + w, r0 + w + 8, ... of its split; warps combined in fixed order.
 template <typename TI>
 __global__ void __launch_bounds__(256) colsum_part_kernel(const TI* __restrict__ X, int N, const int* __restrict__ m_off,
-                                                         int S, float* __restrict__ part) {
+                                                         int S, int shift, float* __restrict__ part) {
   constexpr int V = Vec16<TI>::N;                 // elements per 16-byte vector
   constexpr int COLS = 32 * V;                     // columns per block
   __shared__ float red[8][COLS];
   const int g = blockIdx.z, s = blockIdx.y;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int n0 = blockIdx.x * COLS + lane * V;
-  const int off0 = m_off[g], len = m_off[g + 1] - off0;
+  const int off0 = m_off[g] >> shift, len = (m_off[g + 1] >> shift) - off0;   // rows of X = m_off >> shift
   const int per = (len + S - 1) / S;
   const int r0 = off0 + s * per, r1 = min(off0 + len, r0 + per);
   float acc[V];
@@ -213,27 +213,14 @@ cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int ep
   return launch_typed<float, bf16, float>(g, EPI_F32, s);
 }
 
-__global__ void db1_reduce_kernel(const float* __restrict__ part, int N, const int* __restrict__ m_off,
-                                  float* __restrict__ out) {
-  const int g = blockIdx.y;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  const int rb0 = m_off[g] >> 5, rb1 = m_off[g + 1] >> 5;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  int rb = rb0;
-  for (; rb + 3 < rb1; rb += 4) {
-    a0 += part[(long long)rb * N + n];
-    a1 += part[(long long)(rb + 1) * N + n];
-    a2 += part[(long long)(rb + 2) * N + n];
-    a3 += part[(long long)(rb + 3) * N + n];
-  }
-  for (; rb < rb1; ++rb) a0 += part[(long long)rb * N + n];
-  out[(long long)g * N + n] = (a0 + a1) + (a2 + a3);
-}
-
-cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, cudaStream_t s) {
+// db1[g][n] = sum over the 32-row blocks of group g of part[rb][n]: the same two-phase fixed-order
+// reduction as the column sums, over the [R/32][N] fp32 partial rows (m_off >> 5).
+cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, float* part2,
+                              cudaStream_t s) {
   if (G == 0 || N == 0) return cudaSuccess;
-  db1_reduce_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, m_off, out), count_launch();
+  const int S = kColsumSplits;
+  colsum_part_kernel<float><<<dim3((N + 127) / 128, S, G), 256, 0, s>>>(part, N, m_off, S, 5, part2), count_launch();
+  colsum_final_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part2, N, S, out), count_launch();
   return cudaGetLastError();
 }
 
@@ -244,9 +231,15 @@ cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_of
   const int cols = tin == 0 ? 128 : 256;
   dim3 g1((N + cols - 1) / cols, S, G);
   if (tin == 0)
-    colsum_part_kernel<float><<<g1, 256, 0, s>>>(reinterpret_cast<const float*>(X), N, m_off, S, part), count_launch();
+    colsum_part_kernel<float><<<g1, 256, 0, s>>>(reinterpret_cast<const float*>(X), N, m_off, S, 0, part), count_launch();
   else
-    colsum_part_kernel<bf16><<<g1, 256, 0, s>>>(reinterpret_cast<const bf16*>(X), N, m_off, S, part), count_launch();
+    colsum_part_kernel<bf16><<<g1, 256, 0, s>>>(reinterpret_cast<const bf16*>(X), N, m_off, S, 0, part), count_launch();
+  colsum_final_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, S, out), count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum_final(const float* part, int N, int S, int G, float* out, cudaStream_t s) {
+  if (G == 0 || N == 0) return cudaSuccess;
   colsum_final_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, S, out), count_launch();
   return cudaGetLastError();
 }

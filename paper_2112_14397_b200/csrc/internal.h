@@ -30,6 +30,13 @@ struct moe_ctx {
   int* rq;             // [1 + T] fp64-refine queue of the tcgen05 gate (count, tokens)
   int* tok_off;        // [2] = {0, roundup(T, 128)}: the token range as one row segment
   float* biasf;        // [E_local, roundup(f,256)] b1 then [E_local, roundup(d,256)] b2 in fp32 (tcgen05 epilogues)
+  float* db2part;      // [E_local, db2_S, d] db2 column-sum partials left by moe_combine_bwd (single rank)
+  int db2_S;           // row splits per expert of the fused combine_bwd
+  // which (d_eout, offsets, R_cap) the db2 partials belong to; moe_expert_ffn_bwd uses them only
+  // for exactly that triple (else it sums d_eout itself), then clears this
+  const void* db2_src;
+  const int* db2_off;
+  long long db2_rcap;
   void* gate_scratch;  // tcgen05 gate operands: W_g^T / [W_g|W_g] (bf16) and the hi|lo split of dL
   int* ep_counts;      // [world, E] gathered counts (EP)
   int* ep_off;         // [E_local + 1] recv-layout offsets (EP)
@@ -65,10 +72,13 @@ cudaError_t launch_dispatch(const moe_ctx* c, const void* x, const float* probs,
 cudaError_t launch_combine(const moe_ctx* c, const void* e_out, const float* row_gate,
                            const int32_t* slot, void* y, cudaStream_t s);
 
-cudaError_t launch_combine_bwd(const moe_ctx* c, const void* dy, const void* e_out,
+cudaError_t launch_combine_bwd(moe_ctx* c, const void* dy, const void* e_out,
                                const float* row_gate, const int32_t* row_token,
                                const int32_t* offsets, int64_t R_cap, void* d_eout, float* dG_row,
                                cudaStream_t s);
+
+bool launch_db2_partials(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, cudaStream_t s,
+                         cudaError_t* err);
 
 cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot,
                                 const float* dlogits, const void* Wg, void* dx, cudaStream_t s);
@@ -85,7 +95,7 @@ cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_
                               int64_t R_cap, const void* W1, const void* b1, const void* W2,
                               const void* b2, void* gp, void* h, void* e_out, cudaStream_t s);
 
-cudaError_t launch_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm,
+cudaError_t launch_expert_ffn_bwd(moe_ctx* c, const void* d_eout, const void* x_perm,
                                   const void* gp, const void* h, const int32_t* offsets,
                                   int64_t R_cap, const void* W1, const void* W2, void* da,
                                   void* dx_perm, float* dW1, float* db1, float* dW2, float* db2,
@@ -101,7 +111,8 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
                               const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, float* db1,
                               cudaStream_t s);
 // db1[g][n] = sum over the 32-row blocks of group g of part[rb][n]  (fixed order)
-cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, cudaStream_t s);
+cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, float* part2,
+                              cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 gate contractions (bf16)
 bool gate_tc_supported(const moe_ctx* c);
@@ -144,6 +155,8 @@ cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int ep
 constexpr int kColsumSplits = 8;
 cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_off, int G, float* out,
                                   float* part, cudaStream_t s);
+// out[g][n] = sum_s part[g][s][n]  (fixed order)
+cudaError_t launch_colsum_final(const float* part, int N, int S, int G, float* out, cudaStream_t s);
 
 }  // namespace moe
 

@@ -64,8 +64,15 @@ namespace moe {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carve {
-  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, biasf, total;
+  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, biasf, db2part, total;
 };
+
+// row splits per expert for the fused combine_bwd + db2 partials: about 8 blocks per SM in total
+static int db2_splits(const moe_ctx* c) {
+  const int El = c->E_local > 0 ? c->E_local : 1;
+  int S = (8 * (c->sm_count > 0 ? c->sm_count : 148) + El - 1) / El;
+  return S < 1 ? 1 : (S > 128 ? 128 : S);
+}
 
 static Carve carve(const moe_ctx* c) {
   Carve k;
@@ -97,6 +104,7 @@ static Carve carve(const moe_ctx* c) {
   k.tok_off = take(sizeof(int) * 2);
   // fp32 copies of b1 / b2 for the tensor-core epilogues, rows padded to 256 columns
   k.biasf = take(sizeof(float) * (size_t)c->E_local * (size_t)((c->f + 255) / 256 * 256 + (c->d + 255) / 256 * 256));
+  k.db2part = take(sizeof(float) * (size_t)c->E_local * (size_t)db2_splits(c) * (size_t)c->d);
   k.total = o;
   return k;
 }
@@ -121,6 +129,11 @@ void carve_workspace(moe_ctx* c) {
   c->rq = reinterpret_cast<int*>(c->ws + k.rq);
   c->tok_off = reinterpret_cast<int*>(c->ws + k.tok_off);
   c->biasf = reinterpret_cast<float*>(c->ws + k.biasf);
+  c->db2part = reinterpret_cast<float*>(c->ws + k.db2part);
+  c->db2_S = db2_splits(c);
+  c->db2_src = nullptr;
+  c->db2_off = nullptr;
+  c->db2_rcap = 0;
 }
 
 }  // namespace moe

@@ -153,46 +153,60 @@ __global__ void __launch_bounds__(256) dispatch_copy_kernel(const T* __restrict_
 // One warp per token.  The token's selected rows are found with ballots over its slot row
 // (ascending expert order is the bit order), so the work is O(selected), not O(E).
 // Columns are processed 4 x 16-byte vectors per lane at a time (independent loads in flight).
-template <typename T, bool WEIGHTED, typename TX = float>
+template <typename T, bool WEIGHTED, typename TX = float, int QV = 4>
 __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src, const float* __restrict__ row_gate,
                                                  const int* __restrict__ slot_row, int d, int E,
                                                  const TX* __restrict__ extra, T* __restrict__ out, int lane) {
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
-  for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
-    float acc[4][V];
+  for (int v0 = 0; v0 < nvec; v0 += 32 * QV) {
+    float acc[QV][V];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < QV; ++q)
 #pragma unroll
       for (int k = 0; k < V; ++k) acc[q][k] = 0.f;
     for (int g = 0; g < E; g += 32) {
       const int sv = (g + lane < E) ? slot_row[g + lane] : -1;
       unsigned bal = __ballot_sync(0xffffffffu, sv >= 0);
       while (bal) {
+        // two selected rows per pass (both rows' loads in flight), accumulated in ascending e
         const int b = __ffs(bal) - 1;
         bal &= bal - 1;
+        const bool two = bal != 0;
+        const int b2 = two ? __ffs(bal) - 1 : b;
+        if (two) bal &= bal - 1;
         const int r = __shfl_sync(0xffffffffu, sv, b);
+        const int r2 = __shfl_sync(0xffffffffu, sv, b2);
         const float gw = WEIGHTED ? row_gate[r] : 1.0f;
-        uint4 raw[4];
+        const float gw2 = WEIGHTED && two ? row_gate[r2] : 1.0f;
+        uint4 raw[QV], raw2[QV];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < QV; ++q) {
           const int v = v0 + q * 32 + lane;
-          if (v < nvec) raw[q] = ld_nc_v4(rows_src + (long long)r * d + (long long)v * V);
+          if (v < nvec) {
+            raw[q] = ld_nc_v4(rows_src + (long long)r * d + (long long)v * V);
+            if (two) raw2[q] = ld_nc_v4(rows_src + (long long)r2 * d + (long long)v * V);
+          }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < QV; ++q) {
           const int v = v0 + q * 32 + lane;
           if (v < nvec) {
             float o[V];
             unpack16(raw[q], o, T());
 #pragma unroll
             for (int k = 0; k < V; ++k) acc[q][k] = WEIGHTED ? fmaf(gw, o[k], acc[q][k]) : acc[q][k] + o[k];
+            if (two) {
+              unpack16(raw2[q], o, T());
+#pragma unroll
+              for (int k = 0; k < V; ++k) acc[q][k] = WEIGHTED ? fmaf(gw2, o[k], acc[q][k]) : acc[q][k] + o[k];
+            }
           }
         }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < QV; ++q) {
       const int v = v0 + q * 32 + lane;
       if (v < nvec) {
         if (extra) {
@@ -206,14 +220,20 @@ __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src,
 }
 
 // y[t] = sum_{e asc} row_gate[r] * e_out[r], r = slot[t,e]
-template <typename T>
+template <typename T, int QV>
 __global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ e_out, const float* __restrict__ row_gate,
                                                       const int* __restrict__ slot, int T_, int d, int E,
                                                       T* __restrict__ y) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  gather_sum_token<T, true, float>(e_out, row_gate, slot + (long long)t * E, d, E, nullptr, y + (long long)t * d, lane);
+  gather_sum_token<T, true, float, QV>(e_out, row_gate, slot + (long long)t * E, d, E, nullptr, y + (long long)t * d,
+                                       lane);
+}
+// vectors per lane per pass: the whole row in one pass up to 4 x 16 B per lane
+static inline int pass_vectors(int d, int V) {
+  const int q = (d / V + 31) / 32;
+  return q < 1 ? 1 : (q > 4 ? 4 : q);
 }
 
 // ------------------------------------------------------------------ combine backward
@@ -255,16 +275,117 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
   if (lane == 0) dG_row[r] = dot;
 }
 
+// Fused variant (single rank, d <= 32 * MAXV * V): block (s, g) owns split s of expert g's
+// rows [offsets[g], offsets[g+1]) (8 warps, warp w takes rows r0 + w, r0 + w + 8, ...), writes
+// d_eout / dG_row exactly as above and also the db2 column-sum partial of its rows,
+// part[g][s][n] = sum of the stored (rounded) d_eout[r][n], warps combined in fixed order.
+// COMPUTE = false: only the partials, from an existing d_eout (same row partition and summation
+// order, so both paths give bit-identical db2).
+template <typename T, int MAXV, bool COMPUTE>
+__global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __restrict__ dy, const T* __restrict__ e_out,
+                                                                 const float* __restrict__ row_gate,
+                                                                 const int* __restrict__ row_token,
+                                                                 const int* __restrict__ offsets, int d,
+                                                                 long long R_cap, int S, T* __restrict__ d_eout,
+                                                                 float* __restrict__ dG_row, float* __restrict__ part) {
+  extern __shared__ float red[];                    // [8][d]
+  constexpr int V = Vec16<T>::N;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int s = blockIdx.x, g = blockIdx.y;
+  const long long off0 = offsets[g], off1 = min((long long)offsets[g + 1], R_cap);
+  const long long len = off1 > off0 ? off1 - off0 : 0;
+  const long long per = ((len + S - 1) / S + 7) / 8 * 8;
+  const long long r0 = off0 + (long long)s * per, r1 = min(off1, r0 + per);
+  const int nvec = d / V;
+  float acc[MAXV][V];
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j)
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[j][k] = 0.f;
+  for (long long r = r0 + warp; r < r1; r += 8) {
+    T* dst = d_eout + r * d;
+    if (!COMPUTE) {
+#pragma unroll
+      for (int j = 0; j < MAXV; ++j) {
+        const int v = lane + 32 * j;
+        if (v < nvec) {
+          float o[V];
+          unpack16(ld_nc_v4(dst + (long long)v * V), o, T());
+#pragma unroll
+          for (int k = 0; k < V; ++k) acc[j][k] += o[k];
+        }
+      }
+      continue;
+    }
+    const int t = row_token[r];
+    if (t < 0) {
+#pragma unroll
+      for (int j = 0; j < MAXV; ++j) {
+        const int v = lane + 32 * j;
+        if (v < nvec) st_v4(dst + (long long)v * V, make_uint4(0, 0, 0, 0));
+      }
+      if (lane == 0) dG_row[r] = 0.f;
+      continue;
+    }
+    const float gw = row_gate[r];
+    uint4 qa[MAXV], qb[MAXV];
+#pragma unroll
+    for (int j = 0; j < MAXV; ++j) {
+      const int v = lane + 32 * j;
+      if (v < nvec) {
+        qa[j] = ld_nc_v4(dy + (long long)t * d + (long long)v * V);
+        qb[j] = ld_nc_v4(e_out + r * d + (long long)v * V);
+      }
+    }
+    float dot = 0.f;
+#pragma unroll
+    for (int j = 0; j < MAXV; ++j) {
+      const int v = lane + 32 * j;
+      if (v < nvec) {
+        float a[V], b[V], o[V];
+        unpack16(qa[j], a, T());
+        unpack16(qb[j], b, T());
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          dot = fmaf(a[k], b[k], dot);
+          o[k] = gw * a[k];
+        }
+        const uint4 w = pack16(o, T());
+        st_v4(dst + (long long)v * V, w);
+        unpack16(w, o, T());                        // the stored (rounded) values
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[j][k] += o[k];
+      }
+    }
+    dot = warp_sum(dot);
+    if (lane == 0) dG_row[r] = dot;
+  }
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int v = lane + 32 * j;
+    if (v < nvec)
+#pragma unroll
+      for (int k = 0; k < V; ++k) red[warp * d + v * V + k] = acc[j][k];
+  }
+  __syncthreads();
+  for (int n = threadIdx.x; n < d; n += 256) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w * d + n];
+    part[((long long)g * S + s) * d + n] = t;
+  }
+}
+
 // ------------------------------------------------------------------ dispatch backward
 // One warp per token: dx[t] = sum_{e asc} dx_perm[slot[t,e]] + dxg[t] (fp32, may be NULL).
-template <typename T, typename TX>
+template <typename T, typename TX, int QV>
 __global__ void __launch_bounds__(256) dispatch_bwd_kernel(const T* __restrict__ dx_perm, const int* __restrict__ slot,
                                                            const TX* __restrict__ dxg, int T_, int d, int E,
                                                            T* __restrict__ dx) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  gather_sum_token<T, false, TX>(dx_perm, nullptr, slot + (long long)t * E, d, E,
+  gather_sum_token<T, false, TX, QV>(dx_perm, nullptr, slot + (long long)t * E, d, E,
                                  dxg ? dxg + (long long)t * d : nullptr, dx + (long long)t * d, lane);
 }
 
@@ -368,17 +489,76 @@ cudaError_t launch_combine(const moe_ctx* c, const void* e_out, const float* row
                            void* y, cudaStream_t s) {
   if (c->T == 0) return cudaSuccess;
   const unsigned grid = (c->T + 7) / 8;
-  if (c->dtype == 1)
-    combine_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)e_out, row_gate, slot, c->T, c->d, c->E, (bf16*)y), count_launch();
-  else
-    combine_kernel<float><<<grid, 256, 0, s>>>((const float*)e_out, row_gate, slot, c->T, c->d, c->E, (float*)y), count_launch();
+#define MOE_QV_DISPATCH(qv, ...) \
+  switch (qv) { case 1: { constexpr int QV = 1; __VA_ARGS__; } break; case 2: { constexpr int QV = 2; __VA_ARGS__; } break; \
+                case 3: { constexpr int QV = 3; __VA_ARGS__; } break; default: { constexpr int QV = 4; __VA_ARGS__; } }
+  if (c->dtype == 1) {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), combine_kernel<bf16, QV><<<grid, 256, 0, s>>>(
+        (const bf16*)e_out, row_gate, slot, c->T, c->d, c->E, (bf16*)y), count_launch())
+  } else {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), combine_kernel<float, QV><<<grid, 256, 0, s>>>(
+        (const float*)e_out, row_gate, slot, c->T, c->d, c->E, (float*)y), count_launch())
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_combine_bwd(const moe_ctx* c, const void* dy, const void* e_out, const float* row_gate,
+template <typename T, int MAXV, bool COMPUTE = true>
+static cudaError_t launch_cbc(moe_ctx* c, const void* dy, const void* e_out, const float* row_gate,
+                              const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
+                              float* dG_row, cudaStream_t s) {
+  const size_t smem = sizeof(float) * 8 * c->d;
+  auto k = combine_bwd_colsum_kernel<T, MAXV, COMPUTE>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<dim3(c->db2_S, c->E_local), 256, smem, s>>>((const T*)dy, (const T*)e_out, row_gate, row_token, offsets, c->d,
+                                                 R_cap, c->db2_S, (T*)d_eout, dG_row, c->db2part), count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && COMPUTE) {
+    c->db2_src = d_eout;
+    c->db2_off = offsets;
+    c->db2_rcap = R_cap;
+  }
+  return e;
+}
+
+// db2 partials (c->db2part) of an existing d_eout with the fused kernel's partition; false if
+// d is too wide for it (the caller then uses the generic column sums).
+bool launch_db2_partials(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, cudaStream_t s,
+                         cudaError_t* err) {
+  const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
+  if (R_cap == 0) { *err = cudaSuccess; return false; }
+  if (c->dtype == 1) {
+    if (nvec <= 32) { *err = launch_cbc<bf16, 1, false>(c, nullptr, nullptr, nullptr, nullptr, offsets, R_cap, (void*)d_eout, nullptr, s); return true; }
+    if (nvec <= 64) { *err = launch_cbc<bf16, 2, false>(c, nullptr, nullptr, nullptr, nullptr, offsets, R_cap, (void*)d_eout, nullptr, s); return true; }
+    if (nvec <= 96) { *err = launch_cbc<bf16, 3, false>(c, nullptr, nullptr, nullptr, nullptr, offsets, R_cap, (void*)d_eout, nullptr, s); return true; }
+    if (nvec <= 128) { *err = launch_cbc<bf16, 4, false>(c, nullptr, nullptr, nullptr, nullptr, offsets, R_cap, (void*)d_eout, nullptr, s); return true; }
+  } else {
+    if (nvec <= 32) { *err = launch_cbc<float, 1, false>(c, nullptr, nullptr, nullptr, nullptr, offsets, R_cap, (void*)d_eout, nullptr, s); return true; }
+    if (nvec <= 64) { *err = launch_cbc<float, 2, false>(c, nullptr, nullptr, nullptr, nullptr, offsets, R_cap, (void*)d_eout, nullptr, s); return true; }
+  }
+  return false;
+}
+
+cudaError_t launch_combine_bwd(moe_ctx* c, const void* dy, const void* e_out, const float* row_gate,
                                const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
                                float* dG_row, cudaStream_t s) {
+  c->db2_src = nullptr;
   if (R_cap == 0) return cudaSuccess;
+  if (c->world == 1 && !c->comm && c->E_local == c->E) {
+    // single rank: also leave the db2 partials for moe_expert_ffn_bwd
+    const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
+    if (c->dtype == 1) {
+      if (nvec <= 32) return launch_cbc<bf16, 1>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+      if (nvec <= 64) return launch_cbc<bf16, 2>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+      if (nvec <= 96) return launch_cbc<bf16, 3>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+      if (nvec <= 128) return launch_cbc<bf16, 4>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+    } else {
+      if (nvec <= 32) return launch_cbc<float, 1>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+      if (nvec <= 64) return launch_cbc<float, 2>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+    }
+  }
   const unsigned grid = (unsigned)((R_cap + 7) / 8);
   if (c->dtype == 1)
     combine_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)e_out, row_gate, row_token, offsets,
@@ -397,8 +577,8 @@ cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int
     // gate term dlogits W_g^T on tensor cores (bf16, hi|lo split of dlogits) -> added by the gather pass
     cudaError_t e = gate_tc_dx(c, dlogits, Wg, c->dxg, s);
     if (e != cudaSuccess) return e;
-    dispatch_bwd_kernel<bf16, bf16><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, (const bf16*)c->dxg, c->T,
-                                                         c->d, c->E, (bf16*)dx), count_launch();
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), dispatch_bwd_kernel<bf16, bf16, QV><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, (const bf16*)c->dxg, c->T,
+                                                         c->d, c->E, (bf16*)dx), count_launch())
     return cudaGetLastError();
   }
   const float* dxg = nullptr;
@@ -414,11 +594,11 @@ cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int
     dxg = c->dxg;
   }
   if (c->dtype == 1)
-    dispatch_bwd_kernel<bf16, float><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, dxg, c->T, c->d, c->E,
-                                                          (bf16*)dx), count_launch();
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), dispatch_bwd_kernel<bf16, float, QV><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, dxg, c->T, c->d, c->E,
+                                                          (bf16*)dx), count_launch())
   else
-    dispatch_bwd_kernel<float, float><<<grid, 256, 0, s>>>((const float*)dx_perm, slot, dxg, c->T, c->d, c->E,
-                                                           (float*)dx), count_launch();
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>((const float*)dx_perm, slot, dxg, c->T, c->d, c->E,
+                                                           (float*)dx), count_launch())
   return cudaGetLastError();
 }
 
