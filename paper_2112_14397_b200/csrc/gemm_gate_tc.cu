@@ -1,7 +1,8 @@
 // gemm_gate_tc.cu -- tcgen05 kernels for the three skinny gate contractions (bf16 path):
 //
 //   GATE  L = x W_g                [T, E]   M = 128 tokens / CTA, N = Ep (E padded to 16), K = d
-//         fused with steps 2-3 (gate_token: Gumbel, tau-softmax, threshold, fp64 refine)
+//         (E % 16 != 0: logits to HBM, steps 2-3 in gate_softmax_tpt_kernel + gate_refine_kernel;
+//          E % 16 == 0 uses the persistent fused kernel below, steps 1-3 in one launch)
 //   DXG   dx = dL W_g^T + sum_e dx_perm[slot]   M = 128 tokens, N = 256 of d, K = Kp
 //         (replaces moe_dispatch_bwd's gather pass: the un-permute sum runs in the epilogue)
 //   DWG   dW_g = x^T dL                [d, E]   M = 128 of d, N = Kp, K = T split over CTAs
@@ -16,6 +17,7 @@
 // products near fp32 accuracy.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "gate_token.cuh"
@@ -290,6 +292,307 @@ __global__ void __launch_bounds__(Threads<MODE>::N) gate_tc_kernel(const __grid_
   }
 }
 
+// ---------------------------------------------------------------- fused persistent gate
+// Steps 1-3 in one persistent kernel (E % 16 == 0, E <= 64): x tiles stream through a 4-stage
+// TMA ring, logits accumulate in NG K-group TMEM column blocks (the same grouping and TwoSum as
+// the GATE epilogue above), two TMEM accumulators let tile i+1's loads and MMAs overlap tile i's
+// epilogue.  Epilogue: 4 TMEM warps (thread = token row) add the K groups and write the fp32
+// logits block to a double-buffered shared [128][E+1] buffer; 16 softmax warps then give each
+// token 4 adjacent lanes (E/4 experts each): Gumbel noise, tau-softmax (max / sum combined over
+// the 4 lanes by xor shuffles), threshold / guard / top-1 decision and band test as in
+// gate_softmax_tpt_kernel, u read and probs / slot written as 256-byte row segments.
+// Near-boundary tokens are queued for gate_refine_kernel (fp64), as before.  The logits never
+// reach HBM.
+constexpr int FG_STAGES = 4;
+constexpr int FG_SWARPS = 16;                     // 512 threads = 128 tokens x 4 lanes
+constexpr int FG_THREADS = 64 + 128 + 32 * FG_SWARPS;
+
+struct FgParams {
+  int T, d, E, ng, kb_per_group, nkb, ntiles, nblk;
+  float tau, thr;
+  int top1;
+  const float* u;
+  float* probs;
+  int* slot;
+  int* counts;
+  int* blk_cnt;
+  int* near_band;
+  int* flags;
+  int* rq_count;
+  int* rq_list;
+};
+
+// merge two (best, second, argmax) triples; ties keep the lower expert index as best
+__device__ __forceinline__ void top2_merge(float& b, float& s, int& a, float b2, float s2, int a2) {
+  if (b2 > b || (b2 == b && a2 < a)) {
+    s = fmaxf(b, s2);
+    b = b2;
+    a = a2;
+  } else {
+    s = fmaxf(s, b2);
+  }
+}
+
+template <int E_T>
+__global__ void __launch_bounds__(FG_THREADS, 1)
+    gate_fused_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, FgParams p) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_BYTES = ((E_T * BK * 2) + 1023) & ~1023;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int LP = E_T + 4;                      // row pitch of the logits block (16-byte aligned rows)
+  constexpr int EPT = E_T / 4;                     // experts per lane
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_u32 = tc::smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_u32 & 1023)) & 1023);
+  float* lbuf = reinterpret_cast<float*>(smem + FG_STAGES * STAGE);      // [2][128][LP]
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(lbuf + 2 * 128 * LP);
+  uint64_t* empty_bar = full_bar + FG_STAGES;
+  uint64_t* tfull_bar = empty_bar + FG_STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint64_t* lfull_bar = tempty_bar + 2;
+  uint64_t* lempty_bar = lfull_bar + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(lempty_bar + 2);
+  int* s_cnt0 = reinterpret_cast<int*>(s_tmem + 4);     // [2][E_T] per-tile counts (double-buffered by tile parity)
+  int* s_band0 = s_cnt0 + 2 * E_T;                        // [2]
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch(&tmX);
+    tc::tma_prefetch(&tmW);
+    for (int i = 0; i < FG_STAGES; ++i) {
+      tc::mbar_init(&full_bar[i], 1);
+      tc::mbar_init(&empty_bar[i], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull_bar[a], 1);
+      tc::mbar_init(&tempty_bar[a], 4);
+      tc::mbar_init(&lfull_bar[a], 4);
+      tc::mbar_init(&lempty_bar[a], FG_SWARPS);
+    }
+    tc::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < 2 * E_T; i += FG_THREADS) s_cnt0[i] = 0;
+  if (threadIdx.x < 2) s_band0[threadIdx.x] = 0;
+  if (warp == 1) tc::tmem_alloc(s_tmem, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        const int m0 = tile * BM;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          tc::mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE;
+          tc::mbar_arrive_expect_tx(&full_bar[stage], A_BYTES + E_T * BK * 2);
+          tc::tma_load_2d(sa, &tmX, &full_bar[stage], kb * BK, m0);
+          tc::tma_load_2d(sa + A_BYTES, &tmW, &full_bar[stage], kb * BK, 0);
+          if (++stage == FG_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_bf16(BM, E_T, 0, 0);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      const uint32_t smem_base = tc::smem_u32(smem);
+      for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc::tc_fence_after();
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          tc::mbar_wait(&full_bar[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t sa = smem_base + stage * STAGE;
+          const uint32_t sb = sa + A_BYTES;
+          const int g = kb / p.kb_per_group;
+          const bool first = (kb % p.kb_per_group) == 0;
+          const uint32_t d_tmem = tmem_base + acc * 256 + g * E_T;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc::mma_bf16(d_tmem, tc::smem_desc_sw128(sa + k * 32, 16, 1024), tc::smem_desc_sw128(sb + k * 32, 16, 1024),
+                         idesc, (!first || k) ? 1u : 0u);
+          tc::mma_commit(&empty_bar[stage]);
+          if (++stage == FG_STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::mma_commit(&tfull_bar[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ TMEM warps: logits block
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t t_row = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+    int acc = 0, it = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+      const int b = it & 1;
+      tc::mbar_wait(&tfull_bar[acc], acc_phase);
+      tc::tc_fence_after();
+      tc::mbar_wait(&lempty_bar[b], ((it >> 1) & 1) ^ 1);
+      float* L = lbuf + (b * 128 + row) * LP;
+#pragma unroll
+      for (int c0 = 0; c0 < E_T; c0 += 16) {
+        float sacc[16], cacc[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) sacc[j] = cacc[j] = 0.f;
+        for (int g = 0; g < p.ng; ++g) {
+          uint32_t r[16];
+          tc::tmem_ld16(t_row + acc * 256 + g * E_T + c0, r);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float v = __uint_as_float(r[j]);
+            const float s1 = sacc[j] + v;
+            const float bp = s1 - sacc[j];
+            cacc[j] += (sacc[j] - (s1 - bp)) + (v - bp);
+            sacc[j] = s1;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(L + c0 + j) = make_float4(sacc[j] + cacc[j], sacc[j + 1] + cacc[j + 1],
+                                                               sacc[j + 2] + cacc[j + 2], sacc[j + 3] + cacc[j + 3]);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(&tempty_bar[acc]);
+        tc::mbar_arrive(&lfull_bar[b]);
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    // ------------------------------------------------------------ softmax lanes: steps 2-3
+    const int st = threadIdx.x - 192;                  // 0..511
+    const int tok = st >> 2, q = st & 3;               // token of the tile, quarter of its experts
+    const int e0 = q * EPT;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+      const int b = it & 1;
+      const int t = tile * BM + tok;
+      const bool live = t < p.T;
+      int* s_cnt = s_cnt0 + b * E_T;
+      int* s_band = s_band0 + b;
+      // the noise row segment is fetched before waiting for the logits
+      float U[EPT];
+      if (p.u && live) {
+#pragma unroll
+        for (int j = 0; j < EPT; j += 4) {
+          const float4 w = ld_nc_f4(p.u + (long long)t * p.E + e0 + j);
+          U[j] = w.x; U[j + 1] = w.y; U[j + 2] = w.z; U[j + 3] = w.w;
+        }
+      }
+      tc::mbar_wait(&lfull_bar[b], (it >> 1) & 1);
+      float Z[EPT];
+      const float* L = lbuf + (b * 128 + tok) * LP + e0;
+#pragma unroll
+      for (int j = 0; j < EPT; j += 4) {
+        const float4 w = *reinterpret_cast<const float4*>(L + j);
+        Z[j] = w.x; Z[j + 1] = w.y; Z[j + 2] = w.z; Z[j + 3] = w.w;
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&lempty_bar[b]);
+      // ---- noise, tau-softmax
+      float mx = -INFINITY;
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        if (!isfinite(Z[j])) bad = true;
+        const float zeta = p.u ? -logf(-logf(U[j])) : 0.f;
+        Z[j] = (Z[j] + zeta) / p.tau;
+        mx = fmaxf(mx, Z[j]);
+      }
+      if (bad && live && atomicOr(&p.flags[0], kFlagNonFinite) == 0) p.flags[1] = t;
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      float sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        Z[j] = expf(Z[j] - mx);
+        sum += Z[j];
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      const float inv = 1.0f / sum;
+      bool any_pass = false, near = false, band_thr = false;
+      float best = -1.f, second = -1.f;
+      int am = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const float pe = Z[j] * inv;
+        Z[j] = pe;
+        if (pe > p.thr) any_pass = true;
+        const float dt = fabsf(pe - p.thr);
+        if (dt < kRefine) near = true;
+        if (dt < kBand) band_thr = true;
+        if (pe > best) { second = best; best = pe; am = e0 + j; }
+        else if (pe > second) second = pe;
+      }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        any_pass |= __shfl_xor_sync(0xffffffffu, (int)any_pass, o) != 0;
+        near |= __shfl_xor_sync(0xffffffffu, (int)near, o) != 0;
+        band_thr |= __shfl_xor_sync(0xffffffffu, (int)band_thr, o) != 0;
+        const float b2 = __shfl_xor_sync(0xffffffffu, best, o);
+        const float s2 = __shfl_xor_sync(0xffffffffu, second, o);
+        const int a2 = __shfl_xor_sync(0xffffffffu, am, o);
+        top2_merge(best, second, am, b2, s2, a2);
+      }
+      const bool argmax_decided = p.top1 || !any_pass;
+      if (p.top1) near = false;
+      if (argmax_decided && best - second < kRefine) near = true;
+      uint32_t sv[EPT];
+      if (near) {
+        if (live && q == 0) p.rq_list[atomicAdd(p.rq_count, 1)] = t;   // decided (and counted) by gate_refine_kernel
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) sv[j] = 0xffffffffu;
+      } else {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const bool sel = argmax_decided ? (e0 + j == am) : (Z[j] > p.thr);
+          sv[j] = sel ? 0u : 0xffffffffu;
+          if (sel && live) atomicAdd(&s_cnt[e0 + j], 1);
+        }
+        const bool in_band = argmax_decided ? (best - second) < kBand : band_thr;
+        if (in_band && live && q == 0) atomicAdd(s_band, 1);
+      }
+      if (live) {
+#pragma unroll
+        for (int j = 0; j < EPT; j += 4) {
+          *reinterpret_cast<float4*>(p.probs + (long long)t * p.E + e0 + j) = make_float4(Z[j], Z[j + 1], Z[j + 2], Z[j + 3]);
+          *reinterpret_cast<uint4*>(p.slot + (long long)t * p.E + e0 + j) = make_uint4(sv[j], sv[j + 1], sv[j + 2], sv[j + 3]);
+        }
+      }
+      named_bar_sync(2, 32 * FG_SWARPS);
+      for (int e = st; e < p.E; e += 32 * FG_SWARPS) {
+        const int c = s_cnt[e];
+        p.blk_cnt[(long long)e * p.nblk + tile] = c;
+        if (c) atomicAdd(&p.counts[e], c);
+        s_cnt[e] = 0;
+      }
+      if (st == 0 && s_band[0]) {
+        atomicAdd(p.near_band, s_band[0]);
+        s_band[0] = 0;
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem_base, 512);
+  }
+}
+
 // fp64 decisions for the deferred tokens (block per token)
 __global__ void __launch_bounds__(256) gate_refine_kernel(const bf16* __restrict__ x, const bf16* __restrict__ Wg,
                                                           const float* __restrict__ u, int d, int E, float tau, float thr,
@@ -370,6 +673,24 @@ static bool map2d(CUtensorMap* m, const void* ptr, long long rows, long long col
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int E_T>
+static cudaError_t launch_fused(const CUtensorMap& mX, const CUtensorMap& mW, const FgParams& p, int grid,
+                                cudaStream_t s) {
+  constexpr int STAGE = BM * BK * 2 + (((E_T * BK * 2) + 1023) & ~1023);
+  size_t smem = 1024 + FG_STAGES * STAGE + 2 * 128 * (E_T + 4) * 4 + 1024;
+  if (smem < 120 * 1024) smem = 120 * 1024;      // one CTA per SM (each allocates all 512 TMEM columns)
+  auto k = gate_fused_tc_kernel<E_T>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<grid, FG_THREADS, smem, s>>>(mX, mW, p), count_launch();
+  return cudaGetLastError();
+}
+
+static bool getenv_flag(const char* name) {
+  const char* v = getenv(name);
+  return v && v[0] && v[0] != '0';
+}
+
 static int pow2_cols(int c) {
   int p = 32;
   while (p < c) p <<= 1;
@@ -416,18 +737,39 @@ cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, con
   Params p{};
   p.mode = GATE; p.T = c->T; p.d = d; p.E = E; p.Ep = Ep;
   const int nkb = d / BK;
-  int ng = 256 / Ep;                      // <= 256 TMEM columns (2 CTAs / SM)
+  int ng = 256 / Ep;                      // <= 256 TMEM columns per accumulator
   if (ng > nkb) ng = nkb;
   p.kb_per_group = (nkb + ng - 1) / ng;
   p.ng = (nkb + p.kb_per_group - 1) / p.kb_per_group;
   p.tmem_cols = pow2_cols(p.ng * Ep);
   p.logits = c->logits;
-  const size_t misc = sizeof(int) * 132 + sizeof(float) * 128 * (E + 1);
-  cudaError_t e = cudaMemsetAsync(c->rq, 0, sizeof(int), s);
-  if (e != cudaSuccess) return e;
-  if ((e = launch<GATE>(mA, mB, p, dim3(c->nblk), Ep, misc, s)) != cudaSuccess) return e;
-  if ((e = launch_gate_softmax_tpt(c, c->logits, u, tau, thr, top1, probs, slot, counts, near_band, s)) != cudaSuccess)
-    return e;
+  cudaError_t e = cudaSuccess;
+  const bool fused = E % 16 == 0 && c->T > 0 && !getenv_flag("MOE_GATE_UNFUSED");
+  if (fused) {
+    // steps 1-3 in one persistent kernel (logits stay on chip; near tokens refined inline)
+    FgParams q{};
+    q.T = c->T; q.d = d; q.E = E; q.ng = p.ng; q.kb_per_group = p.kb_per_group; q.nkb = nkb;
+    q.ntiles = c->nblk; q.nblk = c->nblk; q.tau = tau; q.thr = thr; q.top1 = top1;
+    q.u = u; q.probs = probs; q.slot = slot;
+    q.counts = counts; q.blk_cnt = c->blk_cnt; q.near_band = near_band; q.flags = c->flags;
+    q.rq_count = c->rq; q.rq_list = c->rq + 1;
+    if ((e = cudaMemsetAsync(c->rq, 0, sizeof(int), s)) != cudaSuccess) return e;
+    const int grid = c->nblk < c->sm_count ? c->nblk : c->sm_count;
+    switch (E) {
+      case 16: e = launch_fused<16>(mA, mB, q, grid, s); break;
+      case 32: e = launch_fused<32>(mA, mB, q, grid, s); break;
+      case 48: e = launch_fused<48>(mA, mB, q, grid, s); break;
+      default: e = launch_fused<64>(mA, mB, q, grid, s); break;
+    }
+    if (e != cudaSuccess) return e;
+  } else {
+    if ((e = cudaMemsetAsync(c->rq, 0, sizeof(int), s)) != cudaSuccess) return e;
+    const size_t misc = sizeof(int) * 132 + sizeof(float) * 128 * (E + 1);
+    if ((e = launch<GATE>(mA, mB, p, dim3(c->nblk), Ep, misc, s)) != cudaSuccess) return e;
+    if ((e = launch_gate_softmax_tpt(c, c->logits, u, tau, thr, top1, probs, slot, counts, near_band, s)) !=
+        cudaSuccess)
+      return e;
+  }
   gate_refine_kernel<<<c->sm_count, 256, 0, s>>>((const bf16*)x, (const bf16*)Wg, u, d, E, tau, thr, top1, probs, slot,
                                                  counts, c->blk_cnt, c->nblk, near_band, c->rq, c->rq + 1),
       count_launch();
