@@ -182,7 +182,7 @@ cudaError_t launch_gate_typed(const moe_ctx* c, const void* x, const void* Wg, c
 __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     const float* __restrict__ dG_row, const int* __restrict__ slot, const float* __restrict__ probs,
     int T_, int E, float tau, float alpha, const int* __restrict__ counts, double bal_scale,
-    float* __restrict__ dlogits) {
+    float* __restrict__ dlogits, bf16* __restrict__ dL2, int Ep, int Kp) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
@@ -205,8 +205,16 @@ __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
 #pragma unroll
   for (int i = 0; i < kMaxEPL; ++i) {
     int e = lane + 32 * i;
-    if (e < E) dlogits[(long long)t * E + e] = p[i] * (dp[i] - s) * inv_tau;
+    const float v = e < E ? p[i] * (dp[i] - s) * inv_tau : 0.f;
+    if (e < E) dlogits[(long long)t * E + e] = v;
+    if (dL2 && e < Ep) {   // tensor-core operand row [hi | lo | 0] of dlogits (dl_split_kernel's layout)
+      const bf16 hi = __float2bfloat16_rn(v);
+      dL2[(long long)t * Kp + e] = hi;
+      dL2[(long long)t * Kp + Ep + e] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
   }
+  if (dL2)
+    for (int k = 2 * Ep + lane; k < Kp; k += 32) dL2[(long long)t * Kp + k] = __float2bfloat16_rn(0.f);
 }
 
 // out[i] = sum_z part[z][i], fixed order
@@ -261,11 +269,17 @@ cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t
                             float* dWg, float* dlogits, cudaStream_t s) {
   if (c->T == 0) return cudaMemsetAsync(dWg, 0, sizeof(float) * c->d * c->E, s);
   double bal = alpha > 0.f ? (double)alpha * c->E / ((double)B_total * (double)B_total) : 0.0;
+  const bool tc = gate_tc_supported(c);
+  bf16* dL2 = tc ? reinterpret_cast<bf16*>(gate_dl2_buffer(c)) : nullptr;
+  const int Ep = (c->E + 15) / 16 * 16, Kp = (2 * Ep + 63) / 64 * 64;
   gate_bwd_token_kernel<<<(c->T + 7) / 8, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts, bal,
-                                                        dlogits), count_launch();
+                                                        dlogits, dL2, Ep, Kp), count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  if (gate_tc_supported(c)) return gate_tc_dwg(c, x, dlogits, dWg, s);
+  if (tc) {
+    const_cast<moe_ctx*>(c)->dl2_src = dlogits;     // the hi|lo operand of these dlogits is in the workspace
+    return gate_tc_dwg(c, x, dlogits, dWg, s);
+  }
   // dWg [d, E] = x^T [d, T] . dlogits [T, E]  (split-K, deterministic reduction)
   SimtGemm g{};
   g.A = x; g.sAm = 1; g.sAk = c->d;

@@ -34,6 +34,7 @@ struct moe_ctx {
   int db2_S;           // row splits per expert of the fused combine_bwd
   // which (d_eout, offsets, R_cap) the db2 partials belong to; moe_expert_ffn_bwd uses them only
   // for exactly that triple (else it sums d_eout itself), then clears this
+  const float* dl2_src;   // dlogits whose [hi | lo] bf16 split currently sits in gate_scratch (tcgen05 gate bwd)
   const void* db2_src;
   const int* db2_off;
   long long db2_rcap;
@@ -120,6 +121,7 @@ cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, con
                             int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
                             cudaStream_t s);
 cudaError_t gate_tc_dx(const moe_ctx* c, const float* dlogits, const void* Wg, void* dxg_bf16, cudaStream_t s);
+void* gate_dl2_buffer(const moe_ctx* c);   // [T, Kp] bf16 hi|lo operand rows inside gate_scratch
 cudaError_t gate_tc_dwg(const moe_ctx* c, const void* x, const float* dlogits, float* dWg, cudaStream_t s);
 cudaError_t tc_dense_store(const moe_ctx* c, const void* A, long long rows, int K, const void* B, int N, void* out,
                            const int* offsets_dev, cudaStream_t s);

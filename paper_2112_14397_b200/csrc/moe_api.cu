@@ -132,6 +132,7 @@ void carve_workspace(moe_ctx* c) {
   c->db2part = reinterpret_cast<float*>(c->ws + k.db2part);
   c->db2_S = db2_splits(c);
   c->db2_src = nullptr;
+  c->dl2_src = nullptr;
   c->db2_off = nullptr;
   c->db2_rcap = 0;
 }

@@ -159,12 +159,28 @@ __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src,
                                                  const TX* __restrict__ extra, T* __restrict__ out, int lane) {
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
+  constexpr bool TWO = QV <= 3;                     // two rows in flight when registers allow
   for (int v0 = 0; v0 < nvec; v0 += 32 * QV) {
     float acc[QV][V];
 #pragma unroll
     for (int q = 0; q < QV; ++q)
 #pragma unroll
       for (int k = 0; k < V; ++k) acc[q][k] = 0.f;
+    if (extra) {                                      // the extra row term starts the sum (loads issued first)
+#pragma unroll
+      for (int q = 0; q < QV; ++q) {
+        const int v = v0 + q * 32 + lane;
+        if (v < nvec) {
+          if (sizeof(TX) == 2) {
+            unpack16(ld_nc_v4(extra + (long long)v * V), acc[q], bf16());
+          } else {
+#pragma unroll
+            for (int h = 0; h < V / 4; ++h)
+              unpack16(ld_nc_v4(reinterpret_cast<const float*>(extra) + (long long)v * V + 4 * h), acc[q] + 4 * h, float());
+          }
+        }
+      }
+    }
     for (int g = 0; g < E; g += 32) {
       const int sv = (g + lane < E) ? slot_row[g + lane] : -1;
       unsigned bal = __ballot_sync(0xffffffffu, sv >= 0);
@@ -172,7 +188,7 @@ __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src,
         // two selected rows per pass (both rows' loads in flight), accumulated in ascending e
         const int b = __ffs(bal) - 1;
         bal &= bal - 1;
-        const bool two = bal != 0;
+        const bool two = TWO && bal != 0;
         const int b2 = two ? __ffs(bal) - 1 : b;
         if (two) bal &= bal - 1;
         const int r = __shfl_sync(0xffffffffu, sv, b);
@@ -209,10 +225,6 @@ __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src,
     for (int q = 0; q < QV; ++q) {
       const int v = v0 + q * 32 + lane;
       if (v < nvec) {
-        if (extra) {
-#pragma unroll
-          for (int k = 0; k < V; ++k) acc[q][k] += to_f32(extra[(long long)v * V + k]);
-        }
         st_v4(out + (long long)v * V, pack16(acc[q], T()));
       }
     }
@@ -221,7 +233,7 @@ __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src,
 
 // y[t] = sum_{e asc} row_gate[r] * e_out[r], r = slot[t,e]
 template <typename T, int QV>
-__global__ void __launch_bounds__(256) combine_kernel(const T* __restrict__ e_out, const float* __restrict__ row_gate,
+__global__ void __launch_bounds__(256, 4) combine_kernel(const T* __restrict__ e_out, const float* __restrict__ row_gate,
                                                       const int* __restrict__ slot, int T_, int d, int E,
                                                       T* __restrict__ y) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -377,9 +389,9 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
 }
 
 // ------------------------------------------------------------------ dispatch backward
-// One warp per token: dx[t] = sum_{e asc} dx_perm[slot[t,e]] + dxg[t] (fp32, may be NULL).
+// One warp per token: dx[t] = dxg[t] + sum_{e asc} dx_perm[slot[t,e]]  (dxg bf16 or fp32, may be NULL).
 template <typename T, typename TX, int QV>
-__global__ void __launch_bounds__(256) dispatch_bwd_kernel(const T* __restrict__ dx_perm, const int* __restrict__ slot,
+__global__ void __launch_bounds__(256, 4) dispatch_bwd_kernel(const T* __restrict__ dx_perm, const int* __restrict__ slot,
                                                            const TX* __restrict__ dxg, int T_, int d, int E,
                                                            T* __restrict__ dx) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
