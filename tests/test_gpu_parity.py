@@ -231,3 +231,37 @@ def test_recompute_mode_matches_saved_mode(cfg_name, T):
     assert torch.equal(outs[0][0], outs[1][0])
     for k in outs[0][1]:
         assert torch.equal(outs[0][1][k], outs[1][1][k]), k
+
+
+# ---- shapes off the benchmark grid: the other gate paths and partial GEMM tiles ----------
+def _shape(name, T, d, f, E, tau, c, wg_var=None):
+    import math
+    return dataclasses.replace(configs.C3, name=name, T=T, d_model=d, d_ff=f, E=E, tau=tau, threshold=c,
+                               wg_std=math.sqrt((wg_var if wg_var else 1.0) / d))
+
+
+def test_bf16_E48_fused_gate_16_wide_boxes():
+    # E % 32 != 0: fused gate with 12 experts per lane quarter; N=48 gate MMA
+    _run(_shape("E48", 700, 256, 512, 48, 0.5, 0.03))
+
+
+def test_bf16_E24_unfused_gate_path():
+    # E % 16 != 0: tcgen05 logits (padded to 32) to HBM + thread-per-token softmax + fp64 refine queue
+    _run(_shape("E24", 515, 192, 384, 24, 0.7, 0.05))
+
+
+def test_bf16_unfused_gate_env_matches_oracle(monkeypatch):
+    monkeypatch.setenv("MOE_GATE_UNFUSED", "1")
+    _run(_shape("E16u", 400, 128, 256, 16, 1.0, 0.02))
+
+
+def test_bf16_partial_tiles_simt_gate():
+    # E > 64 (SIMT warp-per-token gate with inline fp64 refine); d = 192 and d_ff = 320 are
+    # not multiples of the 256-wide GEMM tile: partial N tiles on every expert GEMM
+    _run(_shape("odd", 300, 192, 320, 80, 0.8, 0.01))
+
+
+def test_bf16_single_expert_is_dense_ffn():
+    # E = 1: every token to the one expert with weight 1 (P:311 special case), dW_g = 0
+    rep, g = _run(_shape("E1", 256, 128, 256, 1, 1.0, 0.0))
+    assert float(np.abs(g.grads["dWg"]).max()) == 0.0
