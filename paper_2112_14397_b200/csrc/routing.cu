@@ -309,11 +309,26 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
   const long long per = ((len + S - 1) / S + 7) / 8 * 8;
   const long long r0 = off0 + (long long)s * per, r1 = min(off1, r0 + per);
   const int nvec = d / V;
-  float acc[MAXV][V];
+  // this warp's column sums live in its own row of red[] (no registers held across rows)
+  float* racc = red + warp * d;
+  for (int n = lane * 4; n < d; n += 128) *reinterpret_cast<float4*>(racc + n) = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();
+  auto acc_add = [&](int v, const float* o) {
 #pragma unroll
-  for (int j = 0; j < MAXV; ++j)
-#pragma unroll
-    for (int k = 0; k < V; ++k) acc[j][k] = 0.f;
+    for (int h = 0; h < V; h += 4) {
+      float4* a = reinterpret_cast<float4*>(racc + v * V + h);
+      float4 w = *a;
+      w.x += o[h]; w.y += o[h + 1]; w.z += o[h + 2]; w.w += o[h + 3];
+      *a = w;
+    }
+  };
+  // row metadata one row ahead: the dy gather of row r does not wait for its row_token load
+  int t_nx = -1;
+  float g_nx = 0.f;
+  if (COMPUTE && r0 + warp < r1) {
+    t_nx = row_token[r0 + warp];
+    g_nx = row_gate[r0 + warp];
+  }
   for (long long r = r0 + warp; r < r1; r += 8) {
     T* dst = d_eout + r * d;
     if (!COMPUTE) {
@@ -323,13 +338,17 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
         if (v < nvec) {
           float o[V];
           unpack16(ld_nc_v4(dst + (long long)v * V), o, T());
-#pragma unroll
-          for (int k = 0; k < V; ++k) acc[j][k] += o[k];
+          acc_add(v, o);
         }
       }
       continue;
     }
-    const int t = row_token[r];
+    const int t = t_nx;
+    const float gw = g_nx;
+    if (r + 8 < r1) {
+      t_nx = row_token[r + 8];
+      g_nx = row_gate[r + 8];
+    }
     if (t < 0) {
 #pragma unroll
       for (int j = 0; j < MAXV; ++j) {
@@ -339,7 +358,6 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
       if (lane == 0) dG_row[r] = 0.f;
       continue;
     }
-    const float gw = row_gate[r];
     uint4 qa[MAXV], qb[MAXV];
 #pragma unroll
     for (int j = 0; j < MAXV; ++j) {
@@ -365,19 +383,11 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
         const uint4 w = pack16(o, T());
         st_v4(dst + (long long)v * V, w);
         unpack16(w, o, T());                        // the stored (rounded) values
-#pragma unroll
-        for (int k = 0; k < V; ++k) acc[j][k] += o[k];
+        acc_add(v, o);
       }
     }
     dot = warp_sum(dot);
     if (lane == 0) dG_row[r] = dot;
-  }
-#pragma unroll
-  for (int j = 0; j < MAXV; ++j) {
-    const int v = lane + 32 * j;
-    if (v < nvec)
-#pragma unroll
-      for (int k = 0; k < V; ++k) red[warp * d + v * V + k] = acc[j][k];
   }
   __syncthreads();
   for (int n = threadIdx.x; n < d; n += 256) {
