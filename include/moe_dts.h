@@ -231,6 +231,33 @@ int moe_ep_dispatch(moe_ctx* ctx, const void* send_rows, void* recv_rows, int wi
                     void* stream);
 int moe_ep_combine(moe_ctx* ctx, const void* recv_rows, void* send_rows, int width, void* stream);
 
+/* ---- NEXT #4: topology-aware hierarchical all-to-all ----
+ * For multi-node EP (nodes of gpus_per_node consecutive ranks).  Rows from node A to node
+ * B != A go source -> relay(A,B) (intra-node gather; relay(X,Y) = local GPU Y mod G of node X)
+ * -> relay(B,A) (ONE inter-node message per ordered node pair, aggregating the G^2 GPU-pair
+ * payloads: the paper's "#GPU^2 times larger" message) -> destination (intra-node scatter,
+ * written straight into the recv layout).  Same-node rows go directly.  The recv / send
+ * layouts and the results are identical to the flat exchange; only the message set differs.
+ * moe_ep_set_topology: gpus_per_node must divide world; world (the default) = flat.  Call
+ * before moe_ep_plan.  After the plan, moe_ep_stage_rows gives the relay staging rows this
+ * rank needs; the caller owns a buffer of that many `width`-element D rows and passes it
+ * with moe_ep_set_stage before moe_ep_dispatch / moe_ep_combine (MOE_ECAPACITY otherwise). */
+int moe_ep_set_topology(moe_ctx* ctx, int gpus_per_node);
+int moe_ep_stage_rows(moe_ctx* ctx, int64_t* rows);
+int moe_ep_set_stage(moe_ctx* ctx, void* stage, int64_t rows_cap);
+/* Host-only accessor for tests: the messages of hierarchical phase 0 / 1 / 2 (dispatch
+ * direction), sends (is_recv = 0) or receives, in NCCL posting order: peer, buffer
+ * (0 send layout, 1 recv layout, 2 relay gather stage, 3 relay receive stage; stage 3 starts
+ * after the gather stage's rows), row offset and rows.  n_out = 0 for a flat plan. */
+int moe_ep_hier_chunks(moe_ctx* ctx, int phase, int is_recv, int32_t* peer, int32_t* buf, int64_t* row,
+                       int32_t* nrows, int max_chunks, int* n_out);
+/* Host-only cost-model identities of both plans on a virtual topology (no ctx, no GPU) for
+ * routing counts_all [world][E]: stats[8] = { flat inter-node (src, dst) GPU pairs with
+ * payload, flat inter-node rows, flat intra-node rows, hierarchical inter-node messages,
+ * hierarchical inter-node rows, hierarchical intra-node rows moved, ordered node pairs with
+ * payload, largest inter-node message (rows) }. */
+int moe_ep_topology_stats(int world, int gpus_per_node, int E, const int32_t* counts_all, int64_t* stats);
+
 /* In-place sum all-reduce over the EP group: fp32 (dW_g, C6) or int32 (global counts, C7). */
 int moe_ep_allreduce(moe_ctx* ctx, void* buf, int64_t n, int is_int32, void* stream);
 

@@ -51,6 +51,11 @@ SIGNATURES = {
     "moe_ep_dispatch": (_I, [_P, _P, _P, _I, _L, _P]),
     "moe_ep_combine": (_I, [_P, _P, _P, _I, _P]),
     "moe_ep_allreduce": (_I, [_P, _P, _L, _I, _P]),
+    "moe_ep_set_topology": (_I, [_P, _I]),
+    "moe_ep_stage_rows": (_I, [_P, C.POINTER(_L)]),
+    "moe_ep_set_stage": (_I, [_P, _P, _L]),
+    "moe_ep_hier_chunks": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, C.POINTER(_I)]),
+    "moe_ep_topology_stats": (_I, [_I, _I, _I, _P, _P]),
 }
 
 
@@ -267,3 +272,43 @@ def moe_ep_combine(ctx, recv_rows, send_rows, width: int, stream=None):
 
 def moe_ep_allreduce(ctx, buf, n: int, is_int32: bool = False, stream=None):
     _call("moe_ep_allreduce", ctx, _ptr(buf), int(n), int(is_int32), _stream(stream))
+
+
+# ---- NEXT #4: topology-aware hierarchical exchange
+def moe_ep_set_topology(ctx, gpus_per_node: int):
+    _call("moe_ep_set_topology", ctx, int(gpus_per_node))
+
+
+def moe_ep_stage_rows(ctx) -> int:
+    r = C.c_int64()
+    _call("moe_ep_stage_rows", ctx, C.byref(r))
+    return int(r.value)
+
+
+def moe_ep_set_stage(ctx, stage, rows_cap: int):
+    _call("moe_ep_set_stage", ctx, _ptr(stage) if stage is not None else None, int(rows_cap))
+
+
+def moe_ep_hier_chunks(ctx, phase: int, is_recv: bool):
+    """Host-only: list of (peer, buf, row, nrows) of hierarchical phase `phase` in NCCL posting
+    order (buf: 0 send layout, 1 recv layout, 2 relay gather stage, 3 relay receive stage)."""
+    import numpy as np
+    n = C.c_int()
+    _call("moe_ep_hier_chunks", ctx, int(phase), int(is_recv), None, None, None, None, 0, C.byref(n))
+    k = max(1, n.value)
+    peer, buf, nr = np.zeros(k, np.int32), np.zeros(k, np.int32), np.zeros(k, np.int32)
+    row = np.zeros(k, np.int64)
+    _call("moe_ep_hier_chunks", ctx, int(phase), int(is_recv), peer.ctypes.data, buf.ctypes.data, row.ctypes.data,
+          nr.ctypes.data, n.value, C.byref(n))
+    return [(int(peer[i]), int(buf[i]), int(row[i]), int(nr[i])) for i in range(n.value)]
+
+
+def moe_ep_topology_stats(world: int, gpus_per_node: int, E: int, counts_all) -> dict:
+    """Host-only cost-model identities of the flat and hierarchical plans (see moe_dts.h)."""
+    import numpy as np
+    ca = np.ascontiguousarray(counts_all, dtype=np.int32)
+    st = np.zeros(8, np.int64)
+    _call("moe_ep_topology_stats", int(world), int(gpus_per_node), int(E), ca.ctypes.data, st.ctypes.data)
+    keys = ("flat_inter_pairs", "flat_inter_rows", "flat_intra_rows", "hier_inter_msgs", "hier_inter_rows",
+            "hier_intra_rows", "node_pairs", "hier_max_msg_rows")
+    return {k: int(v) for k, v in zip(keys, st)}

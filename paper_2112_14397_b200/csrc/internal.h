@@ -43,6 +43,9 @@ struct moe_ctx {
   int* ep_off;         // [E_local + 1] recv-layout offsets (EP)
   int* ep_tot;         // [E_local] recv-layout rows per local expert (EP)
   moe::EpPlan* ep;     // host exchange plan (EP), owned by the ctx
+  int ep_G;            // GPUs per node for the hierarchical exchange (world = flat, the default)
+  void* ep_stage;      // caller-owned relay staging rows of the hierarchical exchange
+  long long ep_stage_rows;
 };
 
 namespace moe {

@@ -384,6 +384,15 @@ int check_ep(moe_ctx* c, const char* fn, bool need_plan) {
   if (need_plan && !c->ep) return fail(MOE_EINVAL, "%s: no exchange plan (call moe_ep_plan first)", fn);
   return MOE_OK;
 }
+// the hierarchical exchange relays rows through the caller's staging buffer
+int check_stage(moe_ctx* c, const char* fn) {
+  if (c->ep->G >= c->world) return MOE_OK;
+  const long long need = c->ep->H.stage_out + c->ep->H.stage_in;
+  if (need > 0 && (!c->ep_stage || c->ep_stage_rows < need))
+    return fail(MOE_ECAPACITY, "%s: hierarchical exchange needs %lld staging rows (moe_ep_set_stage), have %lld", fn,
+                need, (long long)c->ep_stage_rows);
+  return MOE_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -430,6 +439,9 @@ int moe_ep_plan(moe_ctx* ctx, const int32_t* counts_all, int32_t* offsets_send, 
   if (!ctx->ep) ctx->ep = new (std::nothrow) moe::EpPlan();
   if (!ctx->ep) return fail(MOE_EINVAL, "moe_ep_plan: out of host memory");
   moe::ep_build_plan(*ctx->ep, counts_all, ctx->world, ctx->E, ctx->rank);
+  const int G = ctx->ep_G > 0 ? ctx->ep_G : ctx->world;
+  ctx->ep->G = G;
+  if (G < ctx->world) moe::ep_build_hier(ctx->ep->H, counts_all, ctx->world, ctx->E, ctx->rank, G, ctx->ep->offsets_send);
   const moe::EpPlan& P = *ctx->ep;
   if (offsets_send) memcpy(offsets_send, P.offsets_send.data(), sizeof(int) * (ctx->E + 1));
   if (offsets_recv) memcpy(offsets_recv, P.offsets_recv.data(), sizeof(int) * (ctx->E_local + 1));
@@ -452,6 +464,86 @@ int moe_ep_plan_chunks(moe_ctx* ctx, int which, int32_t* peer, int64_t* row, int
     if (row) row[i] = ro[i];
     if (nrows) nrows[i] = nr[i];
   }
+  return MOE_OK;
+}
+
+int moe_ep_set_topology(moe_ctx* ctx, int gpus_per_node) {
+  if (!ctx) return fail(MOE_EINVAL, "moe_ep_set_topology: ctx is NULL");
+  if (gpus_per_node <= 0 || ctx->world % gpus_per_node != 0)
+    return fail(MOE_EINVAL, "moe_ep_set_topology: gpus_per_node=%d must divide world=%d", gpus_per_node, ctx->world);
+  ctx->ep_G = gpus_per_node;
+  return MOE_OK;
+}
+
+int moe_ep_stage_rows(moe_ctx* ctx, int64_t* rows) {
+  if (!ctx || !ctx->ep) return fail(MOE_EINVAL, "moe_ep_stage_rows: no plan");
+  REQUIRE(rows);
+  *rows = ctx->ep->G < ctx->world ? ctx->ep->H.stage_out + ctx->ep->H.stage_in : 0;
+  return MOE_OK;
+}
+
+int moe_ep_set_stage(moe_ctx* ctx, void* stage, int64_t rows_cap) {
+  if (!ctx) return fail(MOE_EINVAL, "moe_ep_set_stage: ctx is NULL");
+  if (rows_cap < 0 || (rows_cap > 0 && !stage)) return fail(MOE_EINVAL, "moe_ep_set_stage: bad buffer");
+  ctx->ep_stage = stage;
+  ctx->ep_stage_rows = rows_cap;
+  return MOE_OK;
+}
+
+int moe_ep_hier_chunks(moe_ctx* ctx, int phase, int is_recv, int32_t* peer, int32_t* buf, int64_t* row,
+                       int32_t* nrows, int max_chunks, int* n_out) {
+  if (!ctx || !ctx->ep) return fail(MOE_EINVAL, "moe_ep_hier_chunks: no plan");
+  if (phase < 0 || phase > 2) return fail(MOE_EINVAL, "moe_ep_hier_chunks: phase %d", phase);
+  REQUIRE(n_out);
+  const std::vector<moe::EpMsg>& v = is_recv ? ctx->ep->H.rcv[phase] : ctx->ep->H.snd[phase];
+  *n_out = ctx->ep->G < ctx->world ? (int)v.size() : 0;
+  for (int i = 0; i < *n_out && i < max_chunks; ++i) {
+    if (peer) peer[i] = v[i].peer;
+    if (buf) buf[i] = v[i].buf;
+    if (row) row[i] = v[i].row;
+    if (nrows) nrows[i] = v[i].rows;
+  }
+  return MOE_OK;
+}
+
+// Host-only cost-model identities of the two exchange plans over a virtual topology
+// (world ranks, G per node) for the routing counts_all [world][E]: stats =
+// { flat: inter-node (src GPU, dst GPU) pairs with payload, inter-node rows, intra-node rows,
+//   hierarchical: inter-node messages, inter-node rows, intra-node rows moved (phases 0 and 2),
+//   ordered node pairs with payload, max rows of one inter-node message }.
+int moe_ep_topology_stats(int world, int gpus_per_node, int E, const int32_t* counts_all, int64_t* stats) {
+  if (world <= 0 || gpus_per_node <= 0 || world % gpus_per_node != 0 || E % world != 0)
+    return fail(MOE_EINVAL, "moe_ep_topology_stats: world=%d G=%d E=%d", world, gpus_per_node, E);
+  REQUIRE(counts_all); REQUIRE(stats);
+  const int G = gpus_per_node, El = E / world;
+  for (int i = 0; i < 8; ++i) stats[i] = 0;
+  std::vector<char> node_pair((size_t)(world / G) * (world / G), 0);
+  for (int q = 0; q < world; ++q)
+    for (int p = 0; p < world; ++p) {
+      long long n = 0;
+      for (int j = 0; j < El; ++j) n += counts_all[(long long)q * E + p * El + j];
+      if (q / G != p / G) {
+        if (n > 0) { stats[0] += 1; node_pair[(size_t)(q / G) * (world / G) + p / G] = 1; }
+        stats[1] += n;
+      } else {
+        stats[2] += n;
+      }
+    }
+  for (char b : node_pair) stats[6] += b;
+  for (int r = 0; r < world; ++r) {
+    moe::EpPlan P;
+    moe::ep_build_plan(P, counts_all, world, E, r);
+    if (G >= world) continue;
+    moe::ep_build_hier(P.H, counts_all, world, E, r, G, P.offsets_send);
+    for (const moe::EpMsg& m : P.H.snd[1]) {
+      stats[3] += 1;
+      stats[4] += m.rows;
+      if (m.rows > stats[7]) stats[7] = m.rows;
+    }
+    for (int ph : {0, 2})
+      for (const moe::EpMsg& m : P.H.snd[ph]) stats[5] += m.rows;
+  }
+  if (G >= world) { stats[5] = stats[2]; }
   return MOE_OK;
 }
 
@@ -500,7 +592,11 @@ int moe_ep_dispatch(moe_ctx* ctx, const void* send_rows, void* recv_rows, int wi
     return fail(MOE_ECAPACITY, "moe_ep_dispatch: R_recv_cap=%lld < plan R_recv=%lld", (long long)R_recv_cap,
                 (long long)ctx->ep->R_recv);
 #ifdef MOE_HAVE_NCCL
-  rc = nccl_status(moe::ep_exchange(ctx, *ctx->ep, send_rows, recv_rows, width, 0, S(stream)), "moe_ep_dispatch");
+  if ((rc = check_stage(ctx, "moe_ep_dispatch"))) return rc;
+  rc = ctx->ep->G < ctx->world
+           ? nccl_status(moe::ep_exchange_hier(ctx, *ctx->ep, send_rows, recv_rows, ctx->ep_stage, width, 0, S(stream)),
+                         "moe_ep_dispatch")
+           : nccl_status(moe::ep_exchange(ctx, *ctx->ep, send_rows, recv_rows, width, 0, S(stream)), "moe_ep_dispatch");
   if (rc) return rc;
   return cuda_status(moe::launch_zero_pads(ctx, recv_rows, ctx->ep_off, ctx->ep_tot, width, S(stream)), "moe_ep_dispatch");
 #else
@@ -514,6 +610,10 @@ int moe_ep_combine(moe_ctx* ctx, const void* recv_rows, void* send_rows, int wid
   if ((rc = check_ep(ctx, "moe_ep_combine", true))) return rc;
   if (width <= 0 || width % 8 != 0) return fail(MOE_ESHAPE, "moe_ep_combine: width=%d must be a positive multiple of 8", width);
 #ifdef MOE_HAVE_NCCL
+  if ((rc = check_stage(ctx, "moe_ep_combine"))) return rc;
+  if (ctx->ep->G < ctx->world)
+    return nccl_status(moe::ep_exchange_hier(ctx, *ctx->ep, recv_rows, send_rows, ctx->ep_stage, width, 1, S(stream)),
+                       "moe_ep_combine");
   return nccl_status(moe::ep_exchange(ctx, *ctx->ep, recv_rows, send_rows, width, 1, S(stream)), "moe_ep_combine");
 #else
   return fail(MOE_ENCCL, "moe_ep_combine: built without NCCL");

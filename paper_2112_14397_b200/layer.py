@@ -60,7 +60,7 @@ class DTSMoELayer:
 
     def __init__(self, T: int, d_model: int, d_ff: int, E: int, dtype: torch.dtype = torch.bfloat16,
                  device: Optional[torch.device] = None, rank: int = 0, world: int = 1, nccl_comm: int = 0,
-                 recompute: bool = False):
+                 recompute: bool = False, gpus_per_node: Optional[int] = None):
         if dtype not in DTYPES:
             raise ValueError(f"dtype must be one of {list(DTYPES)}")
         self.T, self.d, self.f, self.E = T, d_model, d_ff, E
@@ -73,6 +73,10 @@ class DTSMoELayer:
         if world > 1 and not self.ep:
             raise ValueError("world > 1 needs an NCCL communicator (see make_nccl_comm)")
         self.ctx = L.moe_create(T, d_model, d_ff, E, DTYPES[dtype], nccl_comm, rank, world)
+        # NEXT #4: multi-node EP through the topology-aware hierarchical exchange
+        self.hier = bool(self.ep and gpus_per_node and gpus_per_node < world)
+        if self.hier:
+            L.moe_ep_set_topology(self.ctx, gpus_per_node)
         nbytes = L.moe_workspace_bytes(self.ctx)
         self.ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         L.moe_set_workspace(self.ctx, self.ws)
@@ -162,6 +166,9 @@ class DTSMoELayer:
             counts_all = L.moe_ep_exchange_counts(self.ctx, counts, self.world, E, stream)
             _, _, R_send, R_recv = L.moe_ep_plan(self.ctx, counts_all, E, self.E_local)
             rb = self._ensure_rows(R_send, R_recv)
+            if self.hier:
+                stage = self._grow("ep_stage", L.moe_ep_stage_rows(self.ctx), self.d, self.dtype)
+                L.moe_ep_set_stage(self.ctx, stage, stage.shape[0])
             offsets_recv = torch.empty(self.E_local + 1, dtype=torch.int32, device=dev)
             L.moe_ep_upload(self.ctx, offsets_recv, stream)
         else:
