@@ -261,6 +261,49 @@ int moe_ep_topology_stats(int world, int gpus_per_node, int E, const int32_t* co
 /* In-place sum all-reduce over the EP group: fp32 (dW_g, C6) or int32 (global counts, C7). */
 int moe_ep_allreduce(moe_ctx* ctx, void* buf, int64_t n, int is_int32, void* stream);
 
+/* ---------------------------------------------------------------- fused peer-memory EP ("ep2")
+ * The B200-native expert-parallel path: the all-to-all exchanges are fused into the routing
+ * kernels as NVLink peer loads / stores (P:226-227 data flow, no NCCL send/recv of rows).
+ * Every rank's row buffers are symmetric (mapped into every rank, e.g. torch symmetric
+ * memory / CUDA IPC); the `*_peers` arguments are HOST arrays of `world` device pointers
+ * (entry q = that buffer on rank q, entry rank = the local one).  Per step:
+ *   moe_dts_gate -> moe_ep2_counts (counts row into every rank's counts_all) -> barrier ->
+ *   moe_ep2_plan (device: recv offsets, destination bases) -> moe_ep2_prepare_recv (pad rows)
+ *   -> moe_ep2_dispatch (scan + rank: slot[t,e] = row on rank e/E_local, row metadata stored at
+ *   the owner; copy: x rows stored into the owners' x_recv) -> barrier -> moe_expert_ffn on
+ *   x_recv -> barrier -> moe_ep2_combine (token side gathers e_out rows from the owners).
+ *   Backward: barrier -> moe_ep2_combine_bwd (expert side reads dy rows from the token
+ *   owners; d_eout, dG_row and the db2 partials locally) -> moe_expert_ffn_bwd -> barrier ->
+ *   moe_ep2_gate_bwd (dG from the owners) -> moe_ep_allreduce(dWg) -> moe_ep2_dispatch_bwd
+ *   (dx_perm rows from the owners).
+ * Layouts (recv layout of each rank, expert-major, sources in rank order) and results equal
+ * the NCCL path's and, for the global token set, the single-rank layer's.  No host sync:
+ * R_recv_cap is a static capacity, a multiple of 128 (worst case world*T*E_local + 127*E_local,
+ * rounded up); overflow raises
+ * MOE_ECAPACITY at moe_check.  d_model <= 1024 (bf16) / 512 (f32) for moe_ep2_combine_bwd.
+ * nccl_comm == MOE_COMM_EMULATED (moe_create) runs `world` ranks in ONE process on one device
+ * (the tests): moe_ep2_barrier is then a no-op and the caller orders the ranks' launches;
+ * the NCCL exchange calls refuse such a ctx. */
+#define MOE_COMM_EMULATED ((void*)1)
+int moe_ep2_barrier(moe_ctx* ctx, void* stream);
+int moe_ep2_counts(moe_ctx* ctx, const int32_t* counts, int32_t* const* counts_all_peers, void* stream);
+int moe_ep2_plan(moe_ctx* ctx, const int32_t* counts_all, int64_t R_recv_cap, int32_t* offsets_recv, void* stream);
+int moe_ep2_prepare_recv(moe_ctx* ctx, void* x_recv, int32_t* rtok, int32_t* rsrc, float* rgate,
+                         int64_t R_recv_cap, void* stream);
+int moe_ep2_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, void* const* x_recv_peers,
+                     int32_t* const* rtok_peers, int32_t* const* rsrc_peers, float* const* rgate_peers,
+                     int64_t R_recv_cap, void* stream);
+int moe_ep2_combine(moe_ctx* ctx, void* const* e_out_peers, const float* probs, const int32_t* slot, void* y,
+                    void* stream);
+int moe_ep2_combine_bwd(moe_ctx* ctx, void* const* dy_peers, const void* e_out, const float* rgate,
+                        const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets_recv, int64_t R_recv_cap,
+                        void* d_eout, float* dG_row, void* stream);
+int moe_ep2_gate_bwd(moe_ctx* ctx, float* const* dG_peers, const int32_t* slot, const float* probs, const void* x,
+                     float tau, float balance_alpha, const int32_t* counts, int64_t B_total, float* dWg,
+                     float* dlogits, void* stream);
+int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t* slot, const float* dlogits,
+                         const void* Wg, void* dx, void* stream);
+
 /* ---------------------------------------------------------------- NEXT #1 */
 
 /* Balance loss, Eq. 10: loss = alpha N sum_i (counts_i / B^2) sum_s p[s,i]

@@ -56,7 +56,17 @@ SIGNATURES = {
     "moe_ep_set_stage": (_I, [_P, _P, _L]),
     "moe_ep_hier_chunks": (_I, [_P, _I, _I, _P, _P, _P, _P, _I, C.POINTER(_I)]),
     "moe_ep_topology_stats": (_I, [_I, _I, _I, _P, _P]),
+    "moe_ep2_barrier": (_I, [_P, _P]),
+    "moe_ep2_counts": (_I, [_P, _P, _P, _P]),
+    "moe_ep2_plan": (_I, [_P, _P, _L, _P, _P]),
+    "moe_ep2_prepare_recv": (_I, [_P, _P, _P, _P, _P, _L, _P]),
+    "moe_ep2_dispatch": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _P]),
+    "moe_ep2_combine": (_I, [_P, _P, _P, _P, _P, _P]),
+    "moe_ep2_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
+    "moe_ep2_gate_bwd": (_I, [_P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P]),
+    "moe_ep2_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
 }
+MOE_COMM_EMULATED = 1   # moe_create(nccl_comm=MOE_COMM_EMULATED): single-process emulation of `world` ranks
 
 
 class MoEError(RuntimeError):
@@ -312,3 +322,60 @@ def moe_ep_topology_stats(world: int, gpus_per_node: int, E: int, counts_all) ->
     keys = ("flat_inter_pairs", "flat_inter_rows", "flat_intra_rows", "hier_inter_msgs", "hier_inter_rows",
             "hier_intra_rows", "node_pairs", "hier_max_msg_rows")
     return {k: int(v) for k, v in zip(keys, st)}
+
+
+# ---- fused peer-memory EP ("ep2"): peers = list of `world` tensors (the same buffer on every rank)
+def _peers(tensors):
+    arr = (C.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+    return C.cast(arr, C.c_void_p), arr           # keep `arr` alive for the call
+
+
+def moe_ep2_barrier(ctx, stream=None):
+    _call("moe_ep2_barrier", ctx, _stream(stream))
+
+
+def moe_ep2_counts(ctx, counts, counts_all_peers, stream=None):
+    p, keep = _peers(counts_all_peers)
+    _call("moe_ep2_counts", ctx, _ptr(counts), p, _stream(stream))
+
+
+def moe_ep2_plan(ctx, counts_all, R_recv_cap: int, offsets_recv=None, stream=None):
+    _call("moe_ep2_plan", ctx, _ptr(counts_all), int(R_recv_cap), _ptr(offsets_recv), _stream(stream))
+
+
+def moe_ep2_prepare_recv(ctx, x_recv, rtok, rsrc, rgate, R_recv_cap: int, stream=None):
+    _call("moe_ep2_prepare_recv", ctx, _ptr(x_recv), _ptr(rtok), _ptr(rsrc), _ptr(rgate), int(R_recv_cap),
+          _stream(stream))
+
+
+def moe_ep2_dispatch(ctx, x, probs, slot, x_recv_peers, rtok_peers, rsrc_peers, rgate_peers, R_recv_cap: int,
+                     stream=None):
+    a, ka = _peers(x_recv_peers)
+    b, kb = _peers(rtok_peers)
+    c, kc = _peers(rsrc_peers)
+    d, kd = _peers(rgate_peers)
+    _call("moe_ep2_dispatch", ctx, _ptr(x), _ptr(probs), _ptr(slot), a, b, c, d, int(R_recv_cap), _stream(stream))
+
+
+def moe_ep2_combine(ctx, e_out_peers, probs, slot, y, stream=None):
+    a, ka = _peers(e_out_peers)
+    _call("moe_ep2_combine", ctx, a, _ptr(probs), _ptr(slot), _ptr(y), _stream(stream))
+
+
+def moe_ep2_combine_bwd(ctx, dy_peers, e_out, rgate, rtok, rsrc, offsets_recv, R_recv_cap: int, d_eout, dG_row,
+                        stream=None):
+    a, ka = _peers(dy_peers)
+    _call("moe_ep2_combine_bwd", ctx, a, _ptr(e_out), _ptr(rgate), _ptr(rtok), _ptr(rsrc), _ptr(offsets_recv),
+          int(R_recv_cap), _ptr(d_eout), _ptr(dG_row), _stream(stream))
+
+
+def moe_ep2_gate_bwd(ctx, dG_peers, slot, probs, x, tau: float, balance_alpha: float, counts, B_total: int, dWg,
+                     dlogits, stream=None):
+    a, ka = _peers(dG_peers)
+    _call("moe_ep2_gate_bwd", ctx, a, _ptr(slot), _ptr(probs), _ptr(x), float(tau), float(balance_alpha),
+          _ptr(counts), int(B_total), _ptr(dWg), _ptr(dlogits), _stream(stream))
+
+
+def moe_ep2_dispatch_bwd(ctx, dx_perm_peers, slot, dlogits, Wg, dx, stream=None):
+    a, ka = _peers(dx_perm_peers)
+    _call("moe_ep2_dispatch_bwd", ctx, a, _ptr(slot), _ptr(dlogits), _ptr(Wg), _ptr(dx), _stream(stream))

@@ -179,10 +179,14 @@ cudaError_t launch_gate_typed(const moe_ctx* c, const void* x, const void* Wg, c
 
 // ------------------------------------------------------------------ gate backward
 // One warp per token: dp = m dG (+ balance), dz = p (dp - <p,dp>), dlogits = dz / tau.
+// PEER (fused peer-memory EP, token side): dG of (t, e) sits at row slot[t,e] of the rank
+// owning e, read through its NVLink peer pointer dGp.p[e / El].
+template <bool PEER = false>
 __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     const float* __restrict__ dG_row, const int* __restrict__ slot, const float* __restrict__ probs,
     int T_, int E, float tau, float alpha, const int* __restrict__ counts, double bal_scale,
-    float* __restrict__ dlogits, bf16* __restrict__ dL2, int Ep, int Kp) {
+    float* __restrict__ dlogits, bf16* __restrict__ dL2, int Ep, int Kp, int El,
+    const __grid_constant__ PeerTable dGp) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     if (e < E) {
       p[i] = probs[(long long)t * E + e];
       int r = slot[(long long)t * E + e];
-      dp[i] = r >= 0 ? dG_row[r] : 0.f;
+      dp[i] = r >= 0 ? (PEER ? reinterpret_cast<const float*>(dGp.p[e / El])[r] : dG_row[r]) : 0.f;
       if (alpha > 0.f) dp[i] += (float)(bal_scale * (double)counts[e]);
       s += p[i] * dp[i];
     }
@@ -264,16 +268,25 @@ cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const f
   return launch_gate_typed<float>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
 }
 
-cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t* slot, const float* probs,
-                            const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
-                            float* dWg, float* dlogits, cudaStream_t s) {
+static cudaError_t gate_bwd_impl(const moe_ctx* c, const float* dG_row, const PeerTable* dGp, const int32_t* slot,
+                                 const float* probs, const void* x, float tau, float alpha, const int32_t* counts,
+                                 int64_t B_total, float* dWg, float* dlogits, cudaStream_t s) {
   if (c->T == 0) return cudaMemsetAsync(dWg, 0, sizeof(float) * c->d * c->E, s);
   double bal = alpha > 0.f ? (double)alpha * c->E / ((double)B_total * (double)B_total) : 0.0;
   const bool tc = gate_tc_supported(c);
   bf16* dL2 = tc ? reinterpret_cast<bf16*>(gate_dl2_buffer(c)) : nullptr;
   const int Ep = (c->E + 15) / 16 * 16, Kp = (2 * Ep + 63) / 64 * 64;
-  gate_bwd_token_kernel<<<(c->T + 7) / 8, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts, bal,
-                                                        dlogits, dL2, Ep, Kp), count_launch();
+  PeerTable tab{};
+  if (dGp) {
+    tab = *dGp;
+    gate_bwd_token_kernel<true><<<(c->T + 7) / 8, 256, 0, s>>>(nullptr, slot, probs, c->T, c->E, tau, alpha, counts,
+                                                               bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
+        count_launch();
+  } else {
+    gate_bwd_token_kernel<false><<<(c->T + 7) / 8, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts,
+                                                                bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
+        count_launch();
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (tc) {
@@ -294,6 +307,18 @@ cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t
     reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->part, c->dwg_splits, n, dWg), count_launch();
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t* slot, const float* probs,
+                            const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
+                            float* dWg, float* dlogits, cudaStream_t s) {
+  return gate_bwd_impl(c, dG_row, nullptr, slot, probs, x, tau, alpha, counts, B_total, dWg, dlogits, s);
+}
+
+cudaError_t launch_gate_bwd_peer(const moe_ctx* c, const PeerTable& dGp, const int32_t* slot, const float* probs,
+                                 const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
+                                 float* dWg, float* dlogits, cudaStream_t s) {
+  return gate_bwd_impl(c, nullptr, &dGp, slot, probs, x, tau, alpha, counts, B_total, dWg, dlogits, s);
 }
 
 // Steps 2-3 from precomputed fp32 logits, thread per token (kGateBT tokens per block):

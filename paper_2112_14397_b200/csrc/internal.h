@@ -42,6 +42,8 @@ struct moe_ctx {
   int* ep_counts;      // [world, E] gathered counts (EP)
   int* ep_off;         // [E_local + 1] recv-layout offsets (EP)
   int* ep_tot;         // [E_local] recv-layout rows per local expert (EP)
+  int* ep2_scr;        // [E + 2] scan scratch of the fused peer-memory EP dispatch
+  int* ep2_base;       // [E] first destination row of each global expert for this rank's tokens
   moe::EpPlan* ep;     // host exchange plan (EP), owned by the ctx
   int ep_G;            // GPUs per node for the hierarchical exchange (world = flat, the default)
   void* ep_stage;      // caller-owned relay staging rows of the hierarchical exchange
@@ -49,6 +51,11 @@ struct moe_ctx {
 };
 
 namespace moe {
+// NVLink peer pointers of one symmetric buffer, indexed by rank (fused peer-memory EP)
+constexpr int kMaxPeers = 64;
+struct PeerTable {
+  const void* p[kMaxPeers];
+};
 struct EpPlan;
 void ep_build_plan(EpPlan& P, const int* counts_all, int W, int E, int rank);
 cudaError_t launch_zero_pads(const moe_ctx* c, void* buf, const int* offsets_dev, const int* tot_dev, int width,
@@ -104,6 +111,27 @@ cudaError_t launch_expert_ffn_bwd(moe_ctx* c, const void* d_eout, const void* x_
                                   int64_t R_cap, const void* W1, const void* W2, void* da,
                                   void* dx_perm, float* dW1, float* db1, float* dW2, float* db2,
                                   cudaStream_t s);
+
+// ---------------------------------------------------------------- fused peer-memory EP ("ep2")
+cudaError_t launch_ep2_counts(const moe_ctx* c, const int32_t* counts, const PeerTable& all, cudaStream_t s);
+cudaError_t launch_ep2_plan(const moe_ctx* c, const int32_t* counts_all, int64_t R_cap, int32_t* offsets_recv,
+                            cudaStream_t s);
+cudaError_t launch_ep2_prepare(const moe_ctx* c, void* x_recv, int32_t* rtok, int32_t* rsrc, float* rgate,
+                               int64_t R_cap, cudaStream_t s);
+cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot, const PeerTable& xr,
+                                const PeerTable& rtok, const PeerTable& rsrc, const PeerTable& rgate, int64_t R_cap,
+                                cudaStream_t s);
+cudaError_t launch_ep2_combine(const moe_ctx* c, const PeerTable& eo, const float* probs, const int32_t* slot, void* y,
+                               cudaStream_t s);
+bool ep2_width_ok(const moe_ctx* c);
+cudaError_t launch_ep2_combine_bwd(moe_ctx* c, const PeerTable& dyp, const void* e_out, const float* rgate,
+                                   const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets, int64_t R_cap,
+                                   void* d_eout, float* dG_row, cudaStream_t s);
+cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, const float* dlogits,
+                                    const void* Wg, void* dx, cudaStream_t s);
+cudaError_t launch_gate_bwd_peer(const moe_ctx* c, const PeerTable& dGp, const int32_t* slot, const float* probs,
+                                 const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
+                                 float* dWg, float* dlogits, cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 grouped GEMM (bf16)
 bool tc_available();

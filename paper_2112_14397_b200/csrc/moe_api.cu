@@ -64,7 +64,7 @@ namespace moe {
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct Carve {
-  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, biasf, db2part, total;
+  size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, biasf, db2part, ep2_scr, ep2_base, total;
 };
 
 // row splits per expert for the fused combine_bwd + db2 partials: about 8 blocks per SM in total
@@ -105,6 +105,8 @@ static Carve carve(const moe_ctx* c) {
   // fp32 copies of b1 / b2 for the tensor-core epilogues, rows padded to 256 columns
   k.biasf = take(sizeof(float) * (size_t)c->E_local * (size_t)((c->f + 255) / 256 * 256 + (c->d + 255) / 256 * 256));
   k.db2part = take(sizeof(float) * (size_t)c->E_local * (size_t)db2_splits(c) * (size_t)c->d);
+  k.ep2_scr = take(sizeof(int) * ((size_t)c->E + 2));
+  k.ep2_base = take(sizeof(int) * (size_t)c->E);
   k.total = o;
   return k;
 }
@@ -130,6 +132,8 @@ void carve_workspace(moe_ctx* c) {
   c->tok_off = reinterpret_cast<int*>(c->ws + k.tok_off);
   c->biasf = reinterpret_cast<float*>(c->ws + k.biasf);
   c->db2part = reinterpret_cast<float*>(c->ws + k.db2part);
+  c->ep2_scr = reinterpret_cast<int*>(c->ws + k.ep2_scr);
+  c->ep2_base = reinterpret_cast<int*>(c->ws + k.ep2_base);
   c->db2_S = db2_splits(c);
   c->db2_src = nullptr;
   c->dl2_src = nullptr;
@@ -381,6 +385,8 @@ int nccl_status(ncclResult_t r, const char* where) {
 int check_ep(moe_ctx* c, const char* fn, bool need_plan) {
   if (!c) return fail(MOE_EINVAL, "%s: ctx is NULL", fn);
   if (!c->comm) return fail(MOE_EINVAL, "%s: ctx has no NCCL communicator (expert parallelism disabled)", fn);
+  if (c->comm == MOE_COMM_EMULATED && !need_plan)
+    return fail(MOE_EINVAL, "%s: needs a real NCCL communicator (ctx is a single-process emulated rank)", fn);
   if (need_plan && !c->ep) return fail(MOE_EINVAL, "%s: no exchange plan (call moe_ep_plan first)", fn);
   return MOE_OK;
 }
@@ -570,6 +576,7 @@ int moe_ep_upload(moe_ctx* ctx, int32_t* offsets_recv_dev, void* stream) {
   int rc = check_ctx(ctx, "moe_ep_upload");
   if (rc) return rc;
   if ((rc = check_ep(ctx, "moe_ep_upload", true))) return rc;
+  if (ctx->comm == MOE_COMM_EMULATED) return fail(MOE_EINVAL, "moe_ep_upload: emulated rank");
   REQUIRE(offsets_recv_dev);
   const moe::EpPlan& P = *ctx->ep;
   cudaError_t e = cudaMemcpyAsync(offsets_recv_dev, P.offsets_recv.data(), sizeof(int) * (ctx->E_local + 1),
@@ -587,6 +594,7 @@ int moe_ep_dispatch(moe_ctx* ctx, const void* send_rows, void* recv_rows, int wi
   int rc = check_ctx(ctx, "moe_ep_dispatch");
   if (rc) return rc;
   if ((rc = check_ep(ctx, "moe_ep_dispatch", true))) return rc;
+  if (ctx->comm == MOE_COMM_EMULATED) return fail(MOE_EINVAL, "moe_ep_dispatch: emulated rank (use moe_ep2_*)");
   if (width <= 0 || width % 8 != 0) return fail(MOE_ESHAPE, "moe_ep_dispatch: width=%d must be a positive multiple of 8", width);
   if (R_recv_cap < ctx->ep->R_recv)
     return fail(MOE_ECAPACITY, "moe_ep_dispatch: R_recv_cap=%lld < plan R_recv=%lld", (long long)R_recv_cap,
@@ -608,6 +616,7 @@ int moe_ep_combine(moe_ctx* ctx, const void* recv_rows, void* send_rows, int wid
   int rc = check_ctx(ctx, "moe_ep_combine");
   if (rc) return rc;
   if ((rc = check_ep(ctx, "moe_ep_combine", true))) return rc;
+  if (ctx->comm == MOE_COMM_EMULATED) return fail(MOE_EINVAL, "moe_ep_combine: emulated rank (use moe_ep2_*)");
   if (width <= 0 || width % 8 != 0) return fail(MOE_ESHAPE, "moe_ep_combine: width=%d must be a positive multiple of 8", width);
 #ifdef MOE_HAVE_NCCL
   if ((rc = check_stage(ctx, "moe_ep_combine"))) return rc;
@@ -632,6 +641,139 @@ int moe_ep_allreduce(moe_ctx* ctx, void* buf, int64_t n, int is_int32, void* str
 #else
   return fail(MOE_ENCCL, "moe_ep_allreduce: built without NCCL");
 #endif
+}
+
+}  // extern "C"
+
+// ====================================================================== fused peer-memory EP (ep2)
+namespace {
+int ep2_check(moe_ctx* c, const char* fn) {
+  int rc = check_ctx(c, fn);
+  if (rc) return rc;
+  if (!c->comm) return fail(MOE_EINVAL, "%s: ctx has no communicator (expert parallelism disabled)", fn);
+  if (c->world > moe::kMaxPeers) return fail(MOE_ESHAPE, "%s: world=%d > %d", fn, c->world, moe::kMaxPeers);
+  return MOE_OK;
+}
+int ep2_table(moe_ctx* c, const void* const* peers, moe::PeerTable& t, const char* fn) {
+  if (!peers) return fail(MOE_EINVAL, "%s: peer pointer array is NULL", fn);
+  t = moe::PeerTable{};
+  for (int i = 0; i < c->world; ++i) {
+    if (!peers[i]) return fail(MOE_EINVAL, "%s: peer pointer %d is NULL", fn, i);
+    t.p[i] = peers[i];
+  }
+  return MOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int moe_ep2_barrier(moe_ctx* ctx, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_barrier");
+  if (rc) return rc;
+  if (ctx->comm == MOE_COMM_EMULATED || ctx->world == 1) return MOE_OK;
+#ifdef MOE_HAVE_NCCL
+  // stream-ordered barrier: a 1-element all-reduce completes only when every rank reached it
+  return nccl_status(ncclAllReduce(ctx->flags + 8, ctx->flags + 8, 1, ncclInt32, ncclSum,
+                                   reinterpret_cast<ncclComm_t>(ctx->comm), S(stream)),
+                     "moe_ep2_barrier");
+#else
+  return fail(MOE_ENCCL, "moe_ep2_barrier: built without NCCL");
+#endif
+}
+
+int moe_ep2_counts(moe_ctx* ctx, const int32_t* counts, int32_t* const* counts_all_peers, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_counts");
+  if (rc) return rc;
+  REQUIRE(counts);
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(counts_all_peers), t, "moe_ep2_counts"))) return rc;
+  return cuda_status(moe::launch_ep2_counts(ctx, counts, t, S(stream)), "moe_ep2_counts");
+}
+
+int moe_ep2_plan(moe_ctx* ctx, const int32_t* counts_all, int64_t R_recv_cap, int32_t* offsets_recv, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_plan");
+  if (rc) return rc;
+  REQUIRE(counts_all);
+  if (R_recv_cap < 0) return fail(MOE_EINVAL, "moe_ep2_plan: bad R_recv_cap");
+  return cuda_status(moe::launch_ep2_plan(ctx, counts_all, R_recv_cap, offsets_recv, S(stream)), "moe_ep2_plan");
+}
+
+int moe_ep2_prepare_recv(moe_ctx* ctx, void* x_recv, int32_t* rtok, int32_t* rsrc, float* rgate, int64_t R_recv_cap,
+                         void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_prepare_recv");
+  if (rc) return rc;
+  REQUIRE(x_recv); REQUIRE(rtok); REQUIRE(rsrc); REQUIRE(rgate);
+  return cuda_status(moe::launch_ep2_prepare(ctx, x_recv, rtok, rsrc, rgate, R_recv_cap, S(stream)),
+                     "moe_ep2_prepare_recv");
+}
+
+int moe_ep2_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, void* const* x_recv_peers,
+                     int32_t* const* rtok_peers, int32_t* const* rsrc_peers, float* const* rgate_peers,
+                     int64_t R_recv_cap, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_dispatch");
+  if (rc) return rc;
+  REQUIRE_T(x); REQUIRE_T(probs); REQUIRE_T(slot);
+  moe::PeerTable xr, rt, rs, rg;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(x_recv_peers), xr, "moe_ep2_dispatch")) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rtok_peers), rt, "moe_ep2_dispatch")) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rsrc_peers), rs, "moe_ep2_dispatch")) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rgate_peers), rg, "moe_ep2_dispatch")))
+    return rc;
+  return cuda_status(moe::launch_ep2_dispatch(ctx, x, probs, slot, xr, rt, rs, rg, R_recv_cap, S(stream)),
+                     "moe_ep2_dispatch");
+}
+
+int moe_ep2_combine(moe_ctx* ctx, void* const* e_out_peers, const float* probs, const int32_t* slot, void* y,
+                    void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_combine");
+  if (rc) return rc;
+  REQUIRE_T(probs); REQUIRE_T(slot); REQUIRE_T(y);
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(e_out_peers), t, "moe_ep2_combine"))) return rc;
+  return cuda_status(moe::launch_ep2_combine(ctx, t, probs, slot, y, S(stream)), "moe_ep2_combine");
+}
+
+int moe_ep2_combine_bwd(moe_ctx* ctx, void* const* dy_peers, const void* e_out, const float* rgate,
+                        const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets_recv, int64_t R_recv_cap,
+                        void* d_eout, float* dG_row, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_combine_bwd");
+  if (rc) return rc;
+  REQUIRE(e_out); REQUIRE(rgate); REQUIRE(rtok); REQUIRE(rsrc); REQUIRE(offsets_recv); REQUIRE(d_eout); REQUIRE(dG_row);
+  if (!moe::ep2_width_ok(ctx)) return fail(MOE_ESHAPE, "moe_ep2_combine_bwd: d_model=%d too wide (max 1024 bf16 / 512 f32)", ctx->d);
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dy_peers), t, "moe_ep2_combine_bwd"))) return rc;
+  return cuda_status(moe::launch_ep2_combine_bwd(ctx, t, e_out, rgate, rtok, rsrc, offsets_recv, R_recv_cap, d_eout,
+                                                 dG_row, S(stream)),
+                     "moe_ep2_combine_bwd");
+}
+
+int moe_ep2_gate_bwd(moe_ctx* ctx, float* const* dG_peers, const int32_t* slot, const float* probs, const void* x,
+                     float tau, float balance_alpha, const int32_t* counts, int64_t B_total, float* dWg, float* dlogits,
+                     void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_gate_bwd");
+  if (rc) return rc;
+  REQUIRE_T(slot); REQUIRE_T(probs); REQUIRE_T(x); REQUIRE(dWg); REQUIRE_T(dlogits);
+  if (!(tau > 0.0f) || !isfinite(tau)) return fail(MOE_EINVAL, "moe_ep2_gate_bwd: tau=%g must be finite and > 0", tau);
+  if (!(balance_alpha >= 0.0f) || !isfinite(balance_alpha))
+    return fail(MOE_EINVAL, "moe_ep2_gate_bwd: balance_alpha=%g must be finite and >= 0", balance_alpha);
+  if (balance_alpha > 0.0f && (!counts || B_total <= 0))
+    return fail(MOE_EINVAL, "moe_ep2_gate_bwd: balance term needs counts and B_total > 0");
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dG_peers), t, "moe_ep2_gate_bwd"))) return rc;
+  return cuda_status(moe::launch_gate_bwd_peer(ctx, t, slot, probs, x, tau, balance_alpha, counts, B_total, dWg,
+                                               dlogits, S(stream)),
+                     "moe_ep2_gate_bwd");
+}
+
+int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t* slot, const float* dlogits,
+                         const void* Wg, void* dx, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_dispatch_bwd");
+  if (rc) return rc;
+  REQUIRE_T(slot); REQUIRE_T(dx);
+  if (dlogits && !Wg) return fail(MOE_EINVAL, "moe_ep2_dispatch_bwd: dlogits given without Wg");
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dx_perm_peers), t, "moe_ep2_dispatch_bwd"))) return rc;
+  return cuda_status(moe::launch_ep2_dispatch_bwd(ctx, t, slot, dlogits, Wg, dx, S(stream)), "moe_ep2_dispatch_bwd");
 }
 
 }  // extern "C"

@@ -153,9 +153,30 @@ __global__ void __launch_bounds__(256) dispatch_copy_kernel(const T* __restrict_
 // One warp per token.  The token's selected rows are found with ballots over its slot row
 // (ascending expert order is the bit order), so the work is O(selected), not O(E).
 // Columns are processed 4 x 16-byte vectors per lane at a time (independent loads in flight).
-template <typename T, bool WEIGHTED, typename TX = float, int QV = 4>
-__device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src, const float* __restrict__ row_gate,
-                                                 const int* __restrict__ slot_row, int d, int E,
+// Row sources of the gather: this device's row layout (row r of `rows`, weight row_gate[r]),
+// or the expert-parallel peer layouts (row r of the layout on the rank owning expert e, reached
+// through NVLink peer pointers; weight = the token's probs[e]).
+template <typename T>
+struct LocalRows {
+  const T* rows;
+  const float* gate;
+  int d;
+  __device__ __forceinline__ const T* row(int, int r) const { return rows + (long long)r * d; }
+  __device__ __forceinline__ float weight(int, int r) const { return gate[r]; }
+};
+template <typename T>
+struct PeerRows {
+  const PeerTable* peers;      // [rank] -> row layout base on that rank
+  const float* probs_t;        // this token's probs row (weights of its selected experts)
+  int d, El;
+  __device__ __forceinline__ const T* row(int e, int r) const {
+    return reinterpret_cast<const T*>(peers->p[e / El]) + (long long)r * d;
+  }
+  __device__ __forceinline__ float weight(int e, int) const { return probs_t[e]; }
+};
+
+template <typename T, bool WEIGHTED, typename TX = float, int QV = 4, typename Src = LocalRows<T>>
+__device__ __forceinline__ void gather_sum_token(const Src& src, const int* __restrict__ slot_row, int d, int E,
                                                  const TX* __restrict__ extra, T* __restrict__ out, int lane) {
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
@@ -193,15 +214,17 @@ __device__ __forceinline__ void gather_sum_token(const T* __restrict__ rows_src,
         if (two) bal &= bal - 1;
         const int r = __shfl_sync(0xffffffffu, sv, b);
         const int r2 = __shfl_sync(0xffffffffu, sv, b2);
-        const float gw = WEIGHTED ? row_gate[r] : 1.0f;
-        const float gw2 = WEIGHTED && two ? row_gate[r2] : 1.0f;
+        const float gw = WEIGHTED ? src.weight(g + b, r) : 1.0f;
+        const float gw2 = WEIGHTED && two ? src.weight(g + b2, r2) : 1.0f;
+        const T* p1 = src.row(g + b, r);
+        const T* p2 = src.row(g + b2, r2);
         uint4 raw[QV], raw2[QV];
 #pragma unroll
         for (int q = 0; q < QV; ++q) {
           const int v = v0 + q * 32 + lane;
           if (v < nvec) {
-            raw[q] = ld_nc_v4(rows_src + (long long)r * d + (long long)v * V);
-            if (two) raw2[q] = ld_nc_v4(rows_src + (long long)r2 * d + (long long)v * V);
+            raw[q] = ld_nc_v4(p1 + (long long)v * V);
+            if (two) raw2[q] = ld_nc_v4(p2 + (long long)v * V);
           }
         }
 #pragma unroll
@@ -239,8 +262,8 @@ __global__ void __launch_bounds__(256, 4) combine_kernel(const T* __restrict__ e
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  gather_sum_token<T, true, float, QV>(e_out, row_gate, slot + (long long)t * E, d, E, nullptr, y + (long long)t * d,
-                                       lane);
+  gather_sum_token<T, true, float, QV>(LocalRows<T>{e_out, row_gate, d}, slot + (long long)t * E, d, E, nullptr,
+                                       y + (long long)t * d, lane);
 }
 // vectors per lane per pass: the whole row in one pass up to 4 x 16 B per lane
 static inline int pass_vectors(int d, int V) {
@@ -293,13 +316,17 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
 // part[g][s][n] = sum of the stored (rounded) d_eout[r][n], warps combined in fixed order.
 // COMPUTE = false: only the partials, from an existing d_eout (same row partition and summation
 // order, so both paths give bit-identical db2).
-template <typename T, int MAXV, bool COMPUTE>
+// PEER (fused peer-memory EP, expert side): the row's token lives on rank row_src[r]; its dy
+// row is read through that rank's NVLink peer pointer dyp.p[row_src[r]] (no dy exchange).
+template <typename T, int MAXV, bool COMPUTE, bool PEER = false>
 __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __restrict__ dy, const T* __restrict__ e_out,
                                                                  const float* __restrict__ row_gate,
                                                                  const int* __restrict__ row_token,
                                                                  const int* __restrict__ offsets, int d,
                                                                  long long R_cap, int S, T* __restrict__ d_eout,
-                                                                 float* __restrict__ dG_row, float* __restrict__ part) {
+                                                                 float* __restrict__ dG_row, float* __restrict__ part,
+                                                                 const int* __restrict__ row_src,
+                                                                 const __grid_constant__ PeerTable dyp) {
   extern __shared__ float red[];                    // [8][d]
   constexpr int V = Vec16<T>::N;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -323,11 +350,12 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
     }
   };
   // row metadata one row ahead: the dy gather of row r does not wait for its row_token load
-  int t_nx = -1;
+  int t_nx = -1, q_nx = 0;
   float g_nx = 0.f;
   if (COMPUTE && r0 + warp < r1) {
     t_nx = row_token[r0 + warp];
     g_nx = row_gate[r0 + warp];
+    if (PEER) q_nx = row_src[r0 + warp];
   }
   for (long long r = r0 + warp; r < r1; r += 8) {
     T* dst = d_eout + r * d;
@@ -345,9 +373,11 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
     }
     const int t = t_nx;
     const float gw = g_nx;
+    const T* dyb = PEER ? reinterpret_cast<const T*>(dyp.p[q_nx]) : dy;
     if (r + 8 < r1) {
       t_nx = row_token[r + 8];
       g_nx = row_gate[r + 8];
+      if (PEER) q_nx = row_src[r + 8];
     }
     if (t < 0) {
 #pragma unroll
@@ -363,7 +393,7 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
     for (int j = 0; j < MAXV; ++j) {
       const int v = lane + 32 * j;
       if (v < nvec) {
-        qa[j] = ld_nc_v4(dy + (long long)t * d + (long long)v * V);
+        qa[j] = ld_nc_v4(dyb + (long long)t * d + (long long)v * V);
         qb[j] = ld_nc_v4(e_out + r * d + (long long)v * V);
       }
     }
@@ -407,7 +437,7 @@ __global__ void __launch_bounds__(256, 4) dispatch_bwd_kernel(const T* __restric
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
-  gather_sum_token<T, false, TX, QV>(dx_perm, nullptr, slot + (long long)t * E, d, E,
+  gather_sum_token<T, false, TX, QV>(LocalRows<T>{dx_perm, nullptr, d}, slot + (long long)t * E, d, E,
                                  dxg ? dxg + (long long)t * d : nullptr, dx + (long long)t * d, lane);
 }
 
@@ -476,6 +506,181 @@ cudaError_t spawn_typed(const moe_ctx* c, const void* W1s, const void* b1s, cons
   return cudaGetLastError();
 }
 
+// ================================================================== fused peer-memory EP
+// Expert parallelism with the exchanges fused into the routing kernels over NVLink peer
+// memory (every rank's row buffers are mapped into every other rank: symmetric memory).
+// Token side writes its x rows straight into the owning rank's expert-side layout
+// (ep2_copy); the combine, the gate backward and the dispatch backward gather e_out,
+// dG and dx_perm rows from the owning ranks through peer loads; the expert side's
+// combine_bwd reads dy rows from the token owners (combine_bwd_colsum_kernel<PEER>).
+// slot[t, e] holds the row on rank e / E_local.  Layouts equal the NCCL path's.
+
+// counts all-gather by peer stores: counts_all[me][e] on every rank
+__global__ void ep2_counts_kernel(const int* __restrict__ counts, int E, int me, int W,
+                                  const __grid_constant__ PeerTable all) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < W * E; i += gridDim.x * blockDim.x) {
+    const int p = i / E, e = i - p * E;
+    reinterpret_cast<int*>(const_cast<void*>(all.p[p]))[(long long)me * E + e] = counts[e];
+  }
+}
+
+// Plan from counts_all [W][E] (identical on every rank): my recv layout (offsets [El+1],
+// totals [El]) and, for my tokens, the first destination row of every global expert e:
+//   base[e] = off_{e / El}[e % El] + sum_{q < me} counts_all[q][e].
+__global__ void __launch_bounds__(256) ep2_plan_kernel(const int* __restrict__ counts_all, int W, int E, int me,
+                                                       long long R_cap, int* __restrict__ off_me,
+                                                       int* __restrict__ tot_me, int* __restrict__ base,
+                                                       int* __restrict__ flags) {
+  extern __shared__ long long s_tot[];             // [E] column totals
+  const int El = E / W;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    long long t = 0;
+    for (int q = 0; q < W; ++q) t += counts_all[(long long)q * E + e];
+    s_tot[e] = t;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const int p = e / El, j = e - p * El;
+    long long off = 0;
+    for (int j2 = 0; j2 < j; ++j2) off += (s_tot[p * El + j2] + kRowAlign - 1) / kRowAlign * kRowAlign;
+    long long pre = 0;
+    for (int q = 0; q < me; ++q) pre += counts_all[(long long)q * E + e];
+    base[e] = (int)(off + pre);
+    if (p == me) {
+      off_me[j] = (int)off;
+      tot_me[j] = (int)s_tot[e];
+      if (j == El - 1) {
+        const long long end = off + (s_tot[e] + kRowAlign - 1) / kRowAlign * kRowAlign;
+        off_me[El] = (int)end;
+      }
+    }
+    if (j == El - 1) {   // capacity of rank p's layout (every rank raises it, so each rank's check sees it)
+      const long long end = off + (s_tot[e] + kRowAlign - 1) / kRowAlign * kRowAlign;
+      if (end > R_cap) {
+        atomicOr(&flags[0], kFlagCapacity);
+        flags[2] = (int)(end < 0x7fffffff ? end : 0x7fffffff);
+      }
+    }
+  }
+}
+
+// expert side: pad rows of my layout -> zero x, row_token -1, gate 0, source 0
+template <typename T>
+__global__ void ep2_prepare_kernel(T* __restrict__ x_recv, int* __restrict__ rtok, int* __restrict__ rsrc,
+                                   float* __restrict__ rgate, const int* __restrict__ off, const int* __restrict__ tot,
+                                   int El, int d, long long R_cap) {
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int j = blockIdx.y; j < El; j += gridDim.y) {
+    const long long r0 = (long long)off[j] + tot[j], r1 = min((long long)off[j + 1], R_cap);
+    for (long long r = r0 + blockIdx.x * nw + warp; r < r1; r += (long long)gridDim.x * nw) {
+      if (lane == 0) { rtok[r] = -1; rsrc[r] = 0; rgate[r] = 0.f; }
+      for (int v = lane; v < nvec; v += 32) st_v4(x_recv + r * d + (long long)v * V, make_uint4(0, 0, 0, 0));
+    }
+  }
+}
+
+// token side rank pass (as dispatch_rank_kernel): my i-th token of expert e goes to row
+// base[e] + i on rank e / El; slot <- that row; the row's metadata is stored at the owner.
+__global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
+    const float* __restrict__ probs, int* __restrict__ slot, int T_, int E, int El, int me,
+    const int* __restrict__ blk_base, const int* __restrict__ base, long long R_cap,
+    const __grid_constant__ PeerTable rtok, const __grid_constant__ PeerTable rsrc,
+    const __grid_constant__ PeerTable rgate) {
+  __shared__ unsigned s_bal[kGateBT / 32][128];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int t = blockIdx.x * kGateBT + tid;
+  const bool valid = t < T_;
+  for (int e = 0; e < E; ++e) {
+    const bool sel = valid && slot[(long long)t * E + e] >= 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    if (lane == 0) s_bal[warp][e] = bal;
+  }
+  __syncthreads();
+  if (!valid) return;
+  const unsigned lower = (1u << lane) - 1u;
+  for (int e = 0; e < E; ++e) {
+    const unsigned mine = s_bal[warp][e];
+    if (!((mine >> lane) & 1u)) continue;
+    int wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
+    const long long row = (long long)base[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre +
+                          __popc(mine & lower);
+    if (row < R_cap) {
+      const int p = e / El;
+      slot[(long long)t * E + e] = (int)row;
+      reinterpret_cast<int*>(const_cast<void*>(rtok.p[p]))[row] = t;
+      reinterpret_cast<int*>(const_cast<void*>(rsrc.p[p]))[row] = me;
+      reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[row] = probs[(long long)t * E + e];
+    } else {
+      slot[(long long)t * E + e] = -1;           // dropped (MOE_ECAPACITY raised by the plan)
+    }
+  }
+}
+
+// token side copy pass: x_t read once, stored into each selected expert's row on its owner
+template <typename T>
+__global__ void __launch_bounds__(256) ep2_copy_kernel(const T* __restrict__ x, const int* __restrict__ slot, int T_,
+                                                       int d, int E, int El, const __grid_constant__ PeerTable xr) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  const T* src = x + (long long)t * d;
+  const int* srow = slot + (long long)t * E;
+  for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+    uint4 buf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
+    }
+    for (int g = 0; g < E; g += 32) {
+      const int sv = (g + lane < E) ? srow[g + lane] : -1;
+      unsigned bal = __ballot_sync(0xffffffffu, sv >= 0);
+      while (bal) {
+        const int b = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int row = __shfl_sync(0xffffffffu, sv, b);
+        T* dst = reinterpret_cast<T*>(const_cast<void*>(xr.p[(g + b) / El])) + (long long)row * d;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int v = v0 + q * 32 + lane;
+          if (v < nvec) st_v4(dst + (long long)v * V, buf[q]);
+        }
+      }
+    }
+  }
+}
+
+// token side: y[t] = sum_{e asc} probs[t,e] e_out@(e / El)[slot[t,e]]
+template <typename T, int QV>
+__global__ void __launch_bounds__(256, 4) ep2_combine_kernel(const __grid_constant__ PeerTable eo,
+                                                             const float* __restrict__ probs,
+                                                             const int* __restrict__ slot, int T_, int d, int E, int El,
+                                                             T* __restrict__ y) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  gather_sum_token<T, true, float, QV, PeerRows<T>>(PeerRows<T>{&eo, probs + (long long)t * E, d, El},
+                                                     slot + (long long)t * E, d, E, nullptr, y + (long long)t * d, lane);
+}
+
+// token side: dx[t] = dxg[t] + sum_{e asc} dx_perm@(e / El)[slot[t,e]]
+template <typename T, typename TX, int QV>
+__global__ void __launch_bounds__(256, 4) ep2_dispatch_bwd_kernel(const __grid_constant__ PeerTable dxp,
+                                                                  const int* __restrict__ slot,
+                                                                  const TX* __restrict__ dxg, int T_, int d, int E,
+                                                                  int El, T* __restrict__ dx) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  gather_sum_token<T, false, TX, QV, PeerRows<T>>(PeerRows<T>{&dxp, nullptr, d, El}, slot + (long long)t * E, d, E,
+                                                   dxg ? dxg + (long long)t * d : nullptr, dx + (long long)t * d, lane);
+}
+
 }  // namespace
 
 cudaError_t launch_spawn(const moe_ctx* c, const void* W1s, const void* b1s, const void* W2s, const void* b2s,
@@ -524,18 +729,22 @@ cudaError_t launch_combine(const moe_ctx* c, const void* e_out, const float* row
   return cudaGetLastError();
 }
 
-template <typename T, int MAXV, bool COMPUTE = true>
+template <typename T, int MAXV, bool COMPUTE = true, bool PEER = false>
 static cudaError_t launch_cbc(moe_ctx* c, const void* dy, const void* e_out, const float* row_gate,
                               const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
-                              float* dG_row, cudaStream_t s) {
+                              float* dG_row, cudaStream_t s, const int32_t* row_src = nullptr,
+                              const PeerTable* dyp = nullptr) {
   const size_t smem = sizeof(float) * 8 * c->d;
-  auto k = combine_bwd_colsum_kernel<T, MAXV, COMPUTE>;
+  auto k = combine_bwd_colsum_kernel<T, MAXV, COMPUTE, PEER>;
+  PeerTable tab{};
+  if (dyp) tab = *dyp;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   k<<<dim3(c->db2_S, c->E_local), 256, smem, s>>>((const T*)dy, (const T*)e_out, row_gate, row_token, offsets, c->d,
-                                                 R_cap, c->db2_S, (T*)d_eout, dG_row, c->db2part), count_launch();
+                                                 R_cap, c->db2_S, (T*)d_eout, dG_row, c->db2part, row_src, tab),
+      count_launch();
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess && COMPUTE) {
     c->db2_src = d_eout;
@@ -621,6 +830,125 @@ cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int
   else
     MOE_QV_DISPATCH(pass_vectors(c->d, 4), dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>((const float*)dx_perm, slot, dxg, c->T, c->d, c->E,
                                                            (float*)dx), count_launch())
+  return cudaGetLastError();
+}
+
+}  // namespace moe
+
+namespace moe {
+
+// ------------------------------------------------------------------ fused peer-memory EP launchers
+cudaError_t launch_ep2_counts(const moe_ctx* c, const int32_t* counts, const PeerTable& all, cudaStream_t s) {
+  const int n = c->world * c->E;
+  ep2_counts_kernel<<<(n + 255) / 256, 256, 0, s>>>(counts, c->E, c->rank, c->world, all), count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ep2_plan(const moe_ctx* c, const int32_t* counts_all, int64_t R_cap, int32_t* offsets_recv,
+                            cudaStream_t s) {
+  ep2_plan_kernel<<<1, 256, sizeof(long long) * c->E, s>>>(counts_all, c->world, c->E, c->rank, R_cap, c->ep_off,
+                                                          c->ep_tot, c->ep2_base, c->flags), count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess && offsets_recv)
+    e = cudaMemcpyAsync(offsets_recv, c->ep_off, sizeof(int) * (c->E_local + 1), cudaMemcpyDeviceToDevice, s);
+  return e;
+}
+
+cudaError_t launch_ep2_prepare(const moe_ctx* c, void* x_recv, int32_t* rtok, int32_t* rsrc, float* rgate,
+                               int64_t R_cap, cudaStream_t s) {
+  dim3 grid(64, c->E_local < 65535 ? c->E_local : 65535);
+  if (c->dtype == 1)
+    ep2_prepare_kernel<bf16><<<grid, 256, 0, s>>>((bf16*)x_recv, rtok, rsrc, rgate, c->ep_off, c->ep_tot, c->E_local,
+                                                  c->d, R_cap), count_launch();
+  else
+    ep2_prepare_kernel<float><<<grid, 256, 0, s>>>((float*)x_recv, rtok, rsrc, rgate, c->ep_off, c->ep_tot, c->E_local,
+                                                   c->d, R_cap), count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot, const PeerTable& xr,
+                                const PeerTable& rtok, const PeerTable& rsrc, const PeerTable& rgate, int64_t R_cap,
+                                cudaStream_t s) {
+  // per-block ranks (scan over this rank's token blocks; the local layout itself is not built)
+  dispatch_scan_kernel<<<1, 1024, 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot, c->ep2_scr,
+                                          c->ep2_scr + c->E + 1, (long long)1 << 62, c->flags), count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || c->nblk == 0) return e;
+  ep2_rank_kernel<<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->blk_base, c->ep2_base,
+                                              R_cap, rtok, rsrc, rgate), count_launch();
+  if (c->dtype == 1)
+    ep2_copy_kernel<bf16><<<(c->T + 7) / 8, 256, 0, s>>>((const bf16*)x, slot, c->T, c->d, c->E, c->E_local, xr),
+        count_launch();
+  else
+    ep2_copy_kernel<float><<<(c->T + 7) / 8, 256, 0, s>>>((const float*)x, slot, c->T, c->d, c->E, c->E_local, xr),
+        count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ep2_combine(const moe_ctx* c, const PeerTable& eo, const float* probs, const int32_t* slot, void* y,
+                               cudaStream_t s) {
+  if (c->T == 0) return cudaSuccess;
+  const unsigned grid = (c->T + 7) / 8;
+  if (c->dtype == 1) {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_combine_kernel<bf16, QV><<<grid, 256, 0, s>>>(
+        eo, probs, slot, c->T, c->d, c->E, c->E_local, (bf16*)y), count_launch())
+  } else {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2_combine_kernel<float, QV><<<grid, 256, 0, s>>>(
+        eo, probs, slot, c->T, c->d, c->E, c->E_local, (float*)y), count_launch())
+  }
+  return cudaGetLastError();
+}
+
+bool ep2_width_ok(const moe_ctx* c) {
+  const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
+  return c->dtype == 1 ? nvec <= 128 : nvec <= 64;
+}
+
+cudaError_t launch_ep2_combine_bwd(moe_ctx* c, const PeerTable& dyp, const void* e_out, const float* rgate,
+                                   const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets, int64_t R_cap,
+                                   void* d_eout, float* dG_row, cudaStream_t s) {
+  c->db2_src = nullptr;
+  if (R_cap == 0) return cudaSuccess;
+  const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
+  if (c->dtype == 1) {
+    if (nvec <= 32) return launch_cbc<bf16, 1, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+    if (nvec <= 64) return launch_cbc<bf16, 2, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+    if (nvec <= 96) return launch_cbc<bf16, 3, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+    return launch_cbc<bf16, 4, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+  }
+  if (nvec <= 32) return launch_cbc<float, 1, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+  return launch_cbc<float, 2, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+}
+
+cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, const float* dlogits,
+                                    const void* Wg, void* dx, cudaStream_t s) {
+  if (c->T == 0) return cudaSuccess;
+  const unsigned grid = (c->T + 7) / 8;
+  if (dlogits && gate_tc_supported(c)) {
+    cudaError_t e = gate_tc_dx(c, dlogits, Wg, c->dxg, s);
+    if (e != cudaSuccess) return e;
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, bf16, QV><<<grid, 256, 0, s>>>(
+        dxp, slot, (const bf16*)c->dxg, c->T, c->d, c->E, c->E_local, (bf16*)dx), count_launch())
+    return cudaGetLastError();
+  }
+  const float* dxg = nullptr;
+  if (dlogits) {
+    SimtGemm g{};
+    g.A = dlogits; g.sAm = c->E; g.sAk = 1;
+    g.B = Wg; g.sBk = 1; g.sBn = c->E;
+    g.C = c->dxg; g.sCm = c->d;
+    g.M = c->T; g.N = c->d; g.K = c->E; g.G = 1; g.k_split = 1;
+    cudaError_t e = launch_simt_gemm(g, 0, c->dtype, 0, EPI_F32, s);
+    if (e != cudaSuccess) return e;
+    dxg = c->dxg;
+  }
+  if (c->dtype == 1) {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, float, QV><<<grid, 256, 0, s>>>(
+        dxp, slot, dxg, c->T, c->d, c->E, c->E_local, (bf16*)dx), count_launch())
+  } else {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2_dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>(
+        dxp, slot, dxg, c->T, c->d, c->E, c->E_local, (float*)dx), count_launch())
+  }
   return cudaGetLastError();
 }
 

@@ -1,0 +1,229 @@
+"""Fused peer-memory expert parallelism ("ep2", include/moe_dts.h): the B200-native EP path.
+
+The all-to-all exchanges of the DTS-Gate MoE layer are fused into the routing
+kernels as NVLink peer loads / stores: the token side stores its x rows straight into the
+owners' expert-side layouts, the combine / gate backward / dispatch backward gather e_out,
+dG and dx_perm rows from the owners, and the expert side's combine backward reads dy rows
+from the token owners.  Every rank's row buffers are symmetric (mapped into every rank):
+`SymmetricBuffers` allocates them with torch symmetric memory (one process per GPU) or, for
+tests, emulates `world` ranks inside ONE process on one device.
+
+Marshalling only: every step is a libmoe_dts.so kernel (moe_ep2_* + the expert FFN calls).
+
+    ranks = [EP2Rank(T, d, f, E, dtype, dev, r, W, syms) for r in range(W)]   # emulation
+    EP2Rank.step_forward / step_backward run the phases of ONE rank (real multi-GPU: each
+    process calls them; barriers are NCCL all-reduces).  `run_lockstep` drives emulated
+    ranks phase by phase in one process.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Optional
+
+import torch
+
+from . import _lib as L
+
+_DT = {torch.float32: L.MOE_F32, torch.bfloat16: L.MOE_BF16}
+
+
+class SymmetricBuffers:
+    """Named symmetric buffers: buf(name, rank, shape, dtype) -> (local tensor, [peer tensors]).
+
+    mode "emulated": all ranks live in this process on one device (tests).
+    mode "symm_mem": one rank per process; torch.distributed._symmetric_memory maps every
+    rank's allocation into every rank (NVLink P2P)."""
+
+    def __init__(self, world: int, device: torch.device, mode: str = "emulated", group=None):
+        self.world, self.device, self.mode, self.group = world, device, mode, group
+        self._bufs: Dict[str, list] = {}
+
+    def buf(self, name: str, rank: int, shape, dtype):
+        shape = tuple(int(s) for s in shape)
+        key = name
+        have = self._bufs.get(key)
+        if have is None or tuple(have[0].shape) != shape or have[0].dtype != dtype:
+            if self.mode == "emulated":
+                have = [torch.zeros(shape, dtype=dtype, device=self.device) for _ in range(self.world)]
+            else:
+                import torch.distributed._symmetric_memory as symm_mem
+                t = symm_mem.empty(*shape, dtype=dtype, device=self.device)
+                t.zero_()
+                hdl = symm_mem.rendezvous(t, self.group)
+                have = [t if q == rank else hdl.get_buffer(q, shape, dtype) for q in range(self.world)]
+            self._bufs[key] = have
+        return have[rank], have
+
+
+class EP2Rank:
+    """One rank of the fused peer-memory EP layer."""
+
+    def __init__(self, T: int, d_model: int, d_ff: int, E: int, dtype: torch.dtype, device: torch.device, rank: int,
+                 world: int, syms: SymmetricBuffers, comm: Optional[int] = None):
+        self.T, self.d, self.f, self.E, self.El = T, d_model, d_ff, E, E // world
+        self.dtype, self.device, self.rank, self.world, self.syms = dtype, device, rank, world, syms
+        self.ctx = L.moe_create(T, d_model, d_ff, E, _DT[dtype], comm if comm else L.MOE_COMM_EMULATED, rank, world)
+        self.ws = torch.empty(max(256, L.moe_workspace_bytes(self.ctx)), dtype=torch.uint8, device=device)
+        L.moe_set_workspace(self.ctx, self.ws)
+        # static capacity: every rank's tokens to every local expert, 128-aligned per expert
+        self.R_cap = (world * T * self.El + 127 * self.El + 127) // 128 * 128
+        self.Wg = self.W1 = self.b1 = self.W2 = self.b2 = None
+        self.st: Dict[str, torch.Tensor] = {}
+
+    def __del__(self):
+        try:
+            if getattr(self, "ctx", None):
+                L.moe_destroy(self.ctx)
+                self.ctx = None
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ parameters
+    def spawn(self, W1s, b1s, W2s, b2s, M1bits, M2bits):
+        El, d, f, kw = self.El, self.d, self.f, dict(dtype=self.dtype, device=self.device)
+        self.W1, self.b1 = torch.empty(El, f, d, **kw), torch.empty(El, f, **kw)
+        self.W2, self.b2 = torch.empty(El, d, f, **kw), torch.empty(El, d, **kw)
+        L.moe_dts_spawn(self.ctx, W1s, b1s, W2s, b2s, M1bits, M2bits, self.W1, self.b1, self.W2, self.b2)
+
+    def set_gate(self, Wg):
+        self.Wg = Wg
+
+    def _sym(self, name, shape, dtype):
+        return self.syms.buf(name, self.rank, shape, dtype)
+
+    def barrier(self):
+        L.moe_ep2_barrier(self.ctx)
+
+    # ------------------------------------------------------------ forward phases
+    def fwd_gate(self, x, u, tau: float, threshold: float, top1: bool = False):
+        T, E, dev = self.T, self.E, self.device
+        s = self.st
+        s["x"], s["tau"] = x, tau
+        s["probs"] = torch.empty(T, E, dtype=torch.float32, device=dev)
+        s["slot"] = torch.empty(T, E, dtype=torch.int32, device=dev)
+        s["counts"] = torch.empty(E, dtype=torch.int32, device=dev)
+        s["near"] = torch.empty(1, dtype=torch.int32, device=dev)
+        L.moe_dts_gate(self.ctx, x, self.Wg, u, tau, threshold, top1, s["probs"], s["slot"], s["counts"], s["near"])
+        _, peers = self._sym("counts_all", (self.world, E), torch.int32)
+        L.moe_ep2_counts(self.ctx, s["counts"], peers)
+
+    def fwd_plan(self):
+        R, d = self.R_cap, self.d
+        s = self.st
+        ca, _ = self._sym("counts_all", (self.world, self.E), torch.int32)
+        s["off"] = torch.empty(self.El + 1, dtype=torch.int32, device=self.device)
+        L.moe_ep2_plan(self.ctx, ca, R, s["off"])
+        xr, _ = self._sym("x_recv", (R, d), self.dtype)
+        rt, _ = self._sym("rtok", (R,), torch.int32)
+        rs, _ = self._sym("rsrc", (R,), torch.int32)
+        rg, _ = self._sym("rgate", (R,), torch.float32)
+        L.moe_ep2_prepare_recv(self.ctx, xr, rt, rs, rg, R)
+
+    def fwd_dispatch(self):
+        R, d, s = self.R_cap, self.d, self.st
+        L.moe_ep2_dispatch(self.ctx, s["x"], s["probs"], s["slot"], self._sym("x_recv", (R, d), self.dtype)[1],
+                           self._sym("rtok", (R,), torch.int32)[1], self._sym("rsrc", (R,), torch.int32)[1],
+                           self._sym("rgate", (R,), torch.float32)[1], R)
+
+    def fwd_experts(self):
+        R, d, f, s = self.R_cap, self.d, self.f, self.st
+        s["gp"] = torch.empty(R, f, dtype=self.dtype, device=self.device)
+        s["h"] = torch.empty(R, f, dtype=self.dtype, device=self.device)
+        L.moe_expert_ffn(self.ctx, self._sym("x_recv", (R, d), self.dtype)[0], s["off"], R, self.W1, self.b1, self.W2,
+                         self.b2, s["gp"], s["h"], self._sym("e_out", (R, d), self.dtype)[0])
+
+    def fwd_combine(self):
+        R, d, s = self.R_cap, self.d, self.st
+        s["y"] = torch.empty(self.T, d, dtype=self.dtype, device=self.device)
+        L.moe_ep2_combine(self.ctx, self._sym("e_out", (R, d), self.dtype)[1], s["probs"], s["slot"], s["y"])
+        return s["y"]
+
+    # ------------------------------------------------------------ backward phases
+    def bwd_stage_dy(self, dy):
+        buf, _ = self._sym("dy", (self.T, self.d), self.dtype)
+        buf.copy_(dy)
+
+    def bwd_combine(self):
+        R, d, s = self.R_cap, self.d, self.st
+        s["d_eout"] = torch.empty(R, d, dtype=self.dtype, device=self.device)
+        dG, _ = self._sym("dG", (R,), torch.float32)
+        L.moe_ep2_combine_bwd(self.ctx, self._sym("dy", (self.T, d), self.dtype)[1],
+                              self._sym("e_out", (R, d), self.dtype)[0], self._sym("rgate", (R,), torch.float32)[0],
+                              self._sym("rtok", (R,), torch.int32)[0], self._sym("rsrc", (R,), torch.int32)[0],
+                              s["off"], R, s["d_eout"], dG)
+
+    def bwd_experts(self):
+        R, d, f, El, s, dev = self.R_cap, self.d, self.f, self.El, self.st, self.device
+        g = dict(dW1=torch.empty(El, f, d, dtype=torch.float32, device=dev),
+                 db1=torch.empty(El, f, dtype=torch.float32, device=dev),
+                 dW2=torch.empty(El, d, f, dtype=torch.float32, device=dev),
+                 db2=torch.empty(El, d, dtype=torch.float32, device=dev))
+        dxp, _ = self._sym("dx_perm", (R, d), self.dtype)
+        L.moe_expert_ffn_bwd(self.ctx, s["d_eout"], self._sym("x_recv", (R, d), self.dtype)[0], s["gp"], s["h"],
+                             s["off"], R, self.W1, self.W2, s["gp"], dxp, g["dW1"], g["db1"], g["dW2"], g["db2"])
+        s["grads"] = g
+
+    def bwd_gate(self, balance_alpha: float = 0.0, B_total: Optional[int] = None):
+        s, dev = self.st, self.device
+        g = s["grads"]
+        g["dWg"] = torch.empty(self.d, self.E, dtype=torch.float32, device=dev)
+        g["dlogits"] = torch.empty(self.T, self.E, dtype=torch.float32, device=dev)
+        B = self.T * self.world if B_total is None else B_total
+        L.moe_ep2_gate_bwd(self.ctx, self._sym("dG", (self.R_cap,), torch.float32)[1], s["slot"], s["probs"], s["x"],
+                           s["tau"], balance_alpha, s["counts"] if balance_alpha > 0 else None, B, g["dWg"],
+                           g["dlogits"])
+
+    def bwd_dispatch(self):
+        s, g = self.st, self.st["grads"]
+        g["dx"] = torch.empty(self.T, self.d, dtype=self.dtype, device=self.device)
+        L.moe_ep2_dispatch_bwd(self.ctx, self._sym("dx_perm", (self.R_cap, self.d), self.dtype)[1], s["slot"],
+                               g["dlogits"], self.Wg, g["dx"])
+        return g
+
+    def check(self):
+        L.moe_check(self.ctx)
+
+    # ------------------------------------------------------------ one rank, one process (multi-GPU)
+    def forward(self, x, u, tau, threshold, top1=False):
+        self.fwd_gate(x, u, tau, threshold, top1)
+        self.barrier()
+        self.fwd_plan()
+        self.fwd_dispatch()
+        self.barrier()
+        self.fwd_experts()
+        self.barrier()
+        return self.fwd_combine()
+
+    def backward(self, dy, balance_alpha: float = 0.0):
+        self.bwd_stage_dy(dy)
+        self.barrier()
+        self.bwd_combine()
+        self.bwd_experts()
+        self.barrier()
+        self.bwd_gate(balance_alpha)
+        L.moe_ep_allreduce(self.ctx, self.st["grads"]["dWg"], self.d * self.E)
+        return self.bwd_dispatch()
+
+
+def run_lockstep(ranks: List[EP2Rank], xs, us, dys, tau: float, threshold: float, top1: bool = False):
+    """Emulated ranks in one process: each phase runs on every rank before the next phase
+    (the barriers' ordering); dW_g is summed over the ranks (the all-reduce)."""
+    for r, x, u in zip(ranks, xs, us):
+        r.fwd_gate(x, u, tau, threshold, top1)
+    for r in ranks:
+        r.fwd_plan()
+    for r in ranks:
+        r.fwd_dispatch()
+    for r in ranks:
+        r.fwd_experts()
+    ys = [r.fwd_combine() for r in ranks]
+    for r, dy in zip(ranks, dys):
+        r.bwd_stage_dy(dy)
+    for r in ranks:
+        r.bwd_combine()
+    for r in ranks:
+        r.bwd_experts()
+    for r in ranks:
+        r.bwd_gate()
+    dWg = sum(r.st["grads"]["dWg"] for r in ranks)
+    grads = [r.bwd_dispatch() for r in ranks]
+    return ys, grads, dWg

@@ -1,0 +1,214 @@
+"""Fused peer-memory expert parallelism ("ep2") on ONE GPU: `world` ranks emulated in one
+process (moe_create(nccl_comm=MOE_COMM_EMULATED)), each with its own buffers on the device;
+the peer-pointer tables hand every rank the other ranks' buffers, exactly as NVLink
+symmetric memory would on a multi-GPU node, and the ranks' launches are ordered phase by
+phase on one stream (the barriers' role).  No kernel waits on another rank's kernel.
+
+The result must equal the single-rank layer on the GLOBAL token set (all ranks' tokens
+concatenated): bit for bit for routing, y, dx, dlogits and the expert weight gradients of
+each rank's experts (same rows in the same order reach the same kernels); db2 and dW_g to
+fp32 rounding (different partial-sum partitions: db2 splits per local expert, dW_g summed
+over ranks).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from harness import configs, inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2112_14397_b200 import build
+    build.build()
+
+
+def _rel(a, b):
+    a, b = a.double(), b.double()
+    den = float(b.norm())
+    return float((a - b).norm()) / (den if den else 1.0)
+
+
+def _ep2(cfg, W, T):
+    from paper_2112_14397_b200 import _lib as L
+    dev = torch.device("cuda", 0)
+    d, f, E = cfg.d_model, cfg.d_ff, cfg.E
+    El = E // W
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
+    mdt = L.MOE_BF16 if cfg.dtype == "bf16" else L.MOE_F32
+    tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
+    ranks = [inputs.make_inputs(cfg, rank=q, T=T) for q in range(W)]
+    li0 = ranks[0]
+    Wg = li0.Wg.to(dev)
+    R_cap = (W * T * El + 127 * El + 127) // 128 * 128
+    ctx, wsp = [], []
+    for q in range(W):
+        h = L.moe_create(T, d, f, E, mdt, L.MOE_COMM_EMULATED, q, W)
+        ws = torch.empty(max(256, L.moe_workspace_bytes(h)), dtype=torch.uint8, device=dev)
+        L.moe_set_workspace(h, ws)
+        ctx.append(h)
+        wsp.append(ws)
+    z = lambda *shape, dtype=dt: torch.zeros(*shape, dtype=dtype, device=dev)  # noqa: E731
+    # per-rank weights (local experts spawned from the shared expert + global masks)
+    Wt = []
+    for q in range(W):
+        w = dict(W1=z(El, f, d), b1=z(El, f), W2=z(El, d, f), b2=z(El, d))
+        L.moe_dts_spawn(ctx[q], *(t.to(dev) for t in (li0.W1s, li0.b1s, li0.W2s, li0.b2s, li0.M1bits, li0.M2bits)),
+                        w["W1"], w["b1"], w["W2"], w["b2"])
+        Wt.append(w)
+    # symmetric buffers
+    sym = {k: [] for k in ("x_recv", "rtok", "rsrc", "rgate", "e_out", "d_eout", "dG", "dx_perm", "counts_all", "dy")}
+    for q in range(W):
+        sym["x_recv"].append(z(R_cap, d))
+        sym["rtok"].append(z(R_cap, dtype=torch.int32))
+        sym["rsrc"].append(z(R_cap, dtype=torch.int32))
+        sym["rgate"].append(z(R_cap, dtype=torch.float32))
+        sym["e_out"].append(z(R_cap, d))
+        sym["d_eout"].append(z(R_cap, d))
+        sym["dG"].append(z(R_cap, dtype=torch.float32))
+        sym["dx_perm"].append(z(R_cap, d))
+        sym["counts_all"].append(z(W, E, dtype=torch.int32))
+        sym["dy"].append(ranks[q].dy.to(dev))
+    loc = []
+    for q in range(W):
+        li = ranks[q]
+        loc.append(dict(x=li.x.to(dev), u=li.u.to(dev), probs=z(T, E, dtype=torch.float32),
+                        slot=z(T, E, dtype=torch.int32), counts=z(E, dtype=torch.int32),
+                        near=z(1, dtype=torch.int32), off=z(El + 1, dtype=torch.int32), gp=z(R_cap, f), h=z(R_cap, f),
+                        y=z(T, d), dx=z(T, d), dlogits=z(T, E, dtype=torch.float32),
+                        dWg=z(d, E, dtype=torch.float32), dW1=z(El, f, d, dtype=torch.float32),
+                        db1=z(El, f, dtype=torch.float32), dW2=z(El, d, f, dtype=torch.float32),
+                        db2=z(El, d, dtype=torch.float32)))
+    # ---- forward, phase by phase over the ranks
+    for q in range(W):
+        o = loc[q]
+        L.moe_dts_gate(ctx[q], o["x"], Wg, o["u"], tau, c, cfg.top1, o["probs"], o["slot"], o["counts"], o["near"])
+    for q in range(W):
+        L.moe_ep2_counts(ctx[q], loc[q]["counts"], sym["counts_all"])
+        L.moe_ep2_barrier(ctx[q])
+    for q in range(W):
+        L.moe_ep2_plan(ctx[q], sym["counts_all"][q], R_cap, loc[q]["off"])
+        L.moe_ep2_prepare_recv(ctx[q], sym["x_recv"][q], sym["rtok"][q], sym["rsrc"][q], sym["rgate"][q], R_cap)
+    for q in range(W):
+        L.moe_ep2_dispatch(ctx[q], loc[q]["x"], loc[q]["probs"], loc[q]["slot"], sym["x_recv"], sym["rtok"],
+                           sym["rsrc"], sym["rgate"], R_cap)
+    for q in range(W):
+        w, o = Wt[q], loc[q]
+        L.moe_expert_ffn(ctx[q], sym["x_recv"][q], o["off"], R_cap, w["W1"], w["b1"], w["W2"], w["b2"], o["gp"], o["h"],
+                         sym["e_out"][q])
+    for q in range(W):
+        L.moe_ep2_combine(ctx[q], sym["e_out"], loc[q]["probs"], loc[q]["slot"], loc[q]["y"])
+    # ---- backward
+    for q in range(W):
+        L.moe_ep2_combine_bwd(ctx[q], sym["dy"], sym["e_out"][q], sym["rgate"][q], sym["rtok"][q], sym["rsrc"][q],
+                              loc[q]["off"], R_cap, sym["d_eout"][q], sym["dG"][q])
+    for q in range(W):
+        w, o = Wt[q], loc[q]
+        L.moe_expert_ffn_bwd(ctx[q], sym["d_eout"][q], sym["x_recv"][q], o["gp"], o["h"], o["off"], R_cap, w["W1"],
+                             w["W2"], o["gp"], sym["dx_perm"][q], o["dW1"], o["db1"], o["dW2"], o["db2"])
+    for q in range(W):
+        o = loc[q]
+        L.moe_ep2_gate_bwd(ctx[q], sym["dG"], o["slot"], o["probs"], o["x"], tau, 0.0, None, W * T, o["dWg"],
+                           o["dlogits"])
+    for q in range(W):
+        o = loc[q]
+        L.moe_ep2_dispatch_bwd(ctx[q], sym["dx_perm"], o["slot"], o["dlogits"], Wg, o["dx"])
+    torch.cuda.synchronize()
+    for q in range(W):
+        L.moe_check(ctx[q])
+    out = dict(loc=loc, dWg=sum(o["dWg"] for o in loc), counts_all=sym["counts_all"][0].cpu())
+    for h in ctx:
+        L.moe_destroy(h)
+    return out, ranks
+
+
+def _single(cfg, ranks):
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    dev = torch.device("cuda", 0)
+    x = torch.cat([r.x for r in ranks]).to(dev)
+    u = torch.cat([r.u for r in ranks]).to(dev)
+    dy = torch.cat([r.dy for r in ranks]).to(dev)
+    li0 = ranks[0]
+    layer = DTSMoELayer(x.shape[0], cfg.d_model, cfg.d_ff, cfg.E, dtype=x.dtype, device=dev)
+    layer.set_gate(li0.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li0.W1s, li0.b1s, li0.W2s, li0.b2s, li0.M1bits, li0.M2bits)))
+    y = layer.forward(x, u, float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)), top1=cfg.top1)
+    g = layer.backward(dy, inplace_da=False)
+    torch.cuda.synchronize()
+    layer.check()
+    return layer, y, g
+
+
+def _check(cfg, W, T):
+    ep, ranks = _ep2(cfg, W, T)
+    layer, y, g = _single(cfg, ranks)
+    E, El = cfg.E, cfg.E // W
+    st = layer.state
+    for q in range(W):
+        o = ep["loc"][q]
+        sl = slice(q * T, (q + 1) * T)
+        assert torch.equal(o["probs"], st.probs[sl]), f"rank {q} probs"
+        assert torch.equal(o["slot"] >= 0, st.slot[sl] >= 0), f"rank {q} routing"
+        assert torch.equal(o["counts"], (st.slot[sl] >= 0).sum(0).int()), f"rank {q} counts"
+        assert torch.equal(o["y"], y[sl]), f"rank {q} y"
+        assert torch.equal(o["dlogits"], g["dlogits"][sl]), f"rank {q} dlogits"
+        assert torch.equal(o["dx"], g["dx"][sl]), f"rank {q} dx"
+        es = slice(q * El, (q + 1) * El)
+        for k in ("dW1", "dW2", "db1"):
+            assert torch.equal(o[k], g[k][es]), f"rank {q} {k}"
+        assert _rel(o["db2"], g["db2"][es]) < 1e-5, f"rank {q} db2"
+    assert torch.equal(ep["counts_all"].sum(0), st.counts.cpu()), "all-gathered counts"
+    assert _rel(ep["dWg"], g["dWg"]) < 1e-5, "dWg"
+
+
+def test_ep2_c3_shape_two_ranks():
+    _check(configs.C3, 2, 512)
+
+
+def test_ep2_c3_shape_four_ranks_ragged():
+    _check(configs.C3, 4, 300)
+
+
+def test_ep2_c4_shape_eight_ranks_top1():
+    cfg = dataclasses.replace(configs.C4, top1=True)
+    _check(cfg, 8, 160)
+
+
+def test_ep2_fp32_c1_two_ranks():
+    _check(configs.C1, 2, 96)
+
+
+def test_ep2_module_lockstep_c2_shape():
+    # the same through paper_2112_14397_b200.ep2 (EP2Rank phases + SymmetricBuffers emulation)
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers, run_lockstep
+    cfg, W, T = configs.C2, 2, 384
+    dev = torch.device("cuda", 0)
+    ranks_in = [inputs.make_inputs(cfg, rank=q, T=T) for q in range(W)]
+    li0 = ranks_in[0]
+    syms = SymmetricBuffers(W, dev)
+    ranks = []
+    for q in range(W):
+        r = EP2Rank(T, cfg.d_model, cfg.d_ff, cfg.E, torch.bfloat16, dev, q, W, syms)
+        r.set_gate(li0.Wg.to(dev))
+        r.spawn(*(t.to(dev) for t in (li0.W1s, li0.b1s, li0.W2s, li0.b2s, li0.M1bits, li0.M2bits)))
+        ranks.append(r)
+    ys, grads, dWg = run_lockstep(ranks, [ri.x.to(dev) for ri in ranks_in], [ri.u.to(dev) for ri in ranks_in],
+                                  [ri.dy.to(dev) for ri in ranks_in], float(np.float32(cfg.tau)),
+                                  float(np.float32(cfg.threshold)))
+    torch.cuda.synchronize()
+    for r in ranks:
+        r.check()
+    layer, y, g = _single(cfg, ranks_in)
+    El = cfg.E // W
+    for q in range(W):
+        sl, es = slice(q * T, (q + 1) * T), slice(q * El, (q + 1) * El)
+        assert torch.equal(ys[q], y[sl])
+        assert torch.equal(grads[q]["dx"], g["dx"][sl])
+        assert torch.equal(grads[q]["dW1"], g["dW1"][es]) and torch.equal(grads[q]["dW2"], g["dW2"][es])
+    assert _rel(dWg, g["dWg"]) < 1e-5
