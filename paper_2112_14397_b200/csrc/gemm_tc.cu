@@ -67,7 +67,9 @@ template <int EPI> struct EpiCfg {
 #define MOE_EPI_NBUF 2
 #endif
   static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4 : MOE_EPI_NBUF;                 // staging buffers per warp
-  static constexpr int STAGING = NOUT * EPI_WARPS * NBUF * CHUNK_BYTES;
+  // per-warp staging: NBUF chunk buffers of NOUT bf16 32x32 boxes, or of one fp32 32x32 box (F32)
+  static constexpr int WARP_STAGE = EPI == TEPI_F32 ? NBUF * 2 * CHUNK_BYTES : NBUF * NOUT * CHUNK_BYTES;
+  static constexpr int STAGING = EPI_WARPS * WARP_STAGE;
   static constexpr int BAR_BYTES = 2048;
   static constexpr int STAGES = (SMEM_LIMIT - 1024 - BAR_BYTES - STAGING) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 + BAR_BYTES;
@@ -180,7 +182,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch(&tmA);
     tc::tma_prefetch(&tmB);
-    if (Cfg::NOUT >= 1) tc::tma_prefetch(&tmO1);
+    if (Cfg::NOUT >= 1 || EPI == TEPI_F32) tc::tma_prefetch(&tmO1);
     if (Cfg::NOUT >= 2) tc::tma_prefetch(&tmO2);
     if (EPI == TEPI_GELU_BWD) tc::tma_prefetch(&tmX);
     for (int s = 0; s < STAGES; ++s) {
@@ -292,7 +294,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int part = ew >> 2;                          // chunks part, part + 3, part + 6 (< 8) of the 8 x 32 columns
     const int nch = (CHUNKS - part + EPI_PER_Q - 1) / EPI_PER_Q;
     const int row_in_tile = sub * 32 + lane;
-    const uint32_t stage_base = tc::smem_u32(staging) + ew * (Cfg::NBUF * Cfg::NOUT * CHUNK_BYTES);
+    const uint32_t stage_base = tc::smem_u32(staging) + ew * Cfg::WARP_STAGE;
     const uint32_t swz = (uint32_t)((lane >> 1) & 3);  // SWIZZLE_64B: 16-byte chunk q -> q ^ ((row >> 1) & 3)
     const uint32_t tempty_leader = tc::mapa(tc::smem_u32(tempty_bar), 0);
     const uint32_t auxb = tc::smem_u32(aux_bar + ew * 4);
@@ -356,13 +358,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc::tmem_ld_wait();
         TR(8, t);
         if (EPI == TEPI_F32) {
-          if (row < p.M && n < p.N) {
-            float* o = p.out + (long long)tl.g * p.out_g + row * p.ldo + n;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                              __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          // fp32 32x32 box (128-byte rows, SWIZZLE_128B) staged in smem, one TMA store: coalesced
+          // full-line writes instead of 32 scattered 16-byte rows per store instruction
+          const uint32_t fbuf = stage_base + (seq % Cfg::NBUF) * (2 * CHUNK_BYTES);
+          if (seq >= (uint32_t)Cfg::NBUF) {
+            if (lane == 0) tc::bulk_wait_read<Cfg::NBUF - 1>();
+            __syncwarp();
           }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            tc::st_shared_v4(fbuf + lane * 128 + ((q ^ (lane & 7)) << 4),
+                             make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]));
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            // M and N are multiples of 64: a 32x32 box is wholly inside the group's [M, N] block or outside
+            if (tl.m_own + sub * 32 < p.M && n < p.N)
+              tc::tma_store_2d(&tmO1, fbuf, n, tl.g * p.M + tl.m_own + sub * 32);
+            tc::bulk_commit();
+          }
+          __syncwarp();
           continue;
         }
         const bool store = warp_rows_ok && n < p.N;
@@ -501,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (Cfg::NOUT > 0 && lane == 0) tc::bulk_wait<0>();
+    if ((Cfg::NOUT > 0 || EPI == TEPI_F32) && lane == 0) tc::bulk_wait<0>();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -548,6 +563,18 @@ bool make_map(CUtensorMap* m, const void* ptr, long long rows, long long cols, l
 }
 bool make_store_map(CUtensorMap* m, const void* ptr, long long rows, long long cols) {
   return make_map(m, ptr, rows, cols, cols, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+// fp32 [rows, cols] row-major output, 32x32 boxes with 128-byte swizzled rows (weight gradients)
+bool make_store_map_f32(CUtensorMap* m, const void* ptr, long long rows, long long cols) {
+  EncodeTiledFn f = encode_fn();
+  if (!f || !ptr) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int EPI, bool A_MN, bool B_MN, bool KGRP>
@@ -732,14 +759,16 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
   if (!make_map(&mA, d_eout, R_cap, d, d, 64, 64) || !make_map(&mB, h, R_cap, f, f, 64, 64))
     return cudaErrorInvalidValue;
   q.M = d; q.N = f; q.out = dW2; q.ldo = f; q.out_g = (long long)d * f;
-  e = launch_tc<TEPI_F32, true, true, true>(mA, mB, mA, mA, mA, q,
+  if (!make_store_map_f32(&mO, dW2, (long long)El * d, f)) return cudaErrorInvalidValue;
+  e = launch_tc<TEPI_F32, true, true, true>(mA, mB, mO, mO, mO, q,
                                             (long long)El * ((d + 255) / 256) * ((f + BN - 1) / BN), c->sm_count, s);
   if (e != cudaSuccess) return e;
   // wgrad1: dW1_e [f, d] = da_e^T x_perm_e      A(m=f, k=row) = da MN-major; B(k=row, n=d) = x_perm MN-major
   if (!make_map(&mA, da, R_cap, f, f, 64, 64) || !make_map(&mB, x_perm, R_cap, d, d, 64, 64))
     return cudaErrorInvalidValue;
   q.M = f; q.N = d; q.out = dW1; q.ldo = d; q.out_g = (long long)f * d;
-  return launch_tc<TEPI_F32, true, true, true>(mA, mB, mA, mA, mA, q,
+  if (!make_store_map_f32(&mO, dW1, (long long)El * f, d)) return cudaErrorInvalidValue;
+  return launch_tc<TEPI_F32, true, true, true>(mA, mB, mO, mO, mO, q,
                                                (long long)El * ((f + 255) / 256) * ((d + BN - 1) / BN), c->sm_count,
                                                s);
 }

@@ -31,10 +31,13 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--kernel-times", action="store_true")
+    ap.add_argument("--step", type=int, default=None, help="C5 schedule step (tau, c and noise of that step)")
     a = ap.parse_args()
     cfg = configs.get(a.config)
+    if a.step is not None:
+        cfg = cfg.at_step(a.step)
     dev = torch.device("cuda", 0)
-    li = inputs.make_inputs(cfg)
+    li = inputs.make_inputs(cfg, step=a.step or 0)
     dt = inputs.TORCH_DTYPE[cfg.dtype]
     tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
     layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev)
