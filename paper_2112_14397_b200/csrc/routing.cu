@@ -76,10 +76,26 @@ __global__ void __launch_bounds__(kGateBT) dispatch_rank_kernel(
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
-  for (int e = 0; e < E; ++e) {
-    const bool sel = valid && slot[(long long)t * E + e] >= 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, sel);
-    if (lane == 0) s_bal[warp][e] = bal;
+  // 8 selection flags per thread in flight (16-byte loads when the rows allow), then 8 ballots
+  const bool vec = (E & 3) == 0;
+  for (int e0 = 0; e0 < E; e0 += 8) {
+    int v[8];
+    if (vec && e0 + 8 <= E) {
+      int4 a = make_int4(-1, -1, -1, -1), b = a;
+      if (valid) {
+        a = *reinterpret_cast<const int4*>(slot + (long long)t * E + e0);
+        b = *reinterpret_cast<const int4*>(slot + (long long)t * E + e0 + 4);
+      }
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned bal = __ballot_sync(0xffffffffu, v[j] >= 0);
+      if (lane == 0 && e0 + j < E) s_bal[warp][e0 + j] = bal;
+    }
   }
   __syncthreads();
   if (valid) {
@@ -592,10 +608,15 @@ __global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
-  for (int e = 0; e < E; ++e) {
-    const bool sel = valid && slot[(long long)t * E + e] >= 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, sel);
-    if (lane == 0) s_bal[warp][e] = bal;
+  for (int e0 = 0; e0 < E; e0 += 8) {          // 8 flags in flight, then 8 ballots (as dispatch_rank_kernel)
+    int v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned bal = __ballot_sync(0xffffffffu, v[j] >= 0);
+      if (lane == 0 && e0 + j < E) s_bal[warp][e0 + j] = bal;
+    }
   }
   __syncthreads();
   if (!valid) return;
