@@ -260,10 +260,11 @@ cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const f
                         int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
                         cudaStream_t s) {
   cudaError_t e;
+  // the tcgen05 path zeroes counts / near_band in its first kernel (no memset nodes in the step)
+  if (c->T > 0 && gate_tc_supported(c)) return gate_tc_forward(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
   if ((e = cudaMemsetAsync(counts, 0, sizeof(int) * c->E, s)) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(near_band, 0, sizeof(int), s)) != cudaSuccess) return e;
   if (c->T == 0) return cudaSuccess;
-  if (gate_tc_supported(c)) return gate_tc_forward(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
   if (c->dtype == 1) return launch_gate_typed<bf16>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
   return launch_gate_typed<float>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
 }

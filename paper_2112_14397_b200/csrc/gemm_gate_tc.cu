@@ -608,8 +608,14 @@ __global__ void __launch_bounds__(256) gate_refine_kernel(const bf16* __restrict
 }
 
 // ------------------------------------------------------------------ small layout kernels
-// WgT [Ep, d] bf16 (rows >= E zero) from W_g [d, E]
-__global__ void wg_transpose_kernel(const bf16* __restrict__ Wg, int d, int E, int Ep, bf16* __restrict__ WgT) {
+// WgT [Ep, d] bf16 (rows >= E zero) from W_g [d, E]; block 0 also zeroes the step's counters
+// (counts [E], near_band, the refine queue length): no memset nodes before the gate kernel
+__global__ void wg_transpose_kernel(const bf16* __restrict__ Wg, int d, int E, int Ep, bf16* __restrict__ WgT,
+                                    int* __restrict__ counts, int* __restrict__ near_band, int* __restrict__ rq_count) {
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < E; i += blockDim.x) counts[i] = 0;
+    if (threadIdx.x == 0) { *near_band = 0; *rq_count = 0; }
+  }
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)Ep * d) return;
   const int e = (int)(i / d), k = (int)(i % d);
@@ -731,7 +737,8 @@ cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, con
   const int E = c->E, d = c->d, Ep = gate_Ep(E);
   const_cast<moe_ctx*>(c)->dl2_src = nullptr;       // the forward reuses the gate scratch
   bf16* WgT = reinterpret_cast<bf16*>(c->gate_scratch);
-  wg_transpose_kernel<<<(unsigned)(((long long)Ep * d + 255) / 256), 256, 0, s>>>((const bf16*)Wg, d, E, Ep, WgT),
+  wg_transpose_kernel<<<(unsigned)(((long long)Ep * d + 255) / 256), 256, 0, s>>>((const bf16*)Wg, d, E, Ep, WgT,
+                                                                                  counts, near_band, c->rq),
       count_launch();
   CUtensorMap mA, mB;
   if (!map2d(&mA, x, c->T, d, 64, BM) || !map2d(&mB, WgT, Ep, d, 64, Ep)) return cudaErrorInvalidValue;
@@ -754,7 +761,6 @@ cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, con
     q.u = u; q.probs = probs; q.slot = slot;
     q.counts = counts; q.blk_cnt = c->blk_cnt; q.near_band = near_band; q.flags = c->flags;
     q.rq_count = c->rq; q.rq_list = c->rq + 1;
-    if ((e = cudaMemsetAsync(c->rq, 0, sizeof(int), s)) != cudaSuccess) return e;
     const int grid = c->nblk < c->sm_count ? c->nblk : c->sm_count;
     switch (E) {
       case 16: e = launch_fused<16>(mA, mB, q, grid, s); break;
@@ -764,7 +770,6 @@ cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, con
     }
     if (e != cudaSuccess) return e;
   } else {
-    if ((e = cudaMemsetAsync(c->rq, 0, sizeof(int), s)) != cudaSuccess) return e;
     const size_t misc = sizeof(int) * 132 + sizeof(float) * 128 * (E + 1);
     if ((e = launch<GATE>(mA, mB, p, dim3(c->nblk), Ep, misc, s)) != cudaSuccess) return e;
     if ((e = launch_gate_softmax_tpt(c, c->logits, u, tau, thr, top1, probs, slot, counts, near_band, s)) !=
