@@ -197,6 +197,7 @@ def run_ours(args, rank, world):
     graph = None
     n_launch0 = L.moe_kernel_launch_count()
     launches = None
+    stage_ev = {}
     if args.graph and world == 1:
         R_static = layer.state.R_cap
         full_step(False, R_cap=R_static)
@@ -205,8 +206,8 @@ def run_ours(args, rank, world):
         g_ffn, g_bwd = (ev(), ev()), (ev(), ev())
         n0 = L.moe_kernel_launch_count()
         with torch.cuda.graph(graph):
-            layer.forward(x, u, tau, c, R_cap=R_static, events=g_ffn)
-            layer.backward(dy, events=g_bwd)
+            layer.forward(x, u, tau, c, R_cap=R_static, events=g_ffn, stage_events=stage_ev)
+            layer.backward(dy, events=g_bwd, stage_events=stage_ev)
         launches = L.moe_kernel_launch_count() - n0
         for _ in range(max(1, args.warmup)):
             graph.replay()
@@ -219,6 +220,7 @@ def run_ours(args, rank, world):
     torch.cuda.synchronize()
     n_launch1 = L.moe_kernel_launch_count()
     step_ms, ffn_ms, bwd_ms = [], [], []
+    stage_ms = {k: [] for k in stage_ev}
     t_wall = time.perf_counter()
     for _ in range(args.steps):
         flush.fill_(1)                       # L2 flush outside the timed events
@@ -234,6 +236,8 @@ def run_ours(args, rank, world):
         step_ms.append(s0.elapsed_time(s1))
         ffn_ms.append(e_f[0].elapsed_time(e_f[1]))
         bwd_ms.append(e_b[0].elapsed_time(e_b[1]))
+        for k, (a, b) in stage_ev.items():
+            stage_ms[k].append(a.elapsed_time(b))
     torch.cuda.synchronize()
     barrier(world)
     wall = time.perf_counter() - t_wall
@@ -282,6 +286,7 @@ def run_ours(args, rank, world):
                      + cfg.E * cfg.d_model * cfg.d_ff * (4 * (2 if cfg.dtype == "bf16" else 4) + 2 * 4),
                      **_traffic(cfg.name, world)},
         "step_tflops": step_flops / (ms_step / 1e3) / 1e12,
+        "stages": _stages(cfg, layer, counts, {k: sum(v) / len(v) for k, v in stage_ms.items() if v}),
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -293,6 +298,38 @@ def run_ours(args, rank, world):
         out["cpu_baseline"] = {"value": T_sub / dt_cpu, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
                                "sample": f"{T_sub} tokens of {cfg.name} (same d/d_ff/E/tau/c), fwd+bwd, fp64 NumPy, "
                                          f"{dt_cpu:.2f} s"}
+    return out
+
+
+def _stages(cfg, layer, counts, ms):
+    """Per C-ABI stage: mean ms inside the replayed step and achieved GB/s of the stage's
+    algorithmic HBM bytes (SURVEY §8d terms; GEMM operand traffic excluded) or TFLOP/s."""
+    if not ms:
+        return None
+    b = 2 if cfg.dtype == "bf16" else 4
+    T, d, f, E = cfg.T, cfg.d_model, cfg.d_ff, cfg.E
+    R = int(counts.sum())
+    Rp = int(layer.state.offsets[-1].item())
+    Ep = (E + 15) // 16 * 16
+    Kp = (2 * Ep + 63) // 64 * 64
+    byts = {
+        "gate": T * d * b + 3 * T * E * 4,
+        "dispatch": 2 * T * E * 4 + T * d * b + Rp * (d * b + 8),
+        "combine": R * d * b + T * d * b + T * E * 4 + R * 4,
+        "combine_bwd": T * d * b + 2 * Rp * d * b + Rp * 12,
+        "gate_bwd": R * 4 + 3 * T * E * 4 + T * Kp * 2 + T * d * b,
+        "dispatch_bwd": T * E * 4 + R * d * b + 2 * T * d * 2 + T * d * b + T * Kp * 2,
+    }
+    flops = {"expert_ffn": 4.0 * Rp * d * f, "expert_ffn_bwd": 8.0 * Rp * d * f}
+    out = {}
+    for k, v in ms.items():
+        o = {"ms": v}
+        if k in byts:
+            o["GB/s"] = byts[k] / (v / 1e3) / 1e9
+            o["algorithmic_bytes"] = byts[k]
+        if k in flops:
+            o["TFLOP/s"] = flops[k] / (v / 1e3) / 1e12
+        out[k] = o
     return out
 
 

@@ -40,6 +40,21 @@ def make_nccl_comm(rank: int, world: int) -> int:
     return L.moe_nccl_comm_init(bytes(uid.numpy().tobytes()), world, rank)
 
 
+class _Marker:
+    """Records a (start, end) CUDA event pair per stage into `d` (no-op when d is None)."""
+
+    def __init__(self, d):
+        self.d = d
+
+    def __call__(self, name, which):
+        if self.d is None:
+            return
+        if name not in self.d:
+            self.d[name] = (torch.cuda.Event(enable_timing=True, external=True),
+                            torch.cuda.Event(enable_timing=True, external=True))
+        self.d[name][which].record()
+
+
 @dataclass
 class ForwardState:
     tau: float
@@ -151,16 +166,21 @@ class DTSMoELayer:
 
     # ------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor, u: Optional[torch.Tensor], tau: float, threshold: float,
-                top1: bool = False, R_cap: Optional[int] = None, stream=None, events=None) -> torch.Tensor:
+                top1: bool = False, R_cap: Optional[int] = None, stream=None, events=None,
+                stage_events: Optional[dict] = None) -> torch.Tensor:
         """events: optional (start, end) torch.cuda.Event pair recorded around moe_expert_ffn
-        on the current stream (bench roofline timing)."""
+        on the current stream (bench roofline timing).  stage_events: optional dict that
+        receives a (start, end) event pair per C-ABI stage (per-stage breakdown)."""
+        mark = _Marker(stage_events)
         T, E = self.T, self.E
         dev = self.device
         probs = torch.empty(T, E, dtype=torch.float32, device=dev)
         slot = torch.empty(T, E, dtype=torch.int32, device=dev)
         counts = torch.empty(E, dtype=torch.int32, device=dev)
         near = torch.empty(1, dtype=torch.int32, device=dev)
+        mark("gate", 0)
         L.moe_dts_gate(self.ctx, x, self.Wg, u, tau, threshold, top1, probs, slot, counts, near, stream)
+        mark("gate", 1)
         offsets = torch.empty(E + 1, dtype=torch.int32, device=dev)
         if self.ep:
             counts_all = L.moe_ep_exchange_counts(self.ctx, counts, self.world, E, stream)
@@ -182,20 +202,26 @@ class DTSMoELayer:
             offsets_recv = offsets
         R_send_cap, R_recv_cap = rb["R_send_cap"], rb["R_recv_cap"]
         R_out = torch.empty(1, dtype=torch.int32, device=dev)
+        mark("dispatch", 0)
         L.moe_dispatch(self.ctx, x, probs, slot, rb["x_perm"], rb["row_token"], rb["row_gate"], offsets, R_send_cap,
                        R_out, stream)
+        mark("dispatch", 1)
         if self.ep:
             L.moe_ep_dispatch(self.ctx, rb["x_perm"], rb["x_recv"], self.d, R_recv_cap, stream)
         if events:
             events[0].record()
+        mark("expert_ffn", 0)
         L.moe_expert_ffn(self.ctx, rb["x_recv"], offsets_recv, R_recv_cap, self.W1, self.b1, self.W2, self.b2,
                          None if self.recompute else rb["gp"], rb["h"], rb["e_out_recv"], stream)
+        mark("expert_ffn", 1)
         if events:
             events[1].record()
         if self.ep:
             L.moe_ep_combine(self.ctx, rb["e_out_recv"], rb["e_out"], self.d, stream)
         y = torch.empty(T, self.d, dtype=self.dtype, device=dev)
+        mark("combine", 0)
         L.moe_combine(self.ctx, rb["e_out"], rb["row_gate"], slot, y, stream)
+        mark("combine", 1)
         self.state = ForwardState(tau, threshold, top1, x, probs, slot, counts, near, offsets, R_send_cap, y)
         self.state.offsets_recv = offsets_recv
         self.state.R_recv_cap = R_recv_cap
@@ -203,14 +229,17 @@ class DTSMoELayer:
 
     # ------------------------------------------------------------ backward
     def backward(self, dy: torch.Tensor, balance_alpha: float = 0.0, B_total: Optional[int] = None,
-                 inplace_da: bool = True, stream=None, events=None):
+                 inplace_da: bool = True, stream=None, events=None, stage_events: Optional[dict] = None):
         st = self.state
         if st is None:
             raise RuntimeError("backward() before forward()")
         rb = self._rows
         El, d, f, dev = self.E_local, self.d, self.f, self.device
+        mark = _Marker(stage_events)
+        mark("combine_bwd", 0)
         L.moe_combine_bwd(self.ctx, dy, rb["e_out"], rb["row_gate"], rb["row_token"], st.offsets, st.R_cap,
                           rb["d_eout"], rb["dG_row"], stream)
+        mark("combine_bwd", 1)
         if self.ep:
             L.moe_ep_dispatch(self.ctx, rb["d_eout"], rb["d_eout_recv"], d, st.R_recv_cap, stream)
         grads = dict(
@@ -226,9 +255,11 @@ class DTSMoELayer:
         da = rb["gp"] if inplace_da else torch.empty_like(rb["gp"])
         if events:
             events[0].record()
+        mark("expert_ffn_bwd", 0)
         L.moe_expert_ffn_bwd(self.ctx, rb["d_eout_recv"], rb["x_recv"], rb["gp"], rb["h"], st.offsets_recv,
                              st.R_recv_cap, self.W1, self.W2, da, rb["dx_perm_recv"], grads["dW1"], grads["db1"],
                              grads["dW2"], grads["db2"], stream)
+        mark("expert_ffn_bwd", 1)
         if events:
             events[1].record()
         if self.ep:
@@ -239,12 +270,16 @@ class DTSMoELayer:
         if balance_alpha > 0 and self.ep:
             counts = st.counts.clone()
             L.moe_ep_allreduce(self.ctx, counts, self.E, is_int32=True, stream=stream)
+        mark("gate_bwd", 0)
         L.moe_dts_gate_bwd(self.ctx, rb["dG_row"], st.slot, st.probs, st.x, st.tau, balance_alpha,
                            counts if balance_alpha > 0 else None, B, grads["dWg"], dlogits, stream)
+        mark("gate_bwd", 1)
         if self.ep:
             L.moe_ep_allreduce(self.ctx, grads["dWg"], d * self.E, stream=stream)
         dx = torch.empty(self.T, d, dtype=self.dtype, device=dev)
+        mark("dispatch_bwd", 0)
         L.moe_dispatch_bwd(self.ctx, rb["dx_perm"], st.slot, dlogits, self.Wg, dx, stream)
+        mark("dispatch_bwd", 1)
         grads["dx"] = dx
         grads["dlogits"] = dlogits
         grads["da"] = da
