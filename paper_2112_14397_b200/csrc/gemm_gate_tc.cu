@@ -303,7 +303,10 @@ __global__ void __launch_bounds__(Threads<MODE>::N) gate_tc_kernel(const __grid_
 // gate_softmax_tpt_kernel, u read and probs / slot written as 256-byte row segments.
 // Near-boundary tokens are queued for gate_refine_kernel (fp64), as before.  The logits never
 // reach HBM.
-constexpr int FG_STAGES = 4;
+#ifndef MOE_FG_STAGES
+#define MOE_FG_STAGES 4
+#endif
+constexpr int FG_STAGES = MOE_FG_STAGES;   // x-tile ring depth (24 KB stages at E = 64)
 constexpr int FG_SWARPS = 16;                     // 512 threads = 128 tokens x 4 lanes
 constexpr int FG_THREADS = 64 + 128 + 32 * FG_SWARPS;
 
