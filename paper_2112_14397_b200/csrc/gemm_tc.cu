@@ -68,7 +68,11 @@ template <int EPI> struct EpiCfg {
 #endif
   static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4 : MOE_EPI_NBUF;                 // staging buffers per warp
   // per-warp staging: NBUF chunk buffers of NOUT bf16 32x32 boxes, or of one fp32 32x32 box (F32)
+#ifdef MOE_EXP_F32_DIRECT
+  static constexpr int WARP_STAGE = EPI == TEPI_F32 ? 0 : NBUF * NOUT * CHUNK_BYTES;
+#else
   static constexpr int WARP_STAGE = EPI == TEPI_F32 ? NBUF * 2 * CHUNK_BYTES : NBUF * NOUT * CHUNK_BYTES;
+#endif
   static constexpr int STAGING = EPI_WARPS * WARP_STAGE;
   static constexpr int BAR_BYTES = 2048;
   static constexpr int STAGES = (SMEM_LIMIT - 1024 - BAR_BYTES - STAGING) / STAGE_BYTES;
@@ -357,6 +361,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         tc::tmem_ld32(t_row + col, r);
         tc::tmem_ld_wait();
         TR(8, t);
+#ifdef MOE_EXP_F32_DIRECT
+        if (EPI == TEPI_F32) {
+          if (row < p.M && n < p.N) {
+            float* o = p.out + (long long)tl.g * p.out_g + row * p.ldo + n;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                              __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          }
+          continue;
+        }
+#endif
         if (EPI == TEPI_F32) {
           // fp32 32x32 box (128-byte rows, SWIZZLE_128B) staged in smem, one TMA store: coalesced
           // full-line writes instead of 32 scattered 16-byte rows per store instruction
