@@ -221,14 +221,24 @@ __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     for (int k = 2 * Ep + lane; k < Kp; k += 32) dL2[(long long)t * Kp + k] = __float2bfloat16_rn(0.f);
 }
 
-// out[i] = sum_z part[z][i], fixed order
-__global__ void reduce_splits_kernel(const float* __restrict__ part, int splits, long long n,
-                                     float* __restrict__ out) {
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+// out[i] = sum_z part[z][i], fixed order: block = 32 outputs x 8 warps, warp w sums the splits
+// z = w, w + 8, ... of its lane's output, the 8 warp sums are added in order w = 0..7
+__global__ void __launch_bounds__(256) reduce_splits_kernel(const float* __restrict__ part, int splits, long long n,
+                                                           float* __restrict__ out) {
+  __shared__ float red[8][32];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long i = (long long)blockIdx.x * 32 + lane;
   float acc = 0.f;
-  for (int z = 0; z < splits; ++z) acc += part[(long long)z * n + i];
-  out[i] = acc;
+  if (i < n)
+    for (int z = warp; z < splits; z += 8) acc += part[(long long)z * n + i];
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && i < n) {
+    float a = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) a += red[w][lane];
+    out[i] = a;
+  }
 }
 
 // ------------------------------------------------------------------ balance loss
@@ -305,7 +315,7 @@ static cudaError_t gate_bwd_impl(const moe_ctx* c, const float* dG_row, const Pe
   if ((e = launch_simt_gemm(g, c->dtype, 0, 0, EPI_F32, s)) != cudaSuccess) return e;
   if (c->dwg_splits > 1) {
     long long n = (long long)c->d * c->E;
-    reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->part, c->dwg_splits, n, dWg), count_launch();
+    reduce_splits_kernel<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(c->part, c->dwg_splits, n, dWg), count_launch();
   }
   return cudaGetLastError();
 }
@@ -429,7 +439,7 @@ cudaError_t launch_gate_softmax_tpt(const moe_ctx* c, const float* logits, const
 }
 
 cudaError_t launch_reduce_splits(const float* part, int splits, long long n, float* out, cudaStream_t s) {
-  reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, splits, n, out), count_launch();
+  reduce_splits_kernel<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(part, splits, n, out), count_launch();
   return cudaGetLastError();
 }
 

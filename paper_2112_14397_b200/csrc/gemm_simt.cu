@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const TI* __restrict__
   }
 }
 
-__global__ void colsum_final_kernel(const float* __restrict__ part, int N, int S, float* __restrict__ out) {
+// out[g][n] = sum_s part[g][s][n] (few splits): thread per column, splits in order
+__global__ void colsum_final_seq_kernel(const float* __restrict__ part, int N, int S, float* __restrict__ out) {
   const int g = blockIdx.y;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
@@ -201,7 +202,36 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int N, int S
   out[(long long)g * N + n] = t;
 }
 
+// out[g][n] = sum_s part[g][s][n] (many splits): block = 32 columns x 8 warps; warp w sums the splits
+// s = w, w + 8, ... (ascending) of its lane's column, then the 8 warp sums are added in
+// order w = 0..7 (fixed order, deterministic; 8 loads in flight per column instead of S).
+__global__ void __launch_bounds__(256) colsum_final_kernel(const float* __restrict__ part, int N, int S,
+                                                          float* __restrict__ out) {
+  __shared__ float red[8][32];
+  const int g = blockIdx.y, warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = blockIdx.x * 32 + lane;
+  float t = 0.f;
+  if (n < N)
+    for (int sp = warp; sp < S; sp += 8) t += part[((long long)g * S + sp) * N + n];
+  red[warp][lane] = t;
+  __syncthreads();
+  if (warp == 0 && n < N) {
+    float a = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) a += red[w][lane];
+    out[(long long)g * N + n] = a;
+  }
+}
+
 }  // namespace
+
+// the second phase of the column sums: warp-split over the partials when there are many
+static void launch_final(const float* part, int N, int S, int G, float* out, cudaStream_t s) {
+  if (S >= 16)
+    colsum_final_kernel<<<dim3((N + 31) / 32, G), 256, 0, s>>>(part, N, S, out), count_launch();
+  else
+    colsum_final_seq_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, S, out), count_launch();
+}
 
 cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int epi, cudaStream_t s) {
   if (ta == 0 && tb == 0) return launch_typed<float, float, float>(g, epi, s);
@@ -216,11 +246,14 @@ cudaError_t launch_simt_gemm(const SimtGemm& g, int ta, int tb, int tout, int ep
 // db1[g][n] = sum over the 32-row blocks of group g of part[rb][n]: the same two-phase fixed-order
 // reduction as the column sums, over the [R/32][N] fp32 partial rows (m_off >> 5).
 cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, float* part2,
-                              cudaStream_t s) {
+                              long long R_cap, cudaStream_t s) {
   if (G == 0 || N == 0) return cudaSuccess;
-  const int S = kColsumSplits;
+  // splits per expert: ~32 partial rows (of 32 token rows each) per split, at most kColsumSplits
+  long long per = R_cap / 32 / G;
+  int S = (int)((per + 31) / 32);
+  S = S < 1 ? 1 : (S > kColsumSplits ? kColsumSplits : S);
   colsum_part_kernel<float><<<dim3((N + 127) / 128, S, G), 256, 0, s>>>(part, N, m_off, S, 5, part2), count_launch();
-  colsum_final_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part2, N, S, out), count_launch();
+  launch_final(part2, N, S, G, out, s);
   return cudaGetLastError();
 }
 
@@ -234,13 +267,13 @@ cudaError_t launch_colsum_grouped(const void* X, int tin, int N, const int* m_of
     colsum_part_kernel<float><<<g1, 256, 0, s>>>(reinterpret_cast<const float*>(X), N, m_off, S, 0, part), count_launch();
   else
     colsum_part_kernel<bf16><<<g1, 256, 0, s>>>(reinterpret_cast<const bf16*>(X), N, m_off, S, 0, part), count_launch();
-  colsum_final_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, S, out), count_launch();
+  launch_final(part, N, S, G, out, s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_colsum_final(const float* part, int N, int S, int G, float* out, cudaStream_t s) {
   if (G == 0 || N == 0) return cudaSuccess;
-  colsum_final_kernel<<<dim3((N + 255) / 256, G), 256, 0, s>>>(part, N, S, out), count_launch();
+  launch_final(part, N, S, G, out, s);
   return cudaGetLastError();
 }
 

@@ -753,7 +753,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
                                                      c->sm_count, s);
     if (e != cudaSuccess) return e;
     if (fuse_db1) {
-      if ((e = launch_db1_reduce(reinterpret_cast<const float*>(dx_perm), f, offsets, El, db1, c->colpart, s)) !=
+      if ((e = launch_db1_reduce(reinterpret_cast<const float*>(dx_perm), f, offsets, El, db1, c->colpart, R_cap, s)) !=
           cudaSuccess)
         return e;
     } else if (db1) {

@@ -144,7 +144,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
                               cudaStream_t s);
 // db1[g][n] = sum over the 32-row blocks of group g of part[rb][n]  (fixed order)
 cudaError_t launch_db1_reduce(const float* part, int N, const int* m_off, int G, float* out, float* part2,
-                              cudaStream_t s);
+                              long long R_cap, cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 gate contractions (bf16)
 bool gate_tc_supported(const moe_ctx* c);
