@@ -176,43 +176,81 @@ __device__ __forceinline__ void gate_token(const float* L, int t, const T* __res
 
 
 // fp64 decision for one token deferred by the thread-per-token fast path (near the
-// threshold or an argmax tie), computed by a whole 256-thread block: warp w accumulates the
-// fp64 logits over K range w of 8 (lanes = experts, 8 independent loads in flight per lane),
-// partials are added in fixed order, then warp 0 applies noise / softmax / decision in fp64,
-// writes probs / slot and counts with global integer atomics.
+// threshold or an argmax tie), computed by a whole 256-thread block.  The fp64 logits are a
+// latency problem (one token: d * E products), so W_g is staged through shared memory in
+// chunks of up to 32 KB, each chunk's loads all issued before any is used (one memory
+// round trip per chunk, not one per k step); thread (e, sl) then accumulates expert e over
+// the k = sl (mod nsl) rows of the chunk, the nsl partials are added in fixed order, and warp
+// 0 applies noise / softmax / decision in fp64, writes probs / slot and counts with global
+// integer atomics.
+constexpr int kRefineWBytes = 32768;
+constexpr int kRefineKC = 1024;
+struct RefineSmem {
+  uint4 w[kRefineWBytes / 16];     // W_g rows [k0, k0 + KC) of this chunk, raw element type
+  float x[kRefineKC];              // x[k0 .. k0 + KC)
+  double red[256];                 // per-thread partial logits
+};
+
 template <typename T>
 __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restrict__ x, const T* __restrict__ Wg,
                                                         const float* __restrict__ u, int d, int E, float tau,
                                                         float thr, int top1, float* __restrict__ probs,
                                                         int* __restrict__ slot, int* __restrict__ counts,
                                                         int* __restrict__ blk_cnt, int nblk, int blk_tokens,
-                                                        int* __restrict__ near_band, double* s_part /*[8][128]*/) {
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kr = (d + 7) / 8;
-  const int k0 = warp * kr, k1 = min(d, k0 + kr);
+                                                        int* __restrict__ near_band, RefineSmem& sm) {
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const T* xr = x + (long long)t * d;
+  const int nsl = 256 / E;                        // E <= 128: >= 2 k slices
+  const int e_me = tid % E, sl = tid / E;
+  const bool worker = sl < nsl;
+  int KC = kRefineWBytes / (E * (int)sizeof(T));
+  if (KC > kRefineKC) KC = kRefineKC;
+  const T* ws = reinterpret_cast<const T*>(sm.w);
+  const bool vec = ((E * sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(Wg) & 15) == 0);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int k0 = 0; k0 < d; k0 += KC) {
+    const int kc = min(KC, d - k0);
+    const long long n = (long long)kc * E;         // elements of this chunk
+    if (vec) {
+      const uint4* src = reinterpret_cast<const uint4*>(Wg + (long long)k0 * E);
+      const int n16 = (int)(n * sizeof(T) / 16);   // <= 2048 = 8 per thread
+      uint4 r[8];
 #pragma unroll
-  for (int i = 0; i < kMaxEPL; ++i) {
-    const int e = lane + 32 * i;
-    double acc[8];
+      for (int j = 0; j < 8; ++j)
+        if (tid + 256 * j < n16) r[j] = __ldg(src + tid + 256 * j);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
-    if (e < E) {
-      int k = k0;
-      for (; k + 7 < k1; k += 8) {
-        float w[8], xv[8];
+      for (int j = 0; j < 8; ++j)
+        if (tid + 256 * j < n16) sm.w[tid + 256 * j] = r[j];
+    } else {
+      T* wd = reinterpret_cast<T*>(sm.w);
+      for (int b = 0; b < n; b += 256 * 8) {
+        T r[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          w[j] = to_f32(Wg[(long long)(k + j) * E + e]);
-          xv[j] = to_f32(xr[k + j]);
-        }
+        for (int j = 0; j < 8; ++j)
+          if (b + tid + 256 * j < n) r[j] = Wg[(long long)k0 * E + b + tid + 256 * j];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fma((double)xv[j], (double)w[j], acc[j]);
+        for (int j = 0; j < 8; ++j)
+          if (b + tid + 256 * j < n) wd[b + tid + 256 * j] = r[j];
       }
-      for (; k < k1; ++k) acc[0] = fma((double)to_f32(xr[k]), (double)to_f32(Wg[(long long)k * E + e]), acc[0]);
     }
-    s_part[warp * 128 + (lane + 32 * i)] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    {
+      float r[kRefineKC / 256];
+#pragma unroll
+      for (int j = 0; j < kRefineKC / 256; ++j)
+        if (tid + 256 * j < kc) r[j] = to_f32(xr[k0 + tid + 256 * j]);
+#pragma unroll
+      for (int j = 0; j < kRefineKC / 256; ++j)
+        if (tid + 256 * j < kc) sm.x[tid + 256 * j] = r[j];
+    }
+    __syncthreads();
+    if (worker) {
+      int k = sl, j = 0;
+      for (; k < kc; k += nsl, j = (j + 1) & 3)
+        acc[j] = fma((double)sm.x[k], (double)to_f32(ws[(long long)k * E + e_me]), acc[j]);
+    }
+    __syncthreads();
   }
+  sm.red[tid] = worker ? (acc[0] + acc[1]) + (acc[2] + acc[3]) : 0.0;
   __syncthreads();
   if (warp == 0) {
     double z64[kMaxEPL];
@@ -222,7 +260,7 @@ __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restri
       z64[i] = -INFINITY;
       if (e < E) {
         double acc = 0.0;
-        for (int w = 0; w < 8; ++w) acc += s_part[w * 128 + e];
+        for (int q = 0; q < nsl; ++q) acc += sm.red[q * E + e];
         const double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
         z64[i] = (acc + zeta) / (double)tau;
       }

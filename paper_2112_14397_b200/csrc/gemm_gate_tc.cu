@@ -603,11 +603,11 @@ __global__ void __launch_bounds__(256) gate_refine_kernel(const bf16* __restrict
                                                           int* __restrict__ counts, int* __restrict__ blk_cnt, int nblk,
                                                           int* __restrict__ near_band, const int* __restrict__ rq_count,
                                                           const int* __restrict__ rq_list) {
-  __shared__ double s_part[8 * 128];
+  __shared__ RefineSmem sm;
   const int n = *rq_count;
   for (int q = blockIdx.x; q < n; q += gridDim.x)
     gate_token_refine_block<bf16>(rq_list[q], x, Wg, u, d, E, tau, thr, top1, probs, slot, counts, blk_cnt, nblk, BM,
-                                  near_band, s_part);
+                                  near_band, sm);
 }
 
 // ------------------------------------------------------------------ small layout kernels

@@ -265,3 +265,20 @@ def test_bf16_single_expert_is_dense_ffn():
     # E = 1: every token to the one expert with weight 1 (P:311 special case), dW_g = 0
     rep, g = _run(_shape("E1", 256, 128, 256, 1, 1.0, 0.0))
     assert float(np.abs(g.grads["dWg"]).max()) == 0.0
+
+
+# ---- the fp64 refine queue under load: tau = 200 squeezes every p towards 1/E and c = 1/E
+# puts most tokens within the 5e-5 refine margin of the threshold, so most decisions (and
+# the probs of those tokens) come from gate_refine_kernel (tau = 50 at E = 64).  Shapes cover one W_g chunk
+# (E=16, d=768), four chunks (E=64, d=1024: 32 KB = 256 rows of W_g per chunk) and the
+# scalar staging path (E=20: a W_g row is 40 bytes, not a multiple of 16) with a ragged
+# second chunk (d=960, 819 rows per chunk).
+@pytest.mark.parametrize("E,d,T,tau", [(16, 768, 1000, 200.0), (64, 1024, 700, 50.0), (20, 960, 515, 200.0)])
+def test_refine_queue_heavy(E, d, T, tau):
+    cfg = _shape(f"RQ{E}", T, d, 256, E, tau, 1.0 / E)
+    rep, g = _run(cfg, backward=False)
+    from _parity import run_oracle
+    li = inputs.make_inputs(cfg, T=T)
+    _, fw, _ = run_oracle(cfg, li, backward=False)
+    queued = np.any(np.abs(fw.p - np.float32(cfg.threshold)) < 5e-5, axis=1)
+    assert queued.mean() > 0.5, queued.mean()
