@@ -67,10 +67,11 @@ struct Carve {
   size_t flags, blk_cnt, blk_base, logits, part, dxg, colsum, tot, colpart, ep_counts, ep_off, ep_tot, gate_scratch, rq, tok_off, biasf, db2part, ep2_scr, ep2_base, total;
 };
 
-// row splits per expert for the fused combine_bwd + db2 partials: about 8 blocks per SM in total
+// row splits per expert for the fused combine_bwd + db2 partials: one wave of its 2 resident
+// blocks per SM in total
 static int db2_splits(const moe_ctx* c) {
   const int El = c->E_local > 0 ? c->E_local : 1;
-  int S = (8 * (c->sm_count > 0 ? c->sm_count : 148) + El - 1) / El;
+  int S = 2 * (c->sm_count > 0 ? c->sm_count : 148) / El;
   return S < 1 ? 1 : (S > 128 ? 128 : S);
 }
 

@@ -330,12 +330,31 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
 // rows [offsets[g], offsets[g+1]) (8 warps, warp w takes rows r0 + w, r0 + w + 8, ...), writes
 // d_eout / dG_row exactly as above and also the db2 column-sum partial of its rows,
 // part[g][s][n] = sum of the stored (rounded) d_eout[r][n], warps combined in fixed order.
+// The dy and e_out rows stream through a per-warp ring of CB_NB shared-memory stages filled
+// by cp.async (16 B per lane and vector, each lane reads back only its own vectors, so no
+// cross-lane synchronisation): CB_NB - 1 rows per warp are in flight while one is computed,
+// without holding them in registers.  Each lane's column sums (its MAXV * V columns) stay in
+// registers; row metadata is loaded one row ahead of its copies.
 // COMPUTE = false: only the partials, from an existing d_eout (same row partition and summation
 // order, so both paths give bit-identical db2).
 // PEER (fused peer-memory EP, expert side): the row's token lives on rank row_src[r]; its dy
 // row is read through that rank's NVLink peer pointer dyp.p[row_src[r]] (no dy exchange).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// ring depth per MAXV: ~96 KB of stages per 256-thread block (2 blocks / SM)
+template <int MAXV> struct CbDepth { static constexpr int N = MAXV == 1 ? 8 : (MAXV == 2 ? 6 : (MAXV == 3 ? 4 : 3)); };
+template <int MAXV> constexpr size_t cb_smem_bytes() {
+  return (size_t)8 * CbDepth<MAXV>::N * 2 * MAXV * 32 * 16 + 8 * CbDepth<MAXV>::N * sizeof(int2);
+}
+
 template <typename T, int MAXV, bool COMPUTE, bool PEER = false>
-__global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __restrict__ dy, const T* __restrict__ e_out,
+__global__ void __launch_bounds__(256, 2) combine_bwd_colsum_kernel(const T* __restrict__ dy, const T* __restrict__ e_out,
                                                                  const float* __restrict__ row_gate,
                                                                  const int* __restrict__ row_token,
                                                                  const int* __restrict__ offsets, int d,
@@ -343,8 +362,10 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
                                                                  float* __restrict__ dG_row, float* __restrict__ part,
                                                                  const int* __restrict__ row_src,
                                                                  const __grid_constant__ PeerTable dyp) {
-  extern __shared__ float red[];                    // [8][d]
   constexpr int V = Vec16<T>::N;
+  constexpr int NB = CbDepth<MAXV>::N;
+  constexpr int STAGE = 2 * MAXV * 32;              // uint4 per warp stage: [dy | e_out][MAXV][32 lanes]
+  extern __shared__ uint4 cb_smem[];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int s = blockIdx.x, g = blockIdx.y;
   const long long off0 = offsets[g], off1 = min((long long)offsets[g + 1], R_cap);
@@ -352,88 +373,120 @@ __global__ void __launch_bounds__(256, 4) combine_bwd_colsum_kernel(const T* __r
   const long long per = ((len + S - 1) / S + 7) / 8 * 8;
   const long long r0 = off0 + (long long)s * per, r1 = min(off1, r0 + per);
   const int nvec = d / V;
-  // this warp's column sums live in its own row of red[] (no registers held across rows)
-  float* racc = red + warp * d;
-  for (int n = lane * 4; n < d; n += 128) *reinterpret_cast<float4*>(racc + n) = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncwarp();
-  auto acc_add = [&](int v, const float* o) {
+  const long long nrows = r1 > r0 + warp ? (r1 - r0 - warp + 7) / 8 : 0;   // rows r0 + warp + 8k
+  uint4* ring = cb_smem + (size_t)warp * NB * STAGE;
+  int2* meta = reinterpret_cast<int2*>(cb_smem + (size_t)8 * NB * STAGE) + warp * NB;   // (token, gate bits)
+  float acc[MAXV * V];
 #pragma unroll
-    for (int h = 0; h < V; h += 4) {
-      float4* a = reinterpret_cast<float4*>(racc + v * V + h);
-      float4 w = *a;
-      w.x += o[h]; w.y += o[h + 1]; w.z += o[h + 2]; w.w += o[h + 3];
-      *a = w;
-    }
-  };
-  // row metadata one row ahead: the dy gather of row r does not wait for its row_token load
-  int t_nx = -1, q_nx = 0;
-  float g_nx = 0.f;
-  if (COMPUTE && r0 + warp < r1) {
-    t_nx = row_token[r0 + warp];
-    g_nx = row_gate[r0 + warp];
-    if (PEER) q_nx = row_src[r0 + warp];
-  }
-  for (long long r = r0 + warp; r < r1; r += 8) {
-    T* dst = d_eout + r * d;
-    if (!COMPUTE) {
+  for (int i = 0; i < MAXV * V; ++i) acc[i] = 0.f;
+
+  if (!COMPUTE) {
+    for (long long k = 0; k < nrows; ++k) {
+      const T* src = d_eout + (r0 + warp + 8 * k) * d;
 #pragma unroll
       for (int j = 0; j < MAXV; ++j) {
         const int v = lane + 32 * j;
         if (v < nvec) {
           float o[V];
-          unpack16(ld_nc_v4(dst + (long long)v * V), o, T());
-          acc_add(v, o);
+          unpack16(ld_nc_v4(src + (long long)v * V), o, T());
+#pragma unroll
+          for (int h = 0; h < V; ++h) acc[j * V + h] += o[h];
         }
       }
-      continue;
     }
-    const int t = t_nx;
-    const float gw = g_nx;
-    const T* dyb = PEER ? reinterpret_cast<const T*>(dyp.p[q_nx]) : dy;
-    if (r + 8 < r1) {
-      t_nx = row_token[r + 8];
-      g_nx = row_gate[r + 8];
-      if (PEER) q_nx = row_src[r + 8];
+  } else {
+    // metadata of the next row to issue (one row ahead of its copies)
+    int t_nx = -1, q_nx = 0;
+    float g_nx = 0.f;
+    if (nrows > 0) {
+      t_nx = row_token[r0 + warp];
+      g_nx = row_gate[r0 + warp];
+      if (PEER) q_nx = row_src[r0 + warp];
     }
-    if (t < 0) {
+    auto issue = [&](long long k) {
+      if (k < nrows) {
+        const long long r = r0 + warp + 8 * k;
+        const int b = (int)(k % NB);
+        const int t = t_nx;
+        meta[b] = make_int2(t, __float_as_int(g_nx));   // every lane stores the same value
+        if (t >= 0) {
+          const T* dyb = PEER ? reinterpret_cast<const T*>(dyp.p[q_nx]) : dy;
+          uint4* st = ring + b * STAGE;
+#pragma unroll
+          for (int j = 0; j < MAXV; ++j) {
+            const int v = lane + 32 * j;
+            if (v < nvec) {
+              cp_async16(st + j * 32 + lane, dyb + (long long)t * d + (long long)v * V);
+              cp_async16(st + (MAXV + j) * 32 + lane, e_out + r * d + (long long)v * V);
+            }
+          }
+        }
+        if (k + 1 < nrows) {
+          t_nx = row_token[r + 8];
+          g_nx = row_gate[r + 8];
+          if (PEER) q_nx = row_src[r + 8];
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int k = 0; k < NB - 1; ++k) issue(k);
+    for (long long k = 0; k < nrows; ++k) {
+      __syncwarp();                                 // every lane is done with row k - 1's meta slot
+      issue(k + NB - 1);
+      cp_async_wait<NB - 1>();                      // this lane's copies of row k have landed
+      const long long r = r0 + warp + 8 * k;
+      const int b = (int)(k % NB);
+      const int2 m = meta[b];
+      T* dst = d_eout + r * d;
+      if (m.x < 0) {
+#pragma unroll
+        for (int j = 0; j < MAXV; ++j) {
+          const int v = lane + 32 * j;
+          if (v < nvec) st_v4(dst + (long long)v * V, make_uint4(0, 0, 0, 0));
+        }
+        if (lane == 0) dG_row[r] = 0.f;
+        continue;
+      }
+      const float gw = __int_as_float(m.y);
+      const uint4* st = ring + b * STAGE;
+      float dot = 0.f;
 #pragma unroll
       for (int j = 0; j < MAXV; ++j) {
         const int v = lane + 32 * j;
-        if (v < nvec) st_v4(dst + (long long)v * V, make_uint4(0, 0, 0, 0));
-      }
-      if (lane == 0) dG_row[r] = 0.f;
-      continue;
-    }
-    uint4 qa[MAXV], qb[MAXV];
+        if (v < nvec) {
+          float a[V], bb[V], o[V];
+          unpack16(st[j * 32 + lane], a, T());
+          unpack16(st[(MAXV + j) * 32 + lane], bb, T());
 #pragma unroll
-    for (int j = 0; j < MAXV; ++j) {
-      const int v = lane + 32 * j;
-      if (v < nvec) {
-        qa[j] = ld_nc_v4(dyb + (long long)t * d + (long long)v * V);
-        qb[j] = ld_nc_v4(e_out + r * d + (long long)v * V);
-      }
-    }
-    float dot = 0.f;
+          for (int h = 0; h < V; ++h) {
+            dot = fmaf(a[h], bb[h], dot);
+            o[h] = gw * a[h];
+          }
+          const uint4 w = pack16(o, T());
+          st_v4(dst + (long long)v * V, w);
+          unpack16(w, o, T());                      // the stored (rounded) values
 #pragma unroll
-    for (int j = 0; j < MAXV; ++j) {
-      const int v = lane + 32 * j;
-      if (v < nvec) {
-        float a[V], b[V], o[V];
-        unpack16(qa[j], a, T());
-        unpack16(qb[j], b, T());
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          dot = fmaf(a[k], b[k], dot);
-          o[k] = gw * a[k];
+          for (int h = 0; h < V; ++h) acc[j * V + h] += o[h];
         }
-        const uint4 w = pack16(o, T());
-        st_v4(dst + (long long)v * V, w);
-        unpack16(w, o, T());                        // the stored (rounded) values
-        acc_add(v, o);
       }
+      dot = warp_sum(dot);
+      if (lane == 0) dG_row[r] = dot;
     }
-    dot = warp_sum(dot);
-    if (lane == 0) dG_row[r] = dot;
+    cp_async_wait<0>();
+  }
+  // block partial: warp sums through shared memory (the ring is free now), added in warp order
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(cb_smem);   // [8][d]
+#pragma unroll
+  for (int j = 0; j < MAXV; ++j) {
+    const int v = lane + 32 * j;
+    if (v < nvec) {
+#pragma unroll
+      for (int h = 0; h < V; h += 4)
+        *reinterpret_cast<float4*>(red + warp * d + v * V + h) =
+            make_float4(acc[j * V + h], acc[j * V + h + 1], acc[j * V + h + 2], acc[j * V + h + 3]);
+    }
   }
   __syncthreads();
   for (int n = threadIdx.x; n < d; n += 256) {
@@ -755,7 +808,7 @@ static cudaError_t launch_cbc(moe_ctx* c, const void* dy, const void* e_out, con
                               const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
                               float* dG_row, cudaStream_t s, const int32_t* row_src = nullptr,
                               const PeerTable* dyp = nullptr) {
-  const size_t smem = sizeof(float) * 8 * c->d;
+  const size_t smem = cb_smem_bytes<MAXV>();         // >= the [8][d] fp32 block reduction
   auto k = combine_bwd_colsum_kernel<T, MAXV, COMPUTE, PEER>;
   PeerTable tab{};
   if (dyp) tab = *dyp;
