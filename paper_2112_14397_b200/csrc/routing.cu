@@ -66,53 +66,87 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restri
 // Rank pass: one CTA per gate block of kGateBT tokens.  Each warp ballots every expert over
 // its 32 tokens (no block barrier per expert); one barrier; then a token's row for expert e is
 //   offsets[e] + blk_base[e][blk] + (selected tokens of e in lower warps) + (lower lanes).
-// Writes slot (row index), row_token, row_gate; zeroes the pad rows of expert blockIdx.x, ...
+// The first two terms are staged in shared memory while the flags load; each thread keeps a
+// bitmask of its selected experts and walks only those, 8 at a time with their probs loads
+// issued together (the pass is latency-bound: 1-2 memory round trips per token, not one per
+// selected expert).  Writes slot (row index), row_token, row_gate; zeroes the pad rows of
+// expert blockIdx.x, ...
 template <typename T>
 __global__ void __launch_bounds__(kGateBT) dispatch_rank_kernel(
     const float* __restrict__ probs, int* __restrict__ slot, int T_, int d, int E, const int* __restrict__ blk_base,
     const int* __restrict__ offsets, const int* __restrict__ tot, T* __restrict__ x_perm, int* __restrict__ row_token,
     float* __restrict__ row_gate, long long R_cap) {
   __shared__ unsigned s_bal[kGateBT / 32][128];
+  __shared__ int s_base[128];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
-  // 8 selection flags per thread in flight (16-byte loads when the rows allow), then 8 ballots
+  for (int e = tid; e < E; e += kGateBT) s_base[e] = offsets[e] + blk_base[(long long)e * gridDim.x + blockIdx.x];
+  // 16 selection flags per thread in flight (16-byte loads when the rows allow), then 16 ballots
   const bool vec = (E & 3) == 0;
-  for (int e0 = 0; e0 < E; e0 += 8) {
-    int v[8];
-    if (vec && e0 + 8 <= E) {
-      int4 a = make_int4(-1, -1, -1, -1), b = a;
-      if (valid) {
-        a = *reinterpret_cast<const int4*>(slot + (long long)t * E + e0);
-        b = *reinterpret_cast<const int4*>(slot + (long long)t * E + e0 + 4);
+  unsigned selm[4] = {0u, 0u, 0u, 0u};              // this thread's selected experts (E <= 128)
+  for (int e0 = 0; e0 < E; e0 += 16) {
+    int v[16];
+    if (vec && e0 + 16 <= E) {
+      int4 q[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        q[i] = make_int4(-1, -1, -1, -1);
+        if (valid) q[i] = *reinterpret_cast<const int4*>(slot + (long long)t * E + e0 + 4 * i);
       }
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { v[4 * i] = q[i].x; v[4 * i + 1] = q[i].y; v[4 * i + 2] = q[i].z; v[4 * i + 3] = q[i].w; }
     } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
+      for (int j = 0; j < 16; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const unsigned bal = __ballot_sync(0xffffffffu, v[j] >= 0);
+    for (int j = 0; j < 16; ++j) {
+      const bool sel = v[j] >= 0 && e0 + j < E;
+      const unsigned bal = __ballot_sync(0xffffffffu, sel);
       if (lane == 0 && e0 + j < E) s_bal[warp][e0 + j] = bal;
+      if (sel) selm[(e0 + j) >> 5] |= 1u << ((e0 + j) & 31);
     }
   }
   __syncthreads();
   if (valid) {
     const unsigned lower = (1u << lane) - 1u;
-    for (int e = 0; e < E; ++e) {
-      const unsigned mine = s_bal[warp][e];
-      if (!((mine >> lane) & 1u)) continue;
-      int wpre = 0;
-      for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
-      const int row = offsets[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre + __popc(mine & lower);
-      if (row < R_cap) {
-        slot[(long long)t * E + e] = row;
-        row_token[row] = t;
-        row_gate[row] = probs[(long long)t * E + e];
-      } else {
-        slot[(long long)t * E + e] = -1;   // dropped (MOE_ECAPACITY raised by the scan)
+    int word = 0;
+    unsigned bits = selm[0];
+    while (true) {
+      // next batch of up to 8 selected experts
+      int es[8], nb = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        while (bits == 0u && word < 3) bits = selm[++word];
+        es[j] = -1;
+        if (bits) {
+          es[j] = word * 32 + __ffs(bits) - 1;
+          bits &= bits - 1u;
+          ++nb;
+        }
       }
+      if (nb == 0) break;
+      float pg[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pg[j] = es[j] >= 0 ? probs[(long long)t * E + es[j]] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = es[j];
+        if (e < 0) continue;
+        const unsigned mine = s_bal[warp][e];
+        int wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
+        const int row = s_base[e] + wpre + __popc(mine & lower);
+        if (row < R_cap) {
+          slot[(long long)t * E + e] = row;
+          row_token[row] = t;
+          row_gate[row] = pg[j];
+        } else {
+          slot[(long long)t * E + e] = -1;   // dropped (MOE_ECAPACITY raised by the scan)
+        }
+      }
+      if (nb < 8) break;
     }
   }
   // pad rows of experts e = blockIdx.x, blockIdx.x + gridDim.x, ...: zero
