@@ -282,3 +282,28 @@ def test_refine_queue_heavy(E, d, T, tau):
     _, fw, _ = run_oracle(cfg, li, backward=False)
     queued = np.any(np.abs(fw.p - np.float32(cfg.threshold)) < 5e-5, axis=1)
     assert queued.mean() > 0.5, queued.mean()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_empty_token_batch(dtype):
+    # T = 0 (a rank with no tokens): every call succeeds, outputs are empty, the weight
+    # gradients are exactly zero (sums over no rows), and a following non-empty layer is unaffected
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.C1 if dtype == "fp32" else dataclasses.replace(configs.C2, d_model=128, d_ff=256)
+    dt = torch.float32 if dtype == "fp32" else torch.bfloat16
+    dev = torch.device("cuda", 0)
+    li = inputs.make_inputs(cfg, T=4)
+    layer = DTSMoELayer(0, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    x = torch.empty(0, cfg.d_model, dtype=dt, device=dev)
+    u = torch.empty(0, cfg.E, dtype=torch.float32, device=dev)
+    y = layer.forward(x, u, float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)))
+    g = layer.backward(torch.empty(0, cfg.d_model, dtype=dt, device=dev))
+    torch.cuda.synchronize()
+    layer.check()
+    assert y.shape == (0, cfg.d_model)
+    assert g["dx"].shape == (0, cfg.d_model)
+    for k in ("dW1", "db1", "dW2", "db2", "dWg"):
+        assert g[k].numel() > 0 and not torch.any(g[k] != 0), k
+    _run(cfg, T=4)
