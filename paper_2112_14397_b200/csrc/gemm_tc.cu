@@ -6,13 +6,13 @@
 // tcgen05.mma.cta_group::2 (M=256, N=256, K=16) and each CTA's TMEM receives its own
 // 128 accumulator rows.  Two 256-column TMEM accumulators let the epilogue of tile i
 // overlap the mainloop of tile i+1.  Operands arrive by TMA (128-byte swizzle) into a
-// 5-7 stage ring; the epilogue (8 warps, thread = accumulator row, 128 columns per warp)
+// 5-7 stage ring; the epilogue (4 x EpiCfg::PER_Q warps, thread = accumulator row)
 // reads TMEM with tcgen05.ld, applies the fused bias / GELU / GELU' / fp32 variants and
 // writes bf16 results through shared memory with TMA bulk-tensor stores.  The GELU'
 // operand a is TMA-loaded into the same staging buffers two chunks ahead.
 //
-// Roles (320 threads / CTA): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
-//   issuer (leader CTA only), warps 2..9 = epilogue.
+// Roles (64 + 128 x PER_Q threads / CTA): warp 0 = TMA producer, warp 1 = TMEM allocator +
+//   MMA issuer (leader CTA only), warps 2.. = epilogue.
 // Scheduling (static, per pair): ROWS mode (ragged M): a tile is a pair of 128-row blocks
 //   of ONE expert (segments are 128-aligned; an odd last block leaves the second CTA's
 //   half idle) x one 256-wide N block; the expert comes from the device offsets[].
@@ -41,13 +41,7 @@ constexpr int A_BYTES = BM * BK * 2;         // 16 KB
 constexpr int B_BYTES = BNH * BK * 2;        // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;               // 2 accumulators x 256 fp32 columns
-#ifndef MOE_EPI_PER_Q
-#define MOE_EPI_PER_Q 3
-#endif
-constexpr int EPI_PER_Q = MOE_EPI_PER_Q;                 // epilogue warps per TMEM lane quarter
-constexpr int EPI_WARPS = 4 * EPI_PER_Q;     // thread = accumulator row; a warp owns every 3rd 32-column chunk
 constexpr int CHUNKS = 256 / 32;
-constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int CHUNK_BYTES = 32 * 32 * 2;     // one 32x32 bf16 sub-tile (TMA box, 64-byte swizzle)
 constexpr int MAX_G = 128;
 constexpr int SMEM_LIMIT = 232448;
@@ -61,7 +55,34 @@ constexpr int SMEM_LIMIT = 232448;
 // TEPI_BIAS_GELU writes (GELU'(a), GELU(a)); TEPI_BIAS_GELU_H writes GELU(a) only (recompute mode)
 enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 3, TEPI_F32 = 4, TEPI_BIAS_GELU_H = 5 };
 
+// Epilogue warps per TMEM lane quarter, per epilogue kind (measured at C2, C4 and C5 steps
+// 5 / 19, profiles/r01/s2/epi_warps.txt): the GELU epilogues need 3 (ALU + staging work per
+// chunk; 2 is 2% faster for GEMM1 at d >= 768 but 5% slower at d = 512), bias / store run
+// best with 2 and the long-K fp32 weight gradients with 1 (fewer warps contending for shared
+// memory, and a smaller staging area leaves room for more operand stages).
+#ifndef MOE_EPQ_GELU
+#define MOE_EPQ_GELU 3
+#endif
+#ifndef MOE_EPQ_BIAS
+#define MOE_EPQ_BIAS 2
+#endif
+#ifndef MOE_EPQ_GBWD
+#define MOE_EPQ_GBWD 3
+#endif
+#ifndef MOE_EPQ_STORE
+#define MOE_EPQ_STORE 2
+#endif
+#ifndef MOE_EPQ_F32
+#define MOE_EPQ_F32 1
+#endif
 template <int EPI> struct EpiCfg {
+  // thread = accumulator row; epilogue warp (quarter q, part j) owns chunks j, j + PER_Q, ... of the 8 x 32 columns
+  static constexpr int PER_Q = EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_EPQ_GELU
+                               : EPI == TEPI_BIAS ? MOE_EPQ_BIAS
+                               : EPI == TEPI_GELU_BWD ? MOE_EPQ_GBWD
+                               : EPI == TEPI_STORE ? MOE_EPQ_STORE : MOE_EPQ_F32;
+  static constexpr int WARPS = 4 * PER_Q;
+  static constexpr int THREADS = 64 + 32 * WARPS;
   static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
 #ifndef MOE_EPI_NBUF
 #define MOE_EPI_NBUF 2
@@ -73,7 +94,7 @@ template <int EPI> struct EpiCfg {
 #else
   static constexpr int WARP_STAGE = EPI == TEPI_F32 ? NBUF * 2 * CHUNK_BYTES : NBUF * NOUT * CHUNK_BYTES;
 #endif
-  static constexpr int STAGING = EPI_WARPS * WARP_STAGE;
+  static constexpr int STAGING = WARPS * WARP_STAGE;
   static constexpr int BAR_BYTES = 2048;
   static constexpr int STAGES = (SMEM_LIMIT - 1024 - BAR_BYTES - STAGING) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGING + 1024 + BAR_BYTES;
@@ -146,12 +167,13 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, const int* s_off,
 }
 
 template <int EPI, bool A_MN, bool B_MN, bool KGRP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO1, const __grid_constant__ CUtensorMap tmO2,
                    const __grid_constant__ CUtensorMap tmX, TcParams p) {
   using Cfg = EpiCfg<EPI>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int EPI_PER_Q = Cfg::PER_Q, EPI_WARPS = Cfg::WARPS, NUM_THREADS = Cfg::THREADS;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_u32 = tc::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (raw_u32 & 1023)) & 1023);   // 1024-aligned (SWIZZLE_128B atoms)
@@ -629,9 +651,9 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
       if (fp) { fwrite(sbuf, 8, 2 * 16 * (size_t)kTraceN, fp); fclose(fp); }
     });
   }
-  k<<<(unsigned)(2 * pairs), NUM_THREADS, smem, s>>>(a, b, o1, o2, x, pt), count_launch();
+  k<<<(unsigned)(2 * pairs), EpiCfg<EPI>::THREADS, smem, s>>>(a, b, o1, o2, x, pt), count_launch();
 #else
-  k<<<(unsigned)(2 * pairs), NUM_THREADS, smem, s>>>(a, b, o1, o2, x, p), count_launch();
+  k<<<(unsigned)(2 * pairs), EpiCfg<EPI>::THREADS, smem, s>>>(a, b, o1, o2, x, p), count_launch();
 #endif
   return cudaGetLastError();
 }
