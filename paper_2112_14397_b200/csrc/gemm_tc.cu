@@ -75,6 +75,20 @@ enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 
 #ifndef MOE_EPQ_F32
 #define MOE_EPQ_F32 1
 #endif
+// (GELU and fp32 weight-gradient epilogues: 1 buffer per warp -- the smaller staging area buys
+// operand stages, C4 GEMM1 -1.7%, weight gradients -2%; bias / store keep 2, profiles/r01/s2/epi_warps.txt)
+#ifndef MOE_NB_GELU
+#define MOE_NB_GELU 1
+#endif
+#ifndef MOE_NB_BIAS
+#define MOE_NB_BIAS 2
+#endif
+#ifndef MOE_NB_STORE
+#define MOE_NB_STORE 2
+#endif
+#ifndef MOE_NB_F32
+#define MOE_NB_F32 1
+#endif
 template <int EPI> struct EpiCfg {
   // thread = accumulator row; epilogue warp (quarter q, part j) owns chunks j, j + PER_Q, ... of the 8 x 32 columns
   static constexpr int PER_Q = EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_EPQ_GELU
@@ -84,10 +98,11 @@ template <int EPI> struct EpiCfg {
   static constexpr int WARPS = 4 * PER_Q;
   static constexpr int THREADS = 64 + 32 * WARPS;
   static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
-#ifndef MOE_EPI_NBUF
-#define MOE_EPI_NBUF 2
-#endif
-  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4 : MOE_EPI_NBUF;                 // staging buffers per warp
+  // staging buffers per warp (GELU' bwd: 4, its a-operand loads run two chunks ahead)
+  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4
+                              : EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_NB_GELU
+                              : EPI == TEPI_BIAS ? MOE_NB_BIAS
+                              : EPI == TEPI_STORE ? MOE_NB_STORE : MOE_NB_F32;
   // per-warp staging: NBUF chunk buffers of NOUT bf16 32x32 boxes, or of one fp32 32x32 box (F32)
 #ifdef MOE_EXP_F32_DIRECT
   static constexpr int WARP_STAGE = EPI == TEPI_F32 ? 0 : NBUF * NOUT * CHUNK_BYTES;
