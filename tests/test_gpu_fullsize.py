@@ -130,3 +130,41 @@ def test_c5_full_schedule(s):
 
 def test_c1_full_fp32():
     fullsize(configs.C1, n_random=200)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_graph_replay_matches_eager(name):
+    # bench.py times the step as ONE CUDA-graph replay with the row capacity fixed to the
+    # warm-up's (static capacity, no host sync).  That replay must give bit-identical outputs
+    # and gradients to the eager path the checks above use, on every replay.
+    from _parity import f32
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = getattr(configs, name)
+    li = inputs.make_inputs(cfg)
+    dev = torch.device("cuda", 0)
+    tau, c = f32(cfg.tau), f32(cfg.threshold)
+    layer = DTSMoELayer(li.x.shape[0], cfg.d_model, cfg.d_ff, cfg.E, dtype=li.x.dtype, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
+    y0 = layer.forward(x, u, tau, c).clone()
+    g0 = {k: v.clone() for k, v in layer.backward(dy).items()}
+    torch.cuda.synchronize()
+    layer.check()
+    R_static = layer.state.R_cap
+    layer.forward(x, u, tau, c, R_cap=R_static)       # as bench.py: one eager step at the static capacity
+    layer.backward(dy)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        y1 = layer.forward(x, u, tau, c, R_cap=R_static)
+        g1 = layer.backward(dy)
+    for _ in range(2):
+        graph.replay()
+        torch.cuda.synchronize()
+        layer.check()
+        assert torch.equal(y1, y0)
+        for k in g0:
+            if k == "da":
+                continue
+            assert torch.equal(g1[k], g0[k]), k
