@@ -1,11 +1,10 @@
-// gemm_gate_tc.cu -- tcgen05 kernels for the three skinny gate contractions (bf16 path):
+// gemm_gate_tc.cu -- tcgen05 kernels for the skinny gate contractions (bf16 path):
 //
 //   GATE  L = x W_g                [T, E]   M = 128 tokens / CTA, N = Ep (E padded to 16), K = d
 //         (E % 16 != 0: logits to HBM, steps 2-3 in gate_softmax_tpt_kernel + gate_refine_kernel;
 //          E % 16 == 0 uses the persistent fused kernel below, steps 1-3 in one launch)
-//   DXG   dx = dL W_g^T + sum_e dx_perm[slot]   M = 128 tokens, N = 256 of d, K = Kp
-//         (replaces moe_dispatch_bwd's gather pass: the un-permute sum runs in the epilogue)
 //   DWG   dW_g = x^T dL                [d, E]   M = 128 of d, N = Kp, K = T split over CTAs
+//   (the third, dL W_g^T [T, d], runs on the expert GEMM's dense STORE path: gate_tc_dx)
 //
 // One tile per CTA (no persistence), cta_group::1 tcgen05.mma (M = 128), TMA-fed 4-stage
 // ring, single elected MMA thread, 4 epilogue warps reading TMEM with tcgen05.ld.
@@ -29,11 +28,11 @@ namespace moe {
 namespace tcgate {
 
 constexpr int BM = 128, BK = 64;
-// GATE: 2 stages (2 CTAs / SM; the idle ring then holds the noise block); DXG: K = Kp <= 256
+// GATE: 2 stages (2 CTAs / SM; the idle ring then holds the noise block)
 template <int MODE> struct Stages { static constexpr int N = MODE == 2 ? 4 : 2; };
-template <int MODE> struct Threads { static constexpr int N = MODE == 1 ? 64 + 256 : 64 + 128; };
-// warp 0 TMA, warp 1 MMA + TMEM alloc, then 4 (GATE, DWG) or 8 (DXG) epilogue warps
-enum Mode { GATE = 0, DXG = 1, DWG = 2 };
+template <int MODE> struct Threads { static constexpr int N = 64 + 128; };
+// warp 0 TMA, warp 1 MMA + TMEM alloc, then 4 epilogue warps
+enum Mode { GATE = 0, DWG = 2 };
 
 struct Params {
   int mode;
@@ -57,10 +56,6 @@ struct Params {
   int* rq_count;       // deferred (near-boundary) tokens -> gate_refine_kernel
   int* rq_list;
   float* logits;       // GATE output [T, E] fp32
-  // DXG
-  const bf16* dx_perm;
-  const int* slot_in;
-  bf16* dx;
   // DWG
   float* part;         // [splits, d, E]
 };
@@ -78,7 +73,7 @@ __global__ void __launch_bounds__(Threads<MODE>::N) gate_tc_kernel(const __grid_
   uint8_t* smem = smem_raw + ((1024 - (raw_u32 & 1023)) & 1023);
   // operand bytes per stage
   const int a_bytes = BM * BK * 2;
-  const int bn = MODE == GATE ? p.Ep : (MODE == DXG ? 256 : p.Kp);
+  const int bn = MODE == GATE ? p.Ep : p.Kp;
   const int b_bytes = bn * BK * 2;
   const int stage_bytes = a_bytes + ((b_bytes + 1023) & ~1023);
   uint8_t* tail = smem + STAGES * stage_bytes;
@@ -86,17 +81,15 @@ __global__ void __launch_bounds__(Threads<MODE>::N) gate_tc_kernel(const __grid_
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* done_bar = empty_bar + STAGES;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(done_bar + 1);
-  int* s_cnt = reinterpret_cast<int*>(s_tmem + 4);    // [128] expert counts (GATE) / row counts (DXG)
+  int* s_cnt = reinterpret_cast<int*>(s_tmem + 4);    // [128] expert counts (GATE)
   int* s_band = s_cnt + 128;
-  float* s_misc = reinterpret_cast<float*>(s_band + 4);   // GATE logits [128][E+1] / DXG row lists [128][E] ints
+  float* s_misc = reinterpret_cast<float*>(s_band + 4);   // GATE logits [128][E+1]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // tile coordinates
   int m0 = 0, n0 = 0, kb0 = 0, nkb = 0;
   if (MODE == GATE) {
     m0 = blockIdx.x * BM; nkb = (p.d + BK - 1) / BK;
-  } else if (MODE == DXG) {
-    m0 = blockIdx.x * BM; n0 = blockIdx.y * 256; nkb = p.Kp / BK;
   } else {
     m0 = blockIdx.x * BM;                     // rows of dW_g (d index)
     kb0 = blockIdx.y * (p.split_rows / BK);
@@ -221,53 +214,6 @@ __global__ void __launch_bounds__(Threads<MODE>::N) gate_tc_kernel(const __grid_
       const int et = threadIdx.x - 64;
       const int ntok = min(128, p.T - m0);
       for (int i = et; i < ntok * p.E; i += 128) p.logits[(long long)m0 * p.E + i] = ls[(i / p.E) * LP + (i % p.E)];
-    } else if (MODE == DXG) {
-      // ---- dx[t] = (dL W_g^T)[t] + sum_{e asc} dx_perm[slot[t, e]]   (8 warps: 2 per lane quarter)
-      const int et = threadIdx.x - 64;                 // 0..255
-      const int half = (warp - 2) >> 2;                // column half of the 256-wide tile
-      int* sblk = reinterpret_cast<int*>(s_misc);      // [128][E] slot block (coalesced load)
-      int* lst = sblk;                                 // compacted in place, row by row
-      int* nrow = s_cnt;                               // [128] selected rows per token
-      const int ntok = max(0, min(128, p.T - m0));
-      for (int i = et; i < ntok * p.E; i += 256) sblk[i] = p.slot_in[(long long)m0 * p.E + i];
-      named_bar_sync(1, 256);
-      if (half == 0 && row < ntok) {                   // compact (ascending e) in place
-        int n = 0;
-        for (int e = 0; e < p.E; ++e) {
-          const int r = sblk[row * p.E + e];
-          if (r >= 0) lst[row * p.E + n++] = r;
-        }
-        nrow[row] = n;
-      }
-      named_bar_sync(1, 256);
-      const int t = m0 + row;
-      const int n = row < ntok ? nrow[row] : 0;
-      for (int c = half * 128; c < half * 128 + 128; c += 32) {
-        const int col = n0 + c;
-        uint32_t r[32];
-        tc::tmem_ld32(t_row + c, r);
-        tc::tmem_ld_wait();
-        if (row >= ntok || col >= p.d) continue;
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        for (int k = 0; k < n; ++k) {
-          const bf16* src = p.dx_perm + (long long)lst[row * p.E + k] * p.d + col;
-          uint4 q[4];
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) q[qq] = ld_nc_v4(src + qq * 8);
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            float f[8];
-            unpack16(q[qq], f, bf16());
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[qq * 8 + j] += f[j];
-          }
-        }
-        bf16* dst = p.dx + (long long)t * p.d + col;
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) st_v4(dst + qq * 8, pack16(v + qq * 8, bf16()));
-      }
     } else {
       // ---- dW_g partial [split][d][E] = acc[:, e] (hi part) + acc[:, Ep + e] (lo part)
       const int m = m0 + row;
@@ -624,7 +570,7 @@ __global__ void wg_transpose_kernel(const bf16* __restrict__ Wg, int d, int E, i
   const int e = (int)(i / d), k = (int)(i % d);
   WgT[i] = e < E ? Wg[(long long)k * E + e] : __float2bfloat16_rn(0.f);
 }
-// Wg2 [d, Kp] = [W_g | W_g | 0]  (B operand of DXG with the hi | lo split of dL)
+// Wg2 [d, Kp] = [W_g | W_g | 0]  (B operand of the dense dL W_g^T GEMM with the hi | lo split of dL)
 __global__ void wg_double_kernel(const bf16* __restrict__ Wg, int d, int E, int Ep, int Kp, bf16* __restrict__ Wg2) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)d * Kp) return;
