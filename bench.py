@@ -100,11 +100,19 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed plumbing
-def dist_setup(n_gpus: int):
+def dist_setup(n_gpus: int, force_pg: bool = False):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if force_pg and world == 1 and "MASTER_ADDR" not in os.environ:
+        # single process without torchrun: a 1-rank group (the peer-memory path's symmetric
+        # allocations rendezvous through it)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    if world > 1 or force_pg:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -114,7 +122,8 @@ def dist_setup(n_gpus: int):
 
 
 def barrier(world):
-    if world > 1:
+    import torch.distributed as dist
+    if world > 1 or (dist.is_available() and dist.is_initialized()):
         import torch.distributed as dist
         dist.barrier()
 
@@ -349,6 +358,134 @@ def _traffic(name, world):
             "traffic_source": os.path.relpath(hits[-1], ROOT)}
 
 
+def run_ours_p2p(args, rank, world):
+    """The fused peer-memory EP path (paper_2112_14397_b200.ep2, moe_ep2_*): token rows are
+    stored straight into the owners' expert-side layouts and gathered back over NVLink peer
+    pointers inside the routing kernels (torch symmetric memory), no NCCL all-to-all.  Eager
+    phases with stream-ordered NCCL barriers between them; the step and its expert-GEMM part
+    are timed with CUDA events, max over ranks."""
+    import torch.distributed as dist
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
+    from paper_2112_14397_b200.layer import make_nccl_comm
+
+    cfg = configs.get(args.config)
+    if cfg.dtype != "bf16":
+        raise SystemExit("--ep p2p: bf16 configs only")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    li = inputs.make_inputs(cfg, rank=rank)
+    tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
+    comm = make_nccl_comm(rank, world)
+    syms = SymmetricBuffers(world, dev, mode="symm_mem", group=dist.group.WORLD)
+    r = EP2Rank(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, torch.bfloat16, dev, rank, world, syms, comm=comm)
+    r.set_gate(li.Wg.to(dev))
+    r.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step():
+        r.forward(x, u, tau, c)
+        return r.backward(dy)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    r.check()
+    # rows of my experts (all ranks' tokens), for the GEMM FLOPs
+    ca = r._sym("counts_all", (world, cfg.E), torch.int32)[0].cpu().numpy()
+    R_mine = int(ca[:, rank * r.El:(rank + 1) * r.El].sum())
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    n_launch0 = L.moe_kernel_launch_count()
+    step_ms, gemm_ms = [], []
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        r.events = {"experts_fwd": (ev(), ev()), "experts_bwd": (ev(), ev())}
+        s0, s1 = ev(), ev()
+        s0.record(stream)
+        step()
+        s1.record(stream)
+        s1.synchronize()
+        step_ms.append(s0.elapsed_time(s1))
+        gemm_ms.append(sum(a.elapsed_time(b) for a, b in r.events.values()))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    launches = (L.moe_kernel_launch_count() - n_launch0) // max(1, args.steps)
+    r.events = None
+    barrier(world)
+    clk = clocks.stop()
+    r.check()
+    ms_step = max_over_ranks(sum(step_ms) / len(step_ms), world)
+    g_ms = max_over_ranks(sum(gemm_ms) / len(gemm_ms), world)
+    flops = 12.0 * R_mine * cfg.d_model * cfg.d_ff
+    t = torch.tensor([flops], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t)
+    flops_per_gpu = float(t.item()) / world
+    peaks, peak_src = _peaks()
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    achieved = flops_per_gpu / (g_ms / 1e3) / 1e12
+
+    e2e = None
+    if args.e2e:
+        hx, hu, hdy = (tt.pin_memory() for tt in (li.x, li.u, li.dy))
+        hy, hdx = torch.empty_like(li.x).pin_memory(), torch.empty_like(li.x).pin_memory()
+
+        def step_host():
+            x.copy_(hx, non_blocking=True)
+            u.copy_(hu, non_blocking=True)
+            dy.copy_(hdy, non_blocking=True)
+            y = r.forward(x, u, tau, c)
+            g = r.backward(dy)
+            hy.copy_(y, non_blocking=True)
+            hdx.copy_(g["dx"], non_blocking=True)
+
+        step_host()
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_host()
+        e1.record(stream)
+        e1.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        bi = sum(tt.numel() * tt.element_size() for tt in (hx, hu, hdy))
+        bo = 2 * hy.numel() * hy.element_size()
+        e2e = {"value": cfg.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": False}
+        r.check()
+
+    out = {
+        "metric": METRIC, "value": cfg.T * world / (ms_step / 1e3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) tokens, N(0,1/d) gate, N(0,0.02) shared expert, Bernoulli(0.8) masks)",
+        "config": {"workload": f"{cfg.name}: T={cfg.T}/GPU d_model={cfg.d_model} d_ff={cfg.d_ff} E={cfg.E} "
+                               f"tau={cfg.tau} c={cfg.threshold}",
+                   "tokens_per_gpu": cfg.T, "global_tokens": cfg.T * world, "rows_R_rank0": R_mine,
+                   "parallelism": f"ep{world} (E/{world} experts per GPU, fused NVLink peer-memory dispatch / "
+                                  f"combine, moe_ep2_*)",
+                   "l2": "flushed between steps (256 MiB write, outside the events)", "launch": "eager phases",
+                   "wall_s_timed_region": wall},
+        "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained", "gemm_ms_per_step": g_ms,
+                     "flops_per_step_per_gpu": flops_per_gpu, "traffic": None},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if e2e:
+        out["e2e"] = e2e
+    return out
+
+
 def run_e2e(args, layer, li, tau, c, world, graphed=None):
     """Same metric through the public API with host (pinned) buffers: every step copies x, u,
     dy host->device and reads y and dx back device->host.
@@ -484,6 +621,9 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--ep", default="nccl", choices=["nccl", "p2p"],
+                    help="expert-parallel exchange: NCCL grouped send/recv (default) or the fused "
+                         "NVLink peer-memory path (moe_ep2_*, torch symmetric memory)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -494,11 +634,12 @@ def main():
         if out is not None:
             print(json.dumps(out))
         return 0
-    rank, world, local = dist_setup(args.gpus)
-    out = run_ours(args, rank, world)
+    rank, world, local = dist_setup(args.gpus, force_pg=args.ep == "p2p")
+    out = run_ours_p2p(args, rank, world) if args.ep == "p2p" else run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(out))
-    if world > 1:
+    import torch.distributed as dist
+    if dist.is_initialized():
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0

@@ -68,6 +68,13 @@ class EP2Rank:
         self.R_cap = (world * T * self.El + 127 * self.El + 127) // 128 * 128
         self.Wg = self.W1 = self.b1 = self.W2 = self.b2 = None
         self.st: Dict[str, torch.Tensor] = {}
+        # optional {"experts_fwd": (ev0, ev1), "experts_bwd": (ev0, ev1)}: CUDA events recorded
+        # around the expert FFN calls on the current stream (bench.py's GEMM time)
+        self.events: Optional[Dict[str, tuple]] = None
+
+    def _mark(self, name: str, i: int):
+        if self.events and name in self.events:
+            self.events[name][i].record(torch.cuda.current_stream())
 
     def __del__(self):
         try:
@@ -128,8 +135,10 @@ class EP2Rank:
         R, d, f, s = self.R_cap, self.d, self.f, self.st
         s["gp"] = torch.empty(R, f, dtype=self.dtype, device=self.device)
         s["h"] = torch.empty(R, f, dtype=self.dtype, device=self.device)
-        L.moe_expert_ffn(self.ctx, self._sym("x_recv", (R, d), self.dtype)[0], s["off"], R, self.W1, self.b1, self.W2,
-                         self.b2, s["gp"], s["h"], self._sym("e_out", (R, d), self.dtype)[0])
+        xr, eo = self._sym("x_recv", (R, d), self.dtype)[0], self._sym("e_out", (R, d), self.dtype)[0]
+        self._mark("experts_fwd", 0)
+        L.moe_expert_ffn(self.ctx, xr, s["off"], R, self.W1, self.b1, self.W2, self.b2, s["gp"], s["h"], eo)
+        self._mark("experts_fwd", 1)
 
     def fwd_combine(self):
         R, d, s = self.R_cap, self.d, self.st
@@ -158,8 +167,11 @@ class EP2Rank:
                  dW2=torch.empty(El, d, f, dtype=torch.float32, device=dev),
                  db2=torch.empty(El, d, dtype=torch.float32, device=dev))
         dxp, _ = self._sym("dx_perm", (R, d), self.dtype)
-        L.moe_expert_ffn_bwd(self.ctx, s["d_eout"], self._sym("x_recv", (R, d), self.dtype)[0], s["gp"], s["h"],
-                             s["off"], R, self.W1, self.W2, s["gp"], dxp, g["dW1"], g["db1"], g["dW2"], g["db2"])
+        xr = self._sym("x_recv", (R, d), self.dtype)[0]
+        self._mark("experts_bwd", 0)
+        L.moe_expert_ffn_bwd(self.ctx, s["d_eout"], xr, s["gp"], s["h"], s["off"], R, self.W1, self.W2, s["gp"], dxp,
+                             g["dW1"], g["db1"], g["dW2"], g["db2"])
+        self._mark("experts_bwd", 1)
         s["grads"] = g
 
     def bwd_gate(self, balance_alpha: float = 0.0, B_total: Optional[int] = None):
