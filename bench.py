@@ -377,7 +377,8 @@ def run_ours_p2p(args, rank, world):
     tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
     comm = make_nccl_comm(rank, world)
     syms = SymmetricBuffers(world, dev, mode="symm_mem", group=dist.group.WORLD)
-    r = EP2Rank(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, torch.bfloat16, dev, rank, world, syms, comm=comm)
+    r = EP2Rank(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, torch.bfloat16, dev, rank, world, syms, comm=comm,
+                dedup=args.ep == "p2p-dedup")
     r.set_gate(li.Wg.to(dev))
     r.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
     x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
@@ -471,7 +472,8 @@ def run_ours_p2p(args, rank, world):
                                f"tau={cfg.tau} c={cfg.threshold}",
                    "tokens_per_gpu": cfg.T, "global_tokens": cfg.T * world, "rows_R_rank0": R_mine,
                    "parallelism": f"ep{world} (E/{world} experts per GPU, fused NVLink peer-memory dispatch / "
-                                  f"combine, moe_ep2_*)",
+                                  f"combine, " + ("one row per (token, owner), moe_ep2d_*)" if r.dedup
+                                                  else "moe_ep2_*)"),
                    "l2": "flushed between steps (256 MiB write, outside the events)", "launch": "eager phases",
                    "wall_s_timed_region": wall},
         "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
@@ -621,9 +623,10 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--ep", default="nccl", choices=["nccl", "p2p"],
-                    help="expert-parallel exchange: NCCL grouped send/recv (default) or the fused "
-                         "NVLink peer-memory path (moe_ep2_*, torch symmetric memory)")
+    ap.add_argument("--ep", default="nccl", choices=["nccl", "p2p", "p2p-dedup"],
+                    help="expert-parallel exchange: NCCL grouped send/recv (default), the fused NVLink "
+                         "peer-memory path (moe_ep2_*, torch symmetric memory), or the same with one row "
+                         "per (token, owner) each way (moe_ep2d_*)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -634,8 +637,9 @@ def main():
         if out is not None:
             print(json.dumps(out))
         return 0
-    rank, world, local = dist_setup(args.gpus, force_pg=args.ep == "p2p")
-    out = run_ours_p2p(args, rank, world) if args.ep == "p2p" else run_ours(args, rank, world)
+    p2p = args.ep.startswith("p2p")
+    rank, world, local = dist_setup(args.gpus, force_pg=p2p)
+    out = run_ours_p2p(args, rank, world) if p2p else run_ours(args, rank, world)
     if rank == 0:
         print(json.dumps(out))
     import torch.distributed as dist

@@ -304,6 +304,45 @@ int moe_ep2_gate_bwd(moe_ctx* ctx, float* const* dG_peers, const int32_t* slot, 
 int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t* slot, const float* dlogits,
                          const void* Wg, void* dx, void* stream);
 
+/* ---------------------------------------------------------------- ep2 with token dedup ("ep2d")
+ * SURVEY §8(e) "Dedup": a token is sent ONCE to every GPU owning any of its selected
+ * experts, and each owner pre-sums its local experts' contributions before the return trip,
+ * so the NVLink bytes per (token, owner) are one row each way instead of one per selected
+ * expert (up to E_local x fewer).  Unique slot of token t of source rank s on every owner:
+ * u = s * T + t.  Extra symmetric buffers per rank (U = world * T):
+ *   tokbuf [U, d] (D), urows [U, E_local] int32 (expert-side row of (u, local expert j) or
+ *   -1; rewritten whole every step by the token side), ruid [R_recv_cap] int32 (row -> u),
+ *   ysum / dyu / dxu [U, d] (D); token side: uslot [T, world] int32 (u on owner q or -1).
+ * Forward: gate -> ep2_counts -> barrier -> ep2_plan -> ep2_prepare_recv -> moe_ep2d_dispatch
+ *   (rows, row metadata and ruid / urows at the owners, x stored once per owner into tokbuf)
+ *   -> barrier -> moe_ep2d_permute (expert side, local: x_recv[r] = tokbuf[ruid[r]]) ->
+ *   moe_expert_ffn -> moe_ep2d_presum(e_out, rgate) -> ysum (ysum[u] = sum_{j asc} G e_out,
+ *   rounded to D) -> barrier -> moe_ep2d_combine (token side: y = sum_{q asc} ysum@q[uslot]).
+ * Backward: dy staged in a symmetric buffer -> barrier -> moe_ep2d_gather_dy (expert side:
+ *   dyu[u] = dy@s[t], one read per (token, owner)) -> moe_ep2d_combine_bwd (d_eout, dG, db2
+ *   partials from dyu) -> moe_expert_ffn_bwd -> moe_ep2d_presum(dx_perm, NULL) -> dxu ->
+ *   barrier -> moe_ep2_gate_bwd -> moe_ep_allreduce(dWg) -> moe_ep2d_dispatch_bwd (token side:
+ *   dx = dL W_g^T + sum_{q asc} dxu@q[uslot]).
+ * Routing, d_eout, dG, dlogits and the expert weight gradients equal the non-dedup path's bit
+ * for bit; y and dx differ by the rounding of the per-owner partial sums to D (one extra
+ * rounding per owner, ~2^-9 relative for bf16). */
+int moe_ep2d_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, int32_t* uslot,
+                      void* const* tokbuf_peers, int32_t* const* urows_peers, int32_t* const* rtok_peers,
+                      int32_t* const* rsrc_peers, float* const* rgate_peers, int32_t* const* ruid_peers,
+                      int64_t R_recv_cap, void* stream);
+int moe_ep2d_permute(moe_ctx* ctx, const void* tokbuf, const int32_t* rtok, const int32_t* ruid, int64_t R_recv_cap,
+                     void* x_recv, void* stream);
+/* out[u] = sum_{j asc, urows[u][j] >= 0} (rgate[row] *) rows[row]; rgate NULL = unweighted.
+ * Unique slots with no row are left untouched. */
+int moe_ep2d_presum(moe_ctx* ctx, const void* rows, const float* rgate_or_null, const int32_t* urows, void* out,
+                    void* stream);
+int moe_ep2d_gather_dy(moe_ctx* ctx, void* const* dy_peers, const int32_t* urows, void* dyu, void* stream);
+int moe_ep2d_combine(moe_ctx* ctx, void* const* ysum_peers, const int32_t* uslot, void* y, void* stream);
+int moe_ep2d_combine_bwd(moe_ctx* ctx, const void* dyu, const void* e_out, const float* rgate, const int32_t* ruid,
+                         const int32_t* offsets_recv, int64_t R_recv_cap, void* d_eout, float* dG_row, void* stream);
+int moe_ep2d_dispatch_bwd(moe_ctx* ctx, void* const* dxu_peers, const int32_t* uslot, const float* dlogits,
+                          const void* Wg, void* dx, void* stream);
+
 /* ---------------------------------------------------------------- NEXT #1 */
 
 /* Balance loss, Eq. 10: loss = alpha N sum_i (counts_i / B^2) sum_s p[s,i]

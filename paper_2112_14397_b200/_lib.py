@@ -65,6 +65,13 @@ SIGNATURES = {
     "moe_ep2_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
     "moe_ep2_gate_bwd": (_I, [_P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P]),
     "moe_ep2_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "moe_ep2d_dispatch": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _P]),
+    "moe_ep2d_permute": (_I, [_P, _P, _P, _P, _L, _P, _P]),
+    "moe_ep2d_presum": (_I, [_P, _P, _P, _P, _P, _P]),
+    "moe_ep2d_gather_dy": (_I, [_P, _P, _P, _P, _P]),
+    "moe_ep2d_combine": (_I, [_P, _P, _P, _P, _P]),
+    "moe_ep2d_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
+    "moe_ep2d_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
 }
 MOE_COMM_EMULATED = 1   # moe_create(nccl_comm=MOE_COMM_EMULATED): single-process emulation of `world` ranks
 
@@ -379,3 +386,40 @@ def moe_ep2_gate_bwd(ctx, dG_peers, slot, probs, x, tau: float, balance_alpha: f
 def moe_ep2_dispatch_bwd(ctx, dx_perm_peers, slot, dlogits, Wg, dx, stream=None):
     a, ka = _peers(dx_perm_peers)
     _call("moe_ep2_dispatch_bwd", ctx, a, _ptr(slot), _ptr(dlogits), _ptr(Wg), _ptr(dx), _stream(stream))
+
+
+# ---- ep2 with token dedup (include/moe_dts.h "ep2d")
+def moe_ep2d_dispatch(ctx, x, probs, slot, uslot, tokbuf_peers, urows_peers, rtok_peers, rsrc_peers, rgate_peers,
+                      ruid_peers, R_recv_cap: int, stream=None):
+    ps = [_peers(t) for t in (tokbuf_peers, urows_peers, rtok_peers, rsrc_peers, rgate_peers, ruid_peers)]
+    _call("moe_ep2d_dispatch", ctx, _ptr(x), _ptr(probs), _ptr(slot), _ptr(uslot), *[p for p, _ in ps],
+          int(R_recv_cap), _stream(stream))
+
+
+def moe_ep2d_permute(ctx, tokbuf, rtok, ruid, R_recv_cap: int, x_recv, stream=None):
+    _call("moe_ep2d_permute", ctx, _ptr(tokbuf), _ptr(rtok), _ptr(ruid), int(R_recv_cap), _ptr(x_recv),
+          _stream(stream))
+
+
+def moe_ep2d_presum(ctx, rows, rgate, urows, out, stream=None):
+    _call("moe_ep2d_presum", ctx, _ptr(rows), _ptr(rgate), _ptr(urows), _ptr(out), _stream(stream))
+
+
+def moe_ep2d_gather_dy(ctx, dy_peers, urows, dyu, stream=None):
+    a, ka = _peers(dy_peers)
+    _call("moe_ep2d_gather_dy", ctx, a, _ptr(urows), _ptr(dyu), _stream(stream))
+
+
+def moe_ep2d_combine(ctx, ysum_peers, uslot, y, stream=None):
+    a, ka = _peers(ysum_peers)
+    _call("moe_ep2d_combine", ctx, a, _ptr(uslot), _ptr(y), _stream(stream))
+
+
+def moe_ep2d_combine_bwd(ctx, dyu, e_out, rgate, ruid, offsets_recv, R_recv_cap: int, d_eout, dG_row, stream=None):
+    _call("moe_ep2d_combine_bwd", ctx, _ptr(dyu), _ptr(e_out), _ptr(rgate), _ptr(ruid), _ptr(offsets_recv),
+          int(R_recv_cap), _ptr(d_eout), _ptr(dG_row), _stream(stream))
+
+
+def moe_ep2d_dispatch_bwd(ctx, dxu_peers, uslot, dlogits, Wg, dx, stream=None):
+    a, ka = _peers(dxu_peers)
+    _call("moe_ep2d_dispatch_bwd", ctx, a, _ptr(uslot), _ptr(dlogits), _ptr(Wg), _ptr(dx), _stream(stream))

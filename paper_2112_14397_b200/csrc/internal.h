@@ -128,7 +128,22 @@ cudaError_t launch_ep2_combine_bwd(moe_ctx* c, const PeerTable& dyp, const void*
                                    const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets, int64_t R_cap,
                                    void* d_eout, float* dG_row, cudaStream_t s);
 cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, const float* dlogits,
-                                    const void* Wg, void* dx, cudaStream_t s);
+                                    const void* Wg, void* dx, cudaStream_t s, int slot_cols = 0, int cols_per_rank = 0);
+// ep2 with token dedup (one row per (token, owner) each way)
+cudaError_t launch_ep2d_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot, int32_t* uslot,
+                                 const PeerTable& tb, const PeerTable& urows, const PeerTable& rtok,
+                                 const PeerTable& rsrc, const PeerTable& rgate, const PeerTable& ruid, int64_t R_cap,
+                                 cudaStream_t s);
+cudaError_t launch_ep2d_permute(const moe_ctx* c, const void* tokbuf, const int32_t* rtok, const int32_t* ruid,
+                                int64_t R_cap, void* x_recv, cudaStream_t s);
+cudaError_t launch_ep2d_presum(const moe_ctx* c, const void* rows, const float* gate, const int32_t* urows, void* out,
+                               cudaStream_t s);
+cudaError_t launch_ep2d_gather_dy(const moe_ctx* c, const PeerTable& dyp, const int32_t* urows, void* dyu,
+                                  cudaStream_t s);
+cudaError_t launch_ep2d_combine(const moe_ctx* c, const PeerTable& ys, const int32_t* uslot, void* y, cudaStream_t s);
+cudaError_t launch_ep2d_combine_bwd(moe_ctx* c, const void* dyu, const void* e_out, const float* rgate,
+                                    const int32_t* ruid, const int32_t* offsets, int64_t R_cap, void* d_eout,
+                                    float* dG_row, cudaStream_t s);
 cudaError_t launch_gate_bwd_peer(const moe_ctx* c, const PeerTable& dGp, const int32_t* slot, const float* probs,
                                  const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
                                  float* dWg, float* dlogits, cudaStream_t s);

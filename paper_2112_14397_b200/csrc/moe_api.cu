@@ -777,4 +777,86 @@ int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t
   return cuda_status(moe::launch_ep2_dispatch_bwd(ctx, t, slot, dlogits, Wg, dx, S(stream)), "moe_ep2_dispatch_bwd");
 }
 
+// ---------------------------------------------------------------- ep2 with token dedup
+int moe_ep2d_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, int32_t* uslot,
+                      void* const* tokbuf_peers, int32_t* const* urows_peers, int32_t* const* rtok_peers,
+                      int32_t* const* rsrc_peers, float* const* rgate_peers, int32_t* const* ruid_peers,
+                      int64_t R_recv_cap, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2d_dispatch");
+  if (rc) return rc;
+  REQUIRE_T(x); REQUIRE_T(probs); REQUIRE_T(slot); REQUIRE_T(uslot);
+  if ((long long)ctx->world * ctx->T > 0x7fffffffLL) return fail(MOE_ESHAPE, "moe_ep2d_dispatch: world*T exceeds int32");
+  moe::PeerTable tb, ur, rt, rs, rg, ru;
+  const char* fn = "moe_ep2d_dispatch";
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(tokbuf_peers), tb, fn)) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(urows_peers), ur, fn)) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rtok_peers), rt, fn)) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rsrc_peers), rs, fn)) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rgate_peers), rg, fn)) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(ruid_peers), ru, fn)))
+    return rc;
+  return cuda_status(moe::launch_ep2d_dispatch(ctx, x, probs, slot, uslot, tb, ur, rt, rs, rg, ru, R_recv_cap,
+                                               S(stream)), fn);
+}
+
+int moe_ep2d_permute(moe_ctx* ctx, const void* tokbuf, const int32_t* rtok, const int32_t* ruid, int64_t R_recv_cap,
+                     void* x_recv, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2d_permute");
+  if (rc) return rc;
+  REQUIRE(tokbuf); REQUIRE(rtok); REQUIRE(ruid); REQUIRE(x_recv);
+  if (R_recv_cap < 0) return fail(MOE_EINVAL, "moe_ep2d_permute: bad R_recv_cap");
+  return cuda_status(moe::launch_ep2d_permute(ctx, tokbuf, rtok, ruid, R_recv_cap, x_recv, S(stream)),
+                     "moe_ep2d_permute");
+}
+
+int moe_ep2d_presum(moe_ctx* ctx, const void* rows, const float* rgate_or_null, const int32_t* urows, void* out,
+                    void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2d_presum");
+  if (rc) return rc;
+  REQUIRE(rows); REQUIRE(urows); REQUIRE(out);
+  return cuda_status(moe::launch_ep2d_presum(ctx, rows, rgate_or_null, urows, out, S(stream)), "moe_ep2d_presum");
+}
+
+int moe_ep2d_gather_dy(moe_ctx* ctx, void* const* dy_peers, const int32_t* urows, void* dyu, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2d_gather_dy");
+  if (rc) return rc;
+  REQUIRE(urows); REQUIRE(dyu);
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dy_peers), t, "moe_ep2d_gather_dy"))) return rc;
+  return cuda_status(moe::launch_ep2d_gather_dy(ctx, t, urows, dyu, S(stream)), "moe_ep2d_gather_dy");
+}
+
+int moe_ep2d_combine(moe_ctx* ctx, void* const* ysum_peers, const int32_t* uslot, void* y, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2d_combine");
+  if (rc) return rc;
+  REQUIRE_T(uslot); REQUIRE_T(y);
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(ysum_peers), t, "moe_ep2d_combine"))) return rc;
+  return cuda_status(moe::launch_ep2d_combine(ctx, t, uslot, y, S(stream)), "moe_ep2d_combine");
+}
+
+int moe_ep2d_combine_bwd(moe_ctx* ctx, const void* dyu, const void* e_out, const float* rgate, const int32_t* ruid,
+                         const int32_t* offsets_recv, int64_t R_recv_cap, void* d_eout, float* dG_row, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2d_combine_bwd");
+  if (rc) return rc;
+  REQUIRE(dyu); REQUIRE(e_out); REQUIRE(rgate); REQUIRE(ruid); REQUIRE(offsets_recv); REQUIRE(d_eout); REQUIRE(dG_row);
+  if (!moe::ep2_width_ok(ctx))
+    return fail(MOE_ESHAPE, "moe_ep2d_combine_bwd: d_model=%d too wide (max 1024 bf16 / 512 f32)", ctx->d);
+  return cuda_status(moe::launch_ep2d_combine_bwd(ctx, dyu, e_out, rgate, ruid, offsets_recv, R_recv_cap, d_eout,
+                                                  dG_row, S(stream)),
+                     "moe_ep2d_combine_bwd");
+}
+
+int moe_ep2d_dispatch_bwd(moe_ctx* ctx, void* const* dxu_peers, const int32_t* uslot, const float* dlogits,
+                          const void* Wg, void* dx, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2d_dispatch_bwd");
+  if (rc) return rc;
+  REQUIRE_T(uslot); REQUIRE_T(dx);
+  if (dlogits && !Wg) return fail(MOE_EINVAL, "moe_ep2d_dispatch_bwd: dlogits given without Wg");
+  moe::PeerTable t;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dxu_peers), t, "moe_ep2d_dispatch_bwd"))) return rc;
+  return cuda_status(moe::launch_ep2_dispatch_bwd(ctx, t, uslot, dlogits, Wg, dx, S(stream), ctx->world, 1),
+                     "moe_ep2d_dispatch_bwd");
+}
+
 }  // extern "C"

@@ -789,6 +789,177 @@ __global__ void __launch_bounds__(256, 4) ep2_dispatch_bwd_kernel(const __grid_c
                                                    dxg ? dxg + (long long)t * d : nullptr, dx + (long long)t * d, lane);
 }
 
+// ------------------------------------------------------------------ ep2 with token dedup ("ep2d")
+// a token is sent ONCE to each GPU that owns any of its selected experts, and
+// the owner pre-sums its local experts' contributions before the return trip.  Unique slot
+// of token t of source rank s on every owner: u = s * T + t (fixed stride, no counts
+// exchange).  Per owner: tokbuf [W*T, d] (x rows), urows [W*T, El] (the expert-side row of
+// (u, local expert j), -1 if not selected: the token side writes the whole El-row for every
+// owner each step), ruid [R_cap] (row -> u).  Token side: uslot [T, W] = u on owner q, or -1.
+
+// token side rank pass: ep2_rank_kernel's rows and row metadata, plus ruid at the owner,
+// the token's urows rows on every owner and its uslot row
+__global__ void __launch_bounds__(kGateBT) ep2d_rank_kernel(
+    const float* __restrict__ probs, int* __restrict__ slot, int T_, int E, int El, int me, int W,
+    const int* __restrict__ blk_base, const int* __restrict__ base, long long R_cap,
+    const __grid_constant__ PeerTable rtok, const __grid_constant__ PeerTable rsrc,
+    const __grid_constant__ PeerTable rgate, const __grid_constant__ PeerTable ruid,
+    const __grid_constant__ PeerTable urows, int* __restrict__ uslot) {
+  __shared__ unsigned s_bal[kGateBT / 32][128];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int t = blockIdx.x * kGateBT + tid;
+  const bool valid = t < T_;
+  for (int e0 = 0; e0 < E; e0 += 8) {
+    int v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned bal = __ballot_sync(0xffffffffu, v[j] >= 0);
+      if (lane == 0 && e0 + j < E) s_bal[warp][e0 + j] = bal;
+    }
+  }
+  __syncthreads();
+  if (!valid) return;
+  const unsigned lower = (1u << lane) - 1u;
+  const long long u = (long long)me * T_ + t;
+  for (int e = 0; e < E; ++e) {
+    const unsigned mine = s_bal[warp][e];
+    const int p = e / El;
+    int row = -1;
+    if ((mine >> lane) & 1u) {
+      int wpre = 0;
+      for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
+      const long long r = (long long)base[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre +
+                          __popc(mine & lower);
+      if (r < R_cap) {
+        row = (int)r;
+        reinterpret_cast<int*>(const_cast<void*>(rtok.p[p]))[r] = t;
+        reinterpret_cast<int*>(const_cast<void*>(rsrc.p[p]))[r] = me;
+        reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[r] = probs[(long long)t * E + e];
+        reinterpret_cast<int*>(const_cast<void*>(ruid.p[p]))[r] = (int)u;
+      }
+      slot[(long long)t * E + e] = row;
+    }
+    reinterpret_cast<int*>(const_cast<void*>(urows.p[p]))[u * El + (e - p * El)] = row;
+  }
+  for (int p = 0; p < W; ++p) {
+    bool any = false;
+    for (int j = 0; j < El; ++j) any |= ((s_bal[warp][p * El + j] >> lane) & 1u) != 0;
+    uslot[(long long)t * W + p] = any ? (int)u : -1;
+  }
+}
+
+// token side copy pass: x_t read once, stored once into tokbuf[u] of every owner it needs
+template <typename T>
+__global__ void __launch_bounds__(256) ep2d_copy_kernel(const T* __restrict__ x, const int* __restrict__ uslot, int T_,
+                                                        int d, int W, const __grid_constant__ PeerTable tb) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  const int sv = lane < W ? uslot[(long long)t * W + lane] : -1;
+  const unsigned bal0 = __ballot_sync(0xffffffffu, sv >= 0);
+  const T* src = x + (long long)t * d;
+  for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+    uint4 buf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
+    }
+    unsigned bal = bal0;
+    while (bal) {
+      const int p = __ffs(bal) - 1;
+      bal &= bal - 1;
+      const long long u = __shfl_sync(0xffffffffu, sv, p);
+      T* dst = reinterpret_cast<T*>(const_cast<void*>(tb.p[p])) + u * d;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int v = v0 + q * 32 + lane;
+        if (v < nvec) st_v4(dst + (long long)v * V, buf[q]);
+      }
+    }
+  }
+}
+
+// expert side: x_recv[r] = tokbuf[ruid[r]] for the routed rows (pads were zeroed by ep2_prepare)
+template <typename T>
+__global__ void __launch_bounds__(256) ep2d_permute_kernel(const T* __restrict__ tokbuf, const int* __restrict__ rtok,
+                                                           const int* __restrict__ ruid, const int* __restrict__ off,
+                                                           int El, int d, long long R_cap, T* __restrict__ x_recv) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long r = (long long)blockIdx.x * 8 + warp;
+  if (r >= min((long long)off[El], R_cap) || rtok[r] < 0) return;
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  const T* src = tokbuf + (long long)ruid[r] * d;
+  T* dst = x_recv + r * d;
+  for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+    uint4 buf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) st_v4(dst + (long long)v * V, buf[q]);
+    }
+  }
+}
+
+// expert side pre-sum per unique token u: out[u] = sum_{j asc} (gate[row] *) rows[row],
+// row = urows[u][j] >= 0 (local experts in ascending order); u with no row is skipped
+template <typename T, bool WEIGHTED, int QV>
+__global__ void __launch_bounds__(256, 4) ep2d_presum_kernel(const T* __restrict__ rows, const float* __restrict__ gate,
+                                                             const int* __restrict__ urows, long long n_u, int El, int d,
+                                                             T* __restrict__ out) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long u = (long long)blockIdx.x * 8 + warp;
+  if (u >= n_u) return;
+  const int* ur = urows + u * El;
+  bool any = false;
+  for (int j = lane; j < El; j += 32) any |= ur[j] >= 0;
+  if (!__any_sync(0xffffffffu, any)) return;
+  gather_sum_token<T, WEIGHTED, float, QV>(LocalRows<T>{rows, gate, d}, ur, d, El, nullptr, out + u * d, lane);
+}
+
+// expert side: dyu[u] = dy@s[t] for every unique token u = s * T + t routed here (one NVLink
+// read per (token, owner) instead of one per selected expert)
+template <typename T>
+__global__ void __launch_bounds__(256) ep2d_gather_dy_kernel(const __grid_constant__ PeerTable dyp,
+                                                             const int* __restrict__ urows, int T_, int W, int El,
+                                                             int d, T* __restrict__ dyu) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const long long u = (long long)blockIdx.x * 8 + warp;
+  if (u >= (long long)W * T_) return;
+  const int* ur = urows + u * El;
+  bool any = false;
+  for (int j = lane; j < El; j += 32) any |= ur[j] >= 0;
+  if (!__any_sync(0xffffffffu, any)) return;
+  const int s = (int)(u / T_), t = (int)(u - (long long)s * T_);
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  const T* src = reinterpret_cast<const T*>(dyp.p[s]) + (long long)t * d;
+  T* dst = dyu + u * d;
+  for (int v0 = 0; v0 < nvec; v0 += 32 * 4) {
+    uint4 buf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) buf[q] = ld_nc_v4(src + (long long)v * V);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int v = v0 + q * 32 + lane;
+      if (v < nvec) st_v4(dst + (long long)v * V, buf[q]);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_spawn(const moe_ctx* c, const void* W1s, const void* b1s, const void* W2s, const void* b2s,
@@ -1029,14 +1200,15 @@ cudaError_t launch_ep2_combine_bwd(moe_ctx* c, const PeerTable& dyp, const void*
 }
 
 cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, const float* dlogits,
-                                    const void* Wg, void* dx, cudaStream_t s) {
+                                    const void* Wg, void* dx, cudaStream_t s, int slot_cols, int cols_per_rank) {
   if (c->T == 0) return cudaSuccess;
+  const int SE = slot_cols > 0 ? slot_cols : c->E, SEl = cols_per_rank > 0 ? cols_per_rank : c->E_local;
   const unsigned grid = (c->T + 7) / 8;
   if (dlogits && gate_tc_supported(c)) {
     cudaError_t e = gate_tc_dx(c, dlogits, Wg, c->dxg, s);
     if (e != cudaSuccess) return e;
     MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, bf16, QV><<<grid, 256, 0, s>>>(
-        dxp, slot, (const bf16*)c->dxg, c->T, c->d, c->E, c->E_local, (bf16*)dx), count_launch())
+        dxp, slot, (const bf16*)c->dxg, c->T, c->d, SE, SEl, (bf16*)dx), count_launch())
     return cudaGetLastError();
   }
   const float* dxg = nullptr;
@@ -1052,12 +1224,118 @@ cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, cons
   }
   if (c->dtype == 1) {
     MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, float, QV><<<grid, 256, 0, s>>>(
-        dxp, slot, dxg, c->T, c->d, c->E, c->E_local, (bf16*)dx), count_launch())
+        dxp, slot, dxg, c->T, c->d, SE, SEl, (bf16*)dx), count_launch())
   } else {
     MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2_dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>(
-        dxp, slot, dxg, c->T, c->d, c->E, c->E_local, (float*)dx), count_launch())
+        dxp, slot, dxg, c->T, c->d, SE, SEl, (float*)dx), count_launch())
   }
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ ep2 with token dedup
+cudaError_t launch_ep2d_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot, int32_t* uslot,
+                                 const PeerTable& tb, const PeerTable& urows, const PeerTable& rtok,
+                                 const PeerTable& rsrc, const PeerTable& rgate, const PeerTable& ruid, int64_t R_cap,
+                                 cudaStream_t s) {
+  dispatch_scan_kernel<<<1, 1024, 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot, c->ep2_scr,
+                                          c->ep2_scr + c->E + 1, (long long)1 << 62, c->flags), count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || c->nblk == 0) return e;
+  ep2d_rank_kernel<<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->world, c->blk_base,
+                                               c->ep2_base, R_cap, rtok, rsrc, rgate, ruid, urows, uslot),
+      count_launch();
+  if (c->dtype == 1)
+    ep2d_copy_kernel<bf16><<<(c->T + 7) / 8, 256, 0, s>>>((const bf16*)x, uslot, c->T, c->d, c->world, tb),
+        count_launch();
+  else
+    ep2d_copy_kernel<float><<<(c->T + 7) / 8, 256, 0, s>>>((const float*)x, uslot, c->T, c->d, c->world, tb),
+        count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ep2d_permute(const moe_ctx* c, const void* tokbuf, const int32_t* rtok, const int32_t* ruid,
+                                int64_t R_cap, void* x_recv, cudaStream_t s) {
+  if (R_cap == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((R_cap + 7) / 8);
+  if (c->dtype == 1)
+    ep2d_permute_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)tokbuf, rtok, ruid, c->ep_off, c->E_local, c->d,
+                                                   R_cap, (bf16*)x_recv), count_launch();
+  else
+    ep2d_permute_kernel<float><<<grid, 256, 0, s>>>((const float*)tokbuf, rtok, ruid, c->ep_off, c->E_local, c->d,
+                                                    R_cap, (float*)x_recv), count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ep2d_presum(const moe_ctx* c, const void* rows, const float* gate, const int32_t* urows, void* out,
+                               cudaStream_t s) {
+  const long long n_u = (long long)c->world * c->T;
+  if (n_u == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((n_u + 7) / 8);
+  const int El = c->E_local;
+  if (c->dtype == 1) {
+    if (gate) {
+      MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2d_presum_kernel<bf16, true, QV><<<grid, 256, 0, s>>>(
+          (const bf16*)rows, gate, urows, n_u, El, c->d, (bf16*)out), count_launch())
+    } else {
+      MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2d_presum_kernel<bf16, false, QV><<<grid, 256, 0, s>>>(
+          (const bf16*)rows, gate, urows, n_u, El, c->d, (bf16*)out), count_launch())
+    }
+  } else {
+    if (gate) {
+      MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2d_presum_kernel<float, true, QV><<<grid, 256, 0, s>>>(
+          (const float*)rows, gate, urows, n_u, El, c->d, (float*)out), count_launch())
+    } else {
+      MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2d_presum_kernel<float, false, QV><<<grid, 256, 0, s>>>(
+          (const float*)rows, gate, urows, n_u, El, c->d, (float*)out), count_launch())
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ep2d_gather_dy(const moe_ctx* c, const PeerTable& dyp, const int32_t* urows, void* dyu,
+                                  cudaStream_t s) {
+  const long long n_u = (long long)c->world * c->T;
+  if (n_u == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((n_u + 7) / 8);
+  if (c->dtype == 1)
+    ep2d_gather_dy_kernel<bf16><<<grid, 256, 0, s>>>(dyp, urows, c->T, c->world, c->E_local, c->d, (bf16*)dyu),
+        count_launch();
+  else
+    ep2d_gather_dy_kernel<float><<<grid, 256, 0, s>>>(dyp, urows, c->T, c->world, c->E_local, c->d, (float*)dyu),
+        count_launch();
+  return cudaGetLastError();
+}
+
+// token side: y[t] = sum_{q asc} ysum@q[uslot[t, q]] (the owners' pre-summed rows, unweighted)
+cudaError_t launch_ep2d_combine(const moe_ctx* c, const PeerTable& ys, const int32_t* uslot, void* y, cudaStream_t s) {
+  if (c->T == 0) return cudaSuccess;
+  const unsigned grid = (c->T + 7) / 8;
+  if (c->dtype == 1) {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, float, QV><<<grid, 256, 0, s>>>(
+        ys, uslot, nullptr, c->T, c->d, c->world, 1, (bf16*)y), count_launch())
+  } else {
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2_dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>(
+        ys, uslot, nullptr, c->T, c->d, c->world, 1, (float*)y), count_launch())
+  }
+  return cudaGetLastError();
+}
+
+// expert side combine backward with dy from the local dyu (row_token = ruid): the fused
+// d_eout / dG / db2-partials kernel of the single-rank path
+cudaError_t launch_ep2d_combine_bwd(moe_ctx* c, const void* dyu, const void* e_out, const float* rgate,
+                                    const int32_t* ruid, const int32_t* offsets, int64_t R_cap, void* d_eout,
+                                    float* dG_row, cudaStream_t s) {
+  c->db2_src = nullptr;
+  if (R_cap == 0) return cudaSuccess;
+  const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
+  if (c->dtype == 1) {
+    if (nvec <= 32) return launch_cbc<bf16, 1>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+    if (nvec <= 64) return launch_cbc<bf16, 2>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+    if (nvec <= 96) return launch_cbc<bf16, 3>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+    return launch_cbc<bf16, 4>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+  }
+  if (nvec <= 32) return launch_cbc<float, 1>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+  return launch_cbc<float, 2>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
 }
 
 }  // namespace moe

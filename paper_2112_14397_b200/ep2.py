@@ -58,8 +58,10 @@ class EP2Rank:
     """One rank of the fused peer-memory EP layer."""
 
     def __init__(self, T: int, d_model: int, d_ff: int, E: int, dtype: torch.dtype, device: torch.device, rank: int,
-                 world: int, syms: SymmetricBuffers, comm: Optional[int] = None):
+                 world: int, syms: SymmetricBuffers, comm: Optional[int] = None, dedup: bool = False):
         self.T, self.d, self.f, self.E, self.El = T, d_model, d_ff, E, E // world
+        # dedup (moe_ep2d_*): one row per (token, owner) each way; U = world * T unique slots
+        self.dedup, self.U = dedup, world * T
         self.dtype, self.device, self.rank, self.world, self.syms = dtype, device, rank, world, syms
         self.ctx = L.moe_create(T, d_model, d_ff, E, _DT[dtype], comm if comm else L.MOE_COMM_EMULATED, rank, world)
         self.ws = torch.empty(max(256, L.moe_workspace_bytes(self.ctx)), dtype=torch.uint8, device=device)
@@ -124,12 +126,38 @@ class EP2Rank:
         rs, _ = self._sym("rsrc", (R,), torch.int32)
         rg, _ = self._sym("rgate", (R,), torch.float32)
         L.moe_ep2_prepare_recv(self.ctx, xr, rt, rs, rg, R)
+        if self.dedup:
+            self._sym("ruid", (R,), torch.int32)
+            self._sym("tokbuf", (self.U, d), self.dtype)
+            self._sym("urows", (self.U, self.El), torch.int32)
+            s["uslot"] = torch.empty(self.T, self.world, dtype=torch.int32, device=self.device)
 
     def fwd_dispatch(self):
         R, d, s = self.R_cap, self.d, self.st
+        if self.dedup:
+            L.moe_ep2d_dispatch(self.ctx, s["x"], s["probs"], s["slot"], s["uslot"],
+                                self._sym("tokbuf", (self.U, d), self.dtype)[1],
+                                self._sym("urows", (self.U, self.El), torch.int32)[1],
+                                self._sym("rtok", (R,), torch.int32)[1], self._sym("rsrc", (R,), torch.int32)[1],
+                                self._sym("rgate", (R,), torch.float32)[1], self._sym("ruid", (R,), torch.int32)[1], R)
+            return
         L.moe_ep2_dispatch(self.ctx, s["x"], s["probs"], s["slot"], self._sym("x_recv", (R, d), self.dtype)[1],
                            self._sym("rtok", (R,), torch.int32)[1], self._sym("rsrc", (R,), torch.int32)[1],
                            self._sym("rgate", (R,), torch.float32)[1], R)
+
+    def fwd_permute(self):
+        """dedup, expert side: x_recv rows from the once-received token rows (local copy)."""
+        R, d = self.R_cap, self.d
+        L.moe_ep2d_permute(self.ctx, self._sym("tokbuf", (self.U, d), self.dtype)[0],
+                           self._sym("rtok", (R,), torch.int32)[0], self._sym("ruid", (R,), torch.int32)[0], R,
+                           self._sym("x_recv", (R, d), self.dtype)[0])
+
+    def fwd_presum(self):
+        """dedup, expert side: ysum[u] = sum over my experts of G e_out (one row per token and owner)."""
+        R, d = self.R_cap, self.d
+        L.moe_ep2d_presum(self.ctx, self._sym("e_out", (R, d), self.dtype)[0], self._sym("rgate", (R,), torch.float32)[0],
+                          self._sym("urows", (self.U, self.El), torch.int32)[0],
+                          self._sym("ysum", (self.U, d), self.dtype)[0])
 
     def fwd_experts(self):
         R, d, f, s = self.R_cap, self.d, self.f, self.st
@@ -143,7 +171,10 @@ class EP2Rank:
     def fwd_combine(self):
         R, d, s = self.R_cap, self.d, self.st
         s["y"] = torch.empty(self.T, d, dtype=self.dtype, device=self.device)
-        L.moe_ep2_combine(self.ctx, self._sym("e_out", (R, d), self.dtype)[1], s["probs"], s["slot"], s["y"])
+        if self.dedup:
+            L.moe_ep2d_combine(self.ctx, self._sym("ysum", (self.U, d), self.dtype)[1], s["uslot"], s["y"])
+        else:
+            L.moe_ep2_combine(self.ctx, self._sym("e_out", (R, d), self.dtype)[1], s["probs"], s["slot"], s["y"])
         return s["y"]
 
     # ------------------------------------------------------------ backward phases
@@ -151,10 +182,22 @@ class EP2Rank:
         buf, _ = self._sym("dy", (self.T, self.d), self.dtype)
         buf.copy_(dy)
 
+    def bwd_gather_dy(self):
+        """dedup, expert side: dyu[u] = the token's dy row, read once per (token, owner)."""
+        s = self.st
+        s["dyu"] = torch.empty(self.U, self.d, dtype=self.dtype, device=self.device)
+        L.moe_ep2d_gather_dy(self.ctx, self._sym("dy", (self.T, self.d), self.dtype)[1],
+                             self._sym("urows", (self.U, self.El), torch.int32)[0], s["dyu"])
+
     def bwd_combine(self):
         R, d, s = self.R_cap, self.d, self.st
         s["d_eout"] = torch.empty(R, d, dtype=self.dtype, device=self.device)
         dG, _ = self._sym("dG", (R,), torch.float32)
+        if self.dedup:
+            L.moe_ep2d_combine_bwd(self.ctx, s["dyu"], self._sym("e_out", (R, d), self.dtype)[0],
+                                   self._sym("rgate", (R,), torch.float32)[0], self._sym("ruid", (R,), torch.int32)[0],
+                                   s["off"], R, s["d_eout"], dG)
+            return
         L.moe_ep2_combine_bwd(self.ctx, self._sym("dy", (self.T, d), self.dtype)[1],
                               self._sym("e_out", (R, d), self.dtype)[0], self._sym("rgate", (R,), torch.float32)[0],
                               self._sym("rtok", (R,), torch.int32)[0], self._sym("rsrc", (R,), torch.int32)[0],
@@ -174,6 +217,13 @@ class EP2Rank:
         self._mark("experts_bwd", 1)
         s["grads"] = g
 
+    def bwd_presum(self):
+        """dedup, expert side: dxu[u] = sum over my experts of dx_perm (one row per token and owner)."""
+        R, d = self.R_cap, self.d
+        L.moe_ep2d_presum(self.ctx, self._sym("dx_perm", (R, d), self.dtype)[0], None,
+                          self._sym("urows", (self.U, self.El), torch.int32)[0],
+                          self._sym("dxu", (self.U, d), self.dtype)[0])
+
     def bwd_gate(self, balance_alpha: float = 0.0, B_total: Optional[int] = None):
         s, dev = self.st, self.device
         g = s["grads"]
@@ -187,8 +237,12 @@ class EP2Rank:
     def bwd_dispatch(self):
         s, g = self.st, self.st["grads"]
         g["dx"] = torch.empty(self.T, self.d, dtype=self.dtype, device=self.device)
-        L.moe_ep2_dispatch_bwd(self.ctx, self._sym("dx_perm", (self.R_cap, self.d), self.dtype)[1], s["slot"],
-                               g["dlogits"], self.Wg, g["dx"])
+        if self.dedup:
+            L.moe_ep2d_dispatch_bwd(self.ctx, self._sym("dxu", (self.U, self.d), self.dtype)[1], s["uslot"],
+                                    g["dlogits"], self.Wg, g["dx"])
+        else:
+            L.moe_ep2_dispatch_bwd(self.ctx, self._sym("dx_perm", (self.R_cap, self.d), self.dtype)[1], s["slot"],
+                                   g["dlogits"], self.Wg, g["dx"])
         return g
 
     def check(self):
@@ -201,15 +255,23 @@ class EP2Rank:
         self.fwd_plan()
         self.fwd_dispatch()
         self.barrier()
+        if self.dedup:
+            self.fwd_permute()
         self.fwd_experts()
+        if self.dedup:
+            self.fwd_presum()
         self.barrier()
         return self.fwd_combine()
 
     def backward(self, dy, balance_alpha: float = 0.0):
         self.bwd_stage_dy(dy)
         self.barrier()
+        if self.dedup:
+            self.bwd_gather_dy()
         self.bwd_combine()
         self.bwd_experts()
+        if self.dedup:
+            self.bwd_presum()
         self.barrier()
         self.bwd_gate(balance_alpha)
         L.moe_ep_allreduce(self.ctx, self.st["grads"]["dWg"], self.d * self.E)
@@ -226,14 +288,22 @@ def run_lockstep(ranks: List[EP2Rank], xs, us, dys, tau: float, threshold: float
     for r in ranks:
         r.fwd_dispatch()
     for r in ranks:
+        if r.dedup:
+            r.fwd_permute()
         r.fwd_experts()
+        if r.dedup:
+            r.fwd_presum()
     ys = [r.fwd_combine() for r in ranks]
     for r, dy in zip(ranks, dys):
         r.bwd_stage_dy(dy)
     for r in ranks:
+        if r.dedup:
+            r.bwd_gather_dy()
         r.bwd_combine()
     for r in ranks:
         r.bwd_experts()
+        if r.dedup:
+            r.bwd_presum()
     for r in ranks:
         r.bwd_gate()
     dWg = sum(r.st["grads"]["dWg"] for r in ranks)

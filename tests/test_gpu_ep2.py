@@ -213,3 +213,62 @@ def test_ep2_module_lockstep_c2_shape():
         assert torch.equal(grads[q]["dx"], g["dx"][sl])
         assert torch.equal(grads[q]["dW1"], g["dW1"][es]) and torch.equal(grads[q]["dW2"], g["dW2"][es])
     assert _rel(dWg, g["dWg"]) < 1e-5
+
+
+def _lockstep(cfg, W, T, dedup):
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers, run_lockstep
+    dev = torch.device("cuda", 0)
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
+    ranks_in = [inputs.make_inputs(cfg, rank=q, T=T) for q in range(W)]
+    li0 = ranks_in[0]
+    syms = SymmetricBuffers(W, dev)
+    ranks = []
+    for q in range(W):
+        r = EP2Rank(T, cfg.d_model, cfg.d_ff, cfg.E, dt, dev, q, W, syms, dedup=dedup)
+        r.set_gate(li0.Wg.to(dev))
+        r.spawn(*(t.to(dev) for t in (li0.W1s, li0.b1s, li0.W2s, li0.b2s, li0.M1bits, li0.M2bits)))
+        ranks.append(r)
+    ys, grads, dWg = run_lockstep(ranks, [ri.x.to(dev) for ri in ranks_in], [ri.u.to(dev) for ri in ranks_in],
+                                  [ri.dy.to(dev) for ri in ranks_in], float(np.float32(cfg.tau)),
+                                  float(np.float32(cfg.threshold)), top1=cfg.top1)
+    torch.cuda.synchronize()
+    for r in ranks:
+        r.check()
+    out = dict(y=[t.clone() for t in ys], g=[{k: v.clone() for k, v in g.items()} for g in grads], dWg=dWg.clone(),
+               slot=[r.st["slot"].clone() for r in ranks])
+    return out, ranks_in
+
+
+@pytest.mark.parametrize("name,W,T", [("C2", 2, 384), ("C3", 4, 300), ("C4", 8, 160)])
+def test_ep2_dedup_matches_single_rank(name, W, T):
+    # token dedup (moe_ep2d_*): one row per (token, owner) each way.  Routing, dlogits and the
+    # expert weight gradients are bit-identical to the single-rank layer; y and dx differ only
+    # by the rounding of the per-owner partial sums to bf16; the bias / gate weight gradients
+    # to fp32 rounding (partial-sum partitions follow the local expert count).
+    cfg = getattr(configs, name)
+    ep, ranks_in = _lockstep(cfg, W, T, dedup=True)
+    layer, y, g = _single(cfg, ranks_in)
+    st = layer.state
+    El = cfg.E // W
+    for q in range(W):
+        sl, es = slice(q * T, (q + 1) * T), slice(q * El, (q + 1) * El)
+        assert torch.equal(ep["slot"][q] >= 0, st.slot[sl] >= 0), f"rank {q} routing"
+        assert torch.equal(ep["g"][q]["dlogits"], g["dlogits"][sl]), f"rank {q} dlogits"
+        for k in ("dW1", "dW2"):
+            assert torch.equal(ep["g"][q][k], g[k][es]), f"rank {q} {k}"
+        for k in ("db1", "db2"):
+            assert _rel(ep["g"][q][k], g[k][es]) < 1e-5, f"rank {q} {k}"
+        assert _rel(ep["y"][q], y[sl]) < 5e-3, f"rank {q} y {_rel(ep['y'][q], y[sl])}"
+        assert _rel(ep["g"][q]["dx"], g["dx"][sl]) < 5e-3, f"rank {q} dx {_rel(ep['g'][q]['dx'], g['dx'][sl])}"
+    assert _rel(ep["dWg"], g["dWg"]) < 1e-5
+
+
+def test_ep2_dedup_single_owner_rows_are_exact():
+    # with one selected expert per (token, owner) -- top-1 routing -- the pre-sums are single
+    # rows, so y and dx equal the non-dedup path bit for bit
+    cfg = dataclasses.replace(configs.C3, top1=True)
+    a, _ = _lockstep(cfg, 4, 256, dedup=True)
+    b, _ = _lockstep(cfg, 4, 256, dedup=False)
+    for q in range(4):
+        assert torch.equal(a["y"][q], b["y"][q])
+        assert torch.equal(a["g"][q]["dx"], b["g"][q]["dx"])
