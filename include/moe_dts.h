@@ -330,7 +330,8 @@ int moe_ep2d_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* 
                       void* const* tokbuf_peers, int32_t* const* urows_peers, int32_t* const* rtok_peers,
                       int32_t* const* rsrc_peers, float* const* rgate_peers, int32_t* const* ruid_peers,
                       int64_t R_recv_cap, void* stream);
-int moe_ep2d_permute(moe_ctx* ctx, const void* tokbuf, const int32_t* rtok, const int32_t* ruid, int64_t R_recv_cap,
+/* also sets ruid = -1 on the pad rows of the recv layout (moe_ep2d_combine_bwd reads ruid) */
+int moe_ep2d_permute(moe_ctx* ctx, const void* tokbuf, const int32_t* rtok, int32_t* ruid, int64_t R_recv_cap,
                      void* x_recv, void* stream);
 /* out[u] = sum_{j asc, urows[u][j] >= 0} (rgate[row] *) rows[row]; rgate NULL = unweighted.
  * Unique slots with no row are left untouched. */

@@ -134,7 +134,7 @@ cudaError_t launch_ep2d_dispatch(const moe_ctx* c, const void* x, const float* p
                                  const PeerTable& tb, const PeerTable& urows, const PeerTable& rtok,
                                  const PeerTable& rsrc, const PeerTable& rgate, const PeerTable& ruid, int64_t R_cap,
                                  cudaStream_t s);
-cudaError_t launch_ep2d_permute(const moe_ctx* c, const void* tokbuf, const int32_t* rtok, const int32_t* ruid,
+cudaError_t launch_ep2d_permute(const moe_ctx* c, const void* tokbuf, const int32_t* rtok, int32_t* ruid,
                                 int64_t R_cap, void* x_recv, cudaStream_t s);
 cudaError_t launch_ep2d_presum(const moe_ctx* c, const void* rows, const float* gate, const int32_t* urows, void* out,
                                cudaStream_t s);

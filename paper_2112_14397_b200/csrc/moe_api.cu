@@ -799,7 +799,7 @@ int moe_ep2d_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* 
                                                S(stream)), fn);
 }
 
-int moe_ep2d_permute(moe_ctx* ctx, const void* tokbuf, const int32_t* rtok, const int32_t* ruid, int64_t R_recv_cap,
+int moe_ep2d_permute(moe_ctx* ctx, const void* tokbuf, const int32_t* rtok, int32_t* ruid, int64_t R_recv_cap,
                      void* x_recv, void* stream) {
   int rc = ep2_check(ctx, "moe_ep2d_permute");
   if (rc) return rc;

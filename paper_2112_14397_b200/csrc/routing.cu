@@ -885,13 +885,19 @@ __global__ void __launch_bounds__(256) ep2d_copy_kernel(const T* __restrict__ x,
 }
 
 // expert side: x_recv[r] = tokbuf[ruid[r]] for the routed rows (pads were zeroed by ep2_prepare)
+// Pad rows get ruid = -1: the combine backward takes ruid as its row -> token map and must
+// see them as pads (a stale id would pull a dy row into a zero-gate pad row).
 template <typename T>
 __global__ void __launch_bounds__(256) ep2d_permute_kernel(const T* __restrict__ tokbuf, const int* __restrict__ rtok,
-                                                           const int* __restrict__ ruid, const int* __restrict__ off,
+                                                           int* __restrict__ ruid, const int* __restrict__ off,
                                                            int El, int d, long long R_cap, T* __restrict__ x_recv) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long r = (long long)blockIdx.x * 8 + warp;
-  if (r >= min((long long)off[El], R_cap) || rtok[r] < 0) return;
+  if (r >= min((long long)off[El], R_cap)) return;
+  if (rtok[r] < 0) {
+    if (lane == 0) ruid[r] = -1;
+    return;
+  }
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
   const T* src = tokbuf + (long long)ruid[r] * d;
@@ -1253,7 +1259,7 @@ cudaError_t launch_ep2d_dispatch(const moe_ctx* c, const void* x, const float* p
   return cudaGetLastError();
 }
 
-cudaError_t launch_ep2d_permute(const moe_ctx* c, const void* tokbuf, const int32_t* rtok, const int32_t* ruid,
+cudaError_t launch_ep2d_permute(const moe_ctx* c, const void* tokbuf, const int32_t* rtok, int32_t* ruid,
                                 int64_t R_cap, void* x_recv, cudaStream_t s) {
   if (R_cap == 0) return cudaSuccess;
   const unsigned grid = (unsigned)((R_cap + 7) / 8);

@@ -185,7 +185,7 @@ def test_ep2_fp32_c1_two_ranks():
     _check(configs.C1, 2, 96)
 
 
-def test_ep2_module_lockstep_c2_shape():
+def test_ep2_module_lockstep_c2_shape(poison_empty):
     # the same through paper_2112_14397_b200.ep2 (EP2Rank phases + SymmetricBuffers emulation)
     from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers, run_lockstep
     cfg, W, T = configs.C2, 2, 384
@@ -239,8 +239,22 @@ def _lockstep(cfg, W, T, dedup):
     return out, ranks_in
 
 
+@pytest.fixture
+def poison_empty(monkeypatch):
+    """Fill every new floating-point CUDA buffer from torch.empty with NaN, so a read of a row
+    nobody wrote (instead of an exact zero or a finite leftover) fails the comparisons."""
+    real = torch.empty
+
+    def empty(*size, dtype=None, device=None, **kw):
+        t = real(*size, dtype=dtype, device=device, **kw)
+        if t.is_cuda and t.is_floating_point():
+            t.fill_(float("nan"))
+        return t
+    monkeypatch.setattr(torch, "empty", empty)
+
+
 @pytest.mark.parametrize("name,W,T", [("C2", 2, 384), ("C3", 4, 300), ("C4", 8, 160)])
-def test_ep2_dedup_matches_single_rank(name, W, T):
+def test_ep2_dedup_matches_single_rank(poison_empty, name, W, T):
     # token dedup (moe_ep2d_*): one row per (token, owner) each way.  Routing, dlogits and the
     # expert weight gradients are bit-identical to the single-rank layer; y and dx differ only
     # by the rounding of the per-owner partial sums to bf16; the bias / gate weight gradients
@@ -263,7 +277,7 @@ def test_ep2_dedup_matches_single_rank(name, W, T):
     assert _rel(ep["dWg"], g["dWg"]) < 1e-5
 
 
-def test_ep2_dedup_single_owner_rows_are_exact():
+def test_ep2_dedup_single_owner_rows_are_exact(poison_empty):
     # with one selected expert per (token, owner) -- top-1 routing -- the pre-sums are single
     # rows, so y and dx equal the non-dedup path bit for bit
     cfg = dataclasses.replace(configs.C3, top1=True)
