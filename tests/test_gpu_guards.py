@@ -129,3 +129,35 @@ def test_ep2_no_out_of_bounds_writes(monkeypatch, dedup):
     for r in ranks:
         r.check()
     assert g.check() >= 40
+
+
+@pytest.mark.parametrize("name,cfg,recompute", CASES, ids=[c[0] for c in CASES])
+def test_no_reads_of_unwritten_memory(monkeypatch, name, cfg, recompute):
+    # every new float CUDA buffer NaN-filled (ints -1): a step must give bit-identical results
+    # to a step on zero-filled buffers, i.e. no kernel reads a value nobody wrote
+    from paper_2112_14397_b200 import layer as LY
+    real = torch.empty
+    li = inputs.make_inputs(cfg, T=cfg.T)
+    dev = torch.device("cuda", 0)
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
+    outs = []
+    for poison in (False, True):
+        def empty(*size, dtype=None, device=None, **kw):
+            t = real(*size, dtype=dtype, device=device, **kw)
+            if t.is_cuda:
+                t.fill_(float("nan") if poison and t.is_floating_point() else (-1 if poison else 0))
+            return t
+        monkeypatch.setattr(LY.torch, "empty", empty)
+        lay = LY.DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev, recompute=recompute)
+        lay.set_gate(li.Wg.to(dev))
+        lay.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+        y = lay.forward(li.x.to(dev), li.u.to(dev), float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)),
+                        top1=cfg.top1)
+        g = lay.backward(li.dy.to(dev))
+        torch.cuda.synchronize()
+        lay.check()
+        outs.append((y.clone(), {k: v.clone() for k, v in g.items() if k != "da"}))
+        monkeypatch.setattr(LY.torch, "empty", real)
+    assert torch.equal(outs[0][0], outs[1][0])
+    for k in outs[0][1]:
+        assert torch.equal(outs[0][1][k], outs[1][1][k]), k
