@@ -14,7 +14,7 @@ which is exactly representable in fp32 and lies strictly inside (0, 1).
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Dict, Optional
+from typing import Optional
 
 import numpy as np
 import torch

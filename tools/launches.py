@@ -1,4 +1,4 @@
-import csv, sys, collections
+import csv, sys
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = None; out = []
 for r in rows:

@@ -1,4 +1,4 @@
-import csv, collections, sys
+import csv, sys
 rows=list(csv.reader(open(sys.argv[1])))
 hdr=rows[1]; i_src=hdr.index('Source'); i_s=hdr.index('Warp Stall Sampling (All Samples)'); i_e=hdr.index('Instructions Executed'); i_a=hdr.index('Address')
 i_ns = hdr.index('Warp Stall Sampling (Not-issued Samples)')
