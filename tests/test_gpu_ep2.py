@@ -253,7 +253,7 @@ def poison_empty(monkeypatch):
     monkeypatch.setattr(torch, "empty", empty)
 
 
-@pytest.mark.parametrize("name,W,T", [("C2", 2, 384), ("C3", 4, 300), ("C4", 8, 160)])
+@pytest.mark.parametrize("name,W,T", [("C1", 2, 96), ("C2", 2, 384), ("C3", 4, 300), ("C4", 8, 160)])
 def test_ep2_dedup_matches_single_rank(poison_empty, name, W, T):
     # token dedup (moe_ep2d_*): one row per (token, owner) each way.  Routing, dlogits and the
     # expert weight gradients are bit-identical to the single-rank layer; y and dx differ only
@@ -272,8 +272,9 @@ def test_ep2_dedup_matches_single_rank(poison_empty, name, W, T):
             assert torch.equal(ep["g"][q][k], g[k][es]), f"rank {q} {k}"
         for k in ("db1", "db2"):
             assert _rel(ep["g"][q][k], g[k][es]) < 1e-5, f"rank {q} {k}"
-        assert _rel(ep["y"][q], y[sl]) < 5e-3, f"rank {q} y {_rel(ep['y'][q], y[sl])}"
-        assert _rel(ep["g"][q]["dx"], g["dx"][sl]) < 5e-3, f"rank {q} dx {_rel(ep['g'][q]['dx'], g['dx'][sl])}"
+        tol = 5e-3 if cfg.dtype == "bf16" else 1e-6      # fp32: the partial sums are not rounded further
+        assert _rel(ep["y"][q], y[sl]) < tol, f"rank {q} y {_rel(ep['y'][q], y[sl])}"
+        assert _rel(ep["g"][q]["dx"], g["dx"][sl]) < tol, f"rank {q} dx {_rel(ep['g'][q]['dx'], g['dx'][sl])}"
     assert _rel(ep["dWg"], g["dWg"]) < 1e-5
 
 
