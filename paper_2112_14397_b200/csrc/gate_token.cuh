@@ -176,7 +176,7 @@ __device__ __forceinline__ void gate_token(const float* L, int t, const T* __res
 
 
 // fp64 decision for one token deferred by the thread-per-token fast path (near the
-// threshold or an argmax tie), computed by a whole 256-thread block.  The fp64 logits are a
+// threshold or an argmax tie), computed by a whole NT-thread block.  The fp64 logits are a
 // latency problem (one token: d * E products), so W_g is staged through shared memory in
 // chunks of up to 32 KB, each chunk's loads all issued before any is used (one memory
 // round trip per chunk, not one per k step); thread (e, sl) then accumulates expert e over
@@ -188,10 +188,10 @@ constexpr int kRefineKC = 1024;
 struct RefineSmem {
   uint4 w[kRefineWBytes / 16];     // W_g rows [k0, k0 + KC) of this chunk, raw element type
   float x[kRefineKC];              // x[k0 .. k0 + KC)
-  double red[256];                 // per-thread partial logits
+  double red[1024];                // per-thread partial logits (NT <= 1024)
 };
 
-template <typename T>
+template <typename T, int NT = 256>
 __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restrict__ x, const T* __restrict__ Wg,
                                                         const float* __restrict__ u, int d, int E, float tau,
                                                         float thr, int top1, float* __restrict__ probs,
@@ -200,7 +200,8 @@ __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restri
                                                         int* __restrict__ near_band, RefineSmem& sm) {
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const T* xr = x + (long long)t * d;
-  const int nsl = 256 / E;                        // E <= 128: >= 2 k slices
+  static_assert(NT <= 1024 && NT % 32 == 0, "block size");
+  const int nsl = NT / E;                         // E <= 128: >= 2 k slices
   const int e_me = tid % E, sl = tid / E;
   const bool worker = sl < nsl;
   int KC = kRefineWBytes / (E * (int)sizeof(T));
@@ -213,34 +214,36 @@ __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restri
     const long long n = (long long)kc * E;         // elements of this chunk
     if (vec) {
       const uint4* src = reinterpret_cast<const uint4*>(Wg + (long long)k0 * E);
-      const int n16 = (int)(n * sizeof(T) / 16);   // <= 2048 = 8 per thread
-      uint4 r[8];
+      const int n16 = (int)(n * sizeof(T) / 16);   // <= 2048
+      constexpr int WJ = (kRefineWBytes / 16 + NT - 1) / NT;
+      uint4 r[WJ];
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (tid + 256 * j < n16) r[j] = __ldg(src + tid + 256 * j);
+      for (int j = 0; j < WJ; ++j)
+        if (tid + NT * j < n16) r[j] = __ldg(src + tid + NT * j);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (tid + 256 * j < n16) sm.w[tid + 256 * j] = r[j];
+      for (int j = 0; j < WJ; ++j)
+        if (tid + NT * j < n16) sm.w[tid + NT * j] = r[j];
     } else {
       T* wd = reinterpret_cast<T*>(sm.w);
-      for (int b = 0; b < n; b += 256 * 8) {
+      for (int b = 0; b < n; b += NT * 8) {
         T r[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (b + tid + 256 * j < n) r[j] = Wg[(long long)k0 * E + b + tid + 256 * j];
+          if (b + tid + NT * j < n) r[j] = Wg[(long long)k0 * E + b + tid + NT * j];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (b + tid + 256 * j < n) wd[b + tid + 256 * j] = r[j];
+          if (b + tid + NT * j < n) wd[b + tid + NT * j] = r[j];
       }
     }
     {
-      float r[kRefineKC / 256];
+      constexpr int XJ = (kRefineKC + NT - 1) / NT;
+      float r[XJ];
 #pragma unroll
-      for (int j = 0; j < kRefineKC / 256; ++j)
-        if (tid + 256 * j < kc) r[j] = to_f32(xr[k0 + tid + 256 * j]);
+      for (int j = 0; j < XJ; ++j)
+        if (tid + NT * j < kc) r[j] = to_f32(xr[k0 + tid + NT * j]);
 #pragma unroll
-      for (int j = 0; j < kRefineKC / 256; ++j)
-        if (tid + 256 * j < kc) sm.x[tid + 256 * j] = r[j];
+      for (int j = 0; j < XJ; ++j)
+        if (tid + NT * j < kc) sm.x[tid + NT * j] = r[j];
     }
     __syncthreads();
     if (worker) {
