@@ -307,3 +307,9 @@ def test_empty_token_batch(dtype):
     for k in ("dW1", "db1", "dW2", "db2", "dWg"):
         assert g[k].numel() > 0 and not torch.any(g[k] != 0), k
     _run(cfg, T=4)
+
+
+def test_bf16_E128_maximum_experts():
+    # E = 128, the largest expert count the gate supports (4 experts per lane in the
+    # warp-per-token SIMT gate); 64-row experts on average, many partial GEMM tiles
+    _run(_shape("E128", 640, 256, 512, 128, 1.0, 0.004))
