@@ -341,3 +341,24 @@ def test_c5_schedule_endpoints():
     s = configs.c5_schedule()
     assert len(s) == 20 and s[0] == (2.0, 0.0)
     assert abs(s[-1][0] - 0.05) < 1e-15 and abs(s[-1][1] - 0.3) < 1e-15
+
+
+def test_survey_appendix_b_values():
+    """Printed closed-form values (tests/golden/survey_appendix_b.json): DTS probabilities on
+    the paper's worked-example logits at tau = 2, 1, 0.5, 0.1 (no noise), the tau = 1,
+    c = 0.25 selection, Gumbel noise at fixed u (incl. the harness extremes 2^-24 and
+    1 - 2^-24) and GELU at fixed points, each to its printed precision."""
+    g = _gold("survey_appendix_b.json")
+    L = np.array([g["logits"]])
+    for tau, ref in g["dts_no_noise"].items():
+        p = O.gumbel_softmax(np.ones((1, 1)), L, None, float(tau))[0]
+        np.testing.assert_allclose(p, ref, atol=0.6e-6, err_msg=f"tau={tau}")
+    sel = g["threshold_tau1_c0.25"]
+    p1 = O.gumbel_softmax(np.ones((1, 1)), L, None, 1.0)
+    m = O.threshold_select(p1, 0.25)
+    assert m[0].tolist() == sel["selected"]
+    np.testing.assert_allclose(np.where(m, p1, 0.0)[0], sel["G"], atol=0.6e-6)
+    for u, z in g["gumbel"]:
+        assert abs(O.gumbel_noise(np.array([u]))[0] - z) < 0.6e-9, (u, z)
+    for a, v in g["gelu"]:
+        assert abs(O.gelu(np.array([a]))[0] - v) < 0.6e-9, (a, v)
