@@ -684,49 +684,6 @@ __global__ void ep2_prepare_kernel(T* __restrict__ x_recv, int* __restrict__ rto
   }
 }
 
-// token side rank pass (as dispatch_rank_kernel): my i-th token of expert e goes to row
-// base[e] + i on rank e / El; slot <- that row; the row's metadata is stored at the owner.
-__global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
-    const float* __restrict__ probs, int* __restrict__ slot, int T_, int E, int El, int me,
-    const int* __restrict__ blk_base, const int* __restrict__ base, long long R_cap,
-    const __grid_constant__ PeerTable rtok, const __grid_constant__ PeerTable rsrc,
-    const __grid_constant__ PeerTable rgate) {
-  __shared__ unsigned s_bal[kGateBT / 32][128];
-  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const int t = blockIdx.x * kGateBT + tid;
-  const bool valid = t < T_;
-  for (int e0 = 0; e0 < E; e0 += 8) {          // 8 flags in flight, then 8 ballots (as dispatch_rank_kernel)
-    int v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const unsigned bal = __ballot_sync(0xffffffffu, v[j] >= 0);
-      if (lane == 0 && e0 + j < E) s_bal[warp][e0 + j] = bal;
-    }
-  }
-  __syncthreads();
-  if (!valid) return;
-  const unsigned lower = (1u << lane) - 1u;
-  for (int e = 0; e < E; ++e) {
-    const unsigned mine = s_bal[warp][e];
-    if (!((mine >> lane) & 1u)) continue;
-    int wpre = 0;
-    for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
-    const long long row = (long long)base[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre +
-                          __popc(mine & lower);
-    if (row < R_cap) {
-      const int p = e / El;
-      slot[(long long)t * E + e] = (int)row;
-      reinterpret_cast<int*>(const_cast<void*>(rtok.p[p]))[row] = t;
-      reinterpret_cast<int*>(const_cast<void*>(rsrc.p[p]))[row] = me;
-      reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[row] = probs[(long long)t * E + e];
-    } else {
-      slot[(long long)t * E + e] = -1;           // dropped (MOE_ECAPACITY raised by the plan)
-    }
-  }
-}
-
 // token side copy pass: x_t read once, stored into each selected expert's row on its owner
 template <typename T>
 __global__ void __launch_bounds__(256) ep2_copy_kernel(const T* __restrict__ x, const int* __restrict__ slot, int T_,
@@ -797,9 +754,12 @@ __global__ void __launch_bounds__(256, 4) ep2_dispatch_bwd_kernel(const __grid_c
 // (u, local expert j), -1 if not selected: the token side writes the whole El-row for every
 // owner each step), ruid [R_cap] (row -> u).  Token side: uslot [T, W] = u on owner q, or -1.
 
-// token side rank pass: ep2_rank_kernel's rows and row metadata, plus ruid at the owner,
-// the token's urows rows on every owner and its uslot row
-__global__ void __launch_bounds__(kGateBT) ep2d_rank_kernel(
+// token side rank pass (as dispatch_rank_kernel): my i-th token of expert e goes to row
+// base[e] + i on rank e / El; slot <- that row; the row's metadata is stored at the owner.
+// DEDUP (ep2d) also stores ruid at the owner, the token's urows rows on every owner (-1 for
+// unselected experts) and its uslot row.
+template <bool DEDUP>
+__global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
     const float* __restrict__ probs, int* __restrict__ slot, int T_, int E, int El, int me, int W,
     const int* __restrict__ blk_base, const int* __restrict__ base, long long R_cap,
     const __grid_constant__ PeerTable rtok, const __grid_constant__ PeerTable rsrc,
@@ -809,7 +769,7 @@ __global__ void __launch_bounds__(kGateBT) ep2d_rank_kernel(
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
-  for (int e0 = 0; e0 < E; e0 += 8) {
+  for (int e0 = 0; e0 < E; e0 += 8) {          // 8 flags in flight, then 8 ballots (as dispatch_rank_kernel)
     int v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
@@ -837,16 +797,18 @@ __global__ void __launch_bounds__(kGateBT) ep2d_rank_kernel(
         reinterpret_cast<int*>(const_cast<void*>(rtok.p[p]))[r] = t;
         reinterpret_cast<int*>(const_cast<void*>(rsrc.p[p]))[r] = me;
         reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[r] = probs[(long long)t * E + e];
-        reinterpret_cast<int*>(const_cast<void*>(ruid.p[p]))[r] = (int)u;
+        if (DEDUP) reinterpret_cast<int*>(const_cast<void*>(ruid.p[p]))[r] = (int)u;
       }
-      slot[(long long)t * E + e] = row;
+      slot[(long long)t * E + e] = row;            // -1: dropped (MOE_ECAPACITY raised by the plan)
     }
-    reinterpret_cast<int*>(const_cast<void*>(urows.p[p]))[u * El + (e - p * El)] = row;
+    if (DEDUP) reinterpret_cast<int*>(const_cast<void*>(urows.p[p]))[u * El + (e - p * El)] = row;
   }
-  for (int p = 0; p < W; ++p) {
-    bool any = false;
-    for (int j = 0; j < El; ++j) any |= ((s_bal[warp][p * El + j] >> lane) & 1u) != 0;
-    uslot[(long long)t * W + p] = any ? (int)u : -1;
+  if (DEDUP) {
+    for (int p = 0; p < W; ++p) {
+      bool any = false;
+      for (int j = 0; j < El; ++j) any |= ((s_bal[warp][p * El + j] >> lane) & 1u) != 0;
+      uslot[(long long)t * W + p] = any ? (int)u : -1;
+    }
   }
 }
 
@@ -1159,8 +1121,9 @@ cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* pr
                                           c->ep2_scr + c->E + 1, (long long)1 << 62, c->flags), count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || c->nblk == 0) return e;
-  ep2_rank_kernel<<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->blk_base, c->ep2_base,
-                                              R_cap, rtok, rsrc, rgate), count_launch();
+  ep2_rank_kernel<false><<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->world,
+                                                     c->blk_base, c->ep2_base, R_cap, rtok, rsrc, rgate, PeerTable{},
+                                                     PeerTable{}, nullptr), count_launch();
   if (c->dtype == 1)
     ep2_copy_kernel<bf16><<<(c->T + 7) / 8, 256, 0, s>>>((const bf16*)x, slot, c->T, c->d, c->E, c->E_local, xr),
         count_launch();
@@ -1247,9 +1210,9 @@ cudaError_t launch_ep2d_dispatch(const moe_ctx* c, const void* x, const float* p
                                           c->ep2_scr + c->E + 1, (long long)1 << 62, c->flags), count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || c->nblk == 0) return e;
-  ep2d_rank_kernel<<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->world, c->blk_base,
-                                               c->ep2_base, R_cap, rtok, rsrc, rgate, ruid, urows, uslot),
-      count_launch();
+  ep2_rank_kernel<true><<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->world,
+                                                    c->blk_base, c->ep2_base, R_cap, rtok, rsrc, rgate, ruid, urows,
+                                                    uslot), count_launch();
   if (c->dtype == 1)
     ep2d_copy_kernel<bf16><<<(c->T + 7) / 8, 256, 0, s>>>((const bf16*)x, uslot, c->T, c->d, c->world, tb),
         count_launch();
