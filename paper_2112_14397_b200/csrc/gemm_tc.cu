@@ -393,10 +393,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS
         float4 bf[8];                                      // bias of this chunk (broadcast loads)
         if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q) bf[q] = ld_nc_f4(bias_t + col + 4 * q);
+          for (int q = 0; q < 8; ++q)
+#ifdef MOE_EXP_NOBIAS
+            bf[q] = make_float4(0.01f * q, 0.f, 0.f, 0.f);
+#else
+            bf[q] = ld_nc_f4(bias_t + col + 4 * q);
+#endif
         }
+#ifdef MOE_EXP_NOLDTM
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(0.01f * (float)(j + lane));
+#else
         tc::tmem_ld32(t_row + col, r);
         tc::tmem_ld_wait();
+#endif
         TR(8, t);
 #ifdef MOE_EXP_F32_DIRECT
         if (EPI == TEPI_F32) {
@@ -469,7 +479,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               f32x2 h2, g2;
+#ifdef MOE_EXP_NOMATH
+              h2 = v[q * 4 + j]; g2 = v[q * 4 + j];
+#else
               gelu_and_prime_x2(v[q * 4 + j], h2, g2);
+#endif
               hw[j] = f2_to_bf16x2(h2);
               gw[j] = f2_to_bf16x2(g2);
             }
@@ -479,8 +493,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS
               st_v4(p.o2 + row * p.ldo_b + n + q * 8, make_uint4(hw[0], hw[1], hw[2], hw[3]));
             }
 #else
+#ifdef MOE_EXP_NOSTS
+            if ((gw[0] ^ gw[1] ^ gw[2] ^ gw[3] ^ hw[0] ^ hw[1] ^ hw[2] ^ hw[3]) == 0x12345678u)
+#endif
+            {
             tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), make_uint4(gw[0], gw[1], gw[2], gw[3]));
             tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
+            }
 #endif
           }
         } else if (EPI == TEPI_BIAS_GELU_H) {
@@ -503,7 +522,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS
                                         f2_to_bf16x2(v[q * 4 + 3])));
         }
         TR(11, t);
+#ifndef MOE_EXP_NOFENCE
         tc::fence_proxy_async();
+#endif
         __syncwarp();
         TR(12, t);
         if (EPI == TEPI_GELU_BWD && p.colpart && store) {
