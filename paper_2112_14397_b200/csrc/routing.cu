@@ -23,25 +23,29 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restri
     const int* src = blk_cnt + (long long)e * nblk;
     int* dst = blk_base + (long long)e * nblk;
     int carry = 0;
-    for (int b0 = 0; b0 < nblk; b0 += 128) {
-      const int b = b0 + lane * 4;
-      int v[4];
+    // chunks of 1024 block counts: all 32 coalesced loads of a lane issued before any use (one
+    // memory round trip per chunk, not one per 128 entries); block b0 + 32 j + lane sits in v[j],
+    // row j is scanned across the lanes and the rows are chained through the carry
+    for (int b0 = 0; b0 < nblk; b0 += 1024) {
+      int v[32];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = (b + q < nblk) ? src[b + q] : 0;
-      const int lsum = v[0] + v[1] + v[2] + v[3];
-      int inc = lsum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int n = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += n;
+      for (int j = 0; j < 32; ++j) {
+        const int b = b0 + 32 * j + lane;
+        v[j] = b < nblk ? src[b] : 0;
       }
-      int run = carry + inc - lsum;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (b + q < nblk) dst[b + q] = run;
-        run += v[q];
+      for (int j = 0; j < 32; ++j) {
+        if (b0 + 32 * j >= nblk) break;                 // warp-uniform
+        int inc = v[j];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int n = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += n;
+        }
+        const int b = b0 + 32 * j + lane;
+        if (b < nblk) dst[b] = carry + inc - v[j];
+        carry += __shfl_sync(0xffffffffu, inc, 31);
       }
-      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
     if (lane == 0) s_tot[e] = carry;
   }

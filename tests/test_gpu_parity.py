@@ -313,3 +313,10 @@ def test_bf16_E128_maximum_experts():
     # E = 128, the largest expert count the gate supports (4 experts per lane in the
     # warp-per-token SIMT gate); 64-row experts on average, many partial GEMM tiles
     _run(_shape("E128", 640, 256, 512, 128, 1.0, 0.004))
+
+
+def test_bf16_more_than_1024_gate_blocks():
+    # T = 131149 tokens = 1025 gate blocks of 128 (+77): the dispatch scan walks each expert's
+    # per-block counts in chunks of 1024 with a carry, so this is the first shape with two chunks
+    # (C4's 131072 tokens fill exactly one); layout and routing bit-exact against the oracle
+    _run(_shape("scan2", 1024 * 128 + 77, 64, 128, 8, 0.5, 0.05), backward=False)
