@@ -178,13 +178,9 @@ cudaError_t launch_gate_typed(const moe_ctx* c, const void* x, const void* Wg, c
 }
 
 // ------------------------------------------------------------------ gate backward
-// One warp per token, kBwdTPW tokens per warp with their loads issued together (the kernel is
-// latency-bound: probs / slot, then the dependent dG gathers, are two memory round trips per
-// token; batching tokens overlaps them): dp = m dG (+ balance), dz = p (dp - <p,dp>),
-// dlogits = dz / tau.
+// One warp per token: dp = m dG (+ balance), dz = p (dp - <p,dp>), dlogits = dz / tau.
 // PEER (fused peer-memory EP, token side): dG of (t, e) sits at row slot[t,e] of the rank
 // owning e, read through its NVLink peer pointer dGp.p[e / El].
-constexpr int kBwdTPW = 4;
 template <bool PEER = false>
 __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     const float* __restrict__ dG_row, const int* __restrict__ slot, const float* __restrict__ probs,
@@ -192,56 +188,37 @@ __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     float* __restrict__ dlogits, bf16* __restrict__ dL2, int Ep, int Kp, int El,
     const __grid_constant__ PeerTable dGp) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int t0 = (blockIdx.x * 8 + warp) * kBwdTPW;
-  if (t0 >= T_) return;
-  float p[kBwdTPW][kMaxEPL], dp[kBwdTPW][kMaxEPL];
-  int r[kBwdTPW][kMaxEPL];
+  const int t = blockIdx.x * 8 + warp;
+  if (t >= T_) return;
+  float p[kMaxEPL], dp[kMaxEPL];
+  float s = 0.f;
 #pragma unroll
-  for (int k = 0; k < kBwdTPW; ++k)
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      const int e = lane + 32 * i, t = t0 + k;
-      const bool ok = t < T_ && e < E;
-      p[k][i] = ok ? probs[(long long)t * E + e] : 0.f;
-      r[k][i] = ok ? slot[(long long)t * E + e] : -1;
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    p[i] = 0.f; dp[i] = 0.f;
+    if (e < E) {
+      p[i] = probs[(long long)t * E + e];
+      int r = slot[(long long)t * E + e];
+      dp[i] = r >= 0 ? (PEER ? reinterpret_cast<const float*>(dGp.p[e / El])[r] : dG_row[r]) : 0.f;
+      if (alpha > 0.f) dp[i] += (float)(bal_scale * (double)counts[e]);
+      s += p[i] * dp[i];
     }
-#pragma unroll
-  for (int k = 0; k < kBwdTPW; ++k)
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      const int e = lane + 32 * i;
-      const int rr = r[k][i];
-      dp[k][i] = rr >= 0 ? (PEER ? reinterpret_cast<const float*>(dGp.p[e / El])[rr] : dG_row[rr]) : 0.f;
-    }
+  }
+  s = warp_sum(s);
   const float inv_tau = 1.0f / tau;
 #pragma unroll
-  for (int k = 0; k < kBwdTPW; ++k) {
-    const int t = t0 + k;
-    if (t >= T_) break;                                   // warp-uniform
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      const int e = lane + 32 * i;
-      if (e < E) {
-        if (alpha > 0.f) dp[k][i] += (float)(bal_scale * (double)counts[e]);
-        s += p[k][i] * dp[k][i];
-      }
+  for (int i = 0; i < kMaxEPL; ++i) {
+    int e = lane + 32 * i;
+    const float v = e < E ? p[i] * (dp[i] - s) * inv_tau : 0.f;
+    if (e < E) dlogits[(long long)t * E + e] = v;
+    if (dL2 && e < Ep) {   // tensor-core operand row [hi | lo | 0] of dlogits (dl_split_kernel's layout)
+      const bf16 hi = __float2bfloat16_rn(v);
+      dL2[(long long)t * Kp + e] = hi;
+      dL2[(long long)t * Kp + Ep + e] = __float2bfloat16_rn(v - __bfloat162float(hi));
     }
-    s = warp_sum(s);
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      const int e = lane + 32 * i;
-      const float v = e < E ? p[k][i] * (dp[k][i] - s) * inv_tau : 0.f;
-      if (e < E) dlogits[(long long)t * E + e] = v;
-      if (dL2 && e < Ep) {   // tensor-core operand row [hi | lo | 0] of dlogits (dl_split_kernel's layout)
-        const bf16 hi = __float2bfloat16_rn(v);
-        dL2[(long long)t * Kp + e] = hi;
-        dL2[(long long)t * Kp + Ep + e] = __float2bfloat16_rn(v - __bfloat162float(hi));
-      }
-    }
-    if (dL2)
-      for (int kk = 2 * Ep + lane; kk < Kp; kk += 32) dL2[(long long)t * Kp + kk] = __float2bfloat16_rn(0.f);
   }
+  if (dL2)
+    for (int k = 2 * Ep + lane; k < Kp; k += 32) dL2[(long long)t * Kp + k] = __float2bfloat16_rn(0.f);
 }
 
 // out[i] = sum_z part[z][i], fixed order: block = 32 outputs x 8 warps, warp w sums the splits
@@ -313,11 +290,11 @@ static cudaError_t gate_bwd_impl(const moe_ctx* c, const float* dG_row, const Pe
   PeerTable tab{};
   if (dGp) {
     tab = *dGp;
-    gate_bwd_token_kernel<true><<<(c->T + 8 * kBwdTPW - 1) / (8 * kBwdTPW), 256, 0, s>>>(nullptr, slot, probs, c->T, c->E, tau, alpha, counts,
+    gate_bwd_token_kernel<true><<<(c->T + 7) / 8, 256, 0, s>>>(nullptr, slot, probs, c->T, c->E, tau, alpha, counts,
                                                                bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
         count_launch();
   } else {
-    gate_bwd_token_kernel<false><<<(c->T + 8 * kBwdTPW - 1) / (8 * kBwdTPW), 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts,
+    gate_bwd_token_kernel<false><<<(c->T + 7) / 8, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts,
                                                                 bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
         count_launch();
   }
