@@ -9,11 +9,102 @@ namespace moe {
 namespace {
 
 // ------------------------------------------------------------------ scan
-// Single CTA of 1024 threads over the expert-major per-block counts blk_cnt[E][nblk]:
-// warp per expert, each lane 4 consecutive blocks per 128-block step (coalesced), warp
-// scan of lane totals -> exclusive per-block bases blk_base[E][nblk]; then the 128-aligned
-// exclusive prefix of the totals -> offsets[E+1].  Integer arithmetic only (deterministic).
-__global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restrict__ blk_cnt, int nblk, int E,
+// One CTA per expert over the expert-major per-block counts blk_cnt[E][nblk]: thread i takes
+// block b0 + i of each blockDim-block chunk (coalesced; blockDim = nblk rounded up to a warp, <= 1024), a block scan (warp scans + the warp totals
+// in shared memory) gives the exclusive per-block bases blk_base[E][nblk], chained across chunks
+// by a carry; the expert total goes to tot[e].  The last CTA to finish (ticket counter in the
+// flags word kScanTicket, reset by that CTA) forms the 128-aligned exclusive prefix of the
+// totals -> offsets[E+1].  Integer arithmetic only (deterministic).
+constexpr int kScanThreads = 1024;
+constexpr int kScanTicket = 12;
+static inline int scan_threads(int nblk) { return nblk >= kScanThreads ? kScanThreads : (nblk < 32 ? 32 : (nblk + 31) / 32 * 32); }
+__global__ void __launch_bounds__(kScanThreads) dispatch_scan_kernel(const int* __restrict__ blk_cnt, int nblk, int E,
+                                                                     int* __restrict__ blk_base, int* __restrict__ tot,
+                                                                     int* __restrict__ offsets, int* __restrict__ R_out,
+                                                                     long long R_cap, int* __restrict__ flags) {
+  __shared__ int s_w[32];
+  __shared__ bool s_last;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int e = blockIdx.x;
+  const int* src = blk_cnt + (long long)e * nblk;
+  int* dst = blk_base + (long long)e * nblk;
+  int carry = 0;
+  const int nw = blockDim.x / 32;
+  for (int b0 = 0; b0 < nblk; b0 += (int)blockDim.x) {
+    const int b = b0 + (int)threadIdx.x;
+    const int v = b < nblk ? src[b] : 0;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += n;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < nw ? s_w[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += n;
+      }
+      s_w[lane] = w;                                   // inclusive prefix of the warp totals
+    }
+    __syncthreads();
+    const int wbase = warp ? s_w[warp - 1] : 0;
+    if (b < nblk) dst[b] = carry + wbase + inc - v;
+    carry += s_w[nw - 1];
+    __syncthreads();                                   // s_w is rewritten by the next chunk
+  }
+  if (threadIdx.x == 0) {
+    tot[e] = carry;
+    __threadfence();
+    s_last = atomicAdd(&flags[kScanTicket], 1) == E - 1;
+  }
+  __syncthreads();
+  if (s_last && warp == 0) {
+    // the totals of all E (<= 128) experts, loaded together (4 per lane, L2-coherent loads),
+    // aligned to 128 rows and scanned by one warp
+    __threadfence();
+    int a[4], asum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int g = 4 * lane + q;
+      a[q] = g < E ? (__ldcg(tot + g) + kRowAlign - 1) / kRowAlign * kRowAlign : 0;
+      asum += a[q];
+    }
+    int inc = asum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += n;
+    }
+    int run = inc - asum;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int g = 4 * lane + q;
+      if (g < E) offsets[g] = run;
+      run += a[q];
+    }
+    const int R = __shfl_sync(0xffffffffu, inc, 31);
+    if (lane == 0) {
+      flags[kScanTicket] = 0;                          // ready for the next launch on this stream
+      offsets[E] = R;
+      *R_out = R;
+      if ((long long)R > R_cap) {
+        atomicOr(&flags[0], kFlagCapacity);
+        flags[2] = R;
+      }
+    }
+  }
+}
+
+// Small inputs (nblk <= kScanSmallBlocks: C2/C3/C5) take one CTA of 1024 threads, warp per
+// expert, each lane 4 consecutive blocks per 128-block step (coalesced), warp scan of lane
+// totals, then thread 0 forms the offsets: one launch phase, ~2 us, where the per-expert
+// CTAs above pay a second (ticket + L2 round trip) phase.
+constexpr int kScanSmallBlocks = 256;
+__global__ void __launch_bounds__(1024) dispatch_scan_small_kernel(const int* __restrict__ blk_cnt, int nblk, int E,
                                                             int* __restrict__ blk_base, int* __restrict__ tot,
                                                             int* __restrict__ offsets, int* __restrict__ R_out,
                                                             long long R_cap, int* __restrict__ flags) {
@@ -23,29 +114,25 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restri
     const int* src = blk_cnt + (long long)e * nblk;
     int* dst = blk_base + (long long)e * nblk;
     int carry = 0;
-    // chunks of 1024 block counts: all 32 coalesced loads of a lane issued before any use (one
-    // memory round trip per chunk, not one per 128 entries); block b0 + 32 j + lane sits in v[j],
-    // row j is scanned across the lanes and the rows are chained through the carry
-    for (int b0 = 0; b0 < nblk; b0 += 1024) {
-      int v[32];
+    for (int b0 = 0; b0 < nblk; b0 += 128) {
+      const int b = b0 + lane * 4;
+      int v[4];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int b = b0 + 32 * j + lane;
-        v[j] = b < nblk ? src[b] : 0;
+      for (int q = 0; q < 4; ++q) v[q] = (b + q < nblk) ? src[b + q] : 0;
+      const int lsum = v[0] + v[1] + v[2] + v[3];
+      int inc = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int n = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += n;
       }
+      int run = carry + inc - lsum;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (b0 + 32 * j >= nblk) break;                 // warp-uniform
-        int inc = v[j];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int n = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += n;
-        }
-        const int b = b0 + 32 * j + lane;
-        if (b < nblk) dst[b] = carry + inc - v[j];
-        carry += __shfl_sync(0xffffffffu, inc, 31);
+      for (int q = 0; q < 4; ++q) {
+        if (b + q < nblk) dst[b + q] = run;
+        run += v[q];
       }
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
     if (lane == 0) s_tot[e] = carry;
   }
@@ -64,6 +151,16 @@ __global__ void __launch_bounds__(1024) dispatch_scan_kernel(const int* __restri
       flags[2] = (int)off;
     }
   }
+}
+
+// per-block bases + 128-aligned expert offsets from the gate's per-block counts
+static void launch_dispatch_scan(const moe_ctx* c, int* offsets, int* R_out, long long R_cap, cudaStream_t s) {
+  if (c->nblk <= kScanSmallBlocks)
+    dispatch_scan_small_kernel<<<1, 1024, 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot, offsets, R_out, R_cap,
+                                                  c->flags), count_launch();
+  else
+    dispatch_scan_kernel<<<c->E, scan_threads(c->nblk), 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot,
+                                                                 offsets, R_out, R_cap, c->flags), count_launch();
 }
 
 // ------------------------------------------------------------------ permute
@@ -235,6 +332,11 @@ __device__ __forceinline__ void gather_sum_token(const Src& src, const int* __re
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
   constexpr bool TWO = QV <= 3;                     // two rows in flight when registers allow
+  // the whole slot row (E <= 128: up to 4 entries per lane) loaded once, up front: one memory
+  // round trip per token instead of one per 32 experts and pass
+  int svs[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) svs[i] = (32 * i < E && 32 * i + lane < E) ? slot_row[32 * i + lane] : -1;
   for (int v0 = 0; v0 < nvec; v0 += 32 * QV) {
     float acc[QV][V];
 #pragma unroll
@@ -256,8 +358,11 @@ __device__ __forceinline__ void gather_sum_token(const Src& src, const int* __re
         }
       }
     }
-    for (int g = 0; g < E; g += 32) {
-      const int sv = (g + lane < E) ? slot_row[g + lane] : -1;
+#pragma unroll
+    for (int gi = 0; gi < 4; ++gi) {
+      const int g = 32 * gi;
+      if (g >= E) break;                               // warp-uniform
+      const int sv = svs[gi];
       unsigned bal = __ballot_sync(0xffffffffu, sv >= 0);
       while (bal) {
         // two selected rows per pass (both rows' loads in flight), accumulated in ascending e
@@ -944,8 +1049,7 @@ cudaError_t launch_spawn(const moe_ctx* c, const void* W1s, const void* b1s, con
 cudaError_t launch_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot,
                             const int32_t* /*counts*/, void* x_perm, int32_t* row_token, float* row_gate,
                             int32_t* offsets, int64_t R_cap, int32_t* R_out, cudaStream_t s) {
-  dispatch_scan_kernel<<<1, 1024, 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot, offsets, R_out, R_cap,
-                                          c->flags), count_launch();
+  launch_dispatch_scan(c, offsets, R_out, R_cap, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || c->nblk == 0) return e;
   if (c->dtype == 1) {
@@ -1121,8 +1225,7 @@ cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* pr
                                 const PeerTable& rtok, const PeerTable& rsrc, const PeerTable& rgate, int64_t R_cap,
                                 cudaStream_t s) {
   // per-block ranks (scan over this rank's token blocks; the local layout itself is not built)
-  dispatch_scan_kernel<<<1, 1024, 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot, c->ep2_scr,
-                                          c->ep2_scr + c->E + 1, (long long)1 << 62, c->flags), count_launch();
+  launch_dispatch_scan(c, c->ep2_scr, c->ep2_scr + c->E + 1, (long long)1 << 62, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || c->nblk == 0) return e;
   ep2_rank_kernel<false><<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->world,
@@ -1210,8 +1313,7 @@ cudaError_t launch_ep2d_dispatch(const moe_ctx* c, const void* x, const float* p
                                  const PeerTable& tb, const PeerTable& urows, const PeerTable& rtok,
                                  const PeerTable& rsrc, const PeerTable& rgate, const PeerTable& ruid, int64_t R_cap,
                                  cudaStream_t s) {
-  dispatch_scan_kernel<<<1, 1024, 0, s>>>(c->blk_cnt, c->nblk, c->E, c->blk_base, c->tot, c->ep2_scr,
-                                          c->ep2_scr + c->E + 1, (long long)1 << 62, c->flags), count_launch();
+  launch_dispatch_scan(c, c->ep2_scr, c->ep2_scr + c->E + 1, (long long)1 << 62, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || c->nblk == 0) return e;
   ep2_rank_kernel<true><<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->world,
