@@ -131,6 +131,7 @@ struct TcParams {
   long long ldo_b;
   float* colpart;         // TEPI_GELU_BWD: per-32-row column sums of da [R_cap/32][N] (bias gradient db1)
   unsigned long long* trace;   // MOE_EXP_TRACE builds only: per-warp event log of CTAs 0 and 1
+  int a3d, b3d;           // MN-major operand given as a 3D map {64, K rows, MN / 64}: one TMA op per stage
 };
 
 #ifdef MOE_EXP_TRACE
@@ -273,12 +274,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS
           const int k = (tl.kb0 + kb) * BK;
           if (!A_MN) {
             tc::tma_load_2d_pair(sa, &tmA, bar, k, tl.m_own);
+          } else if (p.a3d) {                      // both 64-wide MN chunks ([chunk][k][64]) in one op
+            tc::tma_load_3d_pair(sa, &tmA, bar, 0, k, tl.m_own / 64);
           } else {
             tc::tma_load_2d_pair(sa, &tmA, bar, tl.m_own, k);
             tc::tma_load_2d_pair(sa + 8192, &tmA, bar, tl.m_own + 64, k);
           }
           if (!B_MN) {
             tc::tma_load_2d_pair(sb, &tmB, bar, k, brow + n_own);
+          } else if (p.b3d) {
+            tc::tma_load_3d_pair(sb, &tmB, bar, 0, brow + k, n_own / 64);
           } else {
             tc::tma_load_2d_pair(sb, &tmB, bar, n_own, brow + k);
             tc::tma_load_2d_pair(sb + 8192, &tmB, bar, n_own + 64, brow + k);
@@ -635,6 +640,26 @@ bool make_map(CUtensorMap* m, const void* ptr, long long rows, long long cols, l
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+// MN-major operand as a 3D map {64 (MN, inner), rows (K), cols / 64 (MN chunk)}, box {64, 64, 2}:
+// one TMA op fills the [chunk][k][64] stage layout of two 2D boxes.  Only when cols % 64 == 0
+// (a partial last chunk would read past the row end instead of being zero-filled); returns
+// false otherwise and the caller keeps the 2D map.
+bool make_map_mn3d(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long pitch) {
+  EncodeTiledFn f = encode_fn();
+  if (!f || !ptr || cols % 64 != 0 || getenv("MOE_NO_MN3D")) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, 128};
+  cuuint32_t box[3] = {64, 64, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// MN-major operand map: 3D when possible (flag set), else the 2D {64, 64} box map
+bool make_map_mn(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long pitch, int& is3d) {
+  is3d = make_map_mn3d(m, ptr, rows, cols, pitch) ? 1 : 0;
+  return is3d || make_map(m, ptr, rows, cols, pitch, 64, 64);
+}
 bool make_store_map(CUtensorMap* m, const void* ptr, long long rows, long long cols) {
   return make_map(m, ptr, rows, cols, cols, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
 }
@@ -799,7 +824,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
     TcParams p{};
     p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
     // dgrad2: da = (d_eout W2_e) (.) GELU'(a)   A = d_eout [R, d] K-major; B(k=d, n=f) = W2 [El*d, f] MN-major
-    if (!make_map(&mA, d_eout, R_cap, d, d, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, 64) ||
+    if (!make_map(&mA, d_eout, R_cap, d, d, 64, BM) || !make_map_mn(&mB, W2, (long long)El * d, f, f, p.b3d) ||
         !make_store_map(&mO, da, R_cap, f) || !make_store_map(&mX, gp, R_cap, f))
       return cudaErrorInvalidValue;
     p.N = f; p.K = d; p.b_group_rows = d;
@@ -819,7 +844,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
     }
     p.colpart = nullptr;
     // dgrad1: dx_perm = da W1_e                 A = da [R, f] K-major; B(k=f, n=d) = W1 [El*f, d] MN-major
-    if (!make_map(&mA, da, R_cap, f, f, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, 64) ||
+    if (!make_map(&mA, da, R_cap, f, f, 64, BM) || !make_map_mn(&mB, W1, (long long)El * f, d, d, p.b3d) ||
         !make_store_map(&mO, dx_perm, R_cap, d))
       return cudaErrorInvalidValue;
     p.N = d; p.K = f; p.b_group_rows = f;
@@ -830,7 +855,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
   // wgrad2: dW2_e [d, f] = d_eout_e^T h_e       A(m=d, k=row) = d_eout MN-major; B(k=row, n=f) = h MN-major
   TcParams q{};
   q.G = El; q.offsets = offsets; q.rows_cap = (int)R_cap;
-  if (!make_map(&mA, d_eout, R_cap, d, d, 64, 64) || !make_map(&mB, h, R_cap, f, f, 64, 64))
+  if (!make_map_mn(&mA, d_eout, R_cap, d, d, q.a3d) || !make_map_mn(&mB, h, R_cap, f, f, q.b3d))
     return cudaErrorInvalidValue;
   q.M = d; q.N = f; q.out = dW2; q.ldo = f; q.out_g = (long long)d * f;
   if (!make_store_map_f32(&mO, dW2, (long long)El * d, f)) return cudaErrorInvalidValue;
@@ -838,7 +863,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
                                             (long long)El * ((d + 255) / 256) * ((f + BN - 1) / BN), c->sm_count, s);
   if (e != cudaSuccess) return e;
   // wgrad1: dW1_e [f, d] = da_e^T x_perm_e      A(m=f, k=row) = da MN-major; B(k=row, n=d) = x_perm MN-major
-  if (!make_map(&mA, da, R_cap, f, f, 64, 64) || !make_map(&mB, x_perm, R_cap, d, d, 64, 64))
+  if (!make_map_mn(&mA, da, R_cap, f, f, q.a3d) || !make_map_mn(&mB, x_perm, R_cap, d, d, q.b3d))
     return cudaErrorInvalidValue;
   q.M = f; q.N = d; q.out = dW1; q.ldo = d; q.out_g = (long long)f * d;
   if (!make_store_map_f32(&mO, dW1, (long long)El * f, d)) return cudaErrorInvalidValue;
