@@ -349,11 +349,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS
     uint32_t seq = 0;                                   // this warp's chunk sequence number (nch per tile)
 
     // GELU' operand: TMA-load a[rows, 32 cols] two chunks ahead into the staging buffers
+    // the decoded tile is cached: consecutive sequence numbers stay on one tile for nch chunks,
+    // so the expert search runs once per tile, not once per chunk (lane 0's chunk critical path)
+    int aux_t = -1;
+    Tile tn{};
     auto aux_issue = [&](uint32_t s) {
       const int t = cid + (int)(s / nch) * ncl;
       if (t >= total) return;
-      Tile tn;
-      decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tn);
+      if (t != aux_t) {
+        decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tn);
+        aux_t = t;
+      }
       const int col = tn.n0 + (part + EPI_PER_Q * (int)(s % nch)) * 32;
       const uint32_t b = s % Cfg::NBUF;
       tc::mbar_arrive_expect_tx_u32(auxb + b * 8, CHUNK_BYTES);
