@@ -89,9 +89,9 @@ enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 
 #ifndef MOE_NB_F32
 #define MOE_NB_F32 1
 #endif
-template <int EPI> struct EpiCfg {
+template <int EPI, int QOV = 0> struct EpiCfg {   // QOV: epilogue warps per quarter override (0 = the kind's default)
   // thread = accumulator row; epilogue warp (quarter q, part j) owns chunks j, j + PER_Q, ... of the 8 x 32 columns
-  static constexpr int PER_Q = EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_EPQ_GELU
+  static constexpr int PER_Q = QOV ? QOV : EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_EPQ_GELU
                                : EPI == TEPI_BIAS ? MOE_EPQ_BIAS
                                : EPI == TEPI_GELU_BWD ? MOE_EPQ_GBWD
                                : EPI == TEPI_STORE ? MOE_EPQ_STORE : MOE_EPQ_F32;
@@ -182,12 +182,12 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, const int* s_off,
   return tl.nkb > 0;
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool KGRP>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI>::THREADS, 1)
+template <int EPI, bool A_MN, bool B_MN, bool KGRP, int QOV = 0>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmO1, const __grid_constant__ CUtensorMap tmO2,
                    const __grid_constant__ CUtensorMap tmX, TcParams p) {
-  using Cfg = EpiCfg<EPI>;
+  using Cfg = EpiCfg<EPI, QOV>;
   constexpr int STAGES = Cfg::STAGES;
   constexpr int EPI_PER_Q = Cfg::PER_Q, EPI_WARPS = Cfg::WARPS, NUM_THREADS = Cfg::THREADS;
   extern __shared__ uint8_t smem_raw[];
@@ -682,11 +682,11 @@ bool make_store_map_f32(CUtensorMap* m, const void* ptr, long long rows, long lo
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int EPI, bool A_MN, bool B_MN, bool KGRP>
+template <int EPI, bool A_MN, bool B_MN, bool KGRP, int QOV = 0>
 cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& o1, const CUtensorMap& o2,
                       const CUtensorMap& x, const TcParams& p, long long tiles_upper, int sms, cudaStream_t s) {
-  auto k = tc_gemm_kernel<EPI, A_MN, B_MN, KGRP>;
-  constexpr int smem = EpiCfg<EPI>::SMEM;
+  auto k = tc_gemm_kernel<EPI, A_MN, B_MN, KGRP, QOV>;
+  constexpr int smem = EpiCfg<EPI, QOV>::SMEM;
   static_assert(smem <= SMEM_LIMIT, "shared memory budget");
   static bool attr = false;
   if (!attr) {
@@ -718,9 +718,9 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
       if (fp) { fwrite(sbuf, 8, 2 * 16 * (size_t)kTraceN, fp); fclose(fp); }
     });
   }
-  k<<<(unsigned)(2 * pairs), EpiCfg<EPI>::THREADS, smem, s>>>(a, b, o1, o2, x, pt), count_launch();
+  k<<<(unsigned)(2 * pairs), EpiCfg<EPI, QOV>::THREADS, smem, s>>>(a, b, o1, o2, x, pt), count_launch();
 #else
-  k<<<(unsigned)(2 * pairs), EpiCfg<EPI>::THREADS, smem, s>>>(a, b, o1, o2, x, p), count_launch();
+  k<<<(unsigned)(2 * pairs), EpiCfg<EPI, QOV>::THREADS, smem, s>>>(a, b, o1, o2, x, p), count_launch();
 #endif
   return cudaGetLastError();
 }
@@ -838,8 +838,13 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
     // db1 partials live in dx_perm's memory until dgrad1 overwrites it ([R_cap/32][f] fp32 <= R_cap x d bf16)
     const bool fuse_db1 = db1 && (long long)f * 4 <= (long long)d * 2 * 32;
     p.colpart = fuse_db1 ? reinterpret_cast<float*>(dx_perm) : nullptr;
-    e = launch_tc<TEPI_GELU_BWD, false, true, false>(mA, mB, mO, mO, mX, p, up * ((f + BN - 1) / BN),
-                                                     c->sm_count, s);
+    // 2 epilogue warps per lane quarter from d = 768 up (smaller staging -> 5 operand stages instead
+    // of 4: dgrad2 -6% cycles at C2 / C3, -9% at C4), 3 below (C5's d = 512: +17% with 2;
+    // profiles/r01/s2/ab_epilogue_components.txt)
+    e = d >= 768 ? launch_tc<TEPI_GELU_BWD, false, true, false, 2>(mA, mB, mO, mO, mX, p, up * ((f + BN - 1) / BN),
+                                                                   c->sm_count, s)
+                 : launch_tc<TEPI_GELU_BWD, false, true, false>(mA, mB, mO, mO, mX, p, up * ((f + BN - 1) / BN),
+                                                                c->sm_count, s);
     if (e != cudaSuccess) return e;
     if (fuse_db1) {
       if ((e = launch_db1_reduce(reinterpret_cast<const float*>(dx_perm), f, offsets, El, db1, c->colpart, R_cap, s)) !=
