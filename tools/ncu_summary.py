@@ -34,7 +34,7 @@ def main():
         name = r[hdr.index("Kernel Name")]
         mt = re.search(r"tc_gemm_kernel(<[^>]*>)", name)
         tmpl = mt.group(1) if mt else name
-        kern.append({"kernel": "tc_gemm_kernel" + tmpl, "role": ROLE.get(tmpl, "?"),
+        kern.append({"kernel": "tc_gemm_kernel" + tmpl, "role": ROLE.get(tmpl, ROLE.get(re.sub(r", \d+>$", ">", tmpl), "?")),   # 5th parameter: epilogue warp override
                      "us": d[MET[0]], "dram_read_bytes": d[MET[1]], "dram_write_bytes": d[MET[2]],
                      "tensor_pipe_pct": d[MET[3]], "sm_throughput_pct": d[MET[4]]})
     experts = [k for k in kern if not k["role"].startswith("gate")]
