@@ -21,6 +21,12 @@
  *  - Device-detected faults (non-finite gate logits -> MOE_ENONFINITE, row capacity
  *    exceeded -> MOE_ECAPACITY) set a flag in the workspace; they are returned by
  *    moe_check(), which synchronises `stream`.
+ *  - No hidden state between calls, with ONE documented exception: moe_dts_gate leaves per-block
+ *    expert counts in the workspace for the moe_dispatch / moe_ep2(d)_dispatch that consumes its
+ *    (probs, slot); those calls return MOE_EINVAL for any other (probs, slot) pair (the ctx
+ *    records the pointers of the most recent moe_dts_gate).  Every other value that flows from
+ *    one call to the next is an explicit argument (db2 out of moe_combine_bwd, dx out of
+ *    moe_dts_gate_bwd into an accumulating moe_dispatch_bwd).
  *  - Expert-major permuted ("row") layout: rows of expert e occupy
  *    [offsets[e], offsets[e] + counts[e]) in ascending token order (stable), followed
  *    by zero pad rows up to offsets[e+1]; offsets[e] is a multiple of 128
@@ -37,7 +43,7 @@
 extern "C" {
 #endif
 
-#define MOE_ABI_VERSION 1
+#define MOE_ABI_VERSION 2
 #define MOE_ROW_ALIGN 128
 
 typedef enum {
@@ -116,7 +122,9 @@ int moe_dts_gate(moe_ctx* ctx, const void* x, const void* Wg, const float* u, fl
                  int32_t* near_band, void* stream);
 
 /* Dispatch, step 4 (Alg. 1 lines 9-12 P:299-304; EP P:227).  Uses the per-block
- * counts left in the workspace by the preceding moe_dts_gate on the same stream.
+ * counts left in the workspace by the preceding moe_dts_gate on the same stream; probs and
+ * slot must be that call's outputs, unmodified (else MOE_EINVAL: "not the outputs of the most
+ * recent moe_dts_gate").
  * Writes offsets [E+1] int32 (128-aligned exclusive prefix of counts), fills
  * slot[t,e] with the row index, row_token [R_cap] int32 (-1 on pad rows),
  * row_gate [R_cap] fp32 (= probs[t,e]; 0 on pads), x_perm [R_cap, d] D (copy of x_t;
@@ -157,17 +165,23 @@ int moe_combine(moe_ctx* ctx, const void* e_out, const float* row_gate, const in
 
 /* Combine backward (chain rule of Eq. 7).  For every row r < offsets[E]:
  *   t = row_token[r];  d_eout[r] = row_gate[r] * dy[t];  dG_row[r] = <dy[t], e_out[r]>
- * (0 for pad rows).  dy [T, d] D; d_eout [R_cap, d] D; dG_row [R_cap] fp32. */
+ * (0 for pad rows).  dy [T, d] D; d_eout [R_cap, d] D; dG_row [R_cap] fp32.
+ * db2 [E, d] fp32 (optional, NULL = not computed): the per-expert column sums of the d_eout
+ * rows this call stores (= the expert FFN's b2 gradient, chain rule of Eq. 3), fused into the
+ * same pass; pass db2 = NULL to moe_expert_ffn_bwd then.  Single-rank ctx only (MOE_EINVAL
+ * under the NCCL exchange, where db2 is an expert-side sum over the received rows). */
 int moe_combine_bwd(moe_ctx* ctx, const void* dy, const void* e_out, const float* row_gate,
                     const int32_t* row_token, const int32_t* offsets, int64_t R_cap,
-                    void* d_eout, float* dG_row, void* stream);
+                    void* d_eout, float* dG_row, float* db2, void* stream);
 
 /* Expert FFN backward (chain rule of Eq. 3).  Per expert e over its rows:
  *   dh = d_eout W2[e];  da = dh (.) gp   (gp = GELU'(a) saved by moe_expert_ffn)
  *   dW2[e] = d_eout^T h;  db2[e] = colsum(d_eout);  dW1[e] = da^T x_perm;  db1[e] = colsum(da)
  *   dx_perm = da W1[e]
  * da [R_cap, d_ff] D may ALIAS gp_saved (overwritten in place).  dW1 [E_local, d_ff, d],
- * db1 [E_local, d_ff], dW2 [E_local, d, d_ff], db2 [E_local, d] fp32 (overwritten). */
+ * db1 [E_local, d_ff], dW2 [E_local, d, d_ff], db2 [E_local, d] fp32 (overwritten).  db2 may be
+ * NULL (it was taken from moe_combine_bwd); otherwise it is summed from the d_eout given here,
+ * with the same partition and order as moe_combine_bwd's (bit-identical). */
 int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, const void* gp_saved,
                        const void* h_saved, const int32_t* offsets, int64_t R_cap,
                        const void* W1, const void* W2, void* da, void* dx_perm,
@@ -177,17 +191,19 @@ int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, con
  *   dp_e = m_e dG[slot[t,e]] (+ balance term alpha N count_e / B^2 if balance_alpha > 0,
  *          Eq. 10, counts = global counts, B = global batch size)
  *   dz = p (.) (dp - <p, dp>);  dlogits = dz / tau;   dWg = x^T dlogits  (fp32, [d, E])
- * dlogits [T, E] fp32 is an output consumed by moe_dispatch_bwd (which adds
- * dlogits W_g^T to dx).  counts may be NULL when balance_alpha == 0. */
+ *   dx = dlogits W_g^T  (D, [T, d]; written when dx != NULL, Wg [d, E] then required)
+ * dlogits [T, E] fp32 is an output.  counts may be NULL when balance_alpha == 0.  The expert
+ * path's input gradient is then added onto dx by moe_dispatch_bwd(accumulate = 1). */
 int moe_dts_gate_bwd(moe_ctx* ctx, const float* dG_row, const int32_t* slot, const float* probs,
-                     const void* x, float tau, float balance_alpha, const int32_t* counts,
-                     int64_t B_total, float* dWg, float* dlogits, void* stream);
+                     const void* x, const void* Wg, float tau, float balance_alpha, const int32_t* counts,
+                     int64_t B_total, float* dWg, float* dlogits, void* dx, void* stream);
 
-/* Dispatch backward (inverse of step 4) fused with the gate's input gradient:
- *   dx[t] = sum over selected e in ASCENDING e of dx_perm[slot[t,e]]  +  dlogits[t] W_g^T
- * dx [T, d] D (overwritten).  dlogits may be NULL (then Wg is unused). */
-int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, const float* dlogits,
-                     const void* Wg, void* dx, void* stream);
+/* Dispatch backward (inverse of step 4):
+ *   dx[t] = (accumulate ? dx[t] : 0) + sum over selected e in ASCENDING e of dx_perm[slot[t,e]]
+ * accumulated in fp32 from the stored dx row, stored as D.  With accumulate = 1 after
+ * moe_dts_gate_bwd(dx) this is the layer's full input gradient. */
+int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, int accumulate, void* dx,
+                     void* stream);
 
 /* ---------------------------------------------------------------- expert parallelism */
 /* EP (GShard-style): E/world experts per rank (global ids rank*E_local ...),
@@ -195,8 +211,8 @@ int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, con
  * moe_ep_plan -> moe_ep_upload -> moe_dispatch (token side, "send" layout over all E
  * experts) -> moe_ep_dispatch (send -> expert side "recv" layout) -> moe_expert_ffn on the
  * recv layout -> moe_ep_combine (recv -> send) -> moe_combine.  Backward mirrors it:
- * combine_bwd -> moe_ep_dispatch(d_eout) -> expert_ffn_bwd -> moe_ep_combine(dx_perm) ->
- * gate_bwd -> moe_ep_allreduce(dWg) -> dispatch_bwd.
+ * combine_bwd(db2 = NULL) -> moe_ep_dispatch(d_eout) -> expert_ffn_bwd(db2) -> moe_ep_combine(dx_perm)
+ * -> gate_bwd(dx) -> moe_ep_allreduce(dWg) -> dispatch_bwd(accumulate = 1).
  * Recv layout: local expert j occupies [offsets_recv[j], offsets_recv[j+1]) (128-aligned);
  * inside it the rows of source rank 0, 1, ... in order (ascending global token index);
  * pad rows are zeroed by moe_ep_dispatch.  Messages: one ncclSend/ncclRecv per
@@ -273,9 +289,11 @@ int moe_ep_allreduce(moe_ctx* ctx, void* buf, int64_t n, int is_int32, void* str
  *   the owner; copy: x rows stored into the owners' x_recv) -> barrier -> moe_expert_ffn on
  *   x_recv -> barrier -> moe_ep2_combine (token side gathers e_out rows from the owners).
  *   Backward: barrier -> moe_ep2_combine_bwd (expert side reads dy rows from the token
- *   owners; d_eout, dG_row and the db2 partials locally) -> moe_expert_ffn_bwd -> barrier ->
- *   moe_ep2_gate_bwd (dG from the owners) -> moe_ep_allreduce(dWg) -> moe_ep2_dispatch_bwd
- *   (dx_perm rows from the owners).
+ *   owners; d_eout, dG_row and db2 locally) -> moe_expert_ffn_bwd(db2 = NULL) -> barrier ->
+ *   moe_ep2_gate_bwd (dG from the owners; dx = dlogits W_g^T) -> moe_ep_allreduce(dWg) ->
+ *   moe_ep2_dispatch_bwd(accumulate = 1) (dx_perm rows from the owners).
+ * moe_ep2_gate_bwd's balance term takes counts_all [world][E] (this rank's copy, filled by
+ * moe_ep2_counts): the kernel sums the rows, i.e. uses the GLOBAL counts of Eq. 10.
  * Layouts (recv layout of each rank, expert-major, sources in rank order) and results equal
  * the NCCL path's and, for the global token set, the single-rank layer's.  No host sync:
  * R_recv_cap is a static capacity, a multiple of 128 (worst case world*T*E_local + 127*E_local,
@@ -297,12 +315,12 @@ int moe_ep2_combine(moe_ctx* ctx, void* const* e_out_peers, const float* probs, 
                     void* stream);
 int moe_ep2_combine_bwd(moe_ctx* ctx, void* const* dy_peers, const void* e_out, const float* rgate,
                         const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets_recv, int64_t R_recv_cap,
-                        void* d_eout, float* dG_row, void* stream);
+                        void* d_eout, float* dG_row, float* db2, void* stream);
 int moe_ep2_gate_bwd(moe_ctx* ctx, float* const* dG_peers, const int32_t* slot, const float* probs, const void* x,
-                     float tau, float balance_alpha, const int32_t* counts, int64_t B_total, float* dWg,
-                     float* dlogits, void* stream);
-int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t* slot, const float* dlogits,
-                         const void* Wg, void* dx, void* stream);
+                     const void* Wg, float tau, float balance_alpha, const int32_t* counts_all, int64_t B_total,
+                     float* dWg, float* dlogits, void* dx, void* stream);
+int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t* slot, int accumulate, void* dx,
+                         void* stream);
 
 /* ---------------------------------------------------------------- ep2 with token dedup ("ep2d")
  * SURVEY §8(e) "Dedup": a token is sent ONCE to every GPU owning any of its selected
@@ -320,9 +338,9 @@ int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t
  *   rounded to D) -> barrier -> moe_ep2d_combine (token side: y = sum_{q asc} ysum@q[uslot]).
  * Backward: dy staged in a symmetric buffer -> barrier -> moe_ep2d_gather_dy (expert side:
  *   dyu[u] = dy@s[t], one read per (token, owner)) -> moe_ep2d_combine_bwd (d_eout, dG, db2
- *   partials from dyu) -> moe_expert_ffn_bwd -> moe_ep2d_presum(dx_perm, NULL) -> dxu ->
- *   barrier -> moe_ep2_gate_bwd -> moe_ep_allreduce(dWg) -> moe_ep2d_dispatch_bwd (token side:
- *   dx = dL W_g^T + sum_{q asc} dxu@q[uslot]).
+ *   from dyu) -> moe_expert_ffn_bwd(db2 = NULL) -> moe_ep2d_presum(dx_perm, NULL) -> dxu ->
+ *   barrier -> moe_ep2_gate_bwd(dx = dL W_g^T) -> moe_ep_allreduce(dWg) ->
+ *   moe_ep2d_dispatch_bwd(accumulate = 1) (token side: dx += sum_{q asc} dxu@q[uslot]).
  * Routing, d_eout, dG, dlogits and the expert weight gradients equal the non-dedup path's bit
  * for bit; y and dx differ by the rounding of the per-owner partial sums to D (one extra
  * rounding per owner, ~2^-9 relative for bf16). */
@@ -340,9 +358,10 @@ int moe_ep2d_presum(moe_ctx* ctx, const void* rows, const float* rgate_or_null, 
 int moe_ep2d_gather_dy(moe_ctx* ctx, void* const* dy_peers, const int32_t* urows, void* dyu, void* stream);
 int moe_ep2d_combine(moe_ctx* ctx, void* const* ysum_peers, const int32_t* uslot, void* y, void* stream);
 int moe_ep2d_combine_bwd(moe_ctx* ctx, const void* dyu, const void* e_out, const float* rgate, const int32_t* ruid,
-                         const int32_t* offsets_recv, int64_t R_recv_cap, void* d_eout, float* dG_row, void* stream);
-int moe_ep2d_dispatch_bwd(moe_ctx* ctx, void* const* dxu_peers, const int32_t* uslot, const float* dlogits,
-                          const void* Wg, void* dx, void* stream);
+                         const int32_t* offsets_recv, int64_t R_recv_cap, void* d_eout, float* dG_row, float* db2,
+                         void* stream);
+int moe_ep2d_dispatch_bwd(moe_ctx* ctx, void* const* dxu_peers, const int32_t* uslot, int accumulate, void* dx,
+                          void* stream);
 
 /* ---------------------------------------------------------------- NEXT #1 */
 

@@ -36,10 +36,10 @@ SIGNATURES = {
     "moe_expert_ffn": (_I, [_P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P]),
     "moe_expert_ffn_recompute": (_I, [_P, _P, _P, _L, _P, _P, _P, _P, _P]),
     "moe_combine": (_I, [_P, _P, _P, _P, _P, _P]),
-    "moe_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
+    "moe_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P]),
     "moe_expert_ffn_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
-    "moe_dts_gate_bwd": (_I, [_P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P]),
-    "moe_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "moe_dts_gate_bwd": (_I, [_P, _P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P, _P]),
+    "moe_dispatch_bwd": (_I, [_P, _P, _P, _I, _P, _P]),
     "moe_balance_loss": (_I, [_P, _P, _P, _F, _L, _P, _P]),
     "moe_nccl_unique_id": (_I, [_P, _S]),
     "moe_nccl_comm_init": (_I, [C.POINTER(_P), _P, _I, _I]),
@@ -62,16 +62,16 @@ SIGNATURES = {
     "moe_ep2_prepare_recv": (_I, [_P, _P, _P, _P, _P, _L, _P]),
     "moe_ep2_dispatch": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _P]),
     "moe_ep2_combine": (_I, [_P, _P, _P, _P, _P, _P]),
-    "moe_ep2_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
-    "moe_ep2_gate_bwd": (_I, [_P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P]),
-    "moe_ep2_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "moe_ep2_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P]),
+    "moe_ep2_gate_bwd": (_I, [_P, _P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P, _P]),
+    "moe_ep2_dispatch_bwd": (_I, [_P, _P, _P, _I, _P, _P]),
     "moe_ep2d_dispatch": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _L, _P]),
     "moe_ep2d_permute": (_I, [_P, _P, _P, _P, _L, _P, _P]),
     "moe_ep2d_presum": (_I, [_P, _P, _P, _P, _P, _P]),
     "moe_ep2d_gather_dy": (_I, [_P, _P, _P, _P, _P]),
     "moe_ep2d_combine": (_I, [_P, _P, _P, _P, _P]),
-    "moe_ep2d_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P]),
-    "moe_ep2d_dispatch_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "moe_ep2d_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P]),
+    "moe_ep2d_dispatch_bwd": (_I, [_P, _P, _P, _I, _P, _P]),
 }
 MOE_COMM_EMULATED = 1   # moe_create(nccl_comm=MOE_COMM_EMULATED): single-process emulation of `world` ranks
 
@@ -193,9 +193,9 @@ def moe_combine(ctx, e_out, row_gate, slot, y, stream=None):
     _call("moe_combine", ctx, _ptr(e_out), _ptr(row_gate), _ptr(slot), _ptr(y), _stream(stream))
 
 
-def moe_combine_bwd(ctx, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, stream=None):
+def moe_combine_bwd(ctx, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, db2=None, stream=None):
     _call("moe_combine_bwd", ctx, _ptr(dy), _ptr(e_out), _ptr(row_gate), _ptr(row_token), _ptr(offsets),
-          int(R_cap), _ptr(d_eout), _ptr(dG_row), _stream(stream))
+          int(R_cap), _ptr(d_eout), _ptr(dG_row), _ptr(db2), _stream(stream))
 
 
 def moe_expert_ffn_bwd(ctx, d_eout, x_perm, a_saved, h_saved, offsets, R_cap, W1, W2, da, dx_perm,
@@ -205,15 +205,14 @@ def moe_expert_ffn_bwd(ctx, d_eout, x_perm, a_saved, h_saved, offsets, R_cap, W1
           _ptr(dW2), _ptr(db2), _stream(stream))
 
 
-def moe_dts_gate_bwd(ctx, dG_row, slot, probs, x, tau, balance_alpha, counts, B_total, dWg, dlogits,
+def moe_dts_gate_bwd(ctx, dG_row, slot, probs, x, Wg, tau, balance_alpha, counts, B_total, dWg, dlogits, dx=None,
                      stream=None):
-    _call("moe_dts_gate_bwd", ctx, _ptr(dG_row), _ptr(slot), _ptr(probs), _ptr(x), float(tau),
-          float(balance_alpha), _ptr(counts), int(B_total), _ptr(dWg), _ptr(dlogits), _stream(stream))
+    _call("moe_dts_gate_bwd", ctx, _ptr(dG_row), _ptr(slot), _ptr(probs), _ptr(x), _ptr(Wg), float(tau),
+          float(balance_alpha), _ptr(counts), int(B_total), _ptr(dWg), _ptr(dlogits), _ptr(dx), _stream(stream))
 
 
-def moe_dispatch_bwd(ctx, dx_perm, slot, dlogits, Wg, dx, stream=None):
-    _call("moe_dispatch_bwd", ctx, _ptr(dx_perm), _ptr(slot), _ptr(dlogits), _ptr(Wg), _ptr(dx),
-          _stream(stream))
+def moe_dispatch_bwd(ctx, dx_perm, slot, accumulate, dx, stream=None):
+    _call("moe_dispatch_bwd", ctx, _ptr(dx_perm), _ptr(slot), int(bool(accumulate)), _ptr(dx), _stream(stream))
 
 
 def moe_balance_loss(ctx, probs, counts, alpha, B_total, loss, stream=None):
@@ -370,22 +369,23 @@ def moe_ep2_combine(ctx, e_out_peers, probs, slot, y, stream=None):
 
 
 def moe_ep2_combine_bwd(ctx, dy_peers, e_out, rgate, rtok, rsrc, offsets_recv, R_recv_cap: int, d_eout, dG_row,
-                        stream=None):
+                        db2=None, stream=None):
     a, ka = _peers(dy_peers)
     _call("moe_ep2_combine_bwd", ctx, a, _ptr(e_out), _ptr(rgate), _ptr(rtok), _ptr(rsrc), _ptr(offsets_recv),
-          int(R_recv_cap), _ptr(d_eout), _ptr(dG_row), _stream(stream))
+          int(R_recv_cap), _ptr(d_eout), _ptr(dG_row), _ptr(db2), _stream(stream))
 
 
-def moe_ep2_gate_bwd(ctx, dG_peers, slot, probs, x, tau: float, balance_alpha: float, counts, B_total: int, dWg,
-                     dlogits, stream=None):
+def moe_ep2_gate_bwd(ctx, dG_peers, slot, probs, x, Wg, tau: float, balance_alpha: float, counts_all, B_total: int,
+                     dWg, dlogits, dx=None, stream=None):
+    """counts_all: this rank's [world, E] copy of the all-gathered counts (global counts = column sums)."""
     a, ka = _peers(dG_peers)
-    _call("moe_ep2_gate_bwd", ctx, a, _ptr(slot), _ptr(probs), _ptr(x), float(tau), float(balance_alpha),
-          _ptr(counts), int(B_total), _ptr(dWg), _ptr(dlogits), _stream(stream))
+    _call("moe_ep2_gate_bwd", ctx, a, _ptr(slot), _ptr(probs), _ptr(x), _ptr(Wg), float(tau), float(balance_alpha),
+          _ptr(counts_all), int(B_total), _ptr(dWg), _ptr(dlogits), _ptr(dx), _stream(stream))
 
 
-def moe_ep2_dispatch_bwd(ctx, dx_perm_peers, slot, dlogits, Wg, dx, stream=None):
+def moe_ep2_dispatch_bwd(ctx, dx_perm_peers, slot, accumulate, dx, stream=None):
     a, ka = _peers(dx_perm_peers)
-    _call("moe_ep2_dispatch_bwd", ctx, a, _ptr(slot), _ptr(dlogits), _ptr(Wg), _ptr(dx), _stream(stream))
+    _call("moe_ep2_dispatch_bwd", ctx, a, _ptr(slot), int(bool(accumulate)), _ptr(dx), _stream(stream))
 
 
 # ---- ep2 with token dedup (include/moe_dts.h "ep2d")
@@ -415,11 +415,12 @@ def moe_ep2d_combine(ctx, ysum_peers, uslot, y, stream=None):
     _call("moe_ep2d_combine", ctx, a, _ptr(uslot), _ptr(y), _stream(stream))
 
 
-def moe_ep2d_combine_bwd(ctx, dyu, e_out, rgate, ruid, offsets_recv, R_recv_cap: int, d_eout, dG_row, stream=None):
+def moe_ep2d_combine_bwd(ctx, dyu, e_out, rgate, ruid, offsets_recv, R_recv_cap: int, d_eout, dG_row, db2=None,
+                         stream=None):
     _call("moe_ep2d_combine_bwd", ctx, _ptr(dyu), _ptr(e_out), _ptr(rgate), _ptr(ruid), _ptr(offsets_recv),
-          int(R_recv_cap), _ptr(d_eout), _ptr(dG_row), _stream(stream))
+          int(R_recv_cap), _ptr(d_eout), _ptr(dG_row), _ptr(db2), _stream(stream))
 
 
-def moe_ep2d_dispatch_bwd(ctx, dxu_peers, uslot, dlogits, Wg, dx, stream=None):
+def moe_ep2d_dispatch_bwd(ctx, dxu_peers, uslot, accumulate, dx, stream=None):
     a, ka = _peers(dxu_peers)
-    _call("moe_ep2d_dispatch_bwd", ctx, a, _ptr(uslot), _ptr(dlogits), _ptr(Wg), _ptr(dx), _stream(stream))
+    _call("moe_ep2d_dispatch_bwd", ctx, a, _ptr(uslot), int(bool(accumulate)), _ptr(dx), _stream(stream))

@@ -42,21 +42,6 @@ cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_
   return launch_simt_gemm(g2, dt, dt, dt, EPI_BIAS_T, s);
 }
 
-// db2[e] = colsum(d_eout rows of e): from the partials moe_combine_bwd left for exactly this
-// (d_eout, offsets, R_cap) when it could (single rank), else by reading d_eout.
-static cudaError_t db2_colsum(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, float* db2,
-                              cudaStream_t s) {
-  const bool have = c->db2_src == d_eout && c->db2_off == offsets && c->db2_rcap == R_cap;
-  c->db2_src = nullptr;
-  if (!have) {
-    cudaError_t e = cudaSuccess;
-    if (!launch_db2_partials(c, d_eout, offsets, R_cap, s, &e))
-      return e != cudaSuccess ? e : launch_colsum_grouped(d_eout, c->dtype, c->d, offsets, c->E_local, db2, c->colpart, s);
-    if (e != cudaSuccess) return e;
-  }
-  return launch_colsum_final(c->db2part, c->d, c->db2_S, c->E_local, db2, s);
-}
-
 cudaError_t launch_expert_ffn_bwd(moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                                   const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
                                   const void* W2, void* da, void* dx_perm, float* dW1, float* db1, float* dW2,
@@ -67,7 +52,7 @@ cudaError_t launch_expert_ffn_bwd(moe_ctx* c, const void* d_eout, const void* x_
     if ((e = tc_expert_ffn_bwd(c, d_eout, x_perm, gp, h, offsets, R_cap, W1, W2, da, dx_perm, dW1, dW2, db1, s)) !=
         cudaSuccess)
       return e;
-    return db2_colsum(c, d_eout, offsets, R_cap, db2, s);
+    return db2 ? launch_db2(c, d_eout, offsets, R_cap, db2, s) : cudaSuccess;
   }
   // dgrad2 + GELU': da = (d_eout W2_e) (.) GELU'(a)      (da may alias a)
   SimtGemm g = base_rows(offsets, El, R_cap);
@@ -98,7 +83,7 @@ cudaError_t launch_expert_ffn_bwd(moe_ctx* c, const void* d_eout, const void* x_
   g1.N = d; g1.K = f;
   if ((e = launch_simt_gemm(g1, dt, dt, dt, EPI_T, s)) != cudaSuccess) return e;
   // bias gradients: column sums per expert (pad rows are zero)
-  if ((e = db2_colsum(c, d_eout, offsets, R_cap, db2, s)) != cudaSuccess) return e;
+  if (db2 && (e = launch_db2(c, d_eout, offsets, R_cap, db2, s)) != cudaSuccess) return e;
   return launch_colsum_grouped(da, dt, f, offsets, El, db1, c->colpart, s);
 }
 

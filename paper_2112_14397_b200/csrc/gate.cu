@@ -184,7 +184,7 @@ cudaError_t launch_gate_typed(const moe_ctx* c, const void* x, const void* Wg, c
 template <bool PEER = false>
 __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     const float* __restrict__ dG_row, const int* __restrict__ slot, const float* __restrict__ probs,
-    int T_, int E, float tau, float alpha, const int* __restrict__ counts, double bal_scale,
+    int T_, int E, float tau, float alpha, const int* __restrict__ counts, int count_rows, double bal_scale,
     float* __restrict__ dlogits, bf16* __restrict__ dL2, int Ep, int Kp, int El,
     const __grid_constant__ PeerTable dGp) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -200,7 +200,11 @@ __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
       p[i] = probs[(long long)t * E + e];
       int r = slot[(long long)t * E + e];
       dp[i] = r >= 0 ? (PEER ? reinterpret_cast<const float*>(dGp.p[e / El])[r] : dG_row[r]) : 0.f;
-      if (alpha > 0.f) dp[i] += (float)(bal_scale * (double)counts[e]);
+      if (alpha > 0.f) {                       // global count of e: the column sum of the count rows
+        int ce = 0;
+        for (int q = 0; q < count_rows; ++q) ce += counts[(long long)q * E + e];
+        dp[i] += (float)(bal_scale * (double)ce);
+      }
       s += p[i] * dp[i];
     }
   }
@@ -279,9 +283,17 @@ cudaError_t launch_gate(const moe_ctx* c, const void* x, const void* Wg, const f
   return launch_gate_typed<float>(c, x, Wg, u, tau, thr, top1, probs, slot, counts, near_band, s);
 }
 
+// dx = dlogits W_g^T for the non-tensor-core gate path: fp32 SIMT product into the workspace,
+// stored in the activation dtype
+__global__ void f32_to_act_kernel(const float* __restrict__ in, long long n, bf16* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
 static cudaError_t gate_bwd_impl(const moe_ctx* c, const float* dG_row, const PeerTable* dGp, const int32_t* slot,
-                                 const float* probs, const void* x, float tau, float alpha, const int32_t* counts,
-                                 int64_t B_total, float* dWg, float* dlogits, cudaStream_t s) {
+                                 const float* probs, const void* x, const void* Wg, float tau, float alpha,
+                                 const int32_t* counts, int count_rows, int64_t B_total, float* dWg, float* dlogits,
+                                 void* dx, cudaStream_t s) {
   if (c->T == 0) return cudaMemsetAsync(dWg, 0, sizeof(float) * c->d * c->E, s);
   double bal = alpha > 0.f ? (double)alpha * c->E / ((double)B_total * (double)B_total) : 0.0;
   const bool tc = gate_tc_supported(c);
@@ -291,18 +303,21 @@ static cudaError_t gate_bwd_impl(const moe_ctx* c, const float* dG_row, const Pe
   if (dGp) {
     tab = *dGp;
     gate_bwd_token_kernel<true><<<(c->T + 7) / 8, 256, 0, s>>>(nullptr, slot, probs, c->T, c->E, tau, alpha, counts,
-                                                               bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
+                                                               count_rows, bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
         count_launch();
   } else {
     gate_bwd_token_kernel<false><<<(c->T + 7) / 8, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts,
-                                                                bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
+                                                                count_rows, bal, dlogits, dL2, Ep, Kp, c->E_local,
+                                                                tab),
         count_launch();
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (tc) {
-    const_cast<moe_ctx*>(c)->dl2_src = dlogits;     // the hi|lo operand of these dlogits is in the workspace
-    return gate_tc_dwg(c, x, dlogits, dWg, s);
+    // the token kernel above just wrote the [hi | lo] bf16 operand rows of dlogits: both
+    // tensor-core products of this call use them (nothing is carried to a later call)
+    if ((e = gate_tc_dwg(c, x, dlogits, dWg, true, s)) != cudaSuccess) return e;
+    return dx ? gate_tc_dx(c, dlogits, Wg, dx, true, s) : cudaSuccess;
   }
   // dWg [d, E] = x^T [d, T] . dlogits [T, E]  (split-K, deterministic reduction)
   SimtGemm g{};
@@ -316,20 +331,38 @@ static cudaError_t gate_bwd_impl(const moe_ctx* c, const float* dG_row, const Pe
   if (c->dwg_splits > 1) {
     long long n = (long long)c->d * c->E;
     reduce_splits_kernel<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(c->part, c->dwg_splits, n, dWg), count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (!dx) return cudaSuccess;
+  // dx [T, d] = dlogits [T, E] . Wg^T  (Wg [d, E] -> B(k=e, n=dd) = Wg[dd*E + e]); fp32 straight
+  // into dx for fp32 layers, through the fp32 workspace buffer for bf16 ones
+  SimtGemm h{};
+  h.A = dlogits; h.sAm = c->E; h.sAk = 1;
+  h.B = Wg; h.sBk = 1; h.sBn = c->E;
+  h.C = c->dtype == 1 ? (void*)c->dxg : dx; h.sCm = c->d;
+  h.M = c->T; h.N = c->d; h.K = c->E; h.G = 1; h.k_split = 1;
+  if ((e = launch_simt_gemm(h, 0, c->dtype, 0, EPI_F32, s)) != cudaSuccess) return e;
+  if (c->dtype == 1) {
+    const long long n = (long long)c->T * c->d;
+    const int blocks = (int)((n + 255) / 256 < 8 * c->sm_count ? (n + 255) / 256 : 8 * c->sm_count);
+    f32_to_act_kernel<<<blocks, 256, 0, s>>>(c->dxg, n, reinterpret_cast<bf16*>(dx)), count_launch();
   }
   return cudaGetLastError();
 }
 
 cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t* slot, const float* probs,
-                            const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
-                            float* dWg, float* dlogits, cudaStream_t s) {
-  return gate_bwd_impl(c, dG_row, nullptr, slot, probs, x, tau, alpha, counts, B_total, dWg, dlogits, s);
+                            const void* x, const void* Wg, float tau, float alpha, const int32_t* counts,
+                            int count_rows, int64_t B_total, float* dWg, float* dlogits, void* dx, cudaStream_t s) {
+  return gate_bwd_impl(c, dG_row, nullptr, slot, probs, x, Wg, tau, alpha, counts, count_rows, B_total, dWg, dlogits,
+                       dx, s);
 }
 
 cudaError_t launch_gate_bwd_peer(const moe_ctx* c, const PeerTable& dGp, const int32_t* slot, const float* probs,
-                                 const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
-                                 float* dWg, float* dlogits, cudaStream_t s) {
-  return gate_bwd_impl(c, nullptr, &dGp, slot, probs, x, tau, alpha, counts, B_total, dWg, dlogits, s);
+                                 const void* x, const void* Wg, float tau, float alpha, const int32_t* counts,
+                                 int count_rows, int64_t B_total, float* dWg, float* dlogits, void* dx,
+                                 cudaStream_t s) {
+  return gate_bwd_impl(c, nullptr, &dGp, slot, probs, x, Wg, tau, alpha, counts, count_rows, B_total, dWg, dlogits,
+                       dx, s);
 }
 
 // Steps 2-3 from precomputed fp32 logits, thread per token (kGateBT tokens per block):

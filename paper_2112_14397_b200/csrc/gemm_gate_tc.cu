@@ -685,7 +685,6 @@ cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, con
                             cudaStream_t s) {
   using namespace tcgate;
   const int E = c->E, d = c->d, Ep = gate_Ep(E);
-  const_cast<moe_ctx*>(c)->dl2_src = nullptr;       // the forward reuses the gate scratch
   bf16* WgT = reinterpret_cast<bf16*>(c->gate_scratch);
   wg_transpose_kernel<<<(unsigned)(((long long)Ep * d + 255) / 256), 256, 0, s>>>((const bf16*)Wg, d, E, Ep, WgT,
                                                                                   counts, near_band, c->rq),
@@ -738,27 +737,27 @@ void* gate_dl2_buffer(const moe_ctx* c) {
   return reinterpret_cast<bf16*>(c->gate_scratch) + (size_t)c->d * gate_Kp(c->E);
 }
 
-cudaError_t gate_tc_dx(const moe_ctx* c, const float* dlogits, const void* Wg, void* dxg_bf16, cudaStream_t s) {
+cudaError_t gate_tc_dx(const moe_ctx* c, const float* dlogits, const void* Wg, void* dx_bf16, bool have_split,
+                       cudaStream_t s) {
   using namespace tcgate;
   const int E = c->E, d = c->d, Ep = gate_Ep(E), Kp = gate_Kp(E), T = c->T;
   bf16* Wg2 = reinterpret_cast<bf16*>(c->gate_scratch);
   bf16* dL2 = Wg2 + (size_t)d * Kp;
   wg_double_kernel<<<(unsigned)(((long long)d * Kp + 255) / 256), 256, 0, s>>>((const bf16*)Wg, d, E, Ep, Kp, Wg2),
       count_launch();
-  cudaError_t e = cudaSuccess;
-  if (c->dl2_src != dlogits) e = launch_dl_split(dlogits, T, E, Ep, Kp, dL2, s);
-  const_cast<moe_ctx*>(c)->dl2_src = nullptr;
+  cudaError_t e = have_split ? cudaGetLastError() : launch_dl_split(dlogits, T, E, Ep, Kp, dL2, s);
   if (e != cudaSuccess) return e;
-  return tc_dense_store(c, dL2, T, Kp, Wg2, d, dxg_bf16, c->tok_off, s);
+  return tc_dense_store(c, dL2, T, Kp, Wg2, d, dx_bf16, c->tok_off, s);
 }
 
 // dW_g = x^T dlogits  (split over T, deterministic reduction)
-cudaError_t gate_tc_dwg(const moe_ctx* c, const void* x, const float* dlogits, float* dWg, cudaStream_t s) {
+cudaError_t gate_tc_dwg(const moe_ctx* c, const void* x, const float* dlogits, float* dWg, bool have_split,
+                        cudaStream_t s) {
   using namespace tcgate;
   const int E = c->E, d = c->d, Ep = gate_Ep(E), Kp = gate_Kp(E), T = c->T;
   bf16* Wg2 = reinterpret_cast<bf16*>(c->gate_scratch);
   bf16* dL2 = Wg2 + (size_t)d * Kp;
-  cudaError_t e0 = c->dl2_src == dlogits ? cudaSuccess : launch_dl_split(dlogits, T, E, Ep, Kp, dL2, s);
+  cudaError_t e0 = have_split ? cudaSuccess : launch_dl_split(dlogits, T, E, Ep, Kp, dL2, s);
   if (e0 != cudaSuccess) return e0;
   CUtensorMap mA, mB;
   if (!map2d(&mA, x, T, d, 64, 64) || !map2d(&mB, dL2, T, Kp, 64, 64)) return cudaErrorInvalidValue;

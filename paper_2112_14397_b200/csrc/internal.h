@@ -30,14 +30,14 @@ struct moe_ctx {
   int* rq;             // [1 + T] fp64-refine queue of the tcgen05 gate (count, tokens)
   int* tok_off;        // [2] = {0, roundup(T, 128)}: the token range as one row segment
   float* biasf;        // [E_local, roundup(f,256)] b1 then [E_local, roundup(d,256)] b2 in fp32 (tcgen05 epilogues)
-  float* db2part;      // [E_local, db2_S, d] db2 column-sum partials left by moe_combine_bwd (single rank)
+  float* db2part;      // [E_local, db2_S, d] db2 column-sum partials (scratch within one call)
   int db2_S;           // row splits per expert of the fused combine_bwd
-  // which (d_eout, offsets, R_cap) the db2 partials belong to; moe_expert_ffn_bwd uses them only
-  // for exactly that triple (else it sums d_eout itself), then clears this
-  const float* dl2_src;   // dlogits whose [hi | lo] bf16 split currently sits in gate_scratch (tcgen05 gate bwd)
-  const void* db2_src;
-  const int* db2_off;
-  long long db2_rcap;
+  // the (probs, slot) outputs of the most recent moe_dts_gate on this ctx: the per-block expert
+  // counts it left in the workspace (blk_cnt) belong to them, and moe_dispatch / moe_ep2(d)_dispatch
+  // refuse (MOE_EINVAL) any other pair -- the one piece of state carried from one call to the next
+  const void* gate_probs;
+  const void* gate_slot;
+  unsigned long long gate_seq;
   void* gate_scratch;  // tcgen05 gate operands: W_g^T / [W_g|W_g] (bf16) and the hi|lo split of dL
   int* ep_counts;      // [world, E] gathered counts (EP)
   int* ep_off;         // [E_local + 1] recv-layout offsets (EP)
@@ -86,18 +86,22 @@ cudaError_t launch_combine(const moe_ctx* c, const void* e_out, const float* row
 cudaError_t launch_combine_bwd(moe_ctx* c, const void* dy, const void* e_out,
                                const float* row_gate, const int32_t* row_token,
                                const int32_t* offsets, int64_t R_cap, void* d_eout, float* dG_row,
-                               cudaStream_t s);
+                               float* db2, cudaStream_t s);
 
-bool launch_db2_partials(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, cudaStream_t s,
-                         cudaError_t* err);
+// db2[g] = column sums of the d_eout rows of local expert g (fixed-order partials + final)
+cudaError_t launch_db2(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, float* db2,
+                       cudaStream_t s);
 
-cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot,
-                                const float* dlogits, const void* Wg, void* dx, cudaStream_t s);
+// dx[t] (+)= sum_{e asc} dx_perm[slot[t,e]]   (accumulate: dx's current row starts the sum)
+cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot, int accumulate,
+                                void* dx, cudaStream_t s);
 
+// counts: [count_rows][E] (1 = global counts, world = the all-gathered counts, summed per e);
+// dx (optional): dx = dlogits W_g^T (the gate's input-gradient term, written)
 cudaError_t launch_gate_bwd(const moe_ctx* c, const float* dG_row, const int32_t* slot,
-                            const float* probs, const void* x, float tau, float alpha,
-                            const int32_t* counts, int64_t B_total, float* dWg, float* dlogits,
-                            cudaStream_t s);
+                            const float* probs, const void* x, const void* Wg, float tau, float alpha,
+                            const int32_t* counts, int count_rows, int64_t B_total, float* dWg, float* dlogits,
+                            void* dx, cudaStream_t s);
 
 cudaError_t launch_balance_loss(const moe_ctx* c, const float* probs, const int32_t* counts,
                                 float alpha, int64_t B_total, float* loss, cudaStream_t s);
@@ -126,9 +130,9 @@ cudaError_t launch_ep2_combine(const moe_ctx* c, const PeerTable& eo, const floa
 bool ep2_width_ok(const moe_ctx* c);
 cudaError_t launch_ep2_combine_bwd(moe_ctx* c, const PeerTable& dyp, const void* e_out, const float* rgate,
                                    const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets, int64_t R_cap,
-                                   void* d_eout, float* dG_row, cudaStream_t s);
-cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, const float* dlogits,
-                                    const void* Wg, void* dx, cudaStream_t s, int slot_cols = 0, int cols_per_rank = 0);
+                                   void* d_eout, float* dG_row, float* db2, cudaStream_t s);
+cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, int accumulate,
+                                    void* dx, cudaStream_t s, int slot_cols = 0, int cols_per_rank = 0);
 // ep2 with token dedup (one row per (token, owner) each way)
 cudaError_t launch_ep2d_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot, int32_t* uslot,
                                  const PeerTable& tb, const PeerTable& urows, const PeerTable& rtok,
@@ -143,10 +147,11 @@ cudaError_t launch_ep2d_gather_dy(const moe_ctx* c, const PeerTable& dyp, const 
 cudaError_t launch_ep2d_combine(const moe_ctx* c, const PeerTable& ys, const int32_t* uslot, void* y, cudaStream_t s);
 cudaError_t launch_ep2d_combine_bwd(moe_ctx* c, const void* dyu, const void* e_out, const float* rgate,
                                     const int32_t* ruid, const int32_t* offsets, int64_t R_cap, void* d_eout,
-                                    float* dG_row, cudaStream_t s);
+                                    float* dG_row, float* db2, cudaStream_t s);
 cudaError_t launch_gate_bwd_peer(const moe_ctx* c, const PeerTable& dGp, const int32_t* slot, const float* probs,
-                                 const void* x, float tau, float alpha, const int32_t* counts, int64_t B_total,
-                                 float* dWg, float* dlogits, cudaStream_t s);
+                                 const void* x, const void* Wg, float tau, float alpha, const int32_t* counts,
+                                 int count_rows, int64_t B_total, float* dWg, float* dlogits, void* dx,
+                                 cudaStream_t s);
 
 // ---------------------------------------------------------------- tcgen05 grouped GEMM (bf16)
 bool tc_available();
@@ -166,9 +171,13 @@ bool gate_tc_supported(const moe_ctx* c);
 cudaError_t gate_tc_forward(const moe_ctx* c, const void* x, const void* Wg, const float* u, float tau, float thr,
                             int top1, float* probs, int32_t* slot, int32_t* counts, int32_t* near_band,
                             cudaStream_t s);
-cudaError_t gate_tc_dx(const moe_ctx* c, const float* dlogits, const void* Wg, void* dxg_bf16, cudaStream_t s);
+// have_split: the [hi | lo] bf16 operand rows of these dlogits were just written to gate_dl2_buffer
+// by the same moe_dts_gate_bwd call (else they are rebuilt from dlogits first)
+cudaError_t gate_tc_dx(const moe_ctx* c, const float* dlogits, const void* Wg, void* dx_bf16, bool have_split,
+                       cudaStream_t s);
 void* gate_dl2_buffer(const moe_ctx* c);   // [T, Kp] bf16 hi|lo operand rows inside gate_scratch
-cudaError_t gate_tc_dwg(const moe_ctx* c, const void* x, const float* dlogits, float* dWg, cudaStream_t s);
+cudaError_t gate_tc_dwg(const moe_ctx* c, const void* x, const float* dlogits, float* dWg, bool have_split,
+                        cudaStream_t s);
 cudaError_t tc_dense_store(const moe_ctx* c, const void* A, long long rows, int K, const void* B, int N, void* out,
                            const int* offsets_dev, cudaStream_t s);
 cudaError_t launch_gate_softmax_tpt(const moe_ctx* c, const float* logits, const float* u, float tau, float thr,

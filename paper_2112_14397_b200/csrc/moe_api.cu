@@ -136,10 +136,6 @@ void carve_workspace(moe_ctx* c) {
   c->ep2_scr = reinterpret_cast<int*>(c->ws + k.ep2_scr);
   c->ep2_base = reinterpret_cast<int*>(c->ws + k.ep2_base);
   c->db2_S = db2_splits(c);
-  c->db2_src = nullptr;
-  c->dl2_src = nullptr;
-  c->db2_off = nullptr;
-  c->db2_rcap = 0;
 }
 
 }  // namespace moe
@@ -245,9 +241,25 @@ int moe_dts_gate(moe_ctx* ctx, const void* x, const void* Wg, const float* u, fl
   if (!(tau > 0.0f) || !isfinite(tau)) return fail(MOE_EINVAL, "moe_dts_gate: tau=%g must be finite and > 0", tau);
   if (!(threshold >= 0.0f && threshold < 1.0f))
     return fail(MOE_EINVAL, "moe_dts_gate: threshold=%g must be in [0, 1)", threshold);
-  return cuda_status(moe::launch_gate(ctx, x, Wg, u, tau, threshold, top1, probs, slot, counts, near_band,
-                                      S(stream)),
-                     "moe_dts_gate");
+  rc = cuda_status(moe::launch_gate(ctx, x, Wg, u, tau, threshold, top1, probs, slot, counts, near_band, S(stream)),
+                   "moe_dts_gate");
+  // the per-block expert counts this call left in the workspace belong to (probs, slot)
+  ctx->gate_probs = rc == MOE_OK ? probs : nullptr;
+  ctx->gate_slot = rc == MOE_OK ? slot : nullptr;
+  ++ctx->gate_seq;
+  return rc;
+}
+
+// moe_dispatch / moe_ep2(d)_dispatch read the per-block expert counts moe_dts_gate left in the
+// workspace: accept only the (probs, slot) pair of the most recent moe_dts_gate on this ctx
+static int check_gate_outputs(const moe_ctx* ctx, const float* probs, const int32_t* slot, const char* fn) {
+  if (ctx->T == 0) return MOE_OK;
+  if (ctx->gate_seq == 0)
+    return fail(MOE_EINVAL, "%s: no moe_dts_gate has run on this ctx (its per-block counts are needed)", fn);
+  if ((const void*)probs != ctx->gate_probs || (const void*)slot != ctx->gate_slot)
+    return fail(MOE_EINVAL, "%s: probs/slot are not the outputs of the most recent moe_dts_gate on this ctx "
+                "(gate call #%llu)", fn, (unsigned long long)ctx->gate_seq);
+  return MOE_OK;
 }
 
 int moe_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, void* x_perm,
@@ -258,6 +270,7 @@ int moe_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot,
   REQUIRE_T(x); REQUIRE_T(probs); REQUIRE_T(slot); REQUIRE_R(x_perm); REQUIRE_R(row_token); REQUIRE_R(row_gate);
   REQUIRE(offsets); REQUIRE(R_out);
   if (R_cap < 0 || R_cap > (int64_t)INT32_MAX) return fail(MOE_EINVAL, "moe_dispatch: bad R_cap %lld", (long long)R_cap);
+  if ((rc = check_gate_outputs(ctx, probs, slot, "moe_dispatch"))) return rc;
   return cuda_status(moe::launch_dispatch(ctx, x, probs, slot, nullptr, x_perm, row_token, row_gate,
                                           offsets, R_cap, R_out, S(stream)),
                      "moe_dispatch");
@@ -302,14 +315,17 @@ int moe_combine(moe_ctx* ctx, const void* e_out, const float* row_gate, const in
 
 int moe_combine_bwd(moe_ctx* ctx, const void* dy, const void* e_out, const float* row_gate,
                     const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
-                    float* dG_row, void* stream) {
+                    float* dG_row, float* db2, void* stream) {
   int rc = check_ctx(ctx, "moe_combine_bwd");
   if (rc) return rc;
   REQUIRE_T(dy); REQUIRE_R(e_out); REQUIRE_R(row_gate); REQUIRE_R(row_token); REQUIRE(offsets); REQUIRE_R(d_eout);
   REQUIRE_R(dG_row);
   if (R_cap < 0) return fail(MOE_EINVAL, "moe_combine_bwd: bad R_cap");
+  if (db2 && (ctx->comm || ctx->world > 1))
+    return fail(MOE_EINVAL, "moe_combine_bwd: db2 is an expert-side sum; under the NCCL exchange it comes from "
+                "moe_expert_ffn_bwd on the received d_eout");
   return cuda_status(moe::launch_combine_bwd(ctx, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout,
-                                             dG_row, S(stream)),
+                                             dG_row, db2, S(stream)),
                      "moe_combine_bwd");
 }
 
@@ -320,7 +336,7 @@ int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, con
   int rc = check_ctx(ctx, "moe_expert_ffn_bwd");
   if (rc) return rc;
   REQUIRE_R(d_eout); REQUIRE_R(x_perm); REQUIRE_R(gp_saved); REQUIRE_R(h_saved); REQUIRE(offsets); REQUIRE(W1);
-  REQUIRE(W2); REQUIRE_R(da); REQUIRE_R(dx_perm); REQUIRE(dW1); REQUIRE(db1); REQUIRE(dW2); REQUIRE(db2);
+  REQUIRE(W2); REQUIRE_R(da); REQUIRE_R(dx_perm); REQUIRE(dW1); REQUIRE(db1); REQUIRE(dW2);   // db2 optional
   if (R_cap < 0 || R_cap % moe::kRowAlign != 0)
     return fail(MOE_EINVAL, "moe_expert_ffn_bwd: R_cap=%lld must be a non-negative multiple of %d",
                 (long long)R_cap, moe::kRowAlign);
@@ -330,29 +346,28 @@ int moe_expert_ffn_bwd(moe_ctx* ctx, const void* d_eout, const void* x_perm, con
 }
 
 int moe_dts_gate_bwd(moe_ctx* ctx, const float* dG_row, const int32_t* slot, const float* probs,
-                     const void* x, float tau, float balance_alpha, const int32_t* counts, int64_t B_total,
-                     float* dWg, float* dlogits, void* stream) {
+                     const void* x, const void* Wg, float tau, float balance_alpha, const int32_t* counts,
+                     int64_t B_total, float* dWg, float* dlogits, void* dx, void* stream) {
   int rc = check_ctx(ctx, "moe_dts_gate_bwd");
   if (rc) return rc;
   REQUIRE(dG_row); REQUIRE_T(slot); REQUIRE_T(probs); REQUIRE_T(x); REQUIRE(dWg); REQUIRE_T(dlogits);
+  if (dx && !Wg) return fail(MOE_EINVAL, "moe_dts_gate_bwd: dx (dlogits W_g^T) requested without Wg");
   if (!(tau > 0.0f) || !isfinite(tau)) return fail(MOE_EINVAL, "moe_dts_gate_bwd: tau=%g must be finite and > 0", tau);
   if (!(balance_alpha >= 0.0f) || !isfinite(balance_alpha))
     return fail(MOE_EINVAL, "moe_dts_gate_bwd: balance_alpha=%g must be finite and >= 0", balance_alpha);
   if (balance_alpha > 0.0f && (!counts || B_total <= 0))
     return fail(MOE_EINVAL, "moe_dts_gate_bwd: balance term needs counts and B_total > 0");
-  return cuda_status(moe::launch_gate_bwd(ctx, dG_row, slot, probs, x, tau, balance_alpha, counts, B_total,
-                                          dWg, dlogits, S(stream)),
+  return cuda_status(moe::launch_gate_bwd(ctx, dG_row, slot, probs, x, Wg, tau, balance_alpha, counts, 1, B_total,
+                                          dWg, dlogits, dx, S(stream)),
                      "moe_dts_gate_bwd");
 }
 
-int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, const float* dlogits,
-                     const void* Wg, void* dx, void* stream) {
+int moe_dispatch_bwd(moe_ctx* ctx, const void* dx_perm, const int32_t* slot, int accumulate, void* dx,
+                     void* stream) {
   int rc = check_ctx(ctx, "moe_dispatch_bwd");
   if (rc) return rc;
   REQUIRE(dx_perm); REQUIRE_T(slot); REQUIRE_T(dx);
-  if (dlogits && !Wg) return fail(MOE_EINVAL, "moe_dispatch_bwd: dlogits given without Wg");
-  return cuda_status(moe::launch_dispatch_bwd(ctx, dx_perm, slot, dlogits, Wg, dx, S(stream)),
-                     "moe_dispatch_bwd");
+  return cuda_status(moe::launch_dispatch_bwd(ctx, dx_perm, slot, accumulate, dx, S(stream)), "moe_dispatch_bwd");
 }
 
 int moe_balance_loss(moe_ctx* ctx, const float* probs, const int32_t* counts, float alpha, int64_t B_total,
@@ -714,6 +729,7 @@ int moe_ep2_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* s
   int rc = ep2_check(ctx, "moe_ep2_dispatch");
   if (rc) return rc;
   REQUIRE_T(x); REQUIRE_T(probs); REQUIRE_T(slot);
+  if ((rc = check_gate_outputs(ctx, probs, slot, "moe_ep2_dispatch"))) return rc;
   moe::PeerTable xr, rt, rs, rg;
   if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(x_recv_peers), xr, "moe_ep2_dispatch")) ||
       (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rtok_peers), rt, "moe_ep2_dispatch")) ||
@@ -736,7 +752,7 @@ int moe_ep2_combine(moe_ctx* ctx, void* const* e_out_peers, const float* probs, 
 
 int moe_ep2_combine_bwd(moe_ctx* ctx, void* const* dy_peers, const void* e_out, const float* rgate,
                         const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets_recv, int64_t R_recv_cap,
-                        void* d_eout, float* dG_row, void* stream) {
+                        void* d_eout, float* dG_row, float* db2, void* stream) {
   int rc = ep2_check(ctx, "moe_ep2_combine_bwd");
   if (rc) return rc;
   REQUIRE(e_out); REQUIRE(rgate); REQUIRE(rtok); REQUIRE(rsrc); REQUIRE(offsets_recv); REQUIRE(d_eout); REQUIRE(dG_row);
@@ -744,16 +760,18 @@ int moe_ep2_combine_bwd(moe_ctx* ctx, void* const* dy_peers, const void* e_out, 
   moe::PeerTable t;
   if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dy_peers), t, "moe_ep2_combine_bwd"))) return rc;
   return cuda_status(moe::launch_ep2_combine_bwd(ctx, t, e_out, rgate, rtok, rsrc, offsets_recv, R_recv_cap, d_eout,
-                                                 dG_row, S(stream)),
+                                                 dG_row, db2, S(stream)),
                      "moe_ep2_combine_bwd");
 }
 
 int moe_ep2_gate_bwd(moe_ctx* ctx, float* const* dG_peers, const int32_t* slot, const float* probs, const void* x,
-                     float tau, float balance_alpha, const int32_t* counts, int64_t B_total, float* dWg, float* dlogits,
-                     void* stream) {
+                     const void* Wg, float tau, float balance_alpha, const int32_t* counts_all, int64_t B_total,
+                     float* dWg, float* dlogits, void* dx, void* stream) {
   int rc = ep2_check(ctx, "moe_ep2_gate_bwd");
   if (rc) return rc;
   REQUIRE_T(slot); REQUIRE_T(probs); REQUIRE_T(x); REQUIRE(dWg); REQUIRE_T(dlogits);
+  if (dx && !Wg) return fail(MOE_EINVAL, "moe_ep2_gate_bwd: dx (dlogits W_g^T) requested without Wg");
+  const int32_t* counts = counts_all;
   if (!(tau > 0.0f) || !isfinite(tau)) return fail(MOE_EINVAL, "moe_ep2_gate_bwd: tau=%g must be finite and > 0", tau);
   if (!(balance_alpha >= 0.0f) || !isfinite(balance_alpha))
     return fail(MOE_EINVAL, "moe_ep2_gate_bwd: balance_alpha=%g must be finite and >= 0", balance_alpha);
@@ -761,20 +779,20 @@ int moe_ep2_gate_bwd(moe_ctx* ctx, float* const* dG_peers, const int32_t* slot, 
     return fail(MOE_EINVAL, "moe_ep2_gate_bwd: balance term needs counts and B_total > 0");
   moe::PeerTable t;
   if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dG_peers), t, "moe_ep2_gate_bwd"))) return rc;
-  return cuda_status(moe::launch_gate_bwd_peer(ctx, t, slot, probs, x, tau, balance_alpha, counts, B_total, dWg,
-                                               dlogits, S(stream)),
+  // counts_all [world][E]: the kernel sums the world rows -> the global counts of Eq. 10
+  return cuda_status(moe::launch_gate_bwd_peer(ctx, t, slot, probs, x, Wg, tau, balance_alpha, counts, ctx->world,
+                                               B_total, dWg, dlogits, dx, S(stream)),
                      "moe_ep2_gate_bwd");
 }
 
-int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t* slot, const float* dlogits,
-                         const void* Wg, void* dx, void* stream) {
+int moe_ep2_dispatch_bwd(moe_ctx* ctx, void* const* dx_perm_peers, const int32_t* slot, int accumulate, void* dx,
+                         void* stream) {
   int rc = ep2_check(ctx, "moe_ep2_dispatch_bwd");
   if (rc) return rc;
   REQUIRE_T(slot); REQUIRE_T(dx);
-  if (dlogits && !Wg) return fail(MOE_EINVAL, "moe_ep2_dispatch_bwd: dlogits given without Wg");
   moe::PeerTable t;
   if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dx_perm_peers), t, "moe_ep2_dispatch_bwd"))) return rc;
-  return cuda_status(moe::launch_ep2_dispatch_bwd(ctx, t, slot, dlogits, Wg, dx, S(stream)), "moe_ep2_dispatch_bwd");
+  return cuda_status(moe::launch_ep2_dispatch_bwd(ctx, t, slot, accumulate, dx, S(stream)), "moe_ep2_dispatch_bwd");
 }
 
 // ---------------------------------------------------------------- ep2 with token dedup
@@ -785,6 +803,7 @@ int moe_ep2d_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* 
   int rc = ep2_check(ctx, "moe_ep2d_dispatch");
   if (rc) return rc;
   REQUIRE_T(x); REQUIRE_T(probs); REQUIRE_T(slot); REQUIRE_T(uslot);
+  if ((rc = check_gate_outputs(ctx, probs, slot, "moe_ep2d_dispatch"))) return rc;
   if ((long long)ctx->world * ctx->T > 0x7fffffffLL) return fail(MOE_ESHAPE, "moe_ep2d_dispatch: world*T exceeds int32");
   moe::PeerTable tb, ur, rt, rs, rg, ru;
   const char* fn = "moe_ep2d_dispatch";
@@ -836,26 +855,26 @@ int moe_ep2d_combine(moe_ctx* ctx, void* const* ysum_peers, const int32_t* uslot
 }
 
 int moe_ep2d_combine_bwd(moe_ctx* ctx, const void* dyu, const void* e_out, const float* rgate, const int32_t* ruid,
-                         const int32_t* offsets_recv, int64_t R_recv_cap, void* d_eout, float* dG_row, void* stream) {
+                         const int32_t* offsets_recv, int64_t R_recv_cap, void* d_eout, float* dG_row, float* db2,
+                         void* stream) {
   int rc = ep2_check(ctx, "moe_ep2d_combine_bwd");
   if (rc) return rc;
   REQUIRE(dyu); REQUIRE(e_out); REQUIRE(rgate); REQUIRE(ruid); REQUIRE(offsets_recv); REQUIRE(d_eout); REQUIRE(dG_row);
   if (!moe::ep2_width_ok(ctx))
     return fail(MOE_ESHAPE, "moe_ep2d_combine_bwd: d_model=%d too wide (max 1024 bf16 / 512 f32)", ctx->d);
   return cuda_status(moe::launch_ep2d_combine_bwd(ctx, dyu, e_out, rgate, ruid, offsets_recv, R_recv_cap, d_eout,
-                                                  dG_row, S(stream)),
+                                                  dG_row, db2, S(stream)),
                      "moe_ep2d_combine_bwd");
 }
 
-int moe_ep2d_dispatch_bwd(moe_ctx* ctx, void* const* dxu_peers, const int32_t* uslot, const float* dlogits,
-                          const void* Wg, void* dx, void* stream) {
+int moe_ep2d_dispatch_bwd(moe_ctx* ctx, void* const* dxu_peers, const int32_t* uslot, int accumulate, void* dx,
+                          void* stream) {
   int rc = ep2_check(ctx, "moe_ep2d_dispatch_bwd");
   if (rc) return rc;
   REQUIRE_T(uslot); REQUIRE_T(dx);
-  if (dlogits && !Wg) return fail(MOE_EINVAL, "moe_ep2d_dispatch_bwd: dlogits given without Wg");
   moe::PeerTable t;
   if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dxu_peers), t, "moe_ep2d_dispatch_bwd"))) return rc;
-  return cuda_status(moe::launch_ep2_dispatch_bwd(ctx, t, uslot, dlogits, Wg, dx, S(stream), ctx->world, 1),
+  return cuda_status(moe::launch_ep2_dispatch_bwd(ctx, t, uslot, accumulate, dx, S(stream), ctx->world, 1),
                      "moe_ep2d_dispatch_bwd");
 }
 

@@ -328,7 +328,9 @@ struct PeerRows {
 
 template <typename T, bool WEIGHTED, typename TX = float, int QV = 4, typename Src = LocalRows<T>>
 __device__ __forceinline__ void gather_sum_token(const Src& src, const int* __restrict__ slot_row, int d, int E,
-                                                 const TX* __restrict__ extra, T* __restrict__ out, int lane) {
+                                                 const TX* extra, T* out, int lane) {
+  // `extra` may alias `out` (the accumulating dispatch backward): each lane loads its own
+  // elements of the row with coherent loads before it stores them
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
   constexpr bool TWO = QV <= 3;                     // two rows in flight when registers allow
@@ -349,11 +351,11 @@ __device__ __forceinline__ void gather_sum_token(const Src& src, const int* __re
         const int v = v0 + q * 32 + lane;
         if (v < nvec) {
           if (sizeof(TX) == 2) {
-            unpack16(ld_nc_v4(extra + (long long)v * V), acc[q], bf16());
+            unpack16(ld_v4(extra + (long long)v * V), acc[q], bf16());
           } else {
 #pragma unroll
             for (int h = 0; h < V / 4; ++h)
-              unpack16(ld_nc_v4(reinterpret_cast<const float*>(extra) + (long long)v * V + 4 * h), acc[q] + 4 * h, float());
+              unpack16(ld_v4(reinterpret_cast<const float*>(extra) + (long long)v * V + 4 * h), acc[q] + 4 * h, float());
           }
         }
       }
@@ -641,11 +643,11 @@ __global__ void __launch_bounds__(256, 2) combine_bwd_colsum_kernel(const T* __r
 }
 
 // ------------------------------------------------------------------ dispatch backward
-// One warp per token: dx[t] = dxg[t] + sum_{e asc} dx_perm[slot[t,e]]  (dxg bf16 or fp32, may be NULL).
+// One warp per token: dx[t] = dxg[t] + sum_{e asc} dx_perm[slot[t,e]]  (dxg may be NULL, or dx itself:
+// the accumulating form).
 template <typename T, typename TX, int QV>
 __global__ void __launch_bounds__(256, 4) dispatch_bwd_kernel(const T* __restrict__ dx_perm, const int* __restrict__ slot,
-                                                           const TX* __restrict__ dxg, int T_, int d, int E,
-                                                           T* __restrict__ dx) {
+                                                           const TX* dxg, int T_, int d, int E, T* dx) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
@@ -846,8 +848,8 @@ __global__ void __launch_bounds__(256, 4) ep2_combine_kernel(const __grid_consta
 template <typename T, typename TX, int QV>
 __global__ void __launch_bounds__(256, 4) ep2_dispatch_bwd_kernel(const __grid_constant__ PeerTable dxp,
                                                                   const int* __restrict__ slot,
-                                                                  const TX* __restrict__ dxg, int T_, int d, int E,
-                                                                  int El, T* __restrict__ dx) {
+                                                                  const TX* dxg, int T_, int d, int E,
+                                                                  int El, T* dx) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int t = blockIdx.x * 8 + warp;
   if (t >= T_) return;
@@ -1100,19 +1102,13 @@ static cudaError_t launch_cbc(moe_ctx* c, const void* dy, const void* e_out, con
   k<<<dim3(c->db2_S, c->E_local), 256, smem, s>>>((const T*)dy, (const T*)e_out, row_gate, row_token, offsets, c->d,
                                                  R_cap, c->db2_S, (T*)d_eout, dG_row, c->db2part, row_src, tab),
       count_launch();
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess && COMPUTE) {
-    c->db2_src = d_eout;
-    c->db2_off = offsets;
-    c->db2_rcap = R_cap;
-  }
-  return e;
+  return cudaGetLastError();
 }
 
 // db2 partials (c->db2part) of an existing d_eout with the fused kernel's partition; false if
 // d is too wide for it (the caller then uses the generic column sums).
-bool launch_db2_partials(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, cudaStream_t s,
-                         cudaError_t* err) {
+static bool launch_db2_partials(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, cudaStream_t s,
+                                cudaError_t* err) {
   const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
   if (R_cap == 0) { *err = cudaSuccess; return false; }
   if (c->dtype == 1) {
@@ -1127,22 +1123,39 @@ bool launch_db2_partials(moe_ctx* c, const void* d_eout, const int32_t* offsets,
   return false;
 }
 
+// db2 from an existing d_eout (moe_expert_ffn_bwd): the same partition and fixed order as the
+// partials the fused combine backward produces, so both routes give bit-identical db2
+cudaError_t launch_db2(moe_ctx* c, const void* d_eout, const int32_t* offsets, int64_t R_cap, float* db2,
+                       cudaStream_t s) {
+  if (R_cap == 0) return cudaMemsetAsync(db2, 0, sizeof(float) * c->E_local * c->d, s);
+  cudaError_t e = cudaSuccess;
+  if (!launch_db2_partials(c, d_eout, offsets, R_cap, s, &e))
+    return launch_colsum_grouped(d_eout, c->dtype, c->d, offsets, c->E_local, db2, c->colpart, s);
+  if (e != cudaSuccess) return e;
+  return launch_colsum_final(c->db2part, c->d, c->db2_S, c->E_local, db2, s);
+}
+
+// finish db2 from the partials the fused combine backward just wrote (same call)
+static cudaError_t finish_db2(moe_ctx* c, cudaError_t e, float* db2, cudaStream_t s) {
+  if (e != cudaSuccess || !db2) return e;
+  return launch_colsum_final(c->db2part, c->d, c->db2_S, c->E_local, db2, s);
+}
+
 cudaError_t launch_combine_bwd(moe_ctx* c, const void* dy, const void* e_out, const float* row_gate,
                                const int32_t* row_token, const int32_t* offsets, int64_t R_cap, void* d_eout,
-                               float* dG_row, cudaStream_t s) {
-  c->db2_src = nullptr;
-  if (R_cap == 0) return cudaSuccess;
+                               float* dG_row, float* db2, cudaStream_t s) {
+  if (R_cap == 0) return db2 ? cudaMemsetAsync(db2, 0, sizeof(float) * c->E_local * c->d, s) : cudaSuccess;
   if (c->world == 1 && !c->comm && c->E_local == c->E) {
-    // single rank: also leave the db2 partials for moe_expert_ffn_bwd
+    // single rank: the fused kernel also sums the d_eout it stores into the db2 partials
     const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
     if (c->dtype == 1) {
-      if (nvec <= 32) return launch_cbc<bf16, 1>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
-      if (nvec <= 64) return launch_cbc<bf16, 2>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
-      if (nvec <= 96) return launch_cbc<bf16, 3>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
-      if (nvec <= 128) return launch_cbc<bf16, 4>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+      if (nvec <= 32) return finish_db2(c, launch_cbc<bf16, 1>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s), db2, s);
+      if (nvec <= 64) return finish_db2(c, launch_cbc<bf16, 2>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s), db2, s);
+      if (nvec <= 96) return finish_db2(c, launch_cbc<bf16, 3>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s), db2, s);
+      if (nvec <= 128) return finish_db2(c, launch_cbc<bf16, 4>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s), db2, s);
     } else {
-      if (nvec <= 32) return launch_cbc<float, 1>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
-      if (nvec <= 64) return launch_cbc<float, 2>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s);
+      if (nvec <= 32) return finish_db2(c, launch_cbc<float, 1>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s), db2, s);
+      if (nvec <= 64) return finish_db2(c, launch_cbc<float, 2>(c, dy, e_out, row_gate, row_token, offsets, R_cap, d_eout, dG_row, s), db2, s);
     }
   }
   const unsigned grid = (unsigned)((R_cap + 7) / 8);
@@ -1152,39 +1165,22 @@ cudaError_t launch_combine_bwd(moe_ctx* c, const void* dy, const void* e_out, co
   else
     combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)e_out, row_gate, row_token,
                                                    offsets, c->E, c->d, R_cap, (float*)d_eout, dG_row), count_launch();
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess && db2 ? launch_db2(c, d_eout, offsets, R_cap, db2, s) : e;
 }
 
-cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot, const float* dlogits,
-                                const void* Wg, void* dx, cudaStream_t s) {
+cudaError_t launch_dispatch_bwd(const moe_ctx* c, const void* dx_perm, const int32_t* slot, int accumulate,
+                                void* dx, cudaStream_t s) {
   if (c->T == 0) return cudaSuccess;
   const unsigned grid = (c->T + 7) / 8;
-  if (dlogits && gate_tc_supported(c)) {
-    // gate term dlogits W_g^T on tensor cores (bf16, hi|lo split of dlogits) -> added by the gather pass
-    cudaError_t e = gate_tc_dx(c, dlogits, Wg, c->dxg, s);
-    if (e != cudaSuccess) return e;
-    MOE_QV_DISPATCH(pass_vectors(c->d, 8), dispatch_bwd_kernel<bf16, bf16, QV><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, (const bf16*)c->dxg, c->T,
-                                                         c->d, c->E, (bf16*)dx), count_launch())
-    return cudaGetLastError();
-  }
-  const float* dxg = nullptr;
-  if (dlogits) {
-    // dxg [T, d] fp32 = dlogits [T, E] . Wg^T  (Wg [d, E] -> B(k=e, n=dd) = Wg[dd*E + e])
-    SimtGemm g{};
-    g.A = dlogits; g.sAm = c->E; g.sAk = 1;
-    g.B = Wg; g.sBk = 1; g.sBn = c->E;
-    g.C = c->dxg; g.sCm = c->d;
-    g.M = c->T; g.N = c->d; g.K = c->E; g.G = 1; g.k_split = 1;
-    cudaError_t e = launch_simt_gemm(g, 0, c->dtype, 0, EPI_F32, s);
-    if (e != cudaSuccess) return e;
-    dxg = c->dxg;
-  }
+  // accumulate: each warp loads its token's dx row (written by moe_dts_gate_bwd: dlogits W_g^T)
+  // before it sums the selected dx_perm rows onto it and stores the row back
   if (c->dtype == 1)
-    MOE_QV_DISPATCH(pass_vectors(c->d, 8), dispatch_bwd_kernel<bf16, float, QV><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot, dxg, c->T, c->d, c->E,
-                                                          (bf16*)dx), count_launch())
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), dispatch_bwd_kernel<bf16, bf16, QV><<<grid, 256, 0, s>>>((const bf16*)dx_perm, slot,
+                                                         accumulate ? (const bf16*)dx : nullptr, c->T, c->d, c->E, (bf16*)dx), count_launch())
   else
-    MOE_QV_DISPATCH(pass_vectors(c->d, 4), dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>((const float*)dx_perm, slot, dxg, c->T, c->d, c->E,
-                                                           (float*)dx), count_launch())
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>((const float*)dx_perm, slot,
+                                                           accumulate ? (const float*)dx : nullptr, c->T, c->d, c->E, (float*)dx), count_launch())
   return cudaGetLastError();
 }
 
@@ -1261,49 +1257,34 @@ bool ep2_width_ok(const moe_ctx* c) {
 
 cudaError_t launch_ep2_combine_bwd(moe_ctx* c, const PeerTable& dyp, const void* e_out, const float* rgate,
                                    const int32_t* rtok, const int32_t* rsrc, const int32_t* offsets, int64_t R_cap,
-                                   void* d_eout, float* dG_row, cudaStream_t s) {
-  c->db2_src = nullptr;
-  if (R_cap == 0) return cudaSuccess;
+                                   void* d_eout, float* dG_row, float* db2, cudaStream_t s) {
+  if (R_cap == 0) return db2 ? cudaMemsetAsync(db2, 0, sizeof(float) * c->E_local * c->d, s) : cudaSuccess;
   const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
+  cudaError_t e;
   if (c->dtype == 1) {
-    if (nvec <= 32) return launch_cbc<bf16, 1, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
-    if (nvec <= 64) return launch_cbc<bf16, 2, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
-    if (nvec <= 96) return launch_cbc<bf16, 3, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
-    return launch_cbc<bf16, 4, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+    if (nvec <= 32) e = launch_cbc<bf16, 1, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+    else if (nvec <= 64) e = launch_cbc<bf16, 2, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+    else if (nvec <= 96) e = launch_cbc<bf16, 3, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+    else e = launch_cbc<bf16, 4, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+  } else if (nvec <= 32) {
+    e = launch_cbc<float, 1, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+  } else {
+    e = launch_cbc<float, 2, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
   }
-  if (nvec <= 32) return launch_cbc<float, 1, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
-  return launch_cbc<float, 2, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
+  return finish_db2(c, e, db2, s);
 }
 
-cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, const float* dlogits,
-                                    const void* Wg, void* dx, cudaStream_t s, int slot_cols, int cols_per_rank) {
+cudaError_t launch_ep2_dispatch_bwd(const moe_ctx* c, const PeerTable& dxp, const int32_t* slot, int accumulate,
+                                    void* dx, cudaStream_t s, int slot_cols, int cols_per_rank) {
   if (c->T == 0) return cudaSuccess;
   const int SE = slot_cols > 0 ? slot_cols : c->E, SEl = cols_per_rank > 0 ? cols_per_rank : c->E_local;
   const unsigned grid = (c->T + 7) / 8;
-  if (dlogits && gate_tc_supported(c)) {
-    cudaError_t e = gate_tc_dx(c, dlogits, Wg, c->dxg, s);
-    if (e != cudaSuccess) return e;
-    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, bf16, QV><<<grid, 256, 0, s>>>(
-        dxp, slot, (const bf16*)c->dxg, c->T, c->d, SE, SEl, (bf16*)dx), count_launch())
-    return cudaGetLastError();
-  }
-  const float* dxg = nullptr;
-  if (dlogits) {
-    SimtGemm g{};
-    g.A = dlogits; g.sAm = c->E; g.sAk = 1;
-    g.B = Wg; g.sBk = 1; g.sBn = c->E;
-    g.C = c->dxg; g.sCm = c->d;
-    g.M = c->T; g.N = c->d; g.K = c->E; g.G = 1; g.k_split = 1;
-    cudaError_t e = launch_simt_gemm(g, 0, c->dtype, 0, EPI_F32, s);
-    if (e != cudaSuccess) return e;
-    dxg = c->dxg;
-  }
   if (c->dtype == 1) {
-    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, float, QV><<<grid, 256, 0, s>>>(
-        dxp, slot, dxg, c->T, c->d, SE, SEl, (bf16*)dx), count_launch())
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_dispatch_bwd_kernel<bf16, bf16, QV><<<grid, 256, 0, s>>>(
+        dxp, slot, accumulate ? (const bf16*)dx : nullptr, c->T, c->d, SE, SEl, (bf16*)dx), count_launch())
   } else {
     MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2_dispatch_bwd_kernel<float, float, QV><<<grid, 256, 0, s>>>(
-        dxp, slot, dxg, c->T, c->d, SE, SEl, (float*)dx), count_launch())
+        dxp, slot, accumulate ? (const float*)dx : nullptr, c->T, c->d, SE, SEl, (float*)dx), count_launch())
   }
   return cudaGetLastError();
 }
@@ -1399,18 +1380,21 @@ cudaError_t launch_ep2d_combine(const moe_ctx* c, const PeerTable& ys, const int
 // d_eout / dG / db2-partials kernel of the single-rank path
 cudaError_t launch_ep2d_combine_bwd(moe_ctx* c, const void* dyu, const void* e_out, const float* rgate,
                                     const int32_t* ruid, const int32_t* offsets, int64_t R_cap, void* d_eout,
-                                    float* dG_row, cudaStream_t s) {
-  c->db2_src = nullptr;
-  if (R_cap == 0) return cudaSuccess;
+                                    float* dG_row, float* db2, cudaStream_t s) {
+  if (R_cap == 0) return db2 ? cudaMemsetAsync(db2, 0, sizeof(float) * c->E_local * c->d, s) : cudaSuccess;
   const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
+  cudaError_t e;
   if (c->dtype == 1) {
-    if (nvec <= 32) return launch_cbc<bf16, 1>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
-    if (nvec <= 64) return launch_cbc<bf16, 2>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
-    if (nvec <= 96) return launch_cbc<bf16, 3>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
-    return launch_cbc<bf16, 4>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+    if (nvec <= 32) e = launch_cbc<bf16, 1>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+    else if (nvec <= 64) e = launch_cbc<bf16, 2>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+    else if (nvec <= 96) e = launch_cbc<bf16, 3>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+    else e = launch_cbc<bf16, 4>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+  } else if (nvec <= 32) {
+    e = launch_cbc<float, 1>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+  } else {
+    e = launch_cbc<float, 2>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
   }
-  if (nvec <= 32) return launch_cbc<float, 1>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
-  return launch_cbc<float, 2>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
+  return finish_db2(c, e, db2, s);
 }
 
 }  // namespace moe

@@ -12,12 +12,12 @@ Marshalling only: every step is a libmoe_dts.so kernel (moe_ep2_* + the expert F
 
     ranks = [EP2Rank(T, d, f, E, dtype, dev, r, W, syms) for r in range(W)]   # emulation
     EP2Rank.step_forward / step_backward run the phases of ONE rank (real multi-GPU: each
-    process calls them; barriers are NCCL all-reduces).  `run_lockstep` drives emulated
-    ranks phase by phase in one process.
+    process calls them; barriers are NCCL all-reduces).  The tests drive emulated ranks phase
+    by phase in one process (tests/_ep_lockstep.py).
 """
 from __future__ import annotations
 
-from typing import Dict, List, Optional
+from typing import Dict, Optional
 
 import torch
 
@@ -192,28 +192,29 @@ class EP2Rank:
     def bwd_combine(self):
         R, d, s = self.R_cap, self.d, self.st
         s["d_eout"] = torch.empty(R, d, dtype=self.dtype, device=self.device)
+        s["db2"] = torch.empty(self.El, d, dtype=torch.float32, device=self.device)   # fused into the same pass
         dG, _ = self._sym("dG", (R,), torch.float32)
         if self.dedup:
             L.moe_ep2d_combine_bwd(self.ctx, s["dyu"], self._sym("e_out", (R, d), self.dtype)[0],
                                    self._sym("rgate", (R,), torch.float32)[0], self._sym("ruid", (R,), torch.int32)[0],
-                                   s["off"], R, s["d_eout"], dG)
+                                   s["off"], R, s["d_eout"], dG, s["db2"])
             return
         L.moe_ep2_combine_bwd(self.ctx, self._sym("dy", (self.T, d), self.dtype)[1],
                               self._sym("e_out", (R, d), self.dtype)[0], self._sym("rgate", (R,), torch.float32)[0],
                               self._sym("rtok", (R,), torch.int32)[0], self._sym("rsrc", (R,), torch.int32)[0],
-                              s["off"], R, s["d_eout"], dG)
+                              s["off"], R, s["d_eout"], dG, s["db2"])
 
     def bwd_experts(self):
         R, d, f, El, s, dev = self.R_cap, self.d, self.f, self.El, self.st, self.device
         g = dict(dW1=torch.empty(El, f, d, dtype=torch.float32, device=dev),
                  db1=torch.empty(El, f, dtype=torch.float32, device=dev),
                  dW2=torch.empty(El, d, f, dtype=torch.float32, device=dev),
-                 db2=torch.empty(El, d, dtype=torch.float32, device=dev))
+                 db2=s["db2"])
         dxp, _ = self._sym("dx_perm", (R, d), self.dtype)
         xr = self._sym("x_recv", (R, d), self.dtype)[0]
         self._mark("experts_bwd", 0)
         L.moe_expert_ffn_bwd(self.ctx, s["d_eout"], xr, s["gp"], s["h"], s["off"], R, self.W1, self.W2, s["gp"], dxp,
-                             g["dW1"], g["db1"], g["dW2"], g["db2"])
+                             g["dW1"], g["db1"], g["dW2"], None)
         self._mark("experts_bwd", 1)
         s["grads"] = g
 
@@ -225,24 +226,28 @@ class EP2Rank:
                           self._sym("dxu", (self.U, d), self.dtype)[0])
 
     def bwd_gate(self, balance_alpha: float = 0.0, B_total: Optional[int] = None):
+        """dlogits, dW_g (this rank's tokens) and dx = dlogits W_g^T.  The balance term (Eq. 10)
+        uses the GLOBAL counts: the kernel sums this rank's copy of the all-gathered counts_all."""
         s, dev = self.st, self.device
         g = s["grads"]
         g["dWg"] = torch.empty(self.d, self.E, dtype=torch.float32, device=dev)
         g["dlogits"] = torch.empty(self.T, self.E, dtype=torch.float32, device=dev)
+        g["dx"] = torch.empty(self.T, self.d, dtype=self.dtype, device=dev)
         B = self.T * self.world if B_total is None else B_total
+        ca, _ = self._sym("counts_all", (self.world, self.E), torch.int32)
         L.moe_ep2_gate_bwd(self.ctx, self._sym("dG", (self.R_cap,), torch.float32)[1], s["slot"], s["probs"], s["x"],
-                           s["tau"], balance_alpha, s["counts"] if balance_alpha > 0 else None, B, g["dWg"],
-                           g["dlogits"])
+                           self.Wg, s["tau"], balance_alpha, ca if balance_alpha > 0 else None, B, g["dWg"],
+                           g["dlogits"], g["dx"])
 
     def bwd_dispatch(self):
+        """dx += the expert path's rows (gathered from the owners)."""
         s, g = self.st, self.st["grads"]
-        g["dx"] = torch.empty(self.T, self.d, dtype=self.dtype, device=self.device)
         if self.dedup:
-            L.moe_ep2d_dispatch_bwd(self.ctx, self._sym("dxu", (self.U, self.d), self.dtype)[1], s["uslot"],
-                                    g["dlogits"], self.Wg, g["dx"])
+            L.moe_ep2d_dispatch_bwd(self.ctx, self._sym("dxu", (self.U, self.d), self.dtype)[1], s["uslot"], True,
+                                    g["dx"])
         else:
             L.moe_ep2_dispatch_bwd(self.ctx, self._sym("dx_perm", (self.R_cap, self.d), self.dtype)[1], s["slot"],
-                                   g["dlogits"], self.Wg, g["dx"])
+                                   True, g["dx"])
         return g
 
     def check(self):
@@ -276,36 +281,3 @@ class EP2Rank:
         self.bwd_gate(balance_alpha)
         L.moe_ep_allreduce(self.ctx, self.st["grads"]["dWg"], self.d * self.E)
         return self.bwd_dispatch()
-
-
-def run_lockstep(ranks: List[EP2Rank], xs, us, dys, tau: float, threshold: float, top1: bool = False):
-    """Emulated ranks in one process: each phase runs on every rank before the next phase
-    (the barriers' ordering); dW_g is summed over the ranks (the all-reduce)."""
-    for r, x, u in zip(ranks, xs, us):
-        r.fwd_gate(x, u, tau, threshold, top1)
-    for r in ranks:
-        r.fwd_plan()
-    for r in ranks:
-        r.fwd_dispatch()
-    for r in ranks:
-        if r.dedup:
-            r.fwd_permute()
-        r.fwd_experts()
-        if r.dedup:
-            r.fwd_presum()
-    ys = [r.fwd_combine() for r in ranks]
-    for r, dy in zip(ranks, dys):
-        r.bwd_stage_dy(dy)
-    for r in ranks:
-        if r.dedup:
-            r.bwd_gather_dy()
-        r.bwd_combine()
-    for r in ranks:
-        r.bwd_experts()
-        if r.dedup:
-            r.bwd_presum()
-    for r in ranks:
-        r.bwd_gate()
-    dWg = sum(r.st["grads"]["dWg"] for r in ranks)
-    grads = [r.bwd_dispatch() for r in ranks]
-    return ys, grads, dWg

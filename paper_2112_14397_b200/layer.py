@@ -3,7 +3,8 @@ DTS-Gate MoE layer forward + backward.  Marshalling and buffer management only: 
 step of the path runs in libmoe_dts.so kernels (see include/moe_dts.h).
 
 Forward  : moe_dts_gate -> moe_dispatch -> moe_expert_ffn -> moe_combine
-Backward : moe_combine_bwd -> moe_expert_ffn_bwd -> moe_dts_gate_bwd -> moe_dispatch_bwd
+Backward : moe_combine_bwd (+ db2) -> moe_expert_ffn_bwd -> moe_dts_gate_bwd (dx = dL W_g^T) ->
+           moe_dispatch_bwd (dx += the expert path's rows)
 
 PyTorch provides device memory and streams only.
 """
@@ -236,12 +237,6 @@ class DTSMoELayer:
         rb = self._rows
         El, d, f, dev = self.E_local, self.d, self.f, self.device
         mark = _Marker(stage_events)
-        mark("combine_bwd", 0)
-        L.moe_combine_bwd(self.ctx, dy, rb["e_out"], rb["row_gate"], rb["row_token"], st.offsets, st.R_cap,
-                          rb["d_eout"], rb["dG_row"], stream)
-        mark("combine_bwd", 1)
-        if self.ep:
-            L.moe_ep_dispatch(self.ctx, rb["d_eout"], rb["d_eout_recv"], d, st.R_recv_cap, stream)
         grads = dict(
             dW1=torch.empty(El, f, d, dtype=torch.float32, device=dev),
             db1=torch.empty(El, f, dtype=torch.float32, device=dev),
@@ -249,6 +244,14 @@ class DTSMoELayer:
             db2=torch.empty(El, d, dtype=torch.float32, device=dev),
             dWg=torch.empty(d, self.E, dtype=torch.float32, device=dev),
         )
+        mark("combine_bwd", 0)
+        # single rank: db2 is summed from the d_eout rows in the same pass; under the NCCL exchange it
+        # is an expert-side sum over the received rows (moe_expert_ffn_bwd)
+        L.moe_combine_bwd(self.ctx, dy, rb["e_out"], rb["row_gate"], rb["row_token"], st.offsets, st.R_cap,
+                          rb["d_eout"], rb["dG_row"], None if self.ep else grads["db2"], stream)
+        mark("combine_bwd", 1)
+        if self.ep:
+            L.moe_ep_dispatch(self.ctx, rb["d_eout"], rb["d_eout_recv"], d, st.R_recv_cap, stream)
         if self.recompute:
             L.moe_expert_ffn_recompute(self.ctx, rb["x_recv"], st.offsets_recv, st.R_recv_cap, self.W1, self.b1,
                                        rb["gp"], rb["h"], stream)
@@ -258,7 +261,7 @@ class DTSMoELayer:
         mark("expert_ffn_bwd", 0)
         L.moe_expert_ffn_bwd(self.ctx, rb["d_eout_recv"], rb["x_recv"], rb["gp"], rb["h"], st.offsets_recv,
                              st.R_recv_cap, self.W1, self.W2, da, rb["dx_perm_recv"], grads["dW1"], grads["db1"],
-                             grads["dW2"], grads["db2"], stream)
+                             grads["dW2"], grads["db2"] if self.ep else None, stream)
         mark("expert_ffn_bwd", 1)
         if events:
             events[1].record()
@@ -270,15 +273,15 @@ class DTSMoELayer:
         if balance_alpha > 0 and self.ep:
             counts = st.counts.clone()
             L.moe_ep_allreduce(self.ctx, counts, self.E, is_int32=True, stream=stream)
+        dx = torch.empty(self.T, d, dtype=self.dtype, device=dev)
         mark("gate_bwd", 0)
-        L.moe_dts_gate_bwd(self.ctx, rb["dG_row"], st.slot, st.probs, st.x, st.tau, balance_alpha,
-                           counts if balance_alpha > 0 else None, B, grads["dWg"], dlogits, stream)
+        L.moe_dts_gate_bwd(self.ctx, rb["dG_row"], st.slot, st.probs, st.x, self.Wg, st.tau, balance_alpha,
+                           counts if balance_alpha > 0 else None, B, grads["dWg"], dlogits, dx, stream)
         mark("gate_bwd", 1)
         if self.ep:
             L.moe_ep_allreduce(self.ctx, grads["dWg"], d * self.E, stream=stream)
-        dx = torch.empty(self.T, d, dtype=self.dtype, device=dev)
         mark("dispatch_bwd", 0)
-        L.moe_dispatch_bwd(self.ctx, rb["dx_perm"], st.slot, dlogits, self.Wg, dx, stream)
+        L.moe_dispatch_bwd(self.ctx, rb["dx_perm"], st.slot, True, dx, stream)
         mark("dispatch_bwd", 1)
         grads["dx"] = dx
         grads["dlogits"] = dlogits

@@ -3,6 +3,7 @@
 the band procedure of SURVEY.md §8c.  Test infrastructure only."""
 from __future__ import annotations
 
+import re
 from dataclasses import dataclass
 from typing import Dict, Optional
 
@@ -25,6 +26,47 @@ def rel_err(got: np.ndarray, ref: np.ndarray) -> float:
     if den == 0.0:
         return float(num)
     return float(num / den)
+
+
+def row_err(got: np.ndarray, ref: np.ndarray) -> float:
+    """Worst per-row error (VERDICT r1 "per-row bound"): max over rows i of
+    ||got_i - ref_i|| / max(||ref_i||, median_j ||ref_j||).  A vector is treated as rows of one
+    element.  Unlike the tensor norm, one wrong row (or one wrong 32-column chunk of a row)
+    moves this by its own relative size, not by 1/sqrt(rows)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    if ref.size == 0:
+        return 0.0
+    if ref.ndim == 1:
+        got, ref = got[:, None], ref[:, None]
+    got = got.reshape(-1, ref.shape[-1])
+    ref = ref.reshape(-1, ref.shape[-1])
+    rn = np.linalg.norm(ref, axis=1)
+    floor = float(np.median(rn))
+    if floor == 0.0:
+        floor = float(rn.max()) if rn.max() > 0 else 1.0
+    dn = np.linalg.norm(got - ref, axis=1)
+    return float(np.max(dn / np.maximum(rn, floor)))
+
+
+def maxabs_rel(got: np.ndarray, ref: np.ndarray) -> float:
+    """max |got - ref| / max |ref| (reported beside the norm-wise error)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    if ref.size == 0:
+        return 0.0
+    den = float(np.abs(ref).max())
+    return float(np.abs(got - ref).max() / (den if den else 1.0))
+
+
+def check_values(rep: Dict[str, float], name: str, got: np.ndarray, ref: np.ndarray, tol: float) -> None:
+    """Record the three errors of one value tensor and assert the norm-wise and the per-row
+    bound (both at the BJ:5 tolerance); max-abs / max|ref| is reported, not bounded."""
+    rep[name] = rel_err(got, ref)
+    rep[name + ".row"] = row_err(got, ref)
+    rep[name + ".maxabs"] = maxabs_rel(got, ref)
+    assert rep[name] <= tol, f"{name}: norm-wise rel err {rep[name]:.3e} > {tol}"
+    assert rep[name + ".row"] <= tol, f"{name}: worst row rel err {rep[name + '.row']:.3e} > {tol}"
 
 
 def tol_for(cfg: MoEConfig) -> float:
@@ -66,11 +108,13 @@ def _np(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
 
 
-def run_gpu(cfg: MoEConfig, li: inputs.LayerInputs, backward: bool = True) -> GpuRun:
+def run_gpu(cfg: MoEConfig, li: inputs.LayerInputs, backward: bool = True, recompute: bool = False) -> GpuRun:
+    """recompute: NEXT #3 mode -- the forward keeps no [R, d_ff] activation; the gp rows checked
+    are the ones moe_expert_ffn_recompute rebuilt before the expert backward."""
     from paper_2112_14397_b200.layer import DTSMoELayer
     dev = torch.device("cuda", 0)
     T = li.x.shape[0]
-    layer = DTSMoELayer(T, cfg.d_model, cfg.d_ff, cfg.E, dtype=li.x.dtype, device=dev)
+    layer = DTSMoELayer(T, cfg.d_model, cfg.d_ff, cfg.E, dtype=li.x.dtype, device=dev, recompute=recompute)
     layer.set_gate(li.Wg.to(dev))
     layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
     u = li.u.to(dev) if li.u is not None else None
@@ -80,7 +124,12 @@ def run_gpu(cfg: MoEConfig, li: inputs.LayerInputs, backward: bool = True) -> Gp
     st = layer.state
     rb = layer.rows
     R = int(st.offsets[-1].item())
-    rows = {k: _np(rb[k][:R]) for k in ("x_perm", "row_token", "row_gate", "gp", "h", "e_out")}
+    rows = {k: _np(rb[k][:R]) for k in ("x_perm", "row_token", "row_gate", "h", "e_out")}
+    if not recompute:
+        rows["gp"] = _np(rb["gp"][:R])
+    else:
+        rb["gp"].fill_(float("nan"))            # the backward must rebuild it (and h) from x_perm
+        rb["h"].fill_(float("nan"))
     W = {k: _np(getattr(layer, k)) for k in ("W1", "b1", "W2", "b2")}
     run = GpuRun(layer, _np(y), _np(st.probs), _np(st.slot), _np(st.counts), int(st.near_band.item()),
                  _np(st.offsets), rows, W, None)
@@ -92,6 +141,8 @@ def run_gpu(cfg: MoEConfig, li: inputs.LayerInputs, backward: bool = True) -> Gp
         run.grads["da"] = _np(g["da"][:R])
         for k in ("d_eout", "dG_row", "dx_perm"):
             run.rows[k] = _np(rb[k][:R])
+        if recompute:
+            run.rows["gp"] = _np(rb["gp"][:R])   # inplace_da=False: still the recomputed GELU'(a)
     return run
 
 
@@ -140,28 +191,37 @@ def compare(cfg: MoEConfig, li: inputs.LayerInputs, g: GpuRun, backward: bool = 
     gp_ref = O.to_rows({e: O.gelu_prime(a) for e, a in fw.a.items()}, offsets, cfg.d_ff)
     h_ref = O.to_rows(fw.h, offsets, cfg.d_ff)
     e_ref = O.to_rows(fw.o, offsets, cfg.d_model)
-    rep["gp"] = rel_err(g.rows["gp"][valid], gp_ref[valid])       # saved GELU'(a)
-    rep["h"] = rel_err(g.rows["h"][valid], h_ref[valid])
-    rep["e_out"] = rel_err(g.rows["e_out"][valid], e_ref[valid])
-    rep["y"] = rel_err(g.y, fw.y)
+    # every value tensor: norm-wise AND per-row (each token row of y / dx, each permuted row of
+    # the row-layout tensors, each output row of the per-expert weight gradients)
+    if "gp" in g.rows:
+        check_values(rep, "gp", g.rows["gp"][valid], gp_ref[valid], tol)       # saved GELU'(a)
+    check_values(rep, "h", g.rows["h"][valid], h_ref[valid], tol)
+    check_values(rep, "e_out", g.rows["e_out"][valid], e_ref[valid], tol)
+    check_values(rep, "y", g.y, fw.y, tol)
     if backward:
         do_ref = O.to_rows(bw.do, offsets, cfg.d_model)
         dxe_ref = O.to_rows(bw.dxe, offsets, cfg.d_model)
-        rep["d_eout"] = rel_err(g.rows["d_eout"][valid], do_ref[valid])
+        check_values(rep, "d_eout", g.rows["d_eout"][valid], do_ref[valid], tol)
         assert not np.any(g.rows["d_eout"][~valid]), "d_eout pad rows not zero"
-        rep["dG_row"] = rel_err(g.rows["dG_row"][slot[toks, es]], bw.dG[toks, es])
-        rep["dx_perm"] = rel_err(g.rows["dx_perm"][valid], dxe_ref[valid])
-        rep["dx"] = rel_err(g.grads["dx"], bw.dx)
-        rep["dWg"] = rel_err(g.grads["dWg"], bw.dWg)
-        rep["dlogits"] = rel_err(g.grads["dlogits"], bw.dlogits)
+        check_values(rep, "dG_row", g.rows["dG_row"][slot[toks, es]], bw.dG[toks, es], tol)
+        check_values(rep, "dx_perm", g.rows["dx_perm"][valid], dxe_ref[valid], tol)
+        check_values(rep, "dx", g.grads["dx"], bw.dx, tol)
+        check_values(rep, "dWg", g.grads["dWg"], bw.dWg, tol)
+        check_values(rep, "dlogits", g.grads["dlogits"], bw.dlogits, tol)
         for k, ref in (("dW1", bw.dW1), ("db1", bw.db1), ("dW2", bw.dW2), ("db2", bw.db2)):
-            per = [rel_err(g.grads[k][e], ref[e]) for e in range(cfg.E) if fw.counts[e] > 0]
-            rep[k] = max(per) if per else 0.0
             for e in range(cfg.E):
-                if fw.counts[e] == 0:
+                if fw.counts[e] > 0:
+                    check_values(rep, f"{k}[{e}]", g.grads[k][e], ref[e], tol)
+                else:
                     assert not np.any(g.grads[k][e]), f"{k}[{e}] must be zero for an empty expert"
-    for k, v in rep.items():
-        if k in ("band_tokens", "mask_flips", "probs_maxabs"):
-            continue
-        assert v <= tol, f"{k}: rel err {v:.3e} > {tol} ({rep})"
     return rep
+
+
+def summary(rep: Dict[str, float]) -> Dict[str, float]:
+    """Compact report: the counts, and the worst norm-wise / per-row / max-abs error per tensor
+    (per-expert entries folded into their tensor name)."""
+    out: Dict[str, float] = {}
+    for k, v in rep.items():
+        base = re.sub(r"\[\d+\]", "", k)
+        out[base] = max(out.get(base, 0.0), v)
+    return out

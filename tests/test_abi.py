@@ -86,3 +86,23 @@ def test_status_codes_match_header():
     for code, name in {0: "MOE_OK", 1: "MOE_EINVAL", 2: "MOE_ESHAPE", 6: "MOE_ENONFINITE",
                        7: "MOE_ECAPACITY", 8: "MOE_EWORKSPACE"}.items():
         assert re.search(rf"{name}\s*=\s*{code}\b", src)
+
+
+def _prototypes():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    out = {}
+    for m in re.finditer(r"^\s*(?:int|size_t|uint64_t|const char\*)\s+(moe_\w+)\s*\(([^)]*)\)\s*;", src, flags=re.M):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def test_binding_arity_matches_header(L):
+    # every ctypes signature passes exactly the header's number of arguments (ABI v2 changed
+    # several: db2 out of combine_bwd, Wg / dx into gate_bwd, accumulate into dispatch_bwd)
+    protos = _prototypes()
+    assert set(protos) == set(L.SIGNATURES)
+    for name, n in protos.items():
+        assert len(L.SIGNATURES[name][1]) == n, (name, n, len(L.SIGNATURES[name][1]))
+    assert L.moe_abi_version() == 2

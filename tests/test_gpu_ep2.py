@@ -107,18 +107,18 @@ def _ep2(cfg, W, T):
     # ---- backward
     for q in range(W):
         L.moe_ep2_combine_bwd(ctx[q], sym["dy"], sym["e_out"][q], sym["rgate"][q], sym["rtok"][q], sym["rsrc"][q],
-                              loc[q]["off"], R_cap, sym["d_eout"][q], sym["dG"][q])
+                              loc[q]["off"], R_cap, sym["d_eout"][q], sym["dG"][q], loc[q]["db2"])
     for q in range(W):
         w, o = Wt[q], loc[q]
         L.moe_expert_ffn_bwd(ctx[q], sym["d_eout"][q], sym["x_recv"][q], o["gp"], o["h"], o["off"], R_cap, w["W1"],
-                             w["W2"], o["gp"], sym["dx_perm"][q], o["dW1"], o["db1"], o["dW2"], o["db2"])
+                             w["W2"], o["gp"], sym["dx_perm"][q], o["dW1"], o["db1"], o["dW2"], None)
     for q in range(W):
         o = loc[q]
-        L.moe_ep2_gate_bwd(ctx[q], sym["dG"], o["slot"], o["probs"], o["x"], tau, 0.0, None, W * T, o["dWg"],
-                           o["dlogits"])
+        L.moe_ep2_gate_bwd(ctx[q], sym["dG"], o["slot"], o["probs"], o["x"], Wg, tau, 0.0, None, W * T, o["dWg"],
+                           o["dlogits"], o["dx"])
     for q in range(W):
         o = loc[q]
-        L.moe_ep2_dispatch_bwd(ctx[q], sym["dx_perm"], o["slot"], o["dlogits"], Wg, o["dx"])
+        L.moe_ep2_dispatch_bwd(ctx[q], sym["dx_perm"], o["slot"], True, o["dx"])
     torch.cuda.synchronize()
     for q in range(W):
         L.moe_check(ctx[q])
@@ -145,8 +145,59 @@ def _single(cfg, ranks):
     return layer, y, g
 
 
+def _np(t):
+    return (t.float() if t.dtype == torch.bfloat16 else t).detach().cpu().numpy()
+
+
+def _vs_oracle(cfg, W, T, ranks_in, probs, slots, ys, dxs, dlogits, wgrads, dWg, y_tol=None, balance_alpha=0.0,
+               dy_scale=1.0):
+    """The W-rank result compared DIRECTLY with the fp64 oracle on the global token set (all
+    ranks' tokens concatenated), with the band procedure of SURVEY §8(c): probs <= 1e-5, the
+    mask bit-exact outside the band, every value tensor norm-wise and per row (y / dx /
+    dlogits per token, dW1 / dW2 per output row of every expert on its owner rank, db1 / db2,
+    dW_g summed over the ranks)."""
+    from _parity import band_tokens, check_values, f32, run_oracle, summary
+    import types
+    tol = 2e-2 if cfg.dtype == "bf16" else 1e-4
+    cat = lambda k: torch.cat([getattr(r, k) for r in ranks_in])  # noqa: E731
+    li = types.SimpleNamespace(**{k: getattr(ranks_in[0], k) for k in ("W1s", "b1s", "W2s", "b2s", "M1bits",
+                                                                        "M2bits", "Wg")})
+    li.x, li.u, li.dy = cat("x"), cat("u"), cat("dy") * dy_scale
+    p32 = np.concatenate([_np(t) for t in probs])
+    m_gpu = np.concatenate([_np(t) >= 0 for t in slots])
+    _, fw, _ = run_oracle(cfg, li, backward=False)
+    band = band_tokens(p32, m_gpu, f32(cfg.threshold), cfg.top1)
+    flips = np.any(fw.m != m_gpu, axis=1)
+    assert not np.any(flips & ~band), "routing mismatch outside the band"
+    _, fw, _ = run_oracle(cfg, li, mask_override=m_gpu, backward=False)
+    from oracle import dts_moe as O
+    bw = O.backward(fw, inputs.to_f64(li.dy), balance_alpha=balance_alpha)   # global counts, |B| = W*T (R21)
+    rep = {"band": int(band.sum()), "flips": int(flips.sum()),
+           "probs_maxabs": float(np.abs(p32 - fw.p).max())}
+    assert rep["probs_maxabs"] <= 1e-5, rep
+    check_values(rep, "y", np.concatenate([_np(t) for t in ys]), fw.y, y_tol or tol)
+    check_values(rep, "dx", np.concatenate([_np(t) for t in dxs]), bw.dx, y_tol or tol)
+    check_values(rep, "dlogits", np.concatenate([_np(t) for t in dlogits]), bw.dlogits, tol)
+    check_values(rep, "dWg", _np(dWg), bw.dWg, tol)
+    El = cfg.E // W
+    for q in range(W):
+        for j in range(El):
+            e = q * El + j
+            for k, ref in (("dW1", bw.dW1), ("db1", bw.db1), ("dW2", bw.dW2), ("db2", bw.db2)):
+                got = _np(wgrads[q][k][j])
+                if fw.counts[e]:
+                    check_values(rep, f"{k}[{e}]", got, ref[e], tol)
+                else:
+                    assert not np.any(got), f"{k}[{e}] of an empty expert must be zero"
+    print(cfg.name, f"W={W} T={T} vs oracle", summary(rep))
+    return rep
+
+
 def _check(cfg, W, T):
     ep, ranks = _ep2(cfg, W, T)
+    L_ = ep["loc"]
+    _vs_oracle(cfg, W, T, ranks, [o["probs"] for o in L_], [o["slot"] for o in L_], [o["y"] for o in L_],
+               [o["dx"] for o in L_], [o["dlogits"] for o in L_], L_, ep["dWg"])
     layer, y, g = _single(cfg, ranks)
     E, El = cfg.E, cfg.E // W
     st = layer.state
@@ -187,7 +238,8 @@ def test_ep2_fp32_c1_two_ranks():
 
 def test_ep2_module_lockstep_c2_shape(poison_empty):
     # the same through paper_2112_14397_b200.ep2 (EP2Rank phases + SymmetricBuffers emulation)
-    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers, run_lockstep
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
+    from _ep_lockstep import run_lockstep
     cfg, W, T = configs.C2, 2, 384
     dev = torch.device("cuda", 0)
     ranks_in = [inputs.make_inputs(cfg, rank=q, T=T) for q in range(W)]
@@ -215,8 +267,9 @@ def test_ep2_module_lockstep_c2_shape(poison_empty):
     assert _rel(dWg, g["dWg"]) < 1e-5
 
 
-def _lockstep(cfg, W, T, dedup):
-    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers, run_lockstep
+def _lockstep(cfg, W, T, dedup, balance_alpha=0.0, dy_scale=1.0):
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
+    from _ep_lockstep import run_lockstep
     dev = torch.device("cuda", 0)
     dt = inputs.TORCH_DTYPE[cfg.dtype]
     ranks_in = [inputs.make_inputs(cfg, rank=q, T=T) for q in range(W)]
@@ -229,13 +282,13 @@ def _lockstep(cfg, W, T, dedup):
         r.spawn(*(t.to(dev) for t in (li0.W1s, li0.b1s, li0.W2s, li0.b2s, li0.M1bits, li0.M2bits)))
         ranks.append(r)
     ys, grads, dWg = run_lockstep(ranks, [ri.x.to(dev) for ri in ranks_in], [ri.u.to(dev) for ri in ranks_in],
-                                  [ri.dy.to(dev) for ri in ranks_in], float(np.float32(cfg.tau)),
-                                  float(np.float32(cfg.threshold)), top1=cfg.top1)
+                                  [ri.dy.to(dev) * dy_scale for ri in ranks_in], float(np.float32(cfg.tau)),
+                                  float(np.float32(cfg.threshold)), top1=cfg.top1, balance_alpha=balance_alpha)
     torch.cuda.synchronize()
     for r in ranks:
         r.check()
     out = dict(y=[t.clone() for t in ys], g=[{k: v.clone() for k, v in g.items()} for g in grads], dWg=dWg.clone(),
-               slot=[r.st["slot"].clone() for r in ranks])
+               slot=[r.st["slot"].clone() for r in ranks], probs=[r.st["probs"].clone() for r in ranks])
     return out, ranks_in
 
 
@@ -261,6 +314,8 @@ def test_ep2_dedup_matches_single_rank(poison_empty, name, W, T):
     # to fp32 rounding (partial-sum partitions follow the local expert count).
     cfg = getattr(configs, name)
     ep, ranks_in = _lockstep(cfg, W, T, dedup=True)
+    _vs_oracle(cfg, W, T, ranks_in, ep["probs"], ep["slot"], ep["y"], [gq["dx"] for gq in ep["g"]],
+               [gq["dlogits"] for gq in ep["g"]], ep["g"], ep["dWg"])
     layer, y, g = _single(cfg, ranks_in)
     st = layer.state
     El = cfg.E // W
@@ -287,3 +342,17 @@ def test_ep2_dedup_single_owner_rows_are_exact(poison_empty):
     for q in range(4):
         assert torch.equal(a["y"][q], b["y"][q])
         assert torch.equal(a["g"][q]["dx"], b["g"][q]["dx"])
+
+
+@pytest.mark.parametrize("name,W,T,dedup", [("C1", 2, 96, False), ("C3", 4, 300, True), ("C3", 2, 256, False)])
+def test_ep2_balance_loss_uses_global_counts(poison_empty, name, W, T, dedup):
+    # the peer-memory EP gate backward must take the GLOBAL per-expert counts for the
+    # Eq. 10 term (|B| = the global batch, R21), not this rank's.  Compared with the
+    # oracle's balance-loss gradient on the global token set.
+    # With dy = 0 the balance term is the ONLY source of dlogits / dW_g / dx, so a rank-local count
+    # (1/W of the global one) fails the comparison outright.
+    cfg = getattr(configs, name)
+    for dy_scale in (1.0, 0.0):
+        ep, ranks_in = _lockstep(cfg, W, T, dedup=dedup, balance_alpha=0.1, dy_scale=dy_scale)
+        _vs_oracle(cfg, W, T, ranks_in, ep["probs"], ep["slot"], ep["y"], [gq["dx"] for gq in ep["g"]],
+                   [gq["dlogits"] for gq in ep["g"]], ep["g"], ep["dWg"], balance_alpha=0.1, dy_scale=dy_scale)

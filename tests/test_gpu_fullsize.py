@@ -41,7 +41,7 @@ def _rel(a, b):
 
 
 def fullsize(cfg, step=0, n_random=160, tail=32):
-    from _parity import band_tokens, f32
+    from _parity import band_tokens, check_values, f32, summary
     from paper_2112_14397_b200.layer import DTSMoELayer
     li = inputs.make_inputs(cfg, step=step)
     T, E = li.x.shape[0], cfg.E
@@ -85,9 +85,15 @@ def fullsize(cfg, step=0, n_random=160, tail=32):
                  inputs.bits_u32(li.M1bits), inputs.bits_u32(li.M2bits))
     fw = O.forward(x64[S], Wg64, u64[S], tau, c, ex, mask_override=m_gpu[S])
     bw = O.backward(fw, dy64[S])
-    rep["y"] = _rel(_np(y)[S], fw.y)
-    rep["dx"] = _rel(_np(g["dx"])[S], bw.dx)
-    rep["dlogits"] = _rel(_np(g["dlogits"])[S], bw.dlogits)
+    # per-token rows: norm-wise and per-row bounds (tests/_parity.check_values)
+    check_values(rep, "y", _np(y)[S], fw.y, tol)
+    check_values(rep, "dx", _np(g["dx"])[S], bw.dx, tol)
+    check_values(rep, "dlogits", _np(g["dlogits"])[S], bw.dlogits, tol)
+    # the permuted rows of the sampled tokens (row = slot[t, e]): e_out, d_eout, dx_perm
+    rows = np.concatenate([slot[S[fw.toks[e]], e] for e in sorted(fw.o)])
+    for name, per in (("e_out", fw.o), ("d_eout", bw.do), ("dx_perm", bw.dxe)):
+        ref = np.concatenate([per[e] for e in sorted(fw.o)])
+        check_values(rep, name, _np(layer.rows[name][torch.from_numpy(rows).to(dev).long()]), ref, tol)
 
     # ---- sampled experts: weight gradients over all of that expert's rows
     cnt = m_gpu.sum(0)
@@ -98,16 +104,14 @@ def fullsize(cfg, step=0, n_random=160, tail=32):
         fe = O.forward(x64[toks], Wg64, u64[toks], tau, c, ex, mask_override=only)
         be = O.backward(fe, dy64[toks])
         for k, ref in (("dW1", be.dW1[e]), ("db1", be.db1[e]), ("dW2", be.dW2[e]), ("db2", be.db2[e])):
-            rep[f"{k}[{e}]"] = _rel(_np(g[k][e]), ref) if len(toks) else float(np.abs(_np(g[k][e])).max())
+            if len(toks):
+                check_values(rep, f"{k}[{e}]", _np(g[k][e]), ref, tol)   # every output row of dW1 / dW2
+            else:
+                assert not np.any(_np(g[k][e])), f"{k}[{e}] of an empty expert must be zero"
 
     # ---- dW_g = x^T dlogits (property, fp64 product of the GPU's own dlogits)
-    rep["dWg_property"] = _rel(_np(g["dWg"]), x64.T @ _np(g["dlogits"]).astype(np.float64))
-    print(cfg.name, step, rep)
-    for k, v in rep.items():
-        if k in ("band", "flips", "probs_maxabs"):
-            continue
-        lim = 1e-3 if k == "dWg_property" else tol
-        assert v <= lim, (k, v, rep)
+    check_values(rep, "dWg_property", _np(g["dWg"]), x64.T @ _np(g["dlogits"]).astype(np.float64), 1e-3)
+    print(cfg.name, step, summary(rep))
     return rep
 
 

@@ -107,7 +107,8 @@ def test_no_out_of_bounds_writes(monkeypatch, name, cfg, recompute):
 def test_ep2_no_out_of_bounds_writes(monkeypatch, dedup):
     # the fused peer-memory EP path, 4 emulated ranks: every rank's symmetric and local buffers
     # guarded (peer stores land in other ranks' buffers, so a bad row index shows up here)
-    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers, run_lockstep
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
+    from _ep_lockstep import run_lockstep
     g = _Guarded()
     monkeypatch.setattr(torch, "empty", g.empty)
     monkeypatch.setattr(torch, "zeros", g.zeros)

@@ -24,12 +24,12 @@ def _built():
     build.build()
 
 
-def _run(cfg, T=None, step=0, with_noise=True, backward=True):
-    from _parity import compare, run_gpu
+def _run(cfg, T=None, step=0, with_noise=True, backward=True, recompute=False):
+    from _parity import compare, run_gpu, summary
     li = inputs.make_inputs(cfg, step=step, with_noise=with_noise, T=T)
-    g = run_gpu(cfg, li, backward=backward)
+    g = run_gpu(cfg, li, backward=backward, recompute=recompute)
     rep = compare(cfg, li, g, backward=backward)
-    print(cfg.name, T, rep)
+    print(cfg.name, T, "recompute" if recompute else "", summary(rep))
     return rep, g
 
 
@@ -231,6 +231,50 @@ def test_recompute_mode_matches_saved_mode(cfg_name, T):
     assert torch.equal(outs[0][0], outs[1][0])
     for k in outs[0][1]:
         assert torch.equal(outs[0][1][k], outs[1][1][k]), k
+
+
+@pytest.mark.parametrize("cfg_name,T,step", [("C1", None, 0), ("C3", 700, 0), ("C4", 512, 0), ("C5", 384, 0),
+                                              ("C5", 384, 19)])
+def test_recompute_mode_against_oracle(cfg_name, T, step):
+    """NEXT #3 against the fp64 oracle itself, not only against the saved mode: the
+    forward keeps no [R, d_ff] activation (gp and h are NaN-filled after it), the backward's
+    moe_expert_ffn_recompute rebuilds them from x_perm, and every output, intermediate and
+    gradient passes the same element / row / tensor checks as the saved-activation path."""
+    cfg = configs.get(cfg_name)
+    if cfg_name == "C5":
+        cfg = cfg.at_step(step)
+    rep, g = _run(cfg, T=T, step=step, recompute=True)
+    assert "gp" in rep and "h" in rep
+
+
+@pytest.mark.parametrize("cfg_name,T", [("C1", None), ("C3", 600)])
+def test_balance_gradient_alone(cfg_name, T):
+    """With dy = 0 the Eq. 10 term is the only source of the gate gradient: dlogits,
+    dW_g and dx (= dlogits W_g^T) against the oracle's balance-loss gradient, row by row."""
+    from _parity import check_values, f32, run_oracle
+    from oracle import dts_moe as O
+    from paper_2112_14397_b200.layer import DTSMoELayer
+    cfg = configs.get(cfg_name)
+    li = inputs.make_inputs(cfg, T=T)
+    T_ = li.x.shape[0]
+    dev = torch.device("cuda", 0)
+    layer = DTSMoELayer(T_, cfg.d_model, cfg.d_ff, cfg.E, dtype=li.x.dtype, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    layer.forward(li.x.to(dev), li.u.to(dev), f32(cfg.tau), f32(cfg.threshold))
+    g = layer.backward(torch.zeros_like(li.dy).to(dev), balance_alpha=0.1)
+    torch.cuda.synchronize()
+    layer.check()
+    m_gpu = (layer.state.slot >= 0).cpu().numpy()
+    _, fw, _ = run_oracle(cfg, li, mask_override=m_gpu, backward=False)
+    bw = O.backward(fw, np.zeros_like(inputs.to_f64(li.dy)), balance_alpha=0.1)
+    tol = 1e-4 if cfg.dtype == "f32" else 2e-2
+    rep = {}
+    check_values(rep, "dlogits", g["dlogits"].cpu().numpy(), bw.dlogits, tol)
+    check_values(rep, "dWg", g["dWg"].cpu().numpy(), bw.dWg, tol)
+    check_values(rep, "dx", g["dx"].float().cpu().numpy(), bw.dx, tol)
+    assert np.abs(bw.dlogits).max() > 0
+    print(cfg_name, rep)
 
 
 # ---- shapes off the benchmark grid: the other gate paths and partial GEMM tiles ----------
