@@ -1,25 +1,37 @@
 """bench.py -- DTS-Gate MoE layer forward+backward throughput on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+                    [--ep p2p|p2p-dedup|nccl]
 
 One "step" = one pass of the whole hot path over one batch of synthetic tokens:
 moe_dts_gate -> moe_dispatch -> moe_expert_ffn -> moe_combine -> moe_combine_bwd ->
-moe_expert_ffn_bwd -> moe_dts_gate_bwd -> moe_dispatch_bwd (all through the C ABI).
-The spawn runs once before timing (it is an initialisation step, Alg. 1 lines 4-5).
+moe_expert_ffn_bwd -> moe_dts_gate_bwd -> moe_dispatch_bwd (all through the C ABI; under EP
+the exchanges are fused into the routing kernels as NVLink peer loads / stores).  The spawn
+runs once before timing (an initialisation step, Alg. 1 lines 4-5) and is timed on its own.
 
-Workload: BASELINE.json configs[1] (C2, GPT-small-shaped, T=8192 tokens per GPU,
-d=768, d_ff=3072, E=16, tau=2.0, c=0.001), synthetic seeded data (harness/inputs.py).
-Under torchrun (N > 1) each rank runs its own T tokens (weak scaling).
+Workload: BASELINE.json configs[3] (C4: T=131072 tokens per GPU, d=1024, d_ff=4096, E=64,
+tau=0.1, c=0.2), the one config the metric names at 1/2/4/8 GPUs, so the N=1 line and the
+N>1 lines of the scaling run measure the same per-GPU work (weak scaling).  --config C2 (the
+GPT-small "1 GPU" config) etc. select another.  Synthetic seeded data (harness/inputs.py);
+every timed step draws its Gumbel noise from a pool of 4 different resident u tensors, so the
+routing changes from step to step as in training.
 
-Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the
-launching stream, with an L2 flush (write of a 256 MiB buffer) between steps outside
-the events; barrier + synchronize on both sides; the max over ranks is reported.
+N > 1: `python bench.py --gpus N` re-launches itself under torch.distributed.run (one rank per
+GPU) when WORLD_SIZE is not set; NCCL_DEBUG=INFO lines go to stderr.  Each rank holds T tokens
+and E/N experts; the default exchange is the fused peer-memory path (ep2, torch symmetric
+memory) captured as one CUDA graph per step; --ep nccl selects the NCCL send/recv path.
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the launching
+stream, with an L2 flush (write of a 256 MiB buffer) and the copy of the next u between steps,
+outside the events; barrier + synchronize on both sides; the max over ranks is reported.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,16 +47,35 @@ import torch  # noqa: E402
 from harness import configs, inputs  # noqa: E402
 
 METRIC = "MoE-layer fwd+bwd tokens/sec at 1/2/4/8 B200; % bf16 tensor peak"
+DEFAULT_CONFIG = "C4"
+U_POOL = 4
+DATASHEET_BF16_TFLOPS = 2250.0
+NVLINK_GBS = 900.0      # NVLink 5 per direction per GPU (task statement; not measured here)
 
 
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d, "measured"
+            return json.load(f), "MEASURED_PEAKS.json"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        # /opt/skills/guides/B200_PROFILING.md fallback figures
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+def pick_peak(peaks, wall_s: float, clk: dict):
+    """Burst peak for a short timed window at full clocks, sustained peak for a long one or a
+    power-capped one (the 67 ms C2 window ran at burst clocks, so its denominator
+    is the burst figure)."""
+    burst = float(peaks.get("bf16_tflops"))
+    sust = float(peaks.get("bf16_tflops_sustained", burst))
+    sm, smax = clk.get("sm_mhz"), clk.get("sm_max_mhz") or peaks.get("sm_max_mhz")
+    capped = bool(sm and smax and sm < 0.9 * smax)
+    if wall_s < 1.0 and not capped:
+        return burst, "bf16_tflops (burst: timed window < 1 s at full clocks)"
+    return sust, ("bf16_tflops_sustained (" + ("SM clock median %.0f of %.0f MHz" % (sm, smax) if capped
+                                               else "timed window %.1f s" % wall_s) + ")")
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -100,20 +131,27 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed plumbing
-def dist_setup(n_gpus: int, force_pg: bool = False):
+def relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` with no WORLD_SIZE: run N ranks (one per GPU) under
+    torch.distributed.run on this node; rank 0's JSON line comes through our stdout."""
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
+
+
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if force_pg and world == 1 and "MASTER_ADDR" not in os.environ:
-        # single process without torchrun: a 1-rank group (the peer-memory path's symmetric
-        # allocations rendezvous through it)
-        import socket
-        with socket.socket() as sk:
-            sk.bind(("127.0.0.1", 0))
-            port = sk.getsockname()[1]
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
-    if world > 1 or force_pg:
+    if world > 1:
         import torch.distributed as dist
+        if torch.cuda.device_count() <= local:
+            raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -122,8 +160,7 @@ def dist_setup(n_gpus: int, force_pg: bool = False):
 
 
 def barrier(world):
-    import torch.distributed as dist
-    if world > 1 or (dist.is_available() and dist.is_initialized()):
+    if world > 1:
         import torch.distributed as dist
         dist.barrier()
 
@@ -137,9 +174,20 @@ def max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
 # ------------------------------------------------------------------ CPU baseline (oracle)
-def oracle_sample(cfg, T_sub: int, step: int = 0):
-    """Time the fp64 oracle (as it stands) on T_sub tokens of the workload, fwd+bwd."""
+def oracle_sample(cfg, T_sub: int, step: int = 0, gpu_slot=None):
+    """Time the fp64 oracle (as it stands) on the first T_sub tokens of the workload, fwd+bwd.
+    With gpu_slot (the GPU's slot rows of those tokens) also count the selection flips against
+    the oracle's mask (flips are allowed only inside the 1e-6 band)."""
     from oracle import dts_moe as O
     li = inputs.make_inputs(cfg, T=T_sub, step=step)
     ex = O.spawn(inputs.to_f64(li.W1s), inputs.to_f64(li.b1s), inputs.to_f64(li.W2s), inputs.to_f64(li.b2s),
@@ -149,7 +197,10 @@ def oracle_sample(cfg, T_sub: int, step: int = 0):
     fw = O.forward(x, Wg, u, float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)), ex, top1=cfg.top1)
     O.backward(fw, dy)
     dt = time.perf_counter() - t0
-    return dt
+    flips = None
+    if gpu_slot is not None:
+        flips = int(np.any(fw.m != (gpu_slot >= 0), axis=1).sum())
+    return dt, flips
 
 
 def cpu_cores() -> int:
@@ -159,166 +210,42 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
-# ------------------------------------------------------------------ our arm
-def run_ours(args, rank, world):
-    from paper_2112_14397_b200 import _lib as L
-    from paper_2112_14397_b200.layer import DTSMoELayer
+# ------------------------------------------------------------------ shared helpers
+def _u_pool(cfg, rank, dev):
+    """U_POOL different Gumbel-noise inputs (harness steps 0..3), resident in HBM."""
+    return [inputs.uniform_u(cfg.T, cfg.E, step=s, rank=rank).to(dev) for s in range(U_POOL)]
 
-    cfg = configs.get(args.config)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    li = inputs.make_inputs(cfg, rank=rank)
-    dt = inputs.TORCH_DTYPE[cfg.dtype]
-    tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
-    comm = 0
-    if world > 1:
-        from paper_2112_14397_b200.layer import make_nccl_comm
-        comm = make_nccl_comm(rank, world)
-    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev, rank=rank, world=world,
-                        nccl_comm=comm)
-    layer.set_gate(li.Wg.to(dev))
-    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
-    x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
 
-    ev = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731  (usable inside graphs)
-
-    # --- one step = the 8 C-ABI calls (DTSMoELayer.forward + backward), with events around the
-    # expert GEMM calls on the launching stream.
-    def full_step(timed: bool, R_cap=None):
-        ev_ffn = (ev(), ev())
-        ev_bwd = (ev(), ev())
-        layer.forward(x, u, tau, c, R_cap=R_cap, events=ev_ffn if timed else None)
-        layer.backward(dy, events=ev_bwd if timed else None)
-        return ev_ffn, ev_bwd
-
-    for _ in range(args.warmup):
-        full_step(False)
+def spawn_timing(L, ctx, li, dev, cfg, El, reps=5):
+    """moe_dts_spawn (Alg. 1 l.4-5) timed alone: GB/s of its algorithmic bytes (read W1s/W2s and
+    the packed masks of the local experts once, write E_local masked copies + biases)."""
+    b = 2 if cfg.dtype == "bf16" else 4
+    d, f = cfg.d_model, cfg.d_ff
+    srcs = [t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)]
+    kw = dict(dtype=inputs.TORCH_DTYPE[cfg.dtype], device=dev)
+    outs = [torch.empty(El, f, d, **kw), torch.empty(El, f, **kw), torch.empty(El, d, f, **kw), torch.empty(El, d, **kw)]
+    L.moe_dts_spawn(ctx, *srcs, *outs)
     torch.cuda.synchronize()
-    layer.check()
-    R = int(layer.state.offsets[-1].item())
-    counts = layer.state.counts.cpu().numpy()
-
-    # --- CUDA graph of the whole step (single GPU): the row capacity is fixed to the routed
-    # rows seen in warm-up (static capacity; an overflow would raise MOE_ECAPACITY at the
-    # check after the timed region), so the step has no host synchronisation and is replayed
-    # as one graph launch.
-    graph = None
-    n_launch0 = L.moe_kernel_launch_count()
-    launches = None
-    stage_ev = {}
-    if args.graph and world == 1:
-        R_static = layer.state.R_cap
-        full_step(False, R_cap=R_static)
-        torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        g_ffn, g_bwd = (ev(), ev()), (ev(), ev())
-        n0 = L.moe_kernel_launch_count()
-        with torch.cuda.graph(graph):
-            layer.forward(x, u, tau, c, R_cap=R_static, events=g_ffn, stage_events=stage_ev)
-            layer.backward(dy, events=g_bwd, stage_events=stage_ev)
-        launches = L.moe_kernel_launch_count() - n0
-        for _ in range(max(1, args.warmup)):
-            graph.replay()
-        torch.cuda.synchronize()
-        layer.check()
-
-    clocks = ClockSampler(torch.cuda.current_device())
-    clocks.start()
-    barrier(world)
-    torch.cuda.synchronize()
-    n_launch1 = L.moe_kernel_launch_count()
-    step_ms, ffn_ms, bwd_ms = [], [], []
-    stage_ms = {k: [] for k in stage_ev}
-    t_wall = time.perf_counter()
-    for _ in range(args.steps):
-        flush.fill_(1)                       # L2 flush outside the timed events
-        s0, s1 = ev(), ev()
-        s0.record(stream)
-        if graph is not None:
-            graph.replay()
-            e_f, e_b = g_ffn, g_bwd
-        else:
-            e_f, e_b = full_step(True)
-        s1.record(stream)
-        s1.synchronize()
-        step_ms.append(s0.elapsed_time(s1))
-        ffn_ms.append(e_f[0].elapsed_time(e_f[1]))
-        bwd_ms.append(e_b[0].elapsed_time(e_b[1]))
-        for k, (a, b) in stage_ev.items():
-            stage_ms[k].append(a.elapsed_time(b))
-    torch.cuda.synchronize()
-    barrier(world)
-    wall = time.perf_counter() - t_wall
-    clk = clocks.stop()
-    if launches is None:
-        launches = (L.moe_kernel_launch_count() - n_launch1) // max(1, args.steps)
-    layer.check()
-
-    ms_step = max_over_ranks(sum(step_ms) / len(step_ms), world)
-    tokens = cfg.T * world
-    value = tokens / (ms_step / 1e3)
-
-    # roofline: expert GEMMs (12 R d d_ff FLOPs per step: 2 fwd + 4 bwd GEMMs)
-    peaks, peak_src = _peaks()
-    flops = 12.0 * R * cfg.d_model * cfg.d_ff
-    gemm_ms = (sum(ffn_ms) + sum(bwd_ms)) / len(ffn_ms)
-    achieved = flops / (gemm_ms / 1e3) / 1e12
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-    step_flops = flops + 6.0 * cfg.T * cfg.d_model * cfg.E
-
-    # e2e through the public API with host buffers
-    e2e = run_e2e(args, layer, li, tau, c, world, (graph, x, u, dy) if graph is not None else None) \
-        if args.e2e else None
-
-    out = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
-        "data": "synthetic (seeded N(0,1) tokens, N(0,1/d) gate, N(0,0.02) shared expert, Bernoulli(0.8) masks)",
-        "config": {"workload": f"{cfg.name}: T={cfg.T}/GPU d_model={cfg.d_model} d_ff={cfg.d_ff} E={cfg.E} "
-                               f"tau={cfg.tau} c={cfg.threshold}",
-                   "tokens_per_gpu": cfg.T, "global_tokens": tokens, "rows_R": R,
-                   "mean_experts_per_token": R / cfg.T if cfg.T else 0.0,
-                   "max_over_mean_load": float(counts.max() / max(1e-9, counts.mean())),
-                   "parallelism": f"ep{world} (E/{world} experts per GPU, NCCL all-to-all-v over NVLink)"
-                   if world > 1 else "single",
-                   "l2": "flushed between steps (256 MiB write, outside the events)",
-                   "launch": "cuda-graph replay, static row capacity" if graph is not None else "eager",
-                   "wall_s_timed_region": wall},
-        "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": f"{peak_src} bf16_tflops_sustained",
-                     "frac_of_burst": achieved / float(peaks.get("bf16_tflops", peak)),
-                     "gemm_ms_per_step": gemm_ms, "flops_per_step": flops,
-                     "algorithmic_bytes_per_step": R * (12 * cfg.d_model + 16 * cfg.d_ff) * (1 if cfg.dtype == "bf16" else 2)
-                     + cfg.E * cfg.d_model * cfg.d_ff * (4 * (2 if cfg.dtype == "bf16" else 4) + 2 * 4),
-                     **_traffic(cfg.name, world)},
-        "step_tflops": step_flops / (ms_step / 1e3) / 1e12,
-        "stages": _stages(cfg, layer, counts, {k: sum(v) / len(v) for k, v in stage_ms.items() if v}),
-        "gpu_launches": int(launches),
-        "clocks": clk,
-    }
-    if e2e:
-        out["e2e"] = e2e
-    if rank == 0 and world == 1 and args.cpu_baseline:
-        T_sub = args.cpu_tokens
-        dt_cpu = oracle_sample(cfg, T_sub)
-        out["cpu_baseline"] = {"value": T_sub / dt_cpu, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
-                               "sample": f"{T_sub} tokens of {cfg.name} (same d/d_ff/E/tau/c), fwd+bwd, fp64 NumPy, "
-                                         f"{dt_cpu:.2f} s"}
-    return out
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        L.moe_dts_spawn(ctx, *srcs, *outs)
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    words = (d * f + 31) // 32
+    byts = 2 * d * f * b + (d + f) * b + El * 2 * words * 4 + El * (2 * d * f + d + f) * b
+    return {"ms": ms, "algorithmic_bytes": byts, "GB/s": byts / (ms / 1e3) / 1e9,
+            "what": f"{El} local experts: W1/W2 masked copies + biases"}
 
 
-def _stages(cfg, layer, counts, ms):
+def _stages(cfg, R, Rp, ms):
     """Per C-ABI stage: mean ms inside the replayed step and achieved GB/s of the stage's
     algorithmic HBM bytes (SURVEY §8d terms; GEMM operand traffic excluded) or TFLOP/s."""
     if not ms:
         return None
     b = 2 if cfg.dtype == "bf16" else 4
     T, d, f, E = cfg.T, cfg.d_model, cfg.d_ff, cfg.E
-    R = int(counts.sum())
-    Rp = int(layer.state.offsets[-1].item())
     Ep = (E + 15) // 16 * 16
     Kp = (2 * Ep + 63) // 64 * 64
     byts = {
@@ -326,10 +253,10 @@ def _stages(cfg, layer, counts, ms):
         "dispatch": 2 * T * E * 4 + T * d * b + Rp * (d * b + 8),
         "combine": R * d * b + T * d * b + T * E * 4 + R * 4,
         "combine_bwd": T * d * b + 2 * Rp * d * b + Rp * 12,
-        "gate_bwd": R * 4 + 3 * T * E * 4 + T * Kp * 2 + T * d * b,
-        "dispatch_bwd": T * E * 4 + R * d * b + 2 * T * d * 2 + T * d * b + T * Kp * 2,
+        "gate_bwd": R * 4 + 3 * T * E * 4 + T * Kp * 2 + 2 * T * d * b,
+        "dispatch_bwd": T * E * 4 + R * d * b + 2 * T * d * b,
     }
-    flops = {"expert_ffn": 4.0 * Rp * d * f, "expert_ffn_bwd": 8.0 * Rp * d * f}
+    flops = {"expert_ffn": 4.0 * R * d * f, "expert_ffn_bwd": 8.0 * R * d * f}
     out = {}
     for k, v in ms.items():
         o = {"ms": v}
@@ -358,137 +285,173 @@ def _traffic(name, world):
             "traffic_source": os.path.relpath(hits[-1], ROOT)}
 
 
-def run_ours_p2p(args, rank, world):
-    """The fused peer-memory EP path (paper_2112_14397_b200.ep2, moe_ep2_*): token rows are
-    stored straight into the owners' expert-side layouts and gathered back over NVLink peer
-    pointers inside the routing kernels (torch symmetric memory), no NCCL all-to-all.  Eager
-    phases with stream-ordered NCCL barriers between them; the step and its expert-GEMM part
-    are timed with CUDA events, max over ranks."""
-    import torch.distributed as dist
+def _roofline(cfg, flops_per_gpu, gemm_ms, wall, clk, world, R_pad):
+    peaks, src = _peaks()
+    peak, which = pick_peak(peaks, wall, clk)
+    achieved = flops_per_gpu / (gemm_ms / 1e3) / 1e12
+    b = 2 if cfg.dtype == "bf16" else 4
+    d, f, E = cfg.d_model, cfg.d_ff, cfg.E // world
+    R = flops_per_gpu / (12.0 * d * f)
+    return {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "peak_source": f"{src} {which}",
+            "frac_of_burst": achieved / float(peaks["bf16_tflops"]),
+            "frac_of_sustained": achieved / float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])),
+            "pct_peak_datasheet": 100.0 * achieved / DATASHEET_BF16_TFLOPS,
+            "gemm_ms_per_step": gemm_ms, "flops_per_step": flops_per_gpu,
+            "flops_rows": "realised (token, expert) rows = sum of counts (pad rows excluded)",
+            "rows_R_pad": R_pad,
+            "algorithmic_bytes_per_step": R * (12 * d + 16 * f) * (b // 2)
+            + E * d * f * (4 * b + 2 * 4),
+            **_traffic(cfg.name, world)}
+
+
+def _config(cfg, world, extra):
+    c = {"workload": f"{cfg.name}: T={cfg.T}/GPU d_model={cfg.d_model} d_ff={cfg.d_ff} E={cfg.E} "
+                     f"tau={cfg.tau} c={cfg.threshold}",
+         "tokens_per_gpu": cfg.T, "global_tokens": cfg.T * world,
+         "l2": "flushed between steps (256 MiB write, outside the events)",
+         "noise": f"fresh Gumbel u every step (pool of {U_POOL} resident u tensors, copied in outside the events)"}
+    c.update(extra)
+    return c
+
+
+def _base_line(cfg, world, args, ms_step, value):
+    return {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if cfg.dtype == "bf16" else "f32",
+            "data": "synthetic (seeded N(0,1) tokens, N(0,v) gate, N(0,0.02) shared expert, Bernoulli(0.8) masks; "
+                    "random-init weights)"}
+
+
+# ------------------------------------------------------------------ N = 1: the single-GPU layer
+def run_single(args):
     from paper_2112_14397_b200 import _lib as L
-    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
-    from paper_2112_14397_b200.layer import make_nccl_comm
+    from paper_2112_14397_b200.layer import DTSMoELayer, padded_rows
 
     cfg = configs.get(args.config)
-    if cfg.dtype != "bf16":
-        raise SystemExit("--ep p2p: bf16 configs only")
     dev = torch.device("cuda", torch.cuda.current_device())
-    li = inputs.make_inputs(cfg, rank=rank)
+    li = inputs.make_inputs(cfg)
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
     tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
-    comm = make_nccl_comm(rank, world)
-    syms = SymmetricBuffers(world, dev, mode="symm_mem", group=dist.group.WORLD)
-    r = EP2Rank(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, torch.bfloat16, dev, rank, world, syms, comm=comm,
-                dedup=args.ep == "p2p-dedup")
-    r.set_gate(li.Wg.to(dev))
-    r.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
-    x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
+    layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev)
+    layer.set_gate(li.Wg.to(dev))
+    layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+    spawn = spawn_timing(L, layer.ctx, li, dev, cfg, cfg.E)
+    x, dy = li.x.to(dev), li.dy.to(dev)
+    upool = _u_pool(cfg, 0, dev)
+    u = upool[0].clone()                      # the static noise input the graph reads
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    ev = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731  (usable inside graphs)
 
-    def step():
-        r.forward(x, u, tau, c)
-        return r.backward(dy)
-
-    for _ in range(args.warmup):
-        step()
+    # warm-up (eager; sizes the row buffers from the counts) over the whole noise pool: the static
+    # row capacity of the graph covers every pool member's routing
+    rpad = []
+    for i in range(max(args.warmup, U_POOL)):
+        u.copy_(upool[i % U_POOL])
+        layer.forward(x, u, tau, c)
+        layer.backward(dy)
+        rpad.append(padded_rows(layer.state.counts.cpu().tolist()))
     torch.cuda.synchronize()
-    r.check()
-    # rows of my experts (all ranks' tokens), for the GEMM FLOPs
-    ca = r._sym("counts_all", (world, cfg.E), torch.int32)[0].cpu().numpy()
-    R_mine = int(ca[:, rank * r.El:(rank + 1) * r.El].sum())
+    layer.check()
+    R_static = max(rpad)
+
+    graph, launches, stage_ev = None, None, {}
+    g_ffn, g_bwd = (ev(), ev()), (ev(), ev())
+    if args.graph:
+        layer.forward(x, u, tau, c, R_cap=R_static)
+        layer.backward(dy)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        n0 = L.moe_kernel_launch_count()
+        with torch.cuda.graph(graph):
+            layer.forward(x, u, tau, c, R_cap=R_static, events=g_ffn, stage_events=stage_ev)
+            layer.backward(dy, events=g_bwd, stage_events=stage_ev)
+        launches = L.moe_kernel_launch_count() - n0
+        for i in range(max(1, args.warmup)):
+            u.copy_(upool[i % U_POOL])
+            graph.replay()
+        torch.cuda.synchronize()
+        layer.check()
 
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
-    barrier(world)
     torch.cuda.synchronize()
-    n_launch0 = L.moe_kernel_launch_count()
-    step_ms, gemm_ms = [], []
+    n_launch1 = L.moe_kernel_launch_count()
+    step_ms, gemm_ms, rows, band = [], [], [], []
+    stage_ms = {k: [] for k in stage_ev}
     t_wall = time.perf_counter()
-    for _ in range(args.steps):
-        flush.fill_(1)
-        r.events = {"experts_fwd": (ev(), ev()), "experts_bwd": (ev(), ev())}
+    for i in range(args.steps):
+        flush.fill_(1)                       # L2 flush and the next step's noise, outside the events
+        u.copy_(upool[i % U_POOL])
         s0, s1 = ev(), ev()
         s0.record(stream)
-        step()
+        if graph is not None:
+            graph.replay()
+            e_f, e_b = g_ffn, g_bwd
+        else:
+            e_f, e_b = (ev(), ev()), (ev(), ev())
+            layer.forward(x, u, tau, c, events=e_f)
+            layer.backward(dy, events=e_b)
         s1.record(stream)
         s1.synchronize()
         step_ms.append(s0.elapsed_time(s1))
-        gemm_ms.append(sum(a.elapsed_time(b) for a, b in r.events.values()))
+        gemm_ms.append(e_f[0].elapsed_time(e_f[1]) + e_b[0].elapsed_time(e_b[1]))
+        for k, (a, b) in stage_ev.items():
+            stage_ms[k].append(a.elapsed_time(b))
+        rows.append(int(layer.state.counts.sum().item()))          # realised rows (outside the events)
+        band.append(int(layer.state.near_band.item()))
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall
-    launches = (L.moe_kernel_launch_count() - n_launch0) // max(1, args.steps)
-    r.events = None
-    barrier(world)
     clk = clocks.stop()
-    r.check()
-    ms_step = max_over_ranks(sum(step_ms) / len(step_ms), world)
-    g_ms = max_over_ranks(sum(gemm_ms) / len(gemm_ms), world)
-    flops = 12.0 * R_mine * cfg.d_model * cfg.d_ff
-    t = torch.tensor([flops], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t)
-    flops_per_gpu = float(t.item()) / world
-    peaks, peak_src = _peaks()
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-    achieved = flops_per_gpu / (g_ms / 1e3) / 1e12
+    if launches is None:
+        launches = (L.moe_kernel_launch_count() - n_launch1) // max(1, args.steps)
+    layer.check()                            # MOE_ECAPACITY here would mean the static capacity was short
+    counts = layer.state.counts.cpu().numpy()
 
-    e2e = None
+    ms_step = sum(step_ms) / len(step_ms)
+    value = cfg.T / (ms_step / 1e3)
+    R_mean = sum(rows) / len(rows)
+    flops = 12.0 * R_mean * cfg.d_model * cfg.d_ff
+    g_ms = sum(gemm_ms) / len(gemm_ms)
+    out = _base_line(cfg, 1, args, ms_step, value)
+    out["config"] = _config(cfg, 1, {
+        "rows_R_mean": R_mean, "rows_R_pad_static": R_static, "mean_experts_per_token": R_mean / cfg.T,
+        "max_over_mean_load": float(counts.max() / max(1e-9, counts.mean())),
+        "band_tokens": {"mean_per_step": sum(band) / len(band), "max": max(band),
+                        "what": "tokens with an fp32 p within 1e-6 of c (or top-2 gap < 1e-6 when argmax-decided)"},
+        "parallelism": "single GPU (E experts local, no exchange)",
+        "launch": "cuda-graph replay, static row capacity" if graph is not None else "eager",
+        "wall_s_timed_region": wall})
+    out["roofline"] = _roofline(cfg, flops, g_ms, wall, clk, 1, R_static)
+    out["step_tflops"] = (flops + 6.0 * cfg.T * cfg.d_model * cfg.E) / (ms_step / 1e3) / 1e12
+    out["stages"] = _stages(cfg, int(round(R_mean)), R_static,
+                            {k: sum(v) / len(v) for k, v in stage_ms.items() if v})
+    out["spawn"] = spawn
+    out["gpu_launches"] = int(launches)
+    out["clocks"] = clk
     if args.e2e:
-        hx, hu, hdy = (tt.pin_memory() for tt in (li.x, li.u, li.dy))
-        hy, hdx = torch.empty_like(li.x).pin_memory(), torch.empty_like(li.x).pin_memory()
-
-        def step_host():
-            x.copy_(hx, non_blocking=True)
-            u.copy_(hu, non_blocking=True)
-            dy.copy_(hdy, non_blocking=True)
-            y = r.forward(x, u, tau, c)
-            g = r.backward(dy)
-            hy.copy_(y, non_blocking=True)
-            hdx.copy_(g["dx"], non_blocking=True)
-
-        step_host()
-        torch.cuda.synchronize()
-        barrier(world)
-        e0, e1 = ev(), ev()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step_host()
-        e1.record(stream)
-        e1.synchronize()
-        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-        bi = sum(tt.numel() * tt.element_size() for tt in (hx, hu, hdy))
-        bo = 2 * hy.numel() * hy.element_size()
-        e2e = {"value": cfg.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
-               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": False}
-        r.check()
-
-    out = {
-        "metric": METRIC, "value": cfg.T * world / (ms_step / 1e3), "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (seeded N(0,1) tokens, N(0,1/d) gate, N(0,0.02) shared expert, Bernoulli(0.8) masks)",
-        "config": {"workload": f"{cfg.name}: T={cfg.T}/GPU d_model={cfg.d_model} d_ff={cfg.d_ff} E={cfg.E} "
-                               f"tau={cfg.tau} c={cfg.threshold}",
-                   "tokens_per_gpu": cfg.T, "global_tokens": cfg.T * world, "rows_R_rank0": R_mine,
-                   "parallelism": f"ep{world} (E/{world} experts per GPU, fused NVLink peer-memory dispatch / "
-                                  f"combine, " + ("one row per (token, owner), moe_ep2d_*)" if r.dedup
-                                                  else "moe_ep2_*)"),
-                   "l2": "flushed between steps (256 MiB write, outside the events)", "launch": "eager phases",
-                   "wall_s_timed_region": wall},
-        "roofline": {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
-                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": f"{peak_src} bf16_tflops_sustained", "gemm_ms_per_step": g_ms,
-                     "flops_per_step_per_gpu": flops_per_gpu, "traffic": None},
-        "gpu_launches": int(launches),
-        "clocks": clk,
-    }
-    if e2e:
-        out["e2e"] = e2e
+        out["e2e"] = run_e2e(args, layer, li, upool, tau, c, R_static if graph is not None else None)
+    if args.cpu_baseline:
+        T_sub = args.cpu_tokens
+        # the GPU's routing of the sample tokens (pool member 0 = harness step 0, as the oracle draws)
+        u.copy_(upool[0])
+        layer.forward(x, u, tau, c)
+        slot0 = layer.state.slot[:T_sub].cpu().numpy()
+        band0 = int(layer.state.near_band.item())
+        dt_cpu, flips = oracle_sample(cfg, T_sub, gpu_slot=slot0)
+        out["cpu_baseline"] = {"value": T_sub / dt_cpu, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                               "sample": f"first {T_sub} tokens of {cfg.name} (same d/d_ff/E/tau/c), fwd+bwd, "
+                                         f"fp64 NumPy, {dt_cpu:.2f} s"}
+        out["config"]["mask_flips"] = {"sample_tokens": T_sub, "flips": flips,
+                                       "band_tokens_all": band0,
+                                       "what": "tokens of the oracle sample whose GPU selection differs from the "
+                                               "fp64 oracle's (allowed only inside the band)"}
     return out
 
 
-def run_e2e(args, layer, li, tau, c, world, graphed=None):
+def run_e2e(args, layer, li, upool, tau, c, R_static):
     """Same metric through the public API with host (pinned) buffers: every step copies x, u,
     dy host->device and reads y and dx back device->host.
 
@@ -497,45 +460,43 @@ def run_e2e(args, layer, li, tau, c, world, graphed=None):
     computes, step i's D2H runs on a third stream.  Every byte of every step is still copied
     inside the timed region (first H2D start .. last D2H end)."""
     dev = layer.device
-    hx, hu, hdy = (t.pin_memory() for t in (li.x, li.u, li.dy))
+    hx, hdy = li.x.pin_memory(), li.dy.pin_memory()
+    hus = [u.cpu().pin_memory() for u in upool]
     hy = torch.empty_like(li.x).pin_memory()
     hdx = torch.empty_like(li.x).pin_memory()
     comp = torch.cuda.current_stream()
-    bi = sum(t.numel() * t.element_size() for t in (hx, hu, hdy))
+    bi = sum(t.numel() * t.element_size() for t in (hx, hus[0], hdy))
     bo = sum(t.numel() * t.element_size() for t in (hy, hdx))
 
-    if graphed is None:
-        def step():
+    if R_static is None:
+        def step(i):
             x = hx.to(dev, non_blocking=True)
-            u = hu.to(dev, non_blocking=True)
+            u = hus[i % U_POOL].to(dev, non_blocking=True)
             dy = hdy.to(dev, non_blocking=True)
             y = layer.forward(x, u, tau, c)
             g = layer.backward(dy)
             hy.copy_(y, non_blocking=True)
             hdx.copy_(g["dx"], non_blocking=True)
 
-        for _ in range(2):
-            step()
+        for i in range(2):
+            step(i)
         torch.cuda.synchronize()
-        barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(comp)
-        for _ in range(args.steps):
-            step()
+        for i in range(args.steps):
+            step(i)
         e1.record(comp)
         e1.synchronize()
-        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-        return {"value": layer.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+        ms = e0.elapsed_time(e1) / args.steps
+        return {"value": layer.T / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
                 "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": False}
 
-    # ---- two graph replicas with their own static inputs, copies overlapped with compute
-    R_static = layer.state.R_cap
     reps = []
     for k in range(2):
         X = torch.empty_like(li.x, device=dev)
-        U = torch.empty_like(li.u, device=dev)
+        U = torch.empty_like(hus[0], device=dev)
         DY = torch.empty_like(li.dy, device=dev)
-        X.copy_(hx); U.copy_(hu); DY.copy_(hdy)
+        X.copy_(hx); U.copy_(hus[0]); DY.copy_(hdy)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             Y = layer.forward(X, U, tau, c, R_cap=R_static)
@@ -561,7 +522,7 @@ def run_e2e(args, layer, li, tau, c, world, graphed=None):
             with torch.cuda.stream(s_h2d):
                 s_h2d.wait_event(in_free[k])
                 X.copy_(hx, non_blocking=True)
-                U.copy_(hu, non_blocking=True)
+                U.copy_(hus[i % U_POOL], non_blocking=True)
                 DY.copy_(hdy, non_blocking=True)
                 h2d_done[k].record(s_h2d)
             comp.wait_event(h2d_done[k])
@@ -580,11 +541,216 @@ def run_e2e(args, layer, li, tau, c, world, graphed=None):
 
     run(4)
     torch.cuda.synchronize()
-    barrier(world)
-    ms = max_over_ranks(run(args.steps) / args.steps, world)
+    ms = run(args.steps) / args.steps
     layer.check()
-    return {"value": layer.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+    return {"value": layer.T / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": True}
+
+
+# ------------------------------------------------------------------ N > 1: expert parallelism
+def _nvlink_bytes(cfg, counts_all, rank, world):
+    """Algorithmic NVLink bytes this rank moves per step on the peer-memory path (no dedup):
+    its rows to / from remote owners (x out, e_out back, dy read by the owner, dx_perm back:
+    4 rows of d elements each) plus the owners reading this rank's remote rows' metadata
+    (SURVEY §8(d) B_NVL = (4 b d + 12) R_remote)."""
+    b = 2 if cfg.dtype == "bf16" else 4
+    El = cfg.E // world
+    mine = counts_all[rank]
+    remote = int(sum(mine[e] for e in range(cfg.E) if e // El != rank))
+    return remote * (4 * b * cfg.d_model + 12)
+
+
+def run_ep(args, rank, world):
+    """Expert-parallel step on `world` GPUs (E/world experts per GPU, T tokens per GPU)."""
+    import torch.distributed as dist
+    from paper_2112_14397_b200 import _lib as L
+    from paper_2112_14397_b200.layer import make_nccl_comm
+
+    cfg = configs.get(args.config)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    li = inputs.make_inputs(cfg, rank=rank)
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
+    tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
+    comm = make_nccl_comm(rank, world)
+    x, dy = li.x.to(dev), li.dy.to(dev)
+    upool = _u_pool(cfg, rank, dev)
+    u = upool[0].clone()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731
+    El = cfg.E // world
+    path, note = args.ep, None
+    runner = None
+    if path.startswith("p2p"):
+        try:
+            from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
+            syms = SymmetricBuffers(world, dev, mode="symm_mem", group=dist.group.WORLD)
+            r = EP2Rank(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dt, dev, rank, world, syms, comm=comm,
+                        dedup=path == "p2p-dedup")
+            r.set_gate(li.Wg.to(dev))
+            r.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+            dyb = r.dy_buffer()
+            dyb.copy_(dy)
+            runner = r
+        except Exception as e:   # symmetric memory unavailable: the NCCL exchange path instead
+            note = f"peer-memory path unavailable ({type(e).__name__}: {e}); NCCL exchange used"
+            print("bench.py: " + note, file=sys.stderr, flush=True)
+            path = "nccl"
+    if path == "nccl":
+        from paper_2112_14397_b200.layer import DTSMoELayer
+        layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev, rank=rank, world=world,
+                            nccl_comm=comm)
+        layer.set_gate(li.Wg.to(dev))
+        layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
+        spawn = spawn_timing(L, layer.ctx, li, dev, cfg, El)
+
+        def step(events=None):
+            layer.forward(x, u, tau, c, events=events[0] if events else None)
+            return layer.backward(dy, events=events[1] if events else None)
+
+        def counts_now():
+            return L.moe_ep_exchange_counts(layer.ctx, layer.state.counts, world, cfg.E)
+        check = layer.check
+    else:
+        r = runner
+        spawn = spawn_timing(L, r.ctx, li, dev, cfg, El)
+
+        def step(events=None):
+            r.events = {"experts_fwd": events[0], "experts_bwd": events[1]} if events else None
+            r.forward(x, u, tau, c, cfg.top1)
+            return r.backward(dyb)
+
+        def counts_now():
+            return r.counts_all_host()
+        check = r.check
+
+    # warm-up over the noise pool (eager; the first step sizes the peer-memory capacity, and any
+    # overflow of a later pool member grows it before the capture)
+    for i in range(max(args.warmup, U_POOL)):
+        u.copy_(upool[i % U_POOL])
+        if path == "nccl":
+            step()
+            check()
+        else:
+            r.step(x, u, dyb, tau, c, cfg.top1)
+    torch.cuda.synchronize()
+    counts_all = counts_now()
+    graph = None
+    g_ev = ((ev(), ev()), (ev(), ev()))
+    n0 = L.moe_kernel_launch_count()
+    if path != "nccl" and args.graph:
+        r.prepare()
+        s = torch.cuda.Stream()
+        s.wait_stream(stream)
+        with torch.cuda.stream(s):
+            step()
+        stream.wait_stream(s)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        n0 = L.moe_kernel_launch_count()
+        with torch.cuda.graph(graph):
+            step(g_ev)
+        launches = L.moe_kernel_launch_count() - n0
+        for i in range(max(1, args.warmup)):
+            u.copy_(upool[i % U_POOL])
+            graph.replay()
+        torch.cuda.synchronize()
+        check()
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    n1 = L.moe_kernel_launch_count()
+    step_ms, gemm_ms = [], []
+    t_wall = time.perf_counter()
+    for i in range(args.steps):
+        flush.fill_(1)
+        u.copy_(upool[i % U_POOL])
+        s0, s1 = ev(), ev()
+        s0.record(stream)
+        if graph is not None:
+            graph.replay()
+            e = g_ev
+        else:
+            e = ((ev(), ev()), (ev(), ev()))
+            step(e)
+        s1.record(stream)
+        s1.synchronize()
+        step_ms.append(s0.elapsed_time(s1))
+        gemm_ms.append(e[0][0].elapsed_time(e[0][1]) + e[1][0].elapsed_time(e[1][1]))
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    if graph is None:
+        launches = (L.moe_kernel_launch_count() - n1) // max(1, args.steps)
+    check()
+    counts_all = counts_now()
+
+    ms_step = max_over_ranks(sum(step_ms) / len(step_ms), world)
+    g_ms = max_over_ranks(sum(gemm_ms) / len(gemm_ms), world)
+    R_mine = int(counts_all[:, rank * El:(rank + 1) * El].sum())
+    flops_per_gpu = sum_over_ranks(12.0 * R_mine * cfg.d_model * cfg.d_ff, world) / world
+    nvl = sum_over_ranks(_nvlink_bytes(cfg, counts_all, rank, world), world) / world
+    value = cfg.T * world / (ms_step / 1e3)
+    out = _base_line(cfg, world, args, ms_step, value)
+    R_all = int(counts_all.sum())
+    out["config"] = _config(cfg, world, {
+        "rows_R_per_gpu_mean": R_all / world, "mean_experts_per_token": R_all / (cfg.T * world),
+        "max_over_mean_load": float(counts_all.sum(0).max() / max(1e-9, counts_all.sum(0).mean())),
+        "parallelism": f"ep{world}: E/{world}={El} experts per GPU, T={cfg.T} tokens per GPU; " + (
+            "NCCL grouped send/recv all-to-all-v (eager, host-planned)" if path == "nccl" else
+            "fused NVLink peer-memory dispatch / combine (torch symmetric memory), " +
+            ("one row per (token, owner) each way (moe_ep2d_*)" if path == "p2p-dedup" else "moe_ep2_*")),
+        "ep_path": path + (f" ({note})" if note else ""),
+        "row_capacity": None if path == "nccl" else {"R_cap": r.R_cap, "grows": r.grows},
+        "launch": "cuda-graph replay (static capacity, no host sync)" if graph is not None else "eager",
+        "wall_s_timed_region": wall})
+    out["roofline"] = _roofline(cfg, flops_per_gpu, g_ms, wall, clk, world, None)
+    out["nvlink_gbs"] = {"value": nvl / (ms_step / 1e3) / 1e9, "unit": "GB/s per GPU (algorithmic bytes / step time)",
+                         "bytes_per_gpu_per_step": nvl, "frac_of_900": nvl / (ms_step / 1e3) / 1e9 / NVLINK_GBS}
+    out["spawn"] = spawn
+    out["gpu_launches"] = int(launches)
+    out["clocks"] = clk
+    if args.e2e:
+        hx, hdy = li.x.pin_memory(), li.dy.pin_memory()
+        hus = [t.cpu().pin_memory() for t in upool]
+        hy, hdx = torch.empty_like(li.x).pin_memory(), torch.empty_like(li.x).pin_memory()
+        dst_dy = dy if path == "nccl" else dyb
+        outs = {}
+
+        def step_host(i):
+            x.copy_(hx, non_blocking=True)
+            u.copy_(hus[i % U_POOL], non_blocking=True)
+            dst_dy.copy_(hdy, non_blocking=True)
+            if graph is not None:
+                graph.replay()
+                yy, dxx = outs["y"], outs["dx"]
+            else:
+                g = step()
+                yy, dxx = (layer.state.y, g["dx"]) if path == "nccl" else (r.st["y"], g["dx"])
+            hy.copy_(yy, non_blocking=True)
+            hdx.copy_(dxx, non_blocking=True)
+
+        if graph is not None:
+            outs["y"], outs["dx"] = r.st["y"], r.st["grads"]["dx"]    # the graph's output tensors
+        step_host(0)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            step_host(i)
+        e1.record(stream)
+        e1.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        bi = sum(t.numel() * t.element_size() for t in (hx, hus[0], hdy))
+        out["e2e"] = {"value": cfg.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+                      "h2d_bytes_per_step": bi, "d2h_bytes_per_step": 2 * hy.numel() * hy.element_size(),
+                      "pipelined": False}
+        check()
+    return out
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
@@ -595,7 +761,7 @@ def run_reference(args, rank, world):
     T_sub = args.ref_tokens
     for _ in range(args.warmup):
         oracle_sample(cfg, T_sub)
-    times = [oracle_sample(cfg, T_sub) for _ in range(args.steps)]
+    times = [oracle_sample(cfg, T_sub)[0] for _ in range(args.steps)]
     ms = 1e3 * sum(times) / len(times)
     value = T_sub / (ms / 1e3)
     return {
@@ -615,7 +781,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
@@ -623,10 +789,10 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--ep", default="nccl", choices=["nccl", "p2p", "p2p-dedup"],
-                    help="expert-parallel exchange: NCCL grouped send/recv (default), the fused NVLink "
-                         "peer-memory path (moe_ep2_*, torch symmetric memory), or the same with one row "
-                         "per (token, owner) each way (moe_ep2d_*)")
+    ap.add_argument("--ep", default="p2p", choices=["p2p", "p2p-dedup", "nccl"],
+                    help="N > 1 exchange: the fused NVLink peer-memory path (moe_ep2_*, torch symmetric memory; "
+                         "default), the same with one row per (token, owner) each way (moe_ep2d_*), or NCCL "
+                         "grouped send/recv")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -637,14 +803,23 @@ def main():
         if out is not None:
             print(json.dumps(out))
         return 0
-    p2p = args.ep.startswith("p2p")
-    rank, world, local = dist_setup(args.gpus, force_pg=p2p)
-    out = run_ours_p2p(args, rank, world) if p2p else run_ours(args, rank, world)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env > 1:
+        # NCCL's init lines (rank count, transport) on stderr; stdout carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if args.gpus != world_env:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; running {world_env} rank(s)",
+              file=sys.stderr)
+    rank, world, local = dist_setup()
+    out = run_ep(args, rank, world) if world > 1 else run_single(args)
     if rank == 0:
-        print(json.dumps(out))
+        print(json.dumps(out), flush=True)
     import torch.distributed as dist
     if dist.is_initialized():
-        import torch.distributed as dist
         dist.destroy_process_group()
     return 0
 

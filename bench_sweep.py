@@ -90,7 +90,10 @@ def main():
                 "mean_experts_per_token": float(counts.sum()) / cfg.T, "rows_R_pad": R,
                 "max_over_mean_load": float(counts.max() / max(1e-9, counts.mean())),
                 "near_band": int(layer.state.near_band.item()),
-                "expert_gemm_tflops": 12.0 * R * cfg.d_model * cfg.d_ff / (float(np.median(gms)) / 1e3) / 1e12}
+                "rows_R": int(counts.sum()),
+                # algorithmic FLOPs of the realised rows (pad rows excluded), VERDICT r1 weak #3
+                "expert_gemm_tflops": flops / (float(np.median(gms)) / 1e3) / 1e12,
+                "expert_gemm_tflops_incl_pad_rows": 12.0 * R * cfg.d_model * cfg.d_ff / (float(np.median(gms)) / 1e3) / 1e12}
         print(json.dumps(line), flush=True)
         tot_tokens += cfg.T
         tot_ms += t_ms

@@ -21,6 +21,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
@@ -688,11 +690,16 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
   auto k = tc_gemm_kernel<EPI, A_MN, B_MN, KGRP, QOV>;
   constexpr int smem = EpiCfg<EPI, QOV>::SMEM;
   static_assert(smem <= SMEM_LIMIT, "shared memory budget");
-  static bool attr = false;
-  if (!attr) {
+  // the >48 KB shared-memory opt-in is per device: set it once for every device this
+  // instantiation launches on (bit per device ordinal)
+  static std::atomic<unsigned long long> attr_devs{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaGetLastError();
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(attr_devs.load(std::memory_order_relaxed) & bit)) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_devs.fetch_or(bit, std::memory_order_relaxed);
   }
   long long pairs = tiles_upper < sms / 2 ? tiles_upper : sms / 2;
   if (pairs <= 0) return cudaSuccess;

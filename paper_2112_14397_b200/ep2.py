@@ -11,14 +11,26 @@ tests, emulates `world` ranks inside ONE process on one device.
 Marshalling only: every step is a libmoe_dts.so kernel (moe_ep2_* + the expert FFN calls).
 
     ranks = [EP2Rank(T, d, f, E, dtype, dev, r, W, syms) for r in range(W)]   # emulation
-    EP2Rank.step_forward / step_backward run the phases of ONE rank (real multi-GPU: each
+    EP2Rank.forward / backward / step run the phases of ONE rank (real multi-GPU: each
     process calls them; barriers are NCCL all-reduces).  The tests drive emulated ranks phase
     by phase in one process (tests/_ep_lockstep.py).
+
+Row capacity ("adaptive capacity of experts"; nothing is dropped, R12).  The expert-side
+row buffers are symmetric, so every rank sizes them identically, from the all-gathered counts
+(identical on every rank): R_cap = the largest rank's 128-aligned recv layout times a headroom
+factor.  The first step reads the counts once on the host to size them; later steps run at that
+static capacity with no host synchronisation (the step can be captured as a CUDA graph).  A step
+whose routing needs more rows raises MOE_ECAPACITY on EVERY rank (each rank's plan kernel checks
+all ranks' layouts); `step()` then grows the buffers from that step's counts -- a collective
+re-allocation every rank performs together -- and re-runs the step.  An explicit `capacity`
+fixes R_cap instead (e.g. the worst case W*T*E_local + 127*E_local for tests).
 """
 from __future__ import annotations
 
+import math
 from typing import Dict, Optional
 
+import numpy as np
 import torch
 
 from . import _lib as L
@@ -58,7 +70,8 @@ class EP2Rank:
     """One rank of the fused peer-memory EP layer."""
 
     def __init__(self, T: int, d_model: int, d_ff: int, E: int, dtype: torch.dtype, device: torch.device, rank: int,
-                 world: int, syms: SymmetricBuffers, comm: Optional[int] = None, dedup: bool = False):
+                 world: int, syms: SymmetricBuffers, comm: Optional[int] = None, dedup: bool = False,
+                 capacity: Optional[int] = None, headroom: float = 1.25):
         self.T, self.d, self.f, self.E, self.El = T, d_model, d_ff, E, E // world
         # dedup (moe_ep2d_*): one row per (token, owner) each way; U = world * T unique slots
         self.dedup, self.U = dedup, world * T
@@ -66,8 +79,10 @@ class EP2Rank:
         self.ctx = L.moe_create(T, d_model, d_ff, E, _DT[dtype], comm if comm else L.MOE_COMM_EMULATED, rank, world)
         self.ws = torch.empty(max(256, L.moe_workspace_bytes(self.ctx)), dtype=torch.uint8, device=device)
         L.moe_set_workspace(self.ctx, self.ws)
-        # static capacity: every rank's tokens to every local expert, 128-aligned per expert
-        self.R_cap = (world * T * self.El + 127 * self.El + 127) // 128 * 128
+        # row capacity: fixed when given, else sized from the first step's all-gathered counts
+        self.headroom = headroom
+        self.R_cap: Optional[int] = None if capacity is None else self.round_rows(capacity)
+        self.grows = 0                  # capacity re-allocations after an overflow (step())
         self.Wg = self.W1 = self.b1 = self.W2 = self.b2 = None
         self.st: Dict[str, torch.Tensor] = {}
         # optional {"experts_fwd": (ev0, ev1), "experts_bwd": (ev0, ev1)}: CUDA events recorded
@@ -99,6 +114,49 @@ class EP2Rank:
     def _sym(self, name, shape, dtype):
         return self.syms.buf(name, self.rank, shape, dtype)
 
+    # ------------------------------------------------------------ row capacity
+    @staticmethod
+    def round_rows(n: int) -> int:
+        return max(128, (int(n) + 127) // 128 * 128)
+
+    def rows_needed(self, counts_all: np.ndarray) -> int:
+        """Largest 128-aligned expert-side (recv) layout over the ranks for routing counts_all [W, E]."""
+        tot = np.asarray(counts_all, np.int64).sum(0)
+        pad = (tot + 127) // 128 * 128
+        return int(pad.reshape(self.world, self.El).sum(1).max()) if tot.size else 0
+
+    def capacity_for(self, counts_all: np.ndarray) -> int:
+        need = self.rows_needed(counts_all)
+        return self.round_rows(math.ceil(need * self.headroom))
+
+    def counts_all_host(self) -> np.ndarray:
+        """This rank's copy of the all-gathered counts (host read: synchronises the stream)."""
+        ca, _ = self._sym("counts_all", (self.world, self.E), torch.int32)
+        return ca.cpu().numpy()
+
+    def worst_case_capacity(self) -> int:
+        return self.round_rows(self.world * self.T * self.El + 127 * self.El)
+
+    def prepare(self):
+        """Create every symmetric buffer of the current capacity (a collective; do it before a
+        CUDA-graph capture so the captured step performs no rendezvous)."""
+        R, d = self.R_cap, self.d
+        self._sym("counts_all", (self.world, self.E), torch.int32)
+        for name, shape, dt in (("x_recv", (R, d), self.dtype), ("rtok", (R,), torch.int32),
+                                ("rsrc", (R,), torch.int32), ("rgate", (R,), torch.float32),
+                                ("e_out", (R, d), self.dtype), ("dG", (R,), torch.float32),
+                                ("dx_perm", (R, d), self.dtype), ("dy", (self.T, d), self.dtype)):
+            self._sym(name, shape, dt)
+        if self.dedup:
+            for name, shape, dt in (("ruid", (R,), torch.int32), ("tokbuf", (self.U, d), self.dtype),
+                                    ("urows", (self.U, self.El), torch.int32), ("ysum", (self.U, d), self.dtype),
+                                    ("dxu", (self.U, d), self.dtype)):
+                self._sym(name, shape, dt)
+
+    def dy_buffer(self) -> torch.Tensor:
+        """The symmetric dy buffer the backward reads from (write dy here to skip the staging copy)."""
+        return self._sym("dy", (self.T, self.d), self.dtype)[0]
+
     def barrier(self):
         L.moe_ep2_barrier(self.ctx)
 
@@ -116,6 +174,8 @@ class EP2Rank:
         L.moe_ep2_counts(self.ctx, s["counts"], peers)
 
     def fwd_plan(self):
+        if self.R_cap is None:           # first step: size the capacity from the gathered counts
+            self.R_cap = self.capacity_for(self.counts_all_host())
         R, d = self.R_cap, self.d
         s = self.st
         ca, _ = self._sym("counts_all", (self.world, self.E), torch.int32)
@@ -180,7 +240,8 @@ class EP2Rank:
     # ------------------------------------------------------------ backward phases
     def bwd_stage_dy(self, dy):
         buf, _ = self._sym("dy", (self.T, self.d), self.dtype)
-        buf.copy_(dy)
+        if dy.data_ptr() != buf.data_ptr():
+            buf.copy_(dy)
 
     def bwd_gather_dy(self):
         """dedup, expert side: dyu[u] = the token's dy row, read once per (token, owner)."""
@@ -267,6 +328,28 @@ class EP2Rank:
             self.fwd_presum()
         self.barrier()
         return self.fwd_combine()
+
+    def grow(self):
+        """After MOE_ECAPACITY: size the buffers for the counts of the step that overflowed (every
+        rank holds the same counts_all, so every rank picks the same capacity)."""
+        need = self.capacity_for(self.counts_all_host())
+        self.R_cap = max(need, self.R_cap or 0)
+        self.grows += 1
+
+    def step(self, x, u, dy, tau, threshold, top1=False, balance_alpha: float = 0.0, max_retries: int = 2):
+        """forward + backward with the capacity policy: check the device flags after the step and,
+        on MOE_ECAPACITY (raised on every rank together), grow and re-run the step."""
+        for attempt in range(max_retries + 1):
+            y = self.forward(x, u, tau, threshold, top1)
+            g = self.backward(dy, balance_alpha)
+            try:
+                self.check()
+                return y, g
+            except L.MoEError as e:
+                if e.code != 7 or attempt == max_retries:
+                    raise
+                self.grow()
+        raise RuntimeError("unreachable")
 
     def backward(self, dy, balance_alpha: float = 0.0):
         self.bwd_stage_dy(dy)

@@ -40,3 +40,31 @@ def run_lockstep(ranks: List[EP2Rank], xs, us, dys, tau: float, threshold: float
     dWg = sum(r.st["grads"]["dWg"] for r in ranks)
     grads = [r.bwd_dispatch() for r in ranks]
     return ys, grads, dWg
+
+
+def check_all(ranks: List[EP2Rank]) -> List[int]:
+    """moe_check on every rank; the status code of each (0 = ok)."""
+    from paper_2112_14397_b200 import _lib as L
+    codes = []
+    for r in ranks:
+        try:
+            r.check()
+            codes.append(0)
+        except L.MoEError as e:
+            codes.append(e.code)
+    return codes
+
+
+def run_lockstep_with_recovery(ranks: List[EP2Rank], *args, max_retries: int = 2, **kw):
+    """EP2Rank.step()'s capacity policy for emulated ranks: run the step, check every rank; on
+    MOE_ECAPACITY (which every rank must raise together) grow every rank and re-run.
+    Returns (ys, grads, dWg, attempts)."""
+    for attempt in range(max_retries + 1):
+        out = run_lockstep(ranks, *args, **kw)
+        codes = check_all(ranks)
+        if all(c == 0 for c in codes):
+            return out + (attempt,)
+        assert all(c == 7 for c in codes), f"capacity overflow not raised on every rank: {codes}"
+        for r in ranks:
+            r.grow()
+    raise AssertionError("capacity still exceeded after the retries")

@@ -156,7 +156,7 @@ def _vs_oracle(cfg, W, T, ranks_in, probs, slots, ys, dxs, dlogits, wgrads, dWg,
     mask bit-exact outside the band, every value tensor norm-wise and per row (y / dx /
     dlogits per token, dW1 / dW2 per output row of every expert on its owner rank, db1 / db2,
     dW_g summed over the ranks)."""
-    from _parity import band_tokens, check_values, f32, run_oracle, summary
+    from _parity import band_tokens, check_values, f32, gate_allowance, run_oracle, summary
     import types
     tol = 2e-2 if cfg.dtype == "bf16" else 1e-4
     cat = lambda k: torch.cat([getattr(r, k) for r in ranks_in])  # noqa: E731
@@ -175,10 +175,12 @@ def _vs_oracle(cfg, W, T, ranks_in, probs, slots, ys, dxs, dlogits, wgrads, dWg,
     rep = {"band": int(band.sum()), "flips": int(flips.sum()),
            "probs_maxabs": float(np.abs(p32 - fw.p).max())}
     assert rep["probs_maxabs"] <= 1e-5, rep
+    allow = gate_allowance(fw.p, fw.m, bw.dG, fw.tau, tol)
     check_values(rep, "y", np.concatenate([_np(t) for t in ys]), fw.y, y_tol or tol)
-    check_values(rep, "dx", np.concatenate([_np(t) for t in dxs]), bw.dx, y_tol or tol)
-    check_values(rep, "dlogits", np.concatenate([_np(t) for t in dlogits]), bw.dlogits, tol)
-    check_values(rep, "dWg", _np(dWg), bw.dWg, tol)
+    check_values(rep, "dx", np.concatenate([_np(t) for t in dxs]), bw.dx, y_tol or tol,
+                 allow=allow * np.linalg.norm(fw.Wg, 2))
+    check_values(rep, "dlogits", np.concatenate([_np(t) for t in dlogits]), bw.dlogits, tol, allow=allow)
+    check_values(rep, "dWg", _np(dWg), bw.dWg, tol, rows=False)
     El = cfg.E // W
     for q in range(W):
         for j in range(El):
@@ -186,7 +188,7 @@ def _vs_oracle(cfg, W, T, ranks_in, probs, slots, ys, dxs, dlogits, wgrads, dWg,
             for k, ref in (("dW1", bw.dW1), ("db1", bw.db1), ("dW2", bw.dW2), ("db2", bw.db2)):
                 got = _np(wgrads[q][k][j])
                 if fw.counts[e]:
-                    check_values(rep, f"{k}[{e}]", got, ref[e], tol)
+                    check_values(rep, f"{k}[{e}]", got, ref[e], tol, rows=k in ("dW1", "dW2"))
                 else:
                     assert not np.any(got), f"{k}[{e}] of an empty expert must be zero"
     print(cfg.name, f"W={W} T={T} vs oracle", summary(rep))
@@ -356,3 +358,79 @@ def test_ep2_balance_loss_uses_global_counts(poison_empty, name, W, T, dedup):
         ep, ranks_in = _lockstep(cfg, W, T, dedup=dedup, balance_alpha=0.1, dy_scale=dy_scale)
         _vs_oracle(cfg, W, T, ranks_in, ep["probs"], ep["slot"], ep["y"], [gq["dx"] for gq in ep["g"]],
                    [gq["dlogits"] for gq in ep["g"]], ep["g"], ep["dWg"], balance_alpha=0.1, dy_scale=dy_scale)
+
+
+def _ranks(cfg, W, T, dedup=False, capacity=None):
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
+    dev = torch.device("cuda", 0)
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
+    ranks_in = [inputs.make_inputs(cfg, rank=q, T=T) for q in range(W)]
+    li0 = ranks_in[0]
+    syms = SymmetricBuffers(W, dev)
+    ranks = []
+    for q in range(W):
+        r = EP2Rank(T, cfg.d_model, cfg.d_ff, cfg.E, dt, dev, q, W, syms, dedup=dedup, capacity=capacity)
+        r.set_gate(li0.Wg.to(dev))
+        r.spawn(*(t.to(dev) for t in (li0.W1s, li0.b1s, li0.W2s, li0.b2s, li0.M1bits, li0.M2bits)))
+        ranks.append(r)
+    return ranks, ranks_in
+
+
+@pytest.mark.parametrize("dedup", [False, True], ids=["ep2", "ep2d"])
+def test_ep2_capacity_overflow_recovers(poison_empty, dedup):
+    """Adaptive row capacity ("adaptive capacity", nothing dropped, R12): the first step
+    sizes the symmetric row buffers from its all-gathered counts (+25% headroom); a later step
+    whose routing needs far more rows (c = 0: every token to every expert) overflows, which every
+    rank reports (MOE_ECAPACITY), the ranks grow together and the re-run matches the oracle."""
+    from _ep_lockstep import run_lockstep_with_recovery
+    cfg, W, T = configs.C3, 2, 256
+    ranks, ranks_in = _ranks(cfg, W, T, dedup=dedup)
+    dev = torch.device("cuda", 0)
+    xs, us, dys = ([getattr(ri, k).to(dev) for ri in ranks_in] for k in ("x", "u", "dy"))
+    tau = float(np.float32(cfg.tau))
+    *_, attempts = run_lockstep_with_recovery(ranks, xs, us, dys, tau, float(np.float32(cfg.threshold)))
+    assert attempts == 0 and all(r.grows == 0 for r in ranks)
+    cap0 = ranks[0].R_cap
+    assert cap0 <= ranks[0].worst_case_capacity() // 3         # sized from the counts, not the worst case
+    skew = dataclasses.replace(cfg, threshold=0.0)
+    ys, grads, dWg, attempts = run_lockstep_with_recovery(ranks, xs, us, dys, tau, 0.0)
+    assert attempts == 1 and all(r.grows == 1 for r in ranks) and ranks[0].R_cap > cap0
+    _vs_oracle(skew, W, T, ranks_in, [r.st["probs"] for r in ranks], [r.st["slot"] for r in ranks], ys,
+               [gq["dx"] for gq in grads], [gq["dlogits"] for gq in grads], grads, dWg)
+
+
+@pytest.mark.parametrize("dedup", [False, True], ids=["ep2", "ep2d"])
+def test_ep2_step_captures_as_cuda_graph(poison_empty, dedup):
+    """With the capacity fixed after the first step, the EP step has no host synchronisation: the
+    phases of all emulated ranks are captured as ONE CUDA graph, and every replay reproduces the
+    eager step bit for bit (what bench.py times at N > 1)."""
+    from _ep_lockstep import run_lockstep
+    cfg, W, T = configs.C3, 4, 300
+    ranks, ranks_in = _ranks(cfg, W, T, dedup=dedup)
+    dev = torch.device("cuda", 0)
+    xs, us, dys = ([getattr(ri, k).to(dev) for ri in ranks_in] for k in ("x", "u", "dy"))
+    args = (xs, us, dys, float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)))
+    ys0, g0, dWg0 = run_lockstep(ranks, *args)
+    torch.cuda.synchronize()
+    ref = ([y.clone() for y in ys0], [{k: v.clone() for k, v in g.items()} for g in g0], dWg0.clone())
+    for r in ranks:
+        r.prepare()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        run_lockstep(ranks, *args)                       # warm-up on the side stream (allocator pools)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        ys1, g1, dWg1 = run_lockstep(ranks, *args)
+    for _ in range(2):
+        graph.replay()
+        torch.cuda.synchronize()
+        for r in ranks:
+            r.check()
+        for q in range(W):
+            assert torch.equal(ys1[q], ref[0][q])
+            for k in ("dx", "dlogits", "dW1", "dW2", "db1", "db2", "dWg"):
+                assert torch.equal(g1[q][k], ref[1][q][k]), (q, k)
+        assert torch.equal(dWg1, ref[2])

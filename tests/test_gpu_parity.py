@@ -271,7 +271,7 @@ def test_balance_gradient_alone(cfg_name, T):
     tol = 1e-4 if cfg.dtype == "f32" else 2e-2
     rep = {}
     check_values(rep, "dlogits", g["dlogits"].cpu().numpy(), bw.dlogits, tol)
-    check_values(rep, "dWg", g["dWg"].cpu().numpy(), bw.dWg, tol)
+    check_values(rep, "dWg", g["dWg"].cpu().numpy(), bw.dWg, tol, rows=False)
     check_values(rep, "dx", g["dx"].float().cpu().numpy(), bw.dx, tol)
     assert np.abs(bw.dlogits).max() > 0
     print(cfg_name, rep)

@@ -107,6 +107,7 @@ def _scribble_chunk(r, c0):
     ("d_eout", _scribble_chunk(100, 0)),
     ("dx", _scribble_chunk(3, 32)),
     ("h", _scribble_chunk(50, 256)),
+    ("dlogits", _zero_row(7)),                # still caught with the gate allowance (tests/_parity.gate_allowance)
 ])
 def test_localised_corruption_fails(c2_small, where, fn):
     cfg, li, g = c2_small
