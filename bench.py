@@ -144,11 +144,18 @@ def relaunch_under_torchrun(args) -> int:
     return subprocess.call(cmd, env=env)
 
 
-def dist_setup():
+def dist_setup(force_pg: bool = False):
+    """force_pg: a 1-rank NCCL process group for --ep at N = 1 (the EP code path, its symmetric
+    allocations and barriers, on one GPU)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if force_pg and world == 1 and "MASTER_ADDR" not in os.environ:
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
+    if world > 1 or force_pg:
         import torch.distributed as dist
         if torch.cuda.device_count() <= local:
             raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible")
@@ -160,7 +167,8 @@ def dist_setup():
 
 
 def barrier(world):
-    if world > 1:
+    import torch.distributed as dist
+    if world > 1 or dist.is_initialized():
         import torch.distributed as dist
         dist.barrier()
 
@@ -785,14 +793,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
-    ap.add_argument("--cpu-tokens", type=int, default=1024)
+    ap.add_argument("--cpu-tokens", type=int, default=4096)
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--ep", default="p2p", choices=["p2p", "p2p-dedup", "nccl"],
-                    help="N > 1 exchange: the fused NVLink peer-memory path (moe_ep2_*, torch symmetric memory; "
-                         "default), the same with one row per (token, owner) each way (moe_ep2d_*), or NCCL "
-                         "grouped send/recv")
+    ap.add_argument("--ep", default=None, choices=["p2p", "p2p-dedup", "nccl"],
+                    help="expert-parallel exchange: the fused NVLink peer-memory path (moe_ep2_*, torch symmetric "
+                         "memory; the default at N > 1), the same with one row per (token, owner) each way "
+                         "(moe_ep2d_*), or NCCL grouped send/recv.  Given at N = 1 it runs that EP path on a "
+                         "1-rank group instead of the single-GPU layer")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -814,8 +823,10 @@ def main():
     if args.gpus != world_env:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}; running {world_env} rank(s)",
               file=sys.stderr)
-    rank, world, local = dist_setup()
-    out = run_ep(args, rank, world) if world > 1 else run_single(args)
+    rank, world, local = dist_setup(force_pg=args.ep is not None)
+    if world > 1 and args.ep is None:
+        args.ep = "p2p"
+    out = run_ep(args, rank, world) if args.ep is not None else run_single(args)
     if rank == 0:
         print(json.dumps(out), flush=True)
     import torch.distributed as dist

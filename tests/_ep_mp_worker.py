@@ -3,7 +3,8 @@ tests/test_gpu_ep_multiproc.py through torch.distributed.run, one process per GP
 
     python -m torch.distributed.run --nproc-per-node W tests/_ep_mp_worker.py MODE CONFIG T OUT_DIR
 
-MODE: "nccl" (DTSMoELayer with the NCCL grouped send/recv exchange), "p2p" / "p2p-dedup" (EP2Rank
+MODE: "nccl" (DTSMoELayer with the NCCL grouped send/recv exchange), "nccl-hier" (the same with
+the hierarchical exchange over two virtual nodes of W/2 GPUs), "p2p" / "p2p-dedup" (EP2Rank
 over torch symmetric memory: NVLink peer loads / stores; the step is also captured as a CUDA graph
 and replayed, and the replay must equal the eager step bit for bit).  Each rank saves its tokens'
 outputs and its experts' gradients to OUT_DIR/rank{r}.pt for the parent to compare with the oracle.
@@ -36,9 +37,11 @@ def main():
     comm = make_nccl_comm(rank, world)
     x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
     res = {}
-    if mode == "nccl":
+    if mode in ("nccl", "nccl-hier"):
+        # nccl-hier: NEXT #4, the topology-aware hierarchical exchange with the ranks split into
+        # two virtual nodes of world/2 GPUs; results must equal the flat exchange's
         layer = DTSMoELayer(T, cfg.d_model, cfg.d_ff, cfg.E, dtype=dt, device=dev, rank=rank, world=world,
-                            nccl_comm=comm)
+                            nccl_comm=comm, gpus_per_node=world // 2 if mode == "nccl-hier" else None)
         layer.set_gate(li.Wg.to(dev))
         layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
         y = layer.forward(x, u, tau, c, top1=cfg.top1)

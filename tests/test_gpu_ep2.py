@@ -156,7 +156,7 @@ def _vs_oracle(cfg, W, T, ranks_in, probs, slots, ys, dxs, dlogits, wgrads, dWg,
     mask bit-exact outside the band, every value tensor norm-wise and per row (y / dx /
     dlogits per token, dW1 / dW2 per output row of every expert on its owner rank, db1 / db2,
     dW_g summed over the ranks)."""
-    from _parity import band_tokens, check_values, f32, gate_allowance, run_oracle, summary
+    from _parity import band_tokens, check_values, dG_scale, f32, gate_allowance, run_oracle, summary
     import types
     tol = 2e-2 if cfg.dtype == "bf16" else 1e-4
     cat = lambda k: torch.cat([getattr(r, k) for r in ranks_in])  # noqa: E731
@@ -175,7 +175,7 @@ def _vs_oracle(cfg, W, T, ranks_in, probs, slots, ys, dxs, dlogits, wgrads, dWg,
     rep = {"band": int(band.sum()), "flips": int(flips.sum()),
            "probs_maxabs": float(np.abs(p32 - fw.p).max())}
     assert rep["probs_maxabs"] <= 1e-5, rep
-    allow = gate_allowance(fw.p, fw.m, bw.dG, fw.tau, tol)
+    allow = gate_allowance(fw.p, fw.m, bw.dG, fw.tau, tol, dG_scale(fw, inputs.to_f64(li.dy), cfg.dtype))
     check_values(rep, "y", np.concatenate([_np(t) for t in ys]), fw.y, y_tol or tol)
     check_values(rep, "dx", np.concatenate([_np(t) for t in dxs]), bw.dx, y_tol or tol,
                  allow=allow * np.linalg.norm(fw.Wg, 2))

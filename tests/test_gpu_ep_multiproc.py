@@ -37,6 +37,7 @@ def _free_port():
 def _run(world, mode, cfg_name, T, tmp_path):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs, {torch.cuda.device_count()} visible")
+    os.makedirs(tmp_path, exist_ok=True)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", WORKER, mode, cfg_name, str(T), str(tmp_path)]
     env = dict(os.environ, PYTHONPATH=ROOT, NCCL_DEBUG="WARN")
@@ -61,3 +62,15 @@ def test_multiprocess_ep_matches_oracle(world, mode, cfg_name, T, tmp_path):
         assert torch.equal(res[q]["dWg"], res[0]["dWg"])
     if mode != "nccl":
         assert all(int(r["graph_replay_identical"][0]) == 1 for r in res), "graph replay differs from eager"
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_hierarchical_exchange_bit_identical_to_flat(world, tmp_path):
+    """NEXT #4 on one node: the hierarchical all-to-all with the W ranks split into
+    two virtual nodes of W/2 GPUs (intra-node gather -> one inter-node message per node pair ->
+    intra-node scatter) must give the flat exchange's results bit for bit (same recv layouts)."""
+    flat = _run(world, "nccl", "C3", 384, tmp_path / "flat")
+    hier = _run(world, "nccl-hier", "C3", 384, tmp_path / "hier")
+    for q in range(world):
+        for k in ("y", "dx", "dlogits", "dW1", "db1", "dW2", "db2", "dWg", "slot", "probs"):
+            assert torch.equal(flat[q][k], hier[q][k]), (q, k)

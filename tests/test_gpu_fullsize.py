@@ -41,7 +41,7 @@ def _rel(a, b):
 
 
 def fullsize(cfg, step=0, n_random=160, tail=32):
-    from _parity import band_tokens, check_values, f32, gate_allowance, summary
+    from _parity import band_tokens, check_values, dG_scale, f32, gate_allowance, summary
     from paper_2112_14397_b200.layer import DTSMoELayer
     li = inputs.make_inputs(cfg, step=step)
     T, E = li.x.shape[0], cfg.E
@@ -87,7 +87,7 @@ def fullsize(cfg, step=0, n_random=160, tail=32):
     bw = O.backward(fw, dy64[S])
     # per-token rows: norm-wise and per-row bounds (tests/_parity.check_values)
     check_values(rep, "y", _np(y)[S], fw.y, tol)
-    allow = gate_allowance(fw.p, fw.m, bw.dG, fw.tau, tol)
+    allow = gate_allowance(fw.p, fw.m, bw.dG, fw.tau, tol, dG_scale(fw, dy64[S], cfg.dtype))
     check_values(rep, "dx", _np(g["dx"])[S], bw.dx, tol, allow=allow * np.linalg.norm(Wg64, 2))
     check_values(rep, "dlogits", _np(g["dlogits"])[S], bw.dlogits, tol, allow=allow)
     # the permuted rows of the sampled tokens (row = slot[t, e]): e_out, d_eout, dx_perm
