@@ -131,7 +131,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ distributed plumbing
-def relaunch_under_torchrun(args) -> int:
+def relaunch_under_torchrun(args, out_stream) -> int:
     """`python bench.py --gpus N` with no WORLD_SIZE: run N ranks (one per GPU) under
     torch.distributed.run on this node; rank 0's JSON line comes through our stdout."""
     with socket.socket() as sk:
@@ -141,7 +141,7 @@ def relaunch_under_torchrun(args) -> int:
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
     env = dict(os.environ)
     print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
-    return subprocess.call(cmd, env=env)
+    return subprocess.call(cmd, env=env, stdout=out_stream)
 
 
 def dist_setup(force_pg: bool = False):
@@ -784,7 +784,18 @@ def run_reference(args, rank, world):
     }
 
 
+def _json_stdout():
+    """The contract is ONE JSON line on stdout.  Libraries print there too (NCCL's "NCCL version"
+    banner at communicator init, for one): point fd 1 at stderr for the whole run and keep a
+    private handle on the real stdout for the result line."""
+    real = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
+    return real
+
+
 def main():
+    out_stream = _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
@@ -810,10 +821,10 @@ def main():
         world = int(os.environ.get("WORLD_SIZE", "1"))
         out = run_reference(args, rank, world)
         if out is not None:
-            print(json.dumps(out))
+            print(json.dumps(out), file=out_stream, flush=True)
         return 0
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        return relaunch_under_torchrun(args)
+        return relaunch_under_torchrun(args, out_stream)
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if world_env > 1:
         # NCCL's init lines (rank count, transport) on stderr; stdout carries only the JSON line
@@ -828,7 +839,7 @@ def main():
         args.ep = "p2p"
     out = run_ep(args, rank, world) if args.ep is not None else run_single(args)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=out_stream, flush=True)
     import torch.distributed as dist
     if dist.is_initialized():
         dist.destroy_process_group()

@@ -101,7 +101,14 @@ template <int EPI, int QOV = 0> struct EpiCfg {   // QOV: epilogue warps per qua
   static constexpr int THREADS = 64 + 32 * WARPS;
   static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
   // staging buffers per warp (GELU' bwd: 4, its a-operand loads run two chunks ahead)
-  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4
+#ifdef MOE_EXP_GP_LDG
+  // GELU' operand loaded straight into registers one chunk ahead (no TMA ring through the
+  // staging buffers): the staging holds only the da output, double-buffered
+  static constexpr bool GP_LDG = EPI == TEPI_GELU_BWD;
+#else
+  static constexpr bool GP_LDG = false;
+#endif
+  static constexpr int NBUF = GP_LDG ? 2 : EPI == TEPI_GELU_BWD ? 4
                               : EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_NB_GELU
                               : EPI == TEPI_BIAS ? MOE_NB_BIAS
                               : EPI == TEPI_STORE ? MOE_NB_STORE : MOE_NB_F32;
@@ -132,6 +139,7 @@ struct TcParams {
   bf16* o2;
   long long ldo_b;
   float* colpart;         // TEPI_GELU_BWD: per-32-row column sums of da [R_cap/32][N] (bias gradient db1)
+  const bf16* aux;        // TEPI_GELU_BWD with GP_LDG: GELU'(a) rows [R_cap][N] (pitch N)
   unsigned long long* trace;   // MOE_EXP_TRACE builds only: per-warp event log of CTAs 0 and 1
   int a3d, b3d;           // MN-major operand given as a 3D map {64, K rows, MN / 64}: one TMA op per stage
 };
@@ -367,10 +375,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       tc::mbar_arrive_expect_tx_u32(auxb + b * 8, CHUNK_BYTES);
       tc::tma_load_2d_u32(stage_base + b * CHUNK_BYTES, &tmX, auxb + b * 8, col, tn.m_own + sub * 32);
     };
-    if (EPI == TEPI_GELU_BWD && lane == 0) {
+    if (EPI == TEPI_GELU_BWD && !Cfg::GP_LDG && lane == 0) {
       aux_issue(0);
       aux_issue(1);
     }
+    uint4 gpn[4];                                       // GP_LDG: the next chunk's GELU' operand (this row)
 
     for (int t = cid; t < total; t += ncl) {
       Tile tl;
@@ -390,6 +399,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       const float* bias_t = nullptr;                                 // padded fp32 bias row of this tile
       if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H)
         bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0;
+      const bf16* gp_row = nullptr;
+      if constexpr (Cfg::GP_LDG) {                         // chunk 0's operand while the MMA finishes
+        gp_row = p.aux + row * (long long)p.N + tl.n0;
+        if (tl.m_own + sub * 32 < tl.row_end) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) gpn[q] = ld_nc_v4(gp_row + part * 32 + q * 8);
+        }
+      }
       TR(6, t);
       tc::mbar_wait_sleep(&tfull_bar[acc], acc_phase);
       TR(7, t);
@@ -461,7 +478,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
         f32x2 v[16];                                       // packed fp32 pairs (FFMA2/FMUL2/FADD2)
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = f2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-        if (EPI == TEPI_GELU_BWD) {
+        if (EPI == TEPI_GELU_BWD && Cfg::GP_LDG) {
+          uint4 gpc[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) gpc[q] = gpn[q];
+          if (k + 1 < nch && warp_rows_ok) {               // prefetch the next chunk's operand
+#pragma unroll
+            for (int q = 0; q < 4; ++q) gpn[q] = ld_nc_v4(gp_row + (part + EPI_PER_Q * (k + 1)) * 32 + q * 8);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            v[q * 4 + 0] = mul2(v[q * 4 + 0], bf16x2_to_f2(gpc[q].x));
+            v[q * 4 + 1] = mul2(v[q * 4 + 1], bf16x2_to_f2(gpc[q].y));
+            v[q * 4 + 2] = mul2(v[q * 4 + 2], bf16x2_to_f2(gpc[q].z));
+            v[q * 4 + 3] = mul2(v[q * 4 + 3], bf16x2_to_f2(gpc[q].w));
+          }
+          if (seq >= (uint32_t)Cfg::NBUF) {               // the store that last used this buffer must be read
+            if (lane == 0) tc::bulk_wait_read<Cfg::NBUF - 1>();
+            __syncwarp();
+          }
+        } else if (EPI == TEPI_GELU_BWD) {
           tc::mbar_wait_u32(auxb + (seq % Cfg::NBUF) * 8, (seq / Cfg::NBUF) & 1);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {                        // gp = GELU'(a) saved by the forward
@@ -589,7 +625,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
           }
           tc::bulk_commit();                              // one (possibly empty) group per chunk
           TR(9, t);
-          if (EPI == TEPI_GELU_BWD) {
+          if (EPI == TEPI_GELU_BWD && !Cfg::GP_LDG) {
             tc::bulk_wait_read<2>();                      // buffer (seq+2)%4 was last stored at seq-2
             aux_issue(seq + 2);
           }
@@ -842,6 +878,7 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
       return cudaErrorInvalidValue;
     p.N = f; p.K = d; p.b_group_rows = d;
     p.o1 = reinterpret_cast<bf16*>(da); p.ldo_b = f;
+    p.aux = reinterpret_cast<const bf16*>(gp);
     // db1 partials live in dx_perm's memory until dgrad1 overwrites it ([R_cap/32][f] fp32 <= R_cap x d bf16)
     const bool fuse_db1 = db1 && (long long)f * 4 <= (long long)d * 2 * 32;
     p.colpart = fuse_db1 ? reinterpret_cast<float*>(dx_perm) : nullptr;
