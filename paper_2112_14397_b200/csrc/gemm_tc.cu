@@ -26,10 +26,6 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tc_ptx.cuh"
-#ifdef MOE_EXP_TRACE
-#include <cstdio>
-#include <cstdlib>
-#endif
 
 namespace moe {
 
@@ -47,12 +43,6 @@ constexpr int CHUNKS = 256 / 32;
 constexpr int CHUNK_BYTES = 32 * 32 * 2;     // one 32x32 bf16 sub-tile (TMA box, 64-byte swizzle)
 constexpr int MAX_G = 128;
 constexpr int SMEM_LIMIT = 232448;
-
-#ifdef MOE_EXP_NOAUX
-#define AUX_LOAD(p) make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u)
-#else
-#define AUX_LOAD(p) ld_nc_v4(p)
-#endif
 
 // TEPI_BIAS_GELU writes (GELU'(a), GELU(a)); TEPI_BIAS_GELU_H writes GELU(a) only (recompute mode)
 enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 3, TEPI_F32 = 4, TEPI_BIAS_GELU_H = 5 };
@@ -101,23 +91,12 @@ template <int EPI, int QOV = 0> struct EpiCfg {   // QOV: epilogue warps per qua
   static constexpr int THREADS = 64 + 32 * WARPS;
   static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
   // staging buffers per warp (GELU' bwd: 4, its a-operand loads run two chunks ahead)
-#ifdef MOE_EXP_GP_LDG
-  // GELU' operand loaded straight into registers one chunk ahead (no TMA ring through the
-  // staging buffers): the staging holds only the da output, double-buffered
-  static constexpr bool GP_LDG = EPI == TEPI_GELU_BWD;
-#else
-  static constexpr bool GP_LDG = false;
-#endif
-  static constexpr int NBUF = GP_LDG ? 2 : EPI == TEPI_GELU_BWD ? 4
+  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4
                               : EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_NB_GELU
                               : EPI == TEPI_BIAS ? MOE_NB_BIAS
                               : EPI == TEPI_STORE ? MOE_NB_STORE : MOE_NB_F32;
   // per-warp staging: NBUF chunk buffers of NOUT bf16 32x32 boxes, or of one fp32 32x32 box (F32)
-#ifdef MOE_EXP_F32_DIRECT
-  static constexpr int WARP_STAGE = EPI == TEPI_F32 ? 0 : NBUF * NOUT * CHUNK_BYTES;
-#else
   static constexpr int WARP_STAGE = EPI == TEPI_F32 ? NBUF * 2 * CHUNK_BYTES : NBUF * NOUT * CHUNK_BYTES;
-#endif
   static constexpr int STAGING = WARPS * WARP_STAGE;
   static constexpr int BAR_BYTES = 2048;
   static constexpr int STAGES = (SMEM_LIMIT - 1024 - BAR_BYTES - STAGING) / STAGE_BYTES;
@@ -139,23 +118,10 @@ struct TcParams {
   bf16* o2;
   long long ldo_b;
   float* colpart;         // TEPI_GELU_BWD: per-32-row column sums of da [R_cap/32][N] (bias gradient db1)
-  const bf16* aux;        // TEPI_GELU_BWD with GP_LDG: GELU'(a) rows [R_cap][N] (pitch N)
-  unsigned long long* trace;   // MOE_EXP_TRACE builds only: per-warp event log of CTAs 0 and 1
+  const void* reserved0;  // (unused; keeps the parameter block's layout of the measured builds)
+  void* reserved1;
   int a3d, b3d;           // MN-major operand given as a 3D map {64, K rows, MN / 64}: one TMA op per stage
 };
-
-#ifdef MOE_EXP_TRACE
-constexpr int kTraceN = 4096;
-#define TR(ev, tile)                                                                                        \
-  do {                                                                                                      \
-    if (p.trace && blockIdx.x < 2 && (threadIdx.x & 31) == 0 && tr_n < kTraceN)                             \
-      p.trace[((size_t)blockIdx.x * 16 + threadIdx.x / 32) * kTraceN + tr_n++] =                            \
-          ((unsigned long long)(ev) << 56) | ((unsigned long long)((tile) & 0xffff) << 40) |                \
-          ((unsigned long long)clock64() & 0xFFFFFFFFFFull);                                                \
-  } while (0)
-#else
-#define TR(ev, tile) do { } while (0)
-#endif
 
 struct Tile {
   int g, m_own, n0, kb0, nkb, row_end;
@@ -215,9 +181,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
 
   const uint32_t rank = tc::cluster_rank();
   const bool leader = rank == 0;
-#ifdef MOE_EXP_TRACE
-  uint32_t tr_n = 0;
-#endif
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
@@ -274,9 +237,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
         const int n_own = tl.n0 + BNH * (int)rank;
         const int brow = KGRP ? 0 : tl.g * p.b_group_rows;
         for (int kb = 0; kb < tl.nkb; ++kb) {
-          TR(1, t);
           tc::mbar_wait(&empty_bar[stage], phase ^ 1);
-          TR(2, t);
           if (leader) tc::mbar_arrive_expect_tx(&full_bar[stage], 2 * STAGE_BYTES);
           const uint32_t bar = full_leader + stage * 8;
           const uint32_t sa = smem_base + stage * STAGE_BYTES;
@@ -314,14 +275,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       for (int t = cid; t < total; t += ncl) {
         Tile tl;
         if (!decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tl)) continue;
-        TR(3, t);
         tc::mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-        TR(4, t);
         tc::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < tl.nkb; ++kb) {
           tc::mbar_wait(&full_bar[stage], phase);
-          TR(5, t);
           tc::tc_fence_after();
           const uint32_t sa = smem_base + stage * STAGE_BYTES;
           const uint32_t sb = sa + A_BYTES;
@@ -375,11 +333,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       tc::mbar_arrive_expect_tx_u32(auxb + b * 8, CHUNK_BYTES);
       tc::tma_load_2d_u32(stage_base + b * CHUNK_BYTES, &tmX, auxb + b * 8, col, tn.m_own + sub * 32);
     };
-    if (EPI == TEPI_GELU_BWD && !Cfg::GP_LDG && lane == 0) {
+    if (EPI == TEPI_GELU_BWD && lane == 0) {
       aux_issue(0);
       aux_issue(1);
     }
-    uint4 gpn[4];                                       // GP_LDG: the next chunk's GELU' operand (this row)
 
     for (int t = cid; t < total; t += ncl) {
       Tile tl;
@@ -399,22 +356,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       const float* bias_t = nullptr;                                 // padded fp32 bias row of this tile
       if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H)
         bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0;
-      const bf16* gp_row = nullptr;
-      if constexpr (Cfg::GP_LDG) {                         // chunk 0's operand while the MMA finishes
-        gp_row = p.aux + row * (long long)p.N + tl.n0;
-        if (tl.m_own + sub * 32 < tl.row_end) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) gpn[q] = ld_nc_v4(gp_row + part * 32 + q * 8);
-        }
-      }
-      TR(6, t);
       tc::mbar_wait_sleep(&tfull_bar[acc], acc_phase);
-      TR(7, t);
       tc::tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16);
-#ifdef MOE_EXP_NOEPI
-      if (!KGRP) seq += nch; else
-#endif
 #pragma unroll 1
       for (int k = 0; k < nch; ++k, ++seq) {
         const int col = (part + EPI_PER_Q * k) * 32;
@@ -424,32 +368,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
         if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-#ifdef MOE_EXP_NOBIAS
-            bf[q] = make_float4(0.01f * q, 0.f, 0.f, 0.f);
-#else
             bf[q] = ld_nc_f4(bias_t + col + 4 * q);
-#endif
         }
-#ifdef MOE_EXP_NOLDTM
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(0.01f * (float)(j + lane));
-#else
         tc::tmem_ld32(t_row + col, r);
         tc::tmem_ld_wait();
-#endif
-        TR(8, t);
-#ifdef MOE_EXP_F32_DIRECT
-        if (EPI == TEPI_F32) {
-          if (row < p.M && n < p.N) {
-            float* o = p.out + (long long)tl.g * p.out_g + row * p.ldo + n;
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(o + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                                                              __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
-          }
-          continue;
-        }
-#endif
         if (EPI == TEPI_F32) {
           // fp32 32x32 box (128-byte rows, SWIZZLE_128B) staged in smem, one TMA store: coalesced
           // full-line writes instead of 32 scattered 16-byte rows per store instruction
@@ -478,26 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
         f32x2 v[16];                                       // packed fp32 pairs (FFMA2/FMUL2/FADD2)
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = f2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-        if (EPI == TEPI_GELU_BWD && Cfg::GP_LDG) {
-          uint4 gpc[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) gpc[q] = gpn[q];
-          if (k + 1 < nch && warp_rows_ok) {               // prefetch the next chunk's operand
-#pragma unroll
-            for (int q = 0; q < 4; ++q) gpn[q] = ld_nc_v4(gp_row + (part + EPI_PER_Q * (k + 1)) * 32 + q * 8);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            v[q * 4 + 0] = mul2(v[q * 4 + 0], bf16x2_to_f2(gpc[q].x));
-            v[q * 4 + 1] = mul2(v[q * 4 + 1], bf16x2_to_f2(gpc[q].y));
-            v[q * 4 + 2] = mul2(v[q * 4 + 2], bf16x2_to_f2(gpc[q].z));
-            v[q * 4 + 3] = mul2(v[q * 4 + 3], bf16x2_to_f2(gpc[q].w));
-          }
-          if (seq >= (uint32_t)Cfg::NBUF) {               // the store that last used this buffer must be read
-            if (lane == 0) tc::bulk_wait_read<Cfg::NBUF - 1>();
-            __syncwarp();
-          }
-        } else if (EPI == TEPI_GELU_BWD) {
+        if (EPI == TEPI_GELU_BWD) {
           tc::mbar_wait_u32(auxb + (seq % Cfg::NBUF) * 8, (seq / Cfg::NBUF) & 1);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {                        // gp = GELU'(a) saved by the forward
@@ -528,28 +431,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               f32x2 h2, g2;
-#ifdef MOE_EXP_NOMATH
-              h2 = v[q * 4 + j]; g2 = v[q * 4 + j];
-#else
               gelu_and_prime_x2(v[q * 4 + j], h2, g2);
-#endif
               hw[j] = f2_to_bf16x2(h2);
               gw[j] = f2_to_bf16x2(g2);
             }
-#ifdef MOE_EXP_DIRECT
-            if (store) {
-              st_v4(p.o1 + row * p.ldo_b + n + q * 8, make_uint4(gw[0], gw[1], gw[2], gw[3]));
-              st_v4(p.o2 + row * p.ldo_b + n + q * 8, make_uint4(hw[0], hw[1], hw[2], hw[3]));
-            }
-#else
-#ifdef MOE_EXP_NOSTS
-            if ((gw[0] ^ gw[1] ^ gw[2] ^ gw[3] ^ hw[0] ^ hw[1] ^ hw[2] ^ hw[3]) == 0x12345678u)
-#endif
-            {
             tc::st_shared_v4(buf + lane * 64 + ((q ^ swz) << 4), make_uint4(gw[0], gw[1], gw[2], gw[3]));
             tc::st_shared_v4(buf + CHUNK_BYTES + lane * 64 + ((q ^ swz) << 4), make_uint4(hw[0], hw[1], hw[2], hw[3]));
-            }
-#endif
           }
         } else if (EPI == TEPI_BIAS_GELU_H) {
 #pragma unroll
@@ -570,12 +457,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
                              make_uint4(f2_to_bf16x2(v[q * 4]), f2_to_bf16x2(v[q * 4 + 1]), f2_to_bf16x2(v[q * 4 + 2]),
                                         f2_to_bf16x2(v[q * 4 + 3])));
         }
-        TR(11, t);
-#ifndef MOE_EXP_NOFENCE
         tc::fence_proxy_async();
-#endif
         __syncwarp();
-        TR(12, t);
         if (EPI == TEPI_GELU_BWD && p.colpart && store) {
           // db1 partial of this warp's 32 x 32 bf16 da sub-tile (fixed order): lane = (column pair
           // cp = lane & 15, row parity rp = lane >> 4) sums rows rp, rp+2, ..., then the two parities
@@ -598,34 +481,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
             *reinterpret_cast<float2*>(p.colpart + (long long)((tl.m_own + sub * 32) >> 5) * p.N + n + 2 * cp) =
                 make_float2(c0, c1);
         }
-#ifdef MOE_EXP_STG
-        if (store) {   // coalesced LSU stores from the swizzled smem sub-tile: 8 rows x 64 B per instruction
-          const int row0 = tl.m_own + sub * 32;
-#pragma unroll
-          for (int o = 0; o < Cfg::NOUT; ++o) {
-            bf16* dst = (o == 0 ? p.o1 : p.o2) + n + (lane & 3) * 8;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int r = (lane >> 2) + 8 * i;
-              const uint4 v4 = tc::ld_shared_v4(buf + o * CHUNK_BYTES + r * 64 + (((lane & 3) ^ ((r >> 1) & 3)) << 4));
-              st_v4(dst + (long long)(row0 + r) * p.ldo_b, v4);
-            }
-          }
-        }
-#endif
         if (lane == 0) {
-#if defined(MOE_EXP_NOSTORE) || defined(MOE_EXP_STG) || defined(MOE_EXP_DIRECT)
-          if (false) {
-#else
           if (store) {
-#endif
             const int row0 = tl.m_own + sub * 32;
             tc::tma_store_2d(&tmO1, buf, n, row0);
             if (Cfg::NOUT == 2) tc::tma_store_2d(&tmO2, buf + CHUNK_BYTES, n, row0);
           }
           tc::bulk_commit();                              // one (possibly empty) group per chunk
-          TR(9, t);
-          if (EPI == TEPI_GELU_BWD && !Cfg::GP_LDG) {
+          if (EPI == TEPI_GELU_BWD) {
             tc::bulk_wait_read<2>();                      // buffer (seq+2)%4 was last stored at seq-2
             aux_issue(seq + 2);
           }
@@ -635,7 +498,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive_cluster(tempty_leader + acc * 8);
-      TR(10, t);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -739,32 +601,7 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
   }
   long long pairs = tiles_upper < sms / 2 ? tiles_upper : sms / 2;
   if (pairs <= 0) return cudaSuccess;
-#ifdef MOE_EXP_TRACE
-  // trace the 3rd launch of each ROWS epilogue kind; dumped to gpurun_out/trace_<EPI>.bin at exit
-  static int n_launch = 0;
-  static unsigned long long* buf = nullptr;
-  TcParams pt = p;
-  pt.trace = nullptr;
-  if (!KGRP && ++n_launch == 3) {
-    const size_t bytes = 2 * 16 * (size_t)kTraceN * 8;
-    cudaMallocManaged(&buf, bytes);
-    cudaMemset(buf, 0, bytes);
-    pt.trace = buf;
-    static unsigned long long* sbuf = nullptr;
-    sbuf = buf;
-    static char name[64];
-    snprintf(name, sizeof name, "gpurun_out/trace_%d.bin", EPI);
-    struct D { static void dump() {} };
-    std::atexit([] {
-      cudaDeviceSynchronize();
-      FILE* fp = fopen(name, "wb");
-      if (fp) { fwrite(sbuf, 8, 2 * 16 * (size_t)kTraceN, fp); fclose(fp); }
-    });
-  }
-  k<<<(unsigned)(2 * pairs), EpiCfg<EPI, QOV>::THREADS, smem, s>>>(a, b, o1, o2, x, pt), count_launch();
-#else
   k<<<(unsigned)(2 * pairs), EpiCfg<EPI, QOV>::THREADS, smem, s>>>(a, b, o1, o2, x, p), count_launch();
-#endif
   return cudaGetLastError();
 }
 
@@ -878,7 +715,6 @@ cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* 
       return cudaErrorInvalidValue;
     p.N = f; p.K = d; p.b_group_rows = d;
     p.o1 = reinterpret_cast<bf16*>(da); p.ldo_b = f;
-    p.aux = reinterpret_cast<const bf16*>(gp);
     // db1 partials live in dx_perm's memory until dgrad1 overwrites it ([R_cap/32][f] fp32 <= R_cap x d bf16)
     const bool fuse_db1 = db1 && (long long)f * 4 <= (long long)d * 2 * 32;
     p.colpart = fuse_db1 ? reinterpret_cast<float*>(dx_perm) : nullptr;
