@@ -69,6 +69,14 @@ enum TcEpi { TEPI_BIAS_GELU = 0, TEPI_BIAS = 1, TEPI_GELU_BWD = 2, TEPI_STORE = 
 #endif
 // (GELU and fp32 weight-gradient epilogues: 1 buffer per warp -- the smaller staging area buys
 // operand stages, C4 GEMM1 -1.7%, weight gradients -2%; bias / store keep 2, profiles/r01/s2/epi_warps.txt)
+// GELU' operand ring of the dgrad2 epilogue: MOE_NB_GBWD staging buffers per warp, the operand of
+// chunk seq + MOE_AUXD loaded while chunk seq is processed (MOE_NB_GBWD - MOE_AUXD stores in flight)
+#ifndef MOE_NB_GBWD
+#define MOE_NB_GBWD 4
+#endif
+#ifndef MOE_AUXD
+#define MOE_AUXD 2
+#endif
 #ifndef MOE_NB_GELU
 #define MOE_NB_GELU 1
 #endif
@@ -91,7 +99,7 @@ template <int EPI, int QOV = 0> struct EpiCfg {   // QOV: epilogue warps per qua
   static constexpr int THREADS = 64 + 32 * WARPS;
   static constexpr int NOUT = EPI == TEPI_BIAS_GELU ? 2 : (EPI == TEPI_F32 ? 0 : 1);  // bf16 TMA-stored outputs
   // staging buffers per warp (GELU' bwd: 4, its a-operand loads run two chunks ahead)
-  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? 4
+  static constexpr int NBUF = EPI == TEPI_GELU_BWD ? MOE_NB_GBWD
                               : EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS_GELU_H ? MOE_NB_GELU
                               : EPI == TEPI_BIAS ? MOE_NB_BIAS
                               : EPI == TEPI_STORE ? MOE_NB_STORE : MOE_NB_F32;
@@ -174,8 +182,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;                               // [EPI_WARPS][4] (GELU' operand loads)
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(aux_bar + EPI_WARPS * 4);
+  uint64_t* aux_bar = tempty_bar + 2;                               // [EPI_WARPS][8] (GELU' operand loads)
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(aux_bar + EPI_WARPS * 8);
   int* s_off = reinterpret_cast<int*>(s_tmem + 4);
   int* s_pair = s_off + (MAX_G + 1);
 
@@ -208,7 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       tc::mbar_init(&tfull_bar[a], 1);
       tc::mbar_init(&tempty_bar[a], 2 * EPI_WARPS);
     }
-    for (int i = 0; i < EPI_WARPS * 4; ++i) tc::mbar_init(&aux_bar[i], 1);
+    for (int i = 0; i < EPI_WARPS * 8; ++i) tc::mbar_init(&aux_bar[i], 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) {
@@ -311,7 +319,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
     const uint32_t stage_base = tc::smem_u32(staging) + ew * Cfg::WARP_STAGE;
     const uint32_t swz = (uint32_t)((lane >> 1) & 3);  // SWIZZLE_64B: 16-byte chunk q -> q ^ ((row >> 1) & 3)
     const uint32_t tempty_leader = tc::mapa(tc::smem_u32(tempty_bar), 0);
-    const uint32_t auxb = tc::smem_u32(aux_bar + ew * 4);
+    const uint32_t auxb = tc::smem_u32(aux_bar + ew * 8);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t seq = 0;                                   // this warp's chunk sequence number (nch per tile)
@@ -334,8 +342,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       tc::tma_load_2d_u32(stage_base + b * CHUNK_BYTES, &tmX, auxb + b * 8, col, tn.m_own + sub * 32);
     };
     if (EPI == TEPI_GELU_BWD && lane == 0) {
-      aux_issue(0);
-      aux_issue(1);
+      for (int i = 0; i < MOE_AUXD; ++i) aux_issue(i);
     }
 
     for (int t = cid; t < total; t += ncl) {
@@ -489,8 +496,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
           }
           tc::bulk_commit();                              // one (possibly empty) group per chunk
           if (EPI == TEPI_GELU_BWD) {
-            tc::bulk_wait_read<2>();                      // buffer (seq+2)%4 was last stored at seq-2
-            aux_issue(seq + 2);
+            // buffer (seq + AUXD) % NBUF was last stored at chunk seq + AUXD - NBUF
+            tc::bulk_wait_read<MOE_NB_GBWD - MOE_AUXD>();
+            aux_issue(seq + MOE_AUXD);
           }
         }
         __syncwarp();

@@ -284,6 +284,13 @@ def _shape(name, T, d, f, E, tau, c, wg_var=None):
                                wg_std=math.sqrt((wg_var if wg_var else 1.0) / d))
 
 
+def test_bf16_simt_gemm_debug_path(monkeypatch):
+    # MOE_GEMM=simt: the bf16 expert GEMMs on the CUDA-core grouped GEMM (the fp32 configs'
+    # kernel) instead of tcgen05 -- a debug path, held to the same oracle checks
+    monkeypatch.setenv("MOE_GEMM", "simt")
+    _run(_shape("simt", 300, 256, 512, 16, 0.7, 0.05))
+
+
 def test_bf16_E48_fused_gate_16_wide_boxes():
     # E % 32 != 0: fused gate with 12 experts per lane quarter; N=48 gate MMA
     _run(_shape("E48", 700, 256, 512, 48, 0.5, 0.03))

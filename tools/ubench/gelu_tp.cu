@@ -33,9 +33,52 @@ __device__ __forceinline__ f32x2 exp2_poly2(f32x2 S) {
             __uint_as_float(__float_as_uint(p1) + (__float_as_uint(j1) << 23)));
 }
 
+// V = 5: X = 1 + k|a| as ONE FFMA2 on a sign-carrying constant (LOP3 puts a's sign on k);
+// V = 6: additionally (1 - NS)/2 from the sign bit on the ALU (SHF + LOP3) instead of an FFMA2
+__device__ __forceinline__ uint32_t sign_or(uint32_t a, uint32_t k) {
+  uint32_t d;   // (a & 0x80000000) | k
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "n"(0x80000000u), "r"(k));
+  return d;
+}
+__device__ __forceinline__ uint32_t one_if_nonneg(uint32_t a) {
+  return (uint32_t)(~((int32_t)a >> 31)) & 0x3f800000u;   // a >= 0 (sign clear) -> 1.0f, else 0
+}
+template <int V>
+__device__ __forceinline__ void gelu2_lean(f32x2 A, f32x2& H, f32x2& G) {
+  constexpr float kS2P = 2.5066282746310002f;
+  constexpr float kk = 0.3275911f * 0.70710678118654752f;
+  float a0, a1;
+  f2_split(A, a0, a1);
+  const uint32_t ua0 = __float_as_uint(a0), ua1 = __float_as_uint(a1);
+  const f32x2 SGK = f2(__uint_as_float(sign_or(ua0, __float_as_uint(kk))), __uint_as_float(sign_or(ua1, __float_as_uint(kk))));
+  const f32x2 NS = f2(__uint_as_float(neg_sign_one(ua0, 0x3f800000u)), __uint_as_float(neg_sign_one(ua1, 0x3f800000u)));
+  const f32x2 X = fma2(A, SGK, f2(1.0f));
+  float x0, x1;
+  f2_split(X, x0, x1);
+  const f32x2 T = f2(rcp_approx(x0), rcp_approx(x1));
+  f32x2 P = fma2(f2(0.5f * kS2P * 1.061405429f), T, f2(0.5f * kS2P * -1.453152027f));
+  P = fma2(P, T, f2(0.5f * kS2P * 1.421413741f));
+  P = fma2(P, T, f2(0.5f * kS2P * -0.284496736f));
+  P = fma2(P, T, f2(0.5f * kS2P * 0.254829592f));
+  P = mul2(T, P);
+  const f32x2 S = fma2(A, mul2(A, f2(-0.5f * 1.4426950408889634f)), f2(-1.3257480647361595f));
+  float s0, s1;
+  f2_split(S, s0, s1);
+  const f32x2 E = f2(ex2_approx(s0), ex2_approx(s1));
+  const f32x2 Q = mul2(P, E);
+  f32x2 HS;
+  if (V == 6) HS = f2(__uint_as_float(one_if_nonneg(ua0)), __uint_as_float(one_if_nonneg(ua1)));
+  else HS = fma2(NS, f2(-0.5f), f2(0.5f));
+  const f32x2 PH = fma2(NS, Q, HS);
+  H = mul2(A, PH);
+  G = fma2(A, E, PH);
+}
+
 template <int V>
 __device__ __forceinline__ void gelu2(f32x2 A, f32x2& H, f32x2& G) {
-  if (V == 0) {
+  if (V == 5 || V == 6) {
+    gelu2_lean<V>(A, H, G);
+  } else if (V == 0) {
     float a0, a1, h0, h1, g0, g1; f2_split(A, a0, a1);
     gelu_and_prime_fast(a0, h0, g0); gelu_and_prime_fast(a1, h1, g1);
     H = f2(h0, h1); G = f2(g0, g1);
@@ -132,7 +175,7 @@ int main() {
     double* e; cudaMalloc(&e, 16); double he[2]; const int n = 1 << 22;
 #define ACC(V) cudaMemset(e, 0, 16); acc_k<V><<<n / 512, 256>>>(e, n); cudaMemcpy(he, e, 16, cudaMemcpyDeviceToHost); \
     printf("variant %d: max|h err| %.3e  max|gp err| %.3e\n", V, he[0], he[1]);
-    ACC(0) ACC(1) ACC(2) ACC(3) ACC(4)
+    ACC(0) ACC(1) ACC(2) ACC(3) ACC(4) ACC(5) ACC(6)
   }
   float* out; long long* clk; cudaMalloc(&out, 148 * 384 * 4); cudaMalloc(&clk, 148 * 8);
   long long h[148];
@@ -149,6 +192,8 @@ int main() {
     k<2><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 NR-rcp (elem)", 32);
     k<3><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 poly-exp2 (elem)", 32);
     k<4><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 no MUFU (elem)", 32);
+    k<5><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 sign-k X (elem)", 32);
+    k<6><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 sign-k X + ALU HS (elem)", 32);
     raw<0><<<148, 384>>>(out, clk, iters); report("MUFU.EX2 (+FMUL)", 8);
     raw<1><<<148, 384>>>(out, clk, iters); report("MUFU.RCP", 8);
     raw<2><<<148, 384>>>(out, clk, iters); report("FFMA", 8);
