@@ -645,6 +645,7 @@ def run_ep(args, rank, world):
     counts_all = counts_now()
     graph = None
     g_ev = ((ev(), ev()), (ev(), ev()))
+    stage_ev = {}
     n0 = L.moe_kernel_launch_count()
     if path != "nccl" and args.graph:
         r.prepare()
@@ -656,8 +657,10 @@ def run_ep(args, rank, world):
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         n0 = L.moe_kernel_launch_count()
+        r.stage_events = stage_ev
         with torch.cuda.graph(graph):
             step(g_ev)
+        r.stage_events = None
         launches = L.moe_kernel_launch_count() - n0
         for i in range(max(1, args.warmup)):
             u.copy_(upool[i % U_POOL])
@@ -671,6 +674,7 @@ def run_ep(args, rank, world):
     torch.cuda.synchronize()
     n1 = L.moe_kernel_launch_count()
     step_ms, gemm_ms = [], []
+    stage_ms = {}
     t_wall = time.perf_counter()
     for i in range(args.steps):
         flush.fill_(1)
@@ -687,6 +691,8 @@ def run_ep(args, rank, world):
         s1.synchronize()
         step_ms.append(s0.elapsed_time(s1))
         gemm_ms.append(e[0][0].elapsed_time(e[0][1]) + e[1][0].elapsed_time(e[1][1]))
+        for k, (a, b) in stage_ev.items():
+            stage_ms.setdefault(k, []).append(a.elapsed_time(b))
     torch.cuda.synchronize()
     barrier(world)
     wall = time.perf_counter() - t_wall
@@ -718,6 +724,7 @@ def run_ep(args, rank, world):
     out["roofline"] = _roofline(cfg, flops_per_gpu, g_ms, wall, clk, world, None)
     out["nvlink_gbs"] = {"value": nvl / (ms_step / 1e3) / 1e9, "unit": "GB/s per GPU (algorithmic bytes / step time)",
                          "bytes_per_gpu_per_step": nvl, "frac_of_900": nvl / (ms_step / 1e3) / 1e9 / NVLINK_GBS}
+    out["stages"] = {k: {"ms": max_over_ranks(sum(v) / len(v), world)} for k, v in stage_ms.items()} or None
     out["spawn"] = spawn
     out["gpu_launches"] = int(launches)
     out["clocks"] = clk

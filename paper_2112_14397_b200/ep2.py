@@ -88,10 +88,23 @@ class EP2Rank:
         # optional {"experts_fwd": (ev0, ev1), "experts_bwd": (ev0, ev1)}: CUDA events recorded
         # around the expert FFN calls on the current stream (bench.py's GEMM time)
         self.events: Optional[Dict[str, tuple]] = None
+        # optional dict receiving a (start, end) event pair per phase (per-stage breakdown; the
+        # fused exchanges are inside the phases: dispatch stores rows to the owners, combine and
+        # dispatch_bwd gather from them, combine_bwd reads dy from the token owners)
+        self.stage_events: Optional[Dict[str, tuple]] = None
 
     def _mark(self, name: str, i: int):
         if self.events and name in self.events:
             self.events[name][i].record(torch.cuda.current_stream())
+
+    def _stage(self, name: str, i: int):
+        d = self.stage_events
+        if d is None:
+            return
+        if name not in d:
+            d[name] = (torch.cuda.Event(enable_timing=True, external=True),
+                       torch.cuda.Event(enable_timing=True, external=True))
+        d[name][i].record(torch.cuda.current_stream())
 
     def __del__(self):
         try:
@@ -316,18 +329,28 @@ class EP2Rank:
 
     # ------------------------------------------------------------ one rank, one process (multi-GPU)
     def forward(self, x, u, tau, threshold, top1=False):
+        st = self._stage
+        st("gate", 0)
         self.fwd_gate(x, u, tau, threshold, top1)
+        st("gate", 1)
         self.barrier()
+        st("dispatch", 0)
         self.fwd_plan()
         self.fwd_dispatch()
+        st("dispatch", 1)
         self.barrier()
+        st("expert_ffn", 0)
         if self.dedup:
             self.fwd_permute()
         self.fwd_experts()
         if self.dedup:
             self.fwd_presum()
+        st("expert_ffn", 1)
         self.barrier()
-        return self.fwd_combine()
+        st("combine", 0)
+        y = self.fwd_combine()
+        st("combine", 1)
+        return y
 
     def grow(self):
         """After MOE_ECAPACITY: size the buffers for the counts of the step that overflowed (every
@@ -352,15 +375,25 @@ class EP2Rank:
         raise RuntimeError("unreachable")
 
     def backward(self, dy, balance_alpha: float = 0.0):
+        st = self._stage
         self.bwd_stage_dy(dy)
         self.barrier()
+        st("combine_bwd", 0)
         if self.dedup:
             self.bwd_gather_dy()
         self.bwd_combine()
+        st("combine_bwd", 1)
+        st("expert_ffn_bwd", 0)
         self.bwd_experts()
         if self.dedup:
             self.bwd_presum()
+        st("expert_ffn_bwd", 1)
         self.barrier()
+        st("gate_bwd", 0)
         self.bwd_gate(balance_alpha)
         L.moe_ep_allreduce(self.ctx, self.st["grads"]["dWg"], self.d * self.E)
-        return self.bwd_dispatch()
+        st("gate_bwd", 1)
+        st("dispatch_bwd", 0)
+        g = self.bwd_dispatch()
+        st("dispatch_bwd", 1)
+        return g

@@ -66,17 +66,22 @@ __device__ __forceinline__ void gelu2_lean(f32x2 A, f32x2& H, f32x2& G) {
   f2_split(S, s0, s1);
   const f32x2 E = f2(ex2_approx(s0), ex2_approx(s1));
   const f32x2 Q = mul2(P, E);
-  f32x2 HS;
-  if (V == 6) HS = f2(__uint_as_float(one_if_nonneg(ua0)), __uint_as_float(one_if_nonneg(ua1)));
-  else HS = fma2(NS, f2(-0.5f), f2(0.5f));
-  const f32x2 PH = fma2(NS, Q, HS);
+  f32x2 PH;
+  if (V == 7) {            // Phi = 0.5 + NS (Q - 0.5): one FFMA2 fewer, absolute (not relative) tail accuracy
+    PH = fma2(NS, fma2(P, E, f2(-0.5f)), f2(0.5f));
+  } else {
+    f32x2 HS;
+    if (V == 6) HS = f2(__uint_as_float(one_if_nonneg(ua0)), __uint_as_float(one_if_nonneg(ua1)));
+    else HS = fma2(NS, f2(-0.5f), f2(0.5f));
+    PH = fma2(NS, Q, HS);
+  }
   H = mul2(A, PH);
   G = fma2(A, E, PH);
 }
 
 template <int V>
 __device__ __forceinline__ void gelu2(f32x2 A, f32x2& H, f32x2& G) {
-  if (V == 5 || V == 6) {
+  if (V == 5 || V == 6 || V == 7) {
     gelu2_lean<V>(A, H, G);
   } else if (V == 0) {
     float a0, a1, h0, h1, g0, g1; f2_split(A, a0, a1);
@@ -175,7 +180,7 @@ int main() {
     double* e; cudaMalloc(&e, 16); double he[2]; const int n = 1 << 22;
 #define ACC(V) cudaMemset(e, 0, 16); acc_k<V><<<n / 512, 256>>>(e, n); cudaMemcpy(he, e, 16, cudaMemcpyDeviceToHost); \
     printf("variant %d: max|h err| %.3e  max|gp err| %.3e\n", V, he[0], he[1]);
-    ACC(0) ACC(1) ACC(2) ACC(3) ACC(4) ACC(5) ACC(6)
+    ACC(0) ACC(1) ACC(2) ACC(3) ACC(4) ACC(5) ACC(6) ACC(7)
   }
   float* out; long long* clk; cudaMalloc(&out, 148 * 384 * 4); cudaMalloc(&clk, 148 * 8);
   long long h[148];
@@ -194,6 +199,7 @@ int main() {
     k<4><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 no MUFU (elem)", 32);
     k<5><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 sign-k X (elem)", 32);
     k<6><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 sign-k X + ALU HS (elem)", 32);
+    k<7><<<148, 384>>>(out, clk, iters, 1.f); report("gelu x2 sign-k X + Q-0.5 (elem)", 32);
     raw<0><<<148, 384>>>(out, clk, iters); report("MUFU.EX2 (+FMUL)", 8);
     raw<1><<<148, 384>>>(out, clk, iters); report("MUFU.RCP", 8);
     raw<2><<<148, 384>>>(out, clk, iters); report("FFMA", 8);
