@@ -133,6 +133,7 @@ struct TcParams {
 
 struct Tile {
   int g, m_own, n0, kb0, nkb, row_end;
+  int half;   // ROWS: the odd last 128-row block of an expert, run as an M = 128 pair MMA (64 rows per CTA)
 };
 
 template <bool KGRP>
@@ -146,7 +147,10 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, const int* s_off,
       if (s_pair[mid] <= P) lo = mid; else hi = mid - 1;
     }
     tl.g = lo;
-    tl.m_own = s_off[lo] + 256 * (P - s_pair[lo]) + 128 * (int)rank;
+    const int pl = P - s_pair[lo];
+    const int blocks = (s_off[lo + 1] - s_off[lo]) / BM;        // segments are 128-aligned
+    tl.half = (blocks & 1) && 2 * pl + 1 == blocks;
+    tl.m_own = s_off[lo] + 256 * pl + (tl.half ? 64 : 128) * (int)rank;
     tl.row_end = min(s_off[lo + 1], p.rows_cap);
     tl.n0 = nt * BN;
     tl.kb0 = 0;
@@ -158,6 +162,7 @@ __device__ __forceinline__ bool decode_tile(const TcParams& p, const int* s_off,
     const int r = t - tl.g * per_g;
     const int mt = r / n_tiles, nt = r - mt * n_tiles;
     tl.m_own = mt * 256 + 128 * (int)rank;
+    tl.half = 0;
     tl.row_end = p.M;
     tl.n0 = nt * BN;
     tl.kb0 = s_off[tl.g] / BK;
@@ -275,6 +280,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
     // ------------------------------------------------------------ MMA issuer (pair leader)
     if (leader && lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16(256, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      // half tiles: M = 128 across the pair (each CTA's first 64 A rows); the accumulator then holds
+      // rows 0-63 x columns 0-127 in TMEM lanes 0-63 and the same rows x columns 128-255 in lanes
+      // 64-127, columns 0-127 of the buffer (the 2-SM M = 128 data-path layout)
+      constexpr uint32_t idesc_h = tc::idesc_bf16(128, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -299,7 +308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
                                      : tc::smem_desc_sw128(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? tc::smem_desc_sw128(sb + k * 2048, 8192, 1024)
                                      : tc::smem_desc_sw128(sb + k * 32, 16, 1024);
-            tc::mma_bf16_pair(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            tc::mma_bf16_pair(d_tmem, ad, bd, tl.half ? idesc_h : idesc, (kb | k) != 0);
           }
           tc::mma_commit_pair_mc(tc::smem_u32(&empty_bar[stage]), 0x3);   // frees the slot in both CTAs
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -324,25 +333,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
     uint32_t acc_phase = 0;
     uint32_t seq = 0;                                   // this warp's chunk sequence number (nch per tile)
 
-    // GELU' operand: TMA-load a[rows, 32 cols] two chunks ahead into the staging buffers
-    // the decoded tile is cached: consecutive sequence numbers stay on one tile for nch chunks,
-    // so the expert search runs once per tile, not once per chunk (lane 0's chunk critical path)
-    int aux_t = -1;
+    // this warp's rows / columns / chunk count in a tile: full tiles -> rows sub*32.., all 8 chunks
+    // of 32 columns shared by the quarter's warps; half tiles -> rows (sub&1)*32.. of the CTA's 64,
+    // column half (sub>>1)*128, 4 chunks
+    auto rows0 = [&](const Tile& x) { return x.half ? (sub & 1) * 32 : sub * 32; };
+    auto cols0 = [&](const Tile& x) { return x.half ? (sub >> 1) * 128 : 0; };
+    auto nchunks = [&](const Tile& x) { return x.half ? (CHUNKS / 2 - part + EPI_PER_Q - 1) / EPI_PER_Q : nch; };
+
+    // GELU' operand: TMA-load a[rows, 32 cols] MOE_AUXD chunks ahead into the staging buffers,
+    // following the consumer's (tile, chunk) order with a cursor (the expert search runs once per
+    // tile, not once per chunk: lane 0's chunk critical path)
+    int aux_t = cid, aux_k = 0;
+    uint32_t aux_seq = 0;
+    bool aux_have = false;
     Tile tn{};
-    auto aux_issue = [&](uint32_t s) {
-      const int t = cid + (int)(s / nch) * ncl;
-      if (t >= total) return;
-      if (t != aux_t) {
-        decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tn);
-        aux_t = t;
+    auto aux_issue = [&]() {
+      while (aux_t < total) {
+        if (!aux_have) {
+          decode_tile<KGRP>(p, s_off, s_pair, aux_t, n_tiles, rank, tn);
+          aux_have = true;
+        }
+        if (aux_k < nchunks(tn)) {
+          const int col = tn.n0 + cols0(tn) + (part + EPI_PER_Q * aux_k) * 32;
+          const uint32_t b = aux_seq % Cfg::NBUF;
+          tc::mbar_arrive_expect_tx_u32(auxb + b * 8, CHUNK_BYTES);
+          tc::tma_load_2d_u32(stage_base + b * CHUNK_BYTES, &tmX, auxb + b * 8, col, tn.m_own + rows0(tn));
+          ++aux_seq;
+          ++aux_k;
+          return;
+        }
+        aux_t += ncl;
+        aux_k = 0;
+        aux_have = false;
       }
-      const int col = tn.n0 + (part + EPI_PER_Q * (int)(s % nch)) * 32;
-      const uint32_t b = s % Cfg::NBUF;
-      tc::mbar_arrive_expect_tx_u32(auxb + b * 8, CHUNK_BYTES);
-      tc::tma_load_2d_u32(stage_base + b * CHUNK_BYTES, &tmX, auxb + b * 8, col, tn.m_own + sub * 32);
     };
     if (EPI == TEPI_GELU_BWD && lane == 0) {
-      for (int i = 0; i < MOE_AUXD; ++i) aux_issue(i);
+      for (int i = 0; i < MOE_AUXD; ++i) aux_issue();
     }
 
     for (int t = cid; t < total; t += ncl) {
@@ -359,17 +385,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
         }
         continue;
       }
-      const bool warp_rows_ok = tl.m_own + sub * 32 < tl.row_end;   // warp-uniform for ROWS tiles
+      const int r0 = rows0(tl), coff = cols0(tl), nch_t = nchunks(tl);
+      const bool warp_rows_ok = tl.m_own + r0 < tl.row_end;          // warp-uniform for ROWS tiles
       const float* bias_t = nullptr;                                 // padded fp32 bias row of this tile
       if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H)
-        bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0;
+        bias_t = p.bias + (long long)tl.g * p.bias_g + tl.n0 + coff;
       tc::mbar_wait_sleep(&tfull_bar[acc], acc_phase);
       tc::tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + ((uint32_t)(sub * 32) << 16);
 #pragma unroll 1
-      for (int k = 0; k < nch; ++k, ++seq) {
-        const int col = (part + EPI_PER_Q * k) * 32;
-        const int n = tl.n0 + col;
+      for (int k = 0; k < nch_t; ++k, ++seq) {
+        const int col = (part + EPI_PER_Q * k) * 32;     // TMEM column of the chunk
+        const int n = tl.n0 + coff + col;                // output column
         uint32_t r[32];
         float4 bf[8];                                      // bias of this chunk (broadcast loads)
         if (EPI == TEPI_BIAS_GELU || EPI == TEPI_BIAS || EPI == TEPI_BIAS_GELU_H) {
@@ -395,8 +422,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
           __syncwarp();
           if (lane == 0) {
             // M and N are multiples of 64: a 32x32 box is wholly inside the group's [M, N] block or outside
-            if (tl.m_own + sub * 32 < p.M && n < p.N)
-              tc::tma_store_2d(&tmO1, fbuf, n, tl.g * p.M + tl.m_own + sub * 32);
+            if (tl.m_own + r0 < p.M && n < p.N)
+              tc::tma_store_2d(&tmO1, fbuf, n, tl.g * p.M + tl.m_own + r0);
             tc::bulk_commit();
           }
           __syncwarp();
@@ -485,12 +512,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
           c0 += __shfl_xor_sync(0xffffffffu, c0, 16);
           c1 += __shfl_xor_sync(0xffffffffu, c1, 16);
           if (rp == 0)
-            *reinterpret_cast<float2*>(p.colpart + (long long)((tl.m_own + sub * 32) >> 5) * p.N + n + 2 * cp) =
+            *reinterpret_cast<float2*>(p.colpart + (long long)((tl.m_own + r0) >> 5) * p.N + n + 2 * cp) =
                 make_float2(c0, c1);
         }
         if (lane == 0) {
           if (store) {
-            const int row0 = tl.m_own + sub * 32;
+            const int row0 = tl.m_own + r0;
             tc::tma_store_2d(&tmO1, buf, n, row0);
             if (Cfg::NOUT == 2) tc::tma_store_2d(&tmO2, buf + CHUNK_BYTES, n, row0);
           }
@@ -498,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
           if (EPI == TEPI_GELU_BWD) {
             // buffer (seq + AUXD) % NBUF was last stored at chunk seq + AUXD - NBUF
             tc::bulk_wait_read<MOE_NB_GBWD - MOE_AUXD>();
-            aux_issue(seq + MOE_AUXD);
+            aux_issue();
           }
         }
         __syncwarp();
