@@ -14,8 +14,10 @@
 // Roles (64 + 128 x PER_Q threads / CTA): warp 0 = TMA producer, warp 1 = TMEM allocator +
 //   MMA issuer (leader CTA only), warps 2.. = epilogue.
 // Scheduling (static, per pair): ROWS mode (ragged M): a tile is a pair of 128-row blocks
-//   of ONE expert (segments are 128-aligned; an odd last block leaves the second CTA's
-//   half idle) x one 256-wide N block; the expert comes from the device offsets[].
+//   of ONE expert (segments are 128-aligned) x one 256-wide N block; the expert comes from
+//   the device offsets[].  An expert's odd last block is a HALF tile: an M = 128 pair MMA
+//   (64 rows per CTA), whose accumulator holds rows 0-63 x columns 0-127 in TMEM lanes 0-63
+//   and the same rows x columns 128-255 in lanes 64-127 -- no CTA computes pad rows.
 //   KGRP mode (ragged K, weight gradients): tiles = G x ceil(M/256) x ceil(N/256), K range
 //   of group g = [offsets[g], offsets[g+1]); empty groups store zeros.
 #include <cuda.h>
