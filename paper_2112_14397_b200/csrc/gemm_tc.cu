@@ -128,8 +128,8 @@ struct TcParams {
   bf16* o2;
   long long ldo_b;
   float* colpart;         // TEPI_GELU_BWD: per-32-row column sums of da [R_cap/32][N] (bias gradient db1)
-  const void* reserved0;  // (unused; keeps the parameter block's layout of the measured builds)
-  void* reserved1;
+  int o12;                // GEMM1: gp and h are one [2][R_cap][f] buffer, stored with ONE 3D TMA op per chunk
+  void* reserved1;        // (unused; keeps the parameter block's layout of the measured builds)
   int a3d, b3d;           // MN-major operand given as a 3D map {64, K rows, MN / 64}: one TMA op per stage
 };
 
@@ -520,8 +520,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
         if (lane == 0) {
           if (store) {
             const int row0 = tl.m_own + r0;
-            tc::tma_store_2d(&tmO1, buf, n, row0);
-            if (Cfg::NOUT == 2) tc::tma_store_2d(&tmO2, buf + CHUNK_BYTES, n, row0);
+            if (Cfg::NOUT == 2 && p.o12) {
+              tc::tma_store_3d(&tmO1, buf, n, row0, 0);      // the [2][32][32] staging box: gp then h
+            } else {
+              tc::tma_store_2d(&tmO1, buf, n, row0);
+              if (Cfg::NOUT == 2) tc::tma_store_2d(&tmO2, buf + CHUNK_BYTES, n, row0);
+            }
           }
           tc::bulk_commit();                              // one (possibly empty) group per chunk
           if (EPI == TEPI_GELU_BWD) {
@@ -605,6 +609,20 @@ bool make_map_mn(CUtensorMap* m, const void* ptr, long long rows, long long cols
 }
 bool make_store_map(CUtensorMap* m, const void* ptr, long long rows, long long cols) {
   return make_map(m, ptr, rows, cols, cols, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+}
+// two [rows, cols] bf16 outputs, the second `gap` bytes after the first (gap >= rows*cols*2, a
+// multiple of 16), as one 3D map with {32, 32, 2} boxes: the epilogue's two staged 32x32 boxes
+// leave in one TMA op
+bool make_store_map_pair(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long gap) {
+  EncodeTiledFn f = encode_fn();
+  if (!f || !ptr || gap < rows * cols * 2 || gap % 16 != 0 || gap >= (1ll << 40)) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, (cuuint64_t)gap};
+  cuuint32_t box[3] = {32, 32, 2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 // fp32 [rows, cols] row-major output, 32x32 boxes with 128-byte swizzled rows (weight gradients)
 bool make_store_map_f32(CUtensorMap* m, const void* ptr, long long rows, long long cols) {
@@ -712,6 +730,11 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
   p.N = f; p.K = d; p.b_group_rows = f;
   p.bias = c->biasf; p.bias_g = fp;
   p.o1 = reinterpret_cast<bf16*>(gp ? gp : h); p.o2 = reinterpret_cast<bf16*>(h); p.ldo_b = f;
+  // h above gp in memory (the layer allocates them as one [2][R_cap][f] buffer): one 3D store of
+  // both staged boxes per chunk instead of two 2D stores
+  p.o12 = gp && !getenv("MOE_NO_STORE_PAIR") && reinterpret_cast<uintptr_t>(h) > reinterpret_cast<uintptr_t>(gp) &&
+          make_store_map_pair(&mO1, gp, R_cap, f,
+                              (long long)(reinterpret_cast<uintptr_t>(h) - reinterpret_cast<uintptr_t>(gp)));
   const long long up = rows_pairs_upper(R_cap, El);
   cudaError_t e = gp ? launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p,
                                                                        up * ((f + BN - 1) / BN), c->sm_count, s)

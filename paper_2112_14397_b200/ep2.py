@@ -234,8 +234,8 @@ class EP2Rank:
 
     def fwd_experts(self):
         R, d, f, s = self.R_cap, self.d, self.f, self.st
-        s["gp"] = torch.empty(R, f, dtype=self.dtype, device=self.device)
-        s["h"] = torch.empty(R, f, dtype=self.dtype, device=self.device)
+        gph = torch.empty(2, R, f, dtype=self.dtype, device=self.device)   # one buffer: GEMM1 stores both per TMA op
+        s["gp"], s["h"] = gph[0], gph[1]
         xr, eo = self._sym("x_recv", (R, d), self.dtype)[0], self._sym("e_out", (R, d), self.dtype)[0]
         self._mark("experts_fwd", 0)
         L.moe_expert_ffn(self.ctx, xr, s["off"], R, self.W1, self.b1, self.W2, self.b2, s["gp"], s["h"], eo)

@@ -145,8 +145,12 @@ class DTSMoELayer:
         b["d_eout"] = self._grow("d_eout", R_send, d, D)
         b["dG_row"] = self._grow("dG_row", R_send, 0, torch.float32)
         b["dx_perm"] = self._grow("dx_perm", R_send, d, D)
-        b["gp"] = self._grow("gp", R_recv, f, D)
-        b["h"] = self._grow("h", R_recv, f, D)
+        # gp and h as one [2, rows, d_ff] buffer: GEMM1's epilogue stores both with one TMA op
+        gph = self._buf.get("gph")
+        if gph is None or gph.shape[1] < R_recv:
+            gph = torch.empty((2, max(R_recv, L.ROW_ALIGN), f), dtype=D, device=self.device)
+            self._buf["gph"] = gph
+        b["gp"], b["h"] = gph[0], gph[1]
         if self.ep:
             b["x_recv"] = self._grow("x_recv", R_recv, d, D)
             b["e_out_recv"] = self._grow("e_out_recv", R_recv, d, D)
