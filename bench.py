@@ -440,7 +440,18 @@ def run_single(args):
     out["gpu_launches"] = int(launches)
     out["clocks"] = clk
     if args.e2e:
-        out["e2e"] = run_e2e(args, layer, li, upool, tau, c, R_static if graph is not None else None)
+        def capture(X, U, DY):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                Y = layer.forward(X, U, tau, c, R_cap=R_static)
+                DX = layer.backward(DY)["dx"]
+            return g, Y, DX
+
+        def eager_step(x_, u_, dy_):
+            y_ = layer.forward(x_, u_, tau, c)
+            return y_, layer.backward(dy_)["dx"]
+        out["e2e"] = run_e2e(args, li, upool, cfg.T, 1, eager_step, capture if graph is not None else None,
+                             layer.check)
     if args.cpu_baseline:
         T_sub = args.cpu_tokens
         # the GPU's routing of the sample tokens (pool member 0 = harness step 0, as the oracle draws)
@@ -459,15 +470,17 @@ def run_single(args):
     return out
 
 
-def run_e2e(args, layer, li, upool, tau, c, R_static):
+def run_e2e(args, li, upool, T_all, world, eager_step, capture, check):
     """Same metric through the public API with host (pinned) buffers: every step copies x, u,
     dy host->device and reads y and dx back device->host.
 
+    capture(X, U, DY) -> (graph, Y, DX): one step captured as a CUDA graph on the given device
+    inputs (None: no graph mode, then eager_step(x, u, dy) -> (y, dx) runs each step).
     Graph mode pipelines the copies with compute: two captured replicas of the step (each with
     its own device input buffers) alternate; step i+1's H2D runs on a copy stream while step i
     computes, step i's D2H runs on a third stream.  Every byte of every step is still copied
-    inside the timed region (first H2D start .. last D2H end)."""
-    dev = layer.device
+    inside the timed region (first H2D start .. last D2H end); max over ranks."""
+    dev = torch.device("cuda", torch.cuda.current_device())
     hx, hdy = li.x.pin_memory(), li.dy.pin_memory()
     hus = [u.cpu().pin_memory() for u in upool]
     hy = torch.empty_like(li.x).pin_memory()
@@ -476,27 +489,28 @@ def run_e2e(args, layer, li, upool, tau, c, R_static):
     bi = sum(t.numel() * t.element_size() for t in (hx, hus[0], hdy))
     bo = sum(t.numel() * t.element_size() for t in (hy, hdx))
 
-    if R_static is None:
+    if capture is None:
         def step(i):
             x = hx.to(dev, non_blocking=True)
             u = hus[i % U_POOL].to(dev, non_blocking=True)
             dy = hdy.to(dev, non_blocking=True)
-            y = layer.forward(x, u, tau, c)
-            g = layer.backward(dy)
+            y, dx = eager_step(x, u, dy)
             hy.copy_(y, non_blocking=True)
-            hdx.copy_(g["dx"], non_blocking=True)
+            hdx.copy_(dx, non_blocking=True)
 
         for i in range(2):
             step(i)
         torch.cuda.synchronize()
+        barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(comp)
         for i in range(args.steps):
             step(i)
         e1.record(comp)
         e1.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
-        return {"value": layer.T / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
+        check()
+        return {"value": T_all / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
                 "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": False}
 
     reps = []
@@ -505,10 +519,7 @@ def run_e2e(args, layer, li, upool, tau, c, R_static):
         U = torch.empty_like(hus[0], device=dev)
         DY = torch.empty_like(li.dy, device=dev)
         X.copy_(hx); U.copy_(hus[0]); DY.copy_(hdy)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            Y = layer.forward(X, U, tau, c, R_cap=R_static)
-            DX = layer.backward(DY)["dx"]
+        g, Y, DX = capture(X, U, DY)
         reps.append((g, X, U, DY, Y, DX))
     torch.cuda.synchronize()
     s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
@@ -549,9 +560,10 @@ def run_e2e(args, layer, li, upool, tau, c, R_static):
 
     run(4)
     torch.cuda.synchronize()
-    ms = run(args.steps) / args.steps
-    layer.check()
-    return {"value": layer.T / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+    barrier(world)
+    ms = max_over_ranks(run(args.steps) / args.steps, world)
+    check()
+    return {"value": T_all / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": True}
 
 
@@ -729,42 +741,30 @@ def run_ep(args, rank, world):
     out["gpu_launches"] = int(launches)
     out["clocks"] = clk
     if args.e2e:
-        hx, hdy = li.x.pin_memory(), li.dy.pin_memory()
-        hus = [t.cpu().pin_memory() for t in upool]
-        hy, hdx = torch.empty_like(li.x).pin_memory(), torch.empty_like(li.x).pin_memory()
-        dst_dy = dy if path == "nccl" else dyb
-        outs = {}
+        if path == "nccl":
+            def eager_step(x_, u_, dy_):
+                y_ = layer.forward(x_, u_, tau, c)
+                return y_, layer.backward(dy_)["dx"]
+            capture = None
+        else:
+            def eager_step(x_, u_, dy_):
+                y_ = r.forward(x_, u_, tau, c, cfg.top1)
+                return y_, r.backward(dy_)["dx"]
 
-        def step_host(i):
-            x.copy_(hx, non_blocking=True)
-            u.copy_(hus[i % U_POOL], non_blocking=True)
-            dst_dy.copy_(hdy, non_blocking=True)
-            if graph is not None:
-                graph.replay()
-                yy, dxx = outs["y"], outs["dx"]
-            else:
-                g = step()
-                yy, dxx = (layer.state.y, g["dx"]) if path == "nccl" else (r.st["y"], g["dx"])
-            hy.copy_(yy, non_blocking=True)
-            hdx.copy_(dxx, non_blocking=True)
-
-        if graph is not None:
-            outs["y"], outs["dx"] = r.st["y"], r.st["grads"]["dx"]    # the graph's output tensors
-        step_host(0)
-        torch.cuda.synchronize()
-        barrier(world)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for i in range(args.steps):
-            step_host(i)
-        e1.record(stream)
-        e1.synchronize()
-        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, world)
-        bi = sum(t.numel() * t.element_size() for t in (hx, hus[0], hdy))
-        out["e2e"] = {"value": cfg.T * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
-                      "h2d_bytes_per_step": bi, "d2h_bytes_per_step": 2 * hy.numel() * hy.element_size(),
-                      "pipelined": False}
-        check()
+            def capture(X, U, DY):
+                # DY is staged into the symmetric dy buffer inside the step (bwd_stage_dy)
+                side = torch.cuda.Stream()
+                side.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(side):
+                    eager_step(X, U, DY)
+                torch.cuda.current_stream().wait_stream(side)
+                torch.cuda.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    Y, DX = eager_step(X, U, DY)
+                return g, Y, DX
+        out["e2e"] = run_e2e(args, li, upool, cfg.T * world, world, eager_step,
+                             capture if (path != "nccl" and args.graph) else None, check)
     return out
 
 
