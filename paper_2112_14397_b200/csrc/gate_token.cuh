@@ -187,9 +187,22 @@ constexpr int kRefineWBytes = 32768;
 constexpr int kRefineKC = 1024;
 struct RefineSmem {
   uint4 w[kRefineWBytes / 16];     // W_g rows [k0, k0 + KC) of this chunk, raw element type
-  float x[kRefineKC];              // x[k0 .. k0 + KC)
+  double x[kRefineKC];             // x[k0 .. k0 + KC), converted once per chunk
   double red[1024];                // per-thread partial logits (NT <= 1024)
 };
+static_assert(sizeof(RefineSmem) <= 48 * 1024, "static shared memory");
+
+// Exact bf16 -> fp64 with integer ops (the F2F.F64.F32 conversion runs on a slow pipe and was
+// two per product): a normal value rebiases its exponent (127 -> 1023) and moves its 7
+// mantissa bits to the top of the 52; zero, subnormals, inf and NaN take the conversion.
+__device__ __forceinline__ double to_f64(bf16 v) {
+  const uint32_t b = __bfloat16_as_ushort(v);
+  const uint32_t em = b & 0x7fffu;
+  if (em - 0x0080u < 0x7f00u)
+    return __hiloint2double((int)(((b & 0x8000u) << 16) | ((em << 13) + (896u << 20))), 0);
+  return (double)__uint_as_float(b << 16);
+}
+__device__ __forceinline__ double to_f64(float v) { return (double)v; }
 
 template <typename T, int NT = 256>
 __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restrict__ x, const T* __restrict__ Wg,
@@ -237,19 +250,24 @@ __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restri
     }
     {
       constexpr int XJ = (kRefineKC + NT - 1) / NT;
-      float r[XJ];
+      double r[XJ];
 #pragma unroll
       for (int j = 0; j < XJ; ++j)
-        if (tid + NT * j < kc) r[j] = to_f32(xr[k0 + tid + NT * j]);
+        if (tid + NT * j < kc) r[j] = to_f64(xr[k0 + tid + NT * j]);
 #pragma unroll
       for (int j = 0; j < XJ; ++j)
         if (tid + NT * j < kc) sm.x[tid + NT * j] = r[j];
     }
     __syncthreads();
-    if (worker) {
-      int k = sl, j = 0;
-      for (; k < kc; k += nsl, j = (j + 1) & 3)
-        acc[j] = fma((double)sm.x[k], (double)to_f32(ws[(long long)k * E + e_me]), acc[j]);
+    if (worker) {   // four independent fp64 chains in registers
+      const T* wc = ws + e_me;
+      int k = sl;
+      for (; k + 3 * nsl < kc; k += 4 * nsl) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[j] = fma(sm.x[k + j * nsl], to_f64(wc[(k + j * nsl) * E]), acc[j]);
+      }
+      for (; k < kc; k += nsl) acc[0] = fma(sm.x[k], to_f64(wc[k * E]), acc[0]);
     }
     __syncthreads();
   }
