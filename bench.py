@@ -558,13 +558,40 @@ def run_e2e(args, li, upool, T_all, world, eager_step, capture, check):
         t1.synchronize()
         return t0.elapsed_time(t1)
 
+    def copies_only(n):
+        """The same per-step copies on the same streams with no compute: the host-link bound."""
+        g, X, U, DY, Y, DX = reps[0]
+        t0, t1, t2 = ev(), ev(), ev()
+        t0.record(comp)
+        s_h2d.wait_stream(comp)
+        s_d2h.wait_stream(comp)
+        for i in range(n):
+            with torch.cuda.stream(s_h2d):
+                X.copy_(hx, non_blocking=True)
+                U.copy_(hus[i % U_POOL], non_blocking=True)
+                DY.copy_(hdy, non_blocking=True)
+            with torch.cuda.stream(s_d2h):
+                hy.copy_(Y, non_blocking=True)
+                hdx.copy_(DX, non_blocking=True)
+        t1.record(s_h2d)
+        t2.record(s_d2h)
+        t1.synchronize()
+        t2.synchronize()
+        return max(t0.elapsed_time(t1), t0.elapsed_time(t2))
+
     run(4)
     torch.cuda.synchronize()
     barrier(world)
     ms = max_over_ranks(run(args.steps) / args.steps, world)
     check()
+    n_link = max(2, min(args.steps, 5))
+    link_ms = max_over_ranks(copies_only(n_link) / n_link, world)
     return {"value": T_all / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": True}
+            "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": True,
+            "link_bound": {"ms_per_step": link_ms, "tokens_per_s": T_all / (link_ms / 1e3),
+                           "frac": link_ms / ms, "GB/s_both_directions": (bi + bo) / link_ms / 1e6,
+                           "what": "the step's host<->device copies alone, both directions at once on the "
+                                   "same streams (pinned host memory); frac = link-bound time / e2e time"}}
 
 
 # ------------------------------------------------------------------ N > 1: expert parallelism

@@ -180,9 +180,10 @@ __device__ __forceinline__ void gate_token(const float* L, int t, const T* __res
 // latency problem (one token: d * E products), so W_g is staged through shared memory in
 // chunks of up to 32 KB, each chunk's loads all issued before any is used (one memory
 // round trip per chunk, not one per k step); thread (e, sl) then accumulates expert e over
-// the k = sl (mod nsl) rows of the chunk, the nsl partials are added in fixed order, and warp
-// 0 applies noise / softmax / decision in fp64, writes probs / slot and counts with global
-// integer atomics.
+// the k = sl (mod nsl) rows of the chunk (the next chunk's loads in flight meanwhile), the nsl
+// partials are added in fixed order; noise (computed during the first loads), tau and the
+// exponentials run one expert per thread, and warp 0 takes max / sum / decision in fp64,
+// writes probs / slot and counts with global integer atomics.
 constexpr int kRefineWBytes = 32768;
 constexpr int kRefineKC = 1024;
 struct RefineSmem {
@@ -221,21 +222,37 @@ __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restri
   if (KC > kRefineKC) KC = kRefineKC;
   const T* ws = reinterpret_cast<const T*>(sm.w);
   const bool vec = ((E * sizeof(T)) % 16 == 0) && ((reinterpret_cast<uintptr_t>(Wg) & 15) == 0);
+  // the token's Gumbel noise in fp64 (two dependent logs), one expert per thread, computed
+  // while the first W_g chunk is in flight
+  double zeta_me = 0.0;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  constexpr int WJ = (kRefineWBytes / 16 + NT - 1) / NT;
+  constexpr int XJ = (kRefineKC + NT - 1) / NT;
+  uint4 wr[WJ];                                   // vec path: the next chunk's W_g, prefetched
+  T xv[XJ];                                       // the next chunk's x
+  auto load_chunk = [&](int k0) {
+    const int kc = min(KC, d - k0);
+    if (vec) {
+      const uint4* src = reinterpret_cast<const uint4*>(Wg + (long long)k0 * E);
+      const int n16 = (int)((long long)kc * E * sizeof(T) / 16);   // <= 2048
+#pragma unroll
+      for (int j = 0; j < WJ; ++j)
+        if (tid + NT * j < n16) wr[j] = __ldg(src + tid + NT * j);
+    }
+#pragma unroll
+    for (int j = 0; j < XJ; ++j)
+      if (tid + NT * j < kc) xv[j] = xr[k0 + tid + NT * j];
+  };
+  load_chunk(0);
+  if (tid < E && u) zeta_me = -log(-log((double)u[(long long)t * E + tid]));
   for (int k0 = 0; k0 < d; k0 += KC) {
     const int kc = min(KC, d - k0);
     const long long n = (long long)kc * E;         // elements of this chunk
     if (vec) {
-      const uint4* src = reinterpret_cast<const uint4*>(Wg + (long long)k0 * E);
-      const int n16 = (int)(n * sizeof(T) / 16);   // <= 2048
-      constexpr int WJ = (kRefineWBytes / 16 + NT - 1) / NT;
-      uint4 r[WJ];
+      const int n16 = (int)(n * sizeof(T) / 16);
 #pragma unroll
       for (int j = 0; j < WJ; ++j)
-        if (tid + NT * j < n16) r[j] = __ldg(src + tid + NT * j);
-#pragma unroll
-      for (int j = 0; j < WJ; ++j)
-        if (tid + NT * j < n16) sm.w[tid + NT * j] = r[j];
+        if (tid + NT * j < n16) sm.w[tid + NT * j] = wr[j];
     } else {
       T* wd = reinterpret_cast<T*>(sm.w);
       for (int b = 0; b < n; b += NT * 8) {
@@ -248,17 +265,11 @@ __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restri
           if (b + tid + NT * j < n) wd[b + tid + NT * j] = r[j];
       }
     }
-    {
-      constexpr int XJ = (kRefineKC + NT - 1) / NT;
-      double r[XJ];
 #pragma unroll
-      for (int j = 0; j < XJ; ++j)
-        if (tid + NT * j < kc) r[j] = to_f64(xr[k0 + tid + NT * j]);
-#pragma unroll
-      for (int j = 0; j < XJ; ++j)
-        if (tid + NT * j < kc) sm.x[tid + NT * j] = r[j];
-    }
+    for (int j = 0; j < XJ; ++j)
+      if (tid + NT * j < kc) sm.x[tid + NT * j] = to_f64(xv[j]);
     __syncthreads();
+    if (k0 + KC < d) load_chunk(k0 + KC);          // in flight during this chunk's products
     if (worker) {   // four independent fp64 chains in registers
       const T* wc = ws + e_me;
       int k = sl;
@@ -273,27 +284,31 @@ __device__ __forceinline__ void gate_token_refine_block(int t, const T* __restri
   }
   sm.red[tid] = worker ? (acc[0] + acc[1]) + (acc[2] + acc[3]) : 0.0;
   __syncthreads();
+  // noise and tau, then the softmax exponentials, one expert per thread (the W_g staging area
+  // is free now: zs[0..E) = z, then p unnormalised; zs[128] = max z); warp 0 decides
+  double* zs = reinterpret_cast<double*>(sm.w);
+  if (tid < E) {
+    double a = 0.0;
+    for (int q = 0; q < nsl; ++q) a += sm.red[q * E + tid];
+    zs[tid] = (a + zeta_me) / (double)tau;
+  }
+  __syncthreads();
   if (warp == 0) {
-    double z64[kMaxEPL];
-#pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) {
-      const int e = lane + 32 * i;
-      z64[i] = -INFINITY;
-      if (e < E) {
-        double acc = 0.0;
-        for (int q = 0; q < nsl; ++q) acc += sm.red[q * E + e];
-        const double zeta = u ? -log(-log((double)u[(long long)t * E + e])) : 0.0;
-        z64[i] = (acc + zeta) / (double)tau;
-      }
-    }
     double mx64 = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < kMaxEPL; ++i) mx64 = fmax(mx64, z64[i]);
+    for (int i = 0; i < kMaxEPL; ++i)
+      if (lane + 32 * i < E) mx64 = fmax(mx64, zs[lane + 32 * i]);
     mx64 = warp_maxd(mx64);
+    if (lane == 0) zs[128] = mx64;
+  }
+  __syncthreads();
+  if (tid < E) zs[tid] = exp(zs[tid] - zs[128]);
+  __syncthreads();
+  if (warp == 0) {
     double s64 = 0.0, p64[kMaxEPL];
 #pragma unroll
     for (int i = 0; i < kMaxEPL; ++i) {
-      p64[i] = (lane + 32 * i < E) ? exp(z64[i] - mx64) : 0.0;
+      p64[i] = (lane + 32 * i < E) ? zs[lane + 32 * i] : 0.0;
       s64 += p64[i];
     }
     s64 = warp_sum(s64);

@@ -160,11 +160,13 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const TI* __restrict__
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
   if (n0 < N) {
-    int r = r0 + warp;
-    for (; r + 24 < r1; r += 32) {
+    // rows r, r + 8, r + 16, r + 24 in flight together (a split is often only a few rows per
+    // warp: the ragged tail is predicated, not a serial loop); rows are added in ascending order
+    for (int r = r0 + warp; r < r1; r += 32) {
       uint4 q[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q[u] = ld_nc_v4(X + (long long)(r + 8 * u) * N + n0);
+      for (int u = 0; u < 4; ++u)
+        q[u] = r + 8 * u < r1 ? ld_nc_v4(X + (long long)(r + 8 * u) * N + n0) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         float f[V];
@@ -172,12 +174,6 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(const TI* __restrict__
 #pragma unroll
         for (int k = 0; k < V; ++k) acc[k] += f[k];
       }
-    }
-    for (; r < r1; r += 8) {
-      float f[V];
-      unpack16(ld_nc_v4(X + (long long)r * N + n0), f, TI());
-#pragma unroll
-      for (int k = 0; k < V; ++k) acc[k] += f[k];
     }
   }
 #pragma unroll

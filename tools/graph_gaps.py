@@ -1,7 +1,10 @@
 """Idle time between consecutive kernels inside one replayed CUDA-graph step (CUPTI via
 torch.profiler): how much a step loses to launch gaps / kernel tails.  Dev tool.
 
-    python tools/graph_gaps.py [--config C2]
+    python tools/graph_gaps.py [--config C2] [--step S] [--timeline]
+
+--step S takes tau / threshold and the Gumbel draw of C5's schedule step S; --timeline also
+prints every kernel of the step (start offset, duration, gap before it) as JSON lines.
 """
 import argparse
 import json
@@ -20,6 +23,8 @@ from paper_2112_14397_b200.layer import DTSMoELayer  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--step", type=int, default=None)
+    ap.add_argument("--timeline", action="store_true")
     a = ap.parse_args()
     cfg = configs.get(a.config)
     dev = torch.device("cuda", 0)
@@ -29,6 +34,9 @@ def main():
     layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
     x, u, dy = li.x.to(dev), li.u.to(dev), li.dy.to(dev)
     tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
+    if a.step is not None:
+        tau, c = (float(np.float32(v)) for v in cfg.schedule[a.step])
+        u = inputs.uniform_u(cfg.T, cfg.E, step=a.step).to(dev)
     for _ in range(3):
         layer.forward(x, u, tau, c)
         layer.backward(dy)
@@ -49,11 +57,20 @@ def main():
         g.replay()
         torch.cuda.synchronize()
     ev = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
-    spans = [(e.time_range.start, e.time_range.end, e.name.split("(")[0][-40:]) for e in ev]
+    def short(n):
+        return n.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0][-48:]
+
+    spans = [(e.time_range.start, e.time_range.end, short(e.name)) for e in ev]
     busy = sum(e1 - s1 for s1, e1, _ in spans)
     wall = spans[-1][1] - spans[0][0]
     gaps = [(spans[i + 1][0] - spans[i][1], spans[i][2], spans[i + 1][2]) for i in range(len(spans) - 1)]
-    print(json.dumps({"config": a.config, "kernels": len(spans), "wall_us": wall, "busy_us": busy,
+    if a.timeline:
+        t0 = spans[0][0]
+        prev = t0
+        for s0, s1, nm in spans:
+            print(json.dumps({"k": nm, "at_us": round(s0 - t0, 2), "us": round(s1 - s0, 2), "gap_us": round(s0 - prev, 2)}))
+            prev = s1
+    print(json.dumps({"config": a.config, "step": a.step, "kernels": len(spans), "wall_us": wall, "busy_us": busy,
                       "idle_us": wall - busy, "largest_gaps": sorted(gaps, reverse=True)[:6]}))
 
 

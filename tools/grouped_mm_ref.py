@@ -3,7 +3,7 @@ grouped GEMM (torch._grouped_mm, cuBLAS/CUTLASS inside) on the same ragged per-e
 offsets as our routing of a config, forward GEMM1 / GEMM2 shapes without the fused bias /
 GELU epilogues, plus the dense cuBLAS GEMM of the same total size.  Dev tool.
 
-    python tools/grouped_mm_ref.py [C2|C4]
+    python tools/grouped_mm_ref.py [C2|C4|C5:S]     (C5:S = the C5 schedule's step S)
 """
 import json
 import os
@@ -32,14 +32,20 @@ def timed(fn, reps=10):
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "C2"
-    cfg = configs.get(name)
+    cfg = configs.get(name.split(":")[0])
+    tau, c = float(np.float32(cfg.tau)), float(np.float32(cfg.threshold))
+    u = inputs.make_inputs(cfg).u
+    if ":" in name:
+        step = int(name.split(":")[1])
+        tau, c = (float(np.float32(v)) for v in cfg.schedule[step])
+        u = inputs.uniform_u(cfg.T, cfg.E, step=step)
     from paper_2112_14397_b200.layer import DTSMoELayer
     dev = torch.device("cuda", 0)
     li = inputs.make_inputs(cfg)
     layer = DTSMoELayer(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dtype=torch.bfloat16, device=dev)
     layer.set_gate(li.Wg.to(dev))
     layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
-    layer.forward(li.x.to(dev), li.u.to(dev), float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)))
+    layer.forward(li.x.to(dev), u.to(dev), tau, c)
     torch.cuda.synchronize()
     counts = layer.state.counts.cpu().numpy()
     R = int(counts.sum())
@@ -64,8 +70,8 @@ def main():
     b2 = torch.randn(f, d, device=dev, dtype=torch.bfloat16)
     ms3 = timed(lambda: a @ b)
     ms4 = timed(lambda: h @ b2)
-    out["dense_cublas_gemm1_shape_tflops"] = fl1 / ms3 / 1e9
-    out["dense_cublas_gemm2_shape_tflops"] = fl1 / ms4 / 1e9
+    out["dense_cublas_gemm1_shape_tflops"], out["dense_cublas_gemm1_ms"] = fl1 / ms3 / 1e9, ms3
+    out["dense_cublas_gemm2_shape_tflops"], out["dense_cublas_gemm2_ms"] = fl1 / ms4 / 1e9, ms4
     print(json.dumps(out))
 
 
