@@ -293,6 +293,26 @@ def _traffic(name, world):
             "traffic_source": os.path.relpath(hits[-1], ROOT)}
 
 
+
+def gemm_roofline_us(R, d, f, E, peaks):
+    """Roofline of the six expert GEMMs of one fwd+bwd over R realised rows (E experts with rows,
+    bf16 activations and weights, fp32 weight gradients): per GEMM max(tensor time at the burst
+    bf16 peak, HBM time of its algorithmic bytes at the measured copy bandwidth).  At the sparse
+    end the weights (read four times) and the fp32 weight gradients dominate the bytes, so the
+    late steps are HBM-bound, not tensor-bound."""
+    fl = 2.0 * R * d * f
+    w = 2.0 * E * d * f
+    byts = [2 * R * d + w + 4 * R * f,          # GEMM1: x_perm, W1 -> h, GELU'(a)
+            2 * R * f + w + 2 * R * d,          # GEMM2: h, W2 -> e_out
+            2 * R * d + w + 4 * R * f,          # dgrad2: d_eout, W2, GELU'(a) -> da
+            2 * R * f + w + 2 * R * d,          # dgrad1: da, W1 -> dx_perm
+            2 * R * d + 2 * R * f + 2 * w,      # dW1: x_perm, da -> fp32 dW1
+            2 * R * f + 2 * R * d + 2 * w]      # dW2: h, d_eout -> fp32 dW2
+    t_tc = fl / (peaks["bf16_tflops"] * 1e12) * 1e6
+    parts = [max(t_tc, b / (peaks["hbm_gbs"] * 1e9) * 1e6) for b in byts]
+    return sum(parts), sum(1 for b in byts if b / (peaks["hbm_gbs"] * 1e9) * 1e6 > t_tc)
+
+
 def _roofline(cfg, flops_per_gpu, gemm_ms, wall, clk, world, R_pad):
     peaks, src = _peaks()
     peak, which = pick_peak(peaks, wall, clk)
@@ -311,7 +331,14 @@ def _roofline(cfg, flops_per_gpu, gemm_ms, wall, clk, world, R_pad):
             "rows_R_pad": R_pad,
             "algorithmic_bytes_per_step": R * (12 * d + 16 * f) * (b // 2)
             + E * d * f * (4 * b + 2 * 4),
+            **_gemm_mixed(R, d, f, E, peaks, gemm_ms),
             **_traffic(cfg.name, world)}
+
+
+def _gemm_mixed(R, d, f, E, peaks, gemm_ms):
+    roof_us, n_hbm = gemm_roofline_us(R, d, f, E, peaks)
+    return {"gemm_roofline_ms_max_tensor_hbm": roof_us / 1e3, "gemm_frac_of_max_tensor_hbm": roof_us / 1e3 / gemm_ms,
+            "gemms_hbm_bound": n_hbm}
 
 
 def _config(cfg, world, extra):

@@ -27,6 +27,8 @@ import torch  # noqa: E402
 
 from harness import configs, inputs  # noqa: E402
 
+from bench import gemm_roofline_us  # noqa: E402
+
 
 def _relaunch(args):
     with socket.socket() as sk:
@@ -98,6 +100,8 @@ def main():
 
         def maxr(v):
             return v
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fp:
+        peaks = json.load(fp)
     layer.set_gate(li.Wg.to(dev))
     layer.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
     tot_tokens, tot_ms, tot_flops = 0, 0.0, 0.0
@@ -156,12 +160,19 @@ def main():
         R = int(np.sum(glob))
         flops = 12.0 * R * cfg.d_model * cfg.d_ff            # all ranks' expert GEMM FLOPs
         flops_mine = 12.0 * int(mine) * cfg.d_model * cfg.d_ff
+        E_rows = int(np.count_nonzero(np.asarray(glob)[rank * El:(rank + 1) * El])) if world > 1 else \
+            int(np.count_nonzero(np.asarray(glob)))
+        roof_us, n_hbm = gemm_roofline_us(int(mine), cfg.d_model, cfg.d_ff, E_rows, peaks)
         line = {"step": s, "tau": tau, "threshold": c, "n_gpus": world,
                 "tokens_per_s": cfg.T * world / (t_ms / 1e3), "ms": t_ms,
                 "mean_experts_per_token": float(R) / (cfg.T * world), "rows_R": R,
                 "max_over_mean_load": float(np.max(glob) / max(1e-9, np.mean(glob))),
                 # algorithmic FLOPs of the realised rows (pad rows excluded), VERDICT r1 weak #3
-                "expert_gemm_tflops_per_gpu": flops_mine / (g_ms / 1e3) / 1e12}
+                "expert_gemm_tflops_per_gpu": flops_mine / (g_ms / 1e3) / 1e12,
+                "expert_gemm_ms": g_ms,
+                # per-GEMM max(tensor, HBM) roofline of this rank's realised rows (burst peaks)
+                "expert_gemm_roofline_ms": roof_us / 1e3, "expert_gemm_frac_of_roofline": roof_us / 1e3 / g_ms,
+                "gemms_hbm_bound": n_hbm}
         if world == 1:
             line["near_band"] = int(layer.state.near_band.item())
         if rank == 0:
