@@ -2,6 +2,7 @@
 # path at N=1), the C5 sweep, the reference arm, launch lists, and ncu summaries of the expert GEMMs
 # and of every routing / gate kernel (reports stay in /tmp on the box; summaries come back).
 # usage (on the GPU box): bash tools/final_round_measure.sh [out_dir_name]
+# (then, here: tools/routing_roofline.py on routing_C*.csv; copy the summaries to profiles/)
 set -x
 O=gpurun_out/${1:-final}
 mkdir -p $O
@@ -13,6 +14,10 @@ python bench.py --config C3 > $O/bench_C3.json 2> $O/bench_C3.err
 python bench.py --ep p2p --steps 20 > $O/bench_C4_p2p_n1.json 2> $O/bench_C4_p2p_n1.err
 python bench_sweep.py > $O/c5_sweep.jsonl 2> $O/c5_sweep.err
 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2> $O/bench_reference.err
+python tools/pcie_probe.py > $O/pcie_link.json 2>&1
+for C in C5:19 C5:10 C4; do python tools/grouped_mm_ref.py $C; done > $O/grouped_mm_ref.jsonl 2>&1
+for S in 19 0; do python tools/graph_gaps.py --config C5 --step $S --timeline 2>/dev/null | grep '^{' > $O/timeline_C5_$S.jsonl; done
+for C in C4 C3 C2; do python tools/graph_gaps.py --config $C --timeline 2>/dev/null | grep '^{' > $O/timeline_$C.jsonl; done
 for C in C4 C2; do
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_$C.csv \
     python bench.py --config $C --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_launch_$C.log 2>&1
