@@ -31,3 +31,22 @@ def test_reference_arm_other_ranks_print_nothing():
                         "--warmup", "0", "--ref-tokens", "16", "--config", "C1"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_gemm_mixed_roofline():
+    """The per-GEMM max(tensor, HBM) roofline: closed forms at two shapes (tensor peak 1000 TF/s,
+    1000 GB/s of HBM so that times are FLOPs / 1e15 and bytes / 1e12)."""
+    sys.path.insert(0, ROOT)
+    from bench import gemm_roofline_us
+    pk = {"bf16_tflops": 1000.0, "hbm_gbs": 1000.0}
+    # tiny R, big weights: every GEMM is bound by its bytes (weights dominate)
+    R, d, f, E = 128, 256, 512, 8
+    w = 2 * E * d * f
+    byts = [2 * R * d + w + 4 * R * f, 2 * R * f + w + 2 * R * d, 2 * R * d + w + 4 * R * f,
+            2 * R * f + w + 2 * R * d, 2 * R * d + 2 * R * f + 2 * w, 2 * R * f + 2 * R * d + 2 * w]
+    us, n_hbm = gemm_roofline_us(R, d, f, E, pk)
+    assert n_hbm == 6 and abs(us - sum(byts) / 1e12 * 1e6) < 1e-9
+    # huge R: FLOPs dominate (6 x 2 R d f at the tensor peak), no GEMM is HBM-bound
+    R, d, f, E = 1 << 20, 4096, 16384, 1
+    us, n_hbm = gemm_roofline_us(R, d, f, E, pk)
+    assert n_hbm == 0 and abs(us - 6 * 2.0 * R * d * f / 1e15 * 1e6) < 1e-6 * us
