@@ -424,6 +424,10 @@ __global__ void __launch_bounds__(FG_THREADS, 1)
     const int st = threadIdx.x - 192;                  // 0..511
     const int tok = st >> 2, q = st & 3;               // token of the tile, quarter of its experts
     const int e0 = q * EPT;
+    // the softmax runs in base 2: z2 = (L + zeta) log2(e) / tau, p = 2^(z2 - max z2) (one multiply
+    // and one ex2.approx per entry instead of a division and an expf; the arithmetic per entry,
+    // two logf included, is about the time of the entry's HBM stream at C4)
+    const float s2 = 1.4426950408889634f / p.tau;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
       const int b = it & 1;
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(FG_THREADS, 1)
       for (int j = 0; j < EPT; ++j) {
         if (!isfinite(Z[j])) bad = true;
         const float zeta = p.u ? -logf(-logf(U[j])) : 0.f;
-        Z[j] = (Z[j] + zeta) / p.tau;
+        Z[j] = (Z[j] + zeta) * s2;
         mx = fmaxf(mx, Z[j]);
       }
       if (bad && live && atomicOr(&p.flags[0], kFlagNonFinite) == 0) p.flags[1] = t;
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(FG_THREADS, 1)
       float sum = 0.f;
 #pragma unroll
       for (int j = 0; j < EPT; ++j) {
-        Z[j] = expf(Z[j] - mx);
+        Z[j] = ex2_approx(Z[j] - mx);
         sum += Z[j];
       }
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
