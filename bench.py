@@ -612,7 +612,8 @@ def run_e2e(args, li, upool, T_all, world, eager_step, capture, check):
     ms = max_over_ranks(run(args.steps) / args.steps, world)
     check()
     n_link = max(2, min(args.steps, 5))
-    link_ms = max_over_ranks(copies_only(n_link) / n_link, world)
+    # the faster of two probes (PCIe throughput varies run to run; the bound is the best case)
+    link_ms = max_over_ranks(min(copies_only(n_link), copies_only(n_link)) / n_link, world)
     return {"value": T_all / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "pipelined": True,
             "link_bound": {"ms_per_step": link_ms, "tokens_per_s": T_all / (link_ms / 1e3),
