@@ -323,8 +323,10 @@ def test_bf16_single_expert_is_dense_ffn():
 # the probs of those tokens) come from gate_refine_kernel (tau = 50 at E = 64).  Shapes cover one W_g chunk
 # (E=16, d=768), four chunks (E=64, d=1024: 32 KB = 256 rows of W_g per chunk) and the
 # scalar staging path (E=20: a W_g row is 40 bytes, not a multiple of 16) with a ragged
-# second chunk (d=960, 819 rows per chunk).
-@pytest.mark.parametrize("E,d,T,tau", [(16, 768, 1000, 200.0), (64, 1024, 700, 50.0), (20, 960, 515, 200.0)])
+# second chunk (d=960, 819 rows per chunk); and short queues (fewer queued tokens than SMs:
+# T = 40 at E = 64, T = 20 at E = 48 with d = 832 = 3 x 256 + 64 rows, T = 30 at E = 20).
+@pytest.mark.parametrize("E,d,T,tau", [(16, 768, 1000, 200.0), (64, 1024, 700, 50.0), (20, 960, 515, 200.0),
+                                       (64, 1024, 40, 50.0), (48, 832, 20, 200.0), (20, 960, 30, 200.0)])
 def test_refine_queue_heavy(E, d, T, tau):
     cfg = _shape(f"RQ{E}", T, d, 256, E, tau, 1.0 / E)
     rep, g = _run(cfg, backward=False)
