@@ -313,14 +313,26 @@ def gemm_roofline_us(R, d, f, E, peaks):
     return sum(parts), sum(1 for b in byts if b / (peaks["hbm_gbs"] * 1e9) * 1e6 > t_tc)
 
 
+FP32_FMA_LANES_PER_SM = 128      # fp32 FMA lanes per SM per clock (measured: profiles/r02/ab_epilogue_math.txt)
+
+
 def _roofline(cfg, flops_per_gpu, gemm_ms, wall, clk, world, R_pad):
     peaks, src = _peaks()
     peak, which = pick_peak(peaks, wall, clk)
+    bound = "tensor"
+    if cfg.dtype != "bf16":
+        # the fp32 configuration (C1) runs its expert GEMMs on the CUDA cores (FFMA): bound by plain
+        # ALU arithmetic, against SMs x 128 FMA lanes x 2 FLOP x the SM clock
+        sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        mhz = float(clk.get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0)
+        peak = sms * FP32_FMA_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
+        bound, src, which = "alu", "derived", (f"fp32 FFMA: {sms} SMs x {FP32_FMA_LANES_PER_SM} lanes x 2 FLOP x "
+                                               f"{mhz:.0f} MHz (median SM clock of the timed region)")
     achieved = flops_per_gpu / (gemm_ms / 1e3) / 1e12
     b = 2 if cfg.dtype == "bf16" else 4
     d, f, E = cfg.d_model, cfg.d_ff, cfg.E // world
     R = flops_per_gpu / (12.0 * d * f)
-    return {"bound": "tensor", "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
+    return {"bound": bound, "kernel": "expert grouped GEMMs (moe_expert_ffn + moe_expert_ffn_bwd)",
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "peak_source": f"{src} {which}",
             "frac_of_burst": achieved / float(peaks["bf16_tflops"]),
@@ -820,6 +832,13 @@ def run_ep(args, rank, world):
                 return g, Y, DX
         out["e2e"] = run_e2e(args, li, upool, cfg.T * world, world, eager_step,
                              capture if (path != "nccl" and args.graph) else None, check)
+    if args.cpu_baseline and world == 1:
+        # the oracle on the host (N = 1 only, as the single-GPU line)
+        T_sub = args.cpu_tokens
+        dt_cpu, _ = oracle_sample(cfg, T_sub)
+        out["cpu_baseline"] = {"value": T_sub / dt_cpu, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                               "sample": f"first {T_sub} tokens of {cfg.name} (same d/d_ff/E/tau/c), fwd+bwd, "
+                                         f"fp64 NumPy, {dt_cpu:.2f} s"}
     return out
 
 
