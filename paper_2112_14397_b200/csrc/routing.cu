@@ -326,19 +326,20 @@ struct PeerRows {
   __device__ __forceinline__ float weight(int e, int) const { return probs_t[e]; }
 };
 
+// the whole slot row of a token (E <= 128: up to 4 entries per lane), one memory round trip
+__device__ __forceinline__ void load_slot_row(const int* __restrict__ slot_row, int E, int lane, int (&svs)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) svs[i] = (32 * i < E && 32 * i + lane < E) ? slot_row[32 * i + lane] : -1;
+}
+
 template <typename T, bool WEIGHTED, typename TX = float, int QV = 4, typename Src = LocalRows<T>>
-__device__ __forceinline__ void gather_sum_token(const Src& src, const int* __restrict__ slot_row, int d, int E,
-                                                 const TX* extra, T* out, int lane) {
+__device__ __forceinline__ void gather_sum_token_sv(const Src& src, const int (&svs)[4], int d, int E,
+                                                    const TX* extra, T* out, int lane) {
   // `extra` may alias `out` (the accumulating dispatch backward): each lane loads its own
   // elements of the row with coherent loads before it stores them
   constexpr int V = Vec16<T>::N;
   const int nvec = d / V;
   constexpr bool TWO = QV <= 3;                     // two rows in flight when registers allow
-  // the whole slot row (E <= 128: up to 4 entries per lane) loaded once, up front: one memory
-  // round trip per token instead of one per 32 experts and pass
-  int svs[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) svs[i] = (32 * i < E && 32 * i + lane < E) ? slot_row[32 * i + lane] : -1;
   for (int v0 = 0; v0 < nvec; v0 += 32 * QV) {
     float acc[QV][V];
 #pragma unroll
@@ -415,16 +416,37 @@ __device__ __forceinline__ void gather_sum_token(const Src& src, const int* __re
   }
 }
 
-// y[t] = sum_{e asc} row_gate[r] * e_out[r], r = slot[t,e]
+template <typename T, bool WEIGHTED, typename TX = float, int QV = 4, typename Src = LocalRows<T>>
+__device__ __forceinline__ void gather_sum_token(const Src& src, const int* __restrict__ slot_row, int d, int E,
+                                                 const TX* extra, T* out, int lane) {
+  int svs[4];
+  load_slot_row(slot_row, E, lane, svs);
+  gather_sum_token_sv<T, WEIGHTED, TX, QV, Src>(src, svs, d, E, extra, out, lane);
+}
+
+// y[t] = sum_{e asc} row_gate[r] * e_out[r], r = slot[t,e].  A warp takes two consecutive
+// tokens and loads both slot rows up front, so the second token's slot round trip hides under
+// the first token's row loads (the dispatch backward hides it under its dx-row loads): C4
+// 109 -> 98 us, C5 step 19 8.5 -> 7.7 us.  Not at QV = 3 (d = 768: the extra registers spill,
+// C2 +6%).
+template <int QV> constexpr int combine_tpw() { return QV == 3 ? 1 : 2; }
 template <typename T, int QV>
 __global__ void __launch_bounds__(256, 4) combine_kernel(const T* __restrict__ e_out, const float* __restrict__ row_gate,
                                                       const int* __restrict__ slot, int T_, int d, int E,
                                                       T* __restrict__ y) {
+  constexpr int TPW = combine_tpw<QV>();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int t = blockIdx.x * 8 + warp;
-  if (t >= T_) return;
-  gather_sum_token<T, true, float, QV>(LocalRows<T>{e_out, row_gate, d}, slot + (long long)t * E, d, E, nullptr,
-                                       y + (long long)t * d, lane);
+  const int t0 = (blockIdx.x * 8 + warp) * TPW;
+  if (t0 >= T_) return;
+  int sv[TPW][4];
+#pragma unroll
+  for (int j = 0; j < TPW; ++j)
+    if (t0 + j < T_) load_slot_row(slot + (long long)(t0 + j) * E, E, lane, sv[j]);
+#pragma unroll
+  for (int j = 0; j < TPW; ++j)
+    if (t0 + j < T_)
+      gather_sum_token_sv<T, true, float, QV>(LocalRows<T>{e_out, row_gate, d}, sv[j], d, E, (const float*)nullptr,
+                                              y + (long long)(t0 + j) * d, lane);
 }
 // vectors per lane per pass: the whole row in one pass up to 4 x 16 B per lane
 static inline int pass_vectors(int d, int V) {
@@ -1071,15 +1093,16 @@ cudaError_t launch_dispatch(const moe_ctx* c, const void* x, const float* probs,
 cudaError_t launch_combine(const moe_ctx* c, const void* e_out, const float* row_gate, const int32_t* slot,
                            void* y, cudaStream_t s) {
   if (c->T == 0) return cudaSuccess;
-  const unsigned grid = (c->T + 7) / 8;
 #define MOE_QV_DISPATCH(qv, ...) \
   switch (qv) { case 1: { constexpr int QV = 1; __VA_ARGS__; } break; case 2: { constexpr int QV = 2; __VA_ARGS__; } break; \
                 case 3: { constexpr int QV = 3; __VA_ARGS__; } break; default: { constexpr int QV = 4; __VA_ARGS__; } }
   if (c->dtype == 1) {
-    MOE_QV_DISPATCH(pass_vectors(c->d, 8), combine_kernel<bf16, QV><<<grid, 256, 0, s>>>(
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), combine_kernel<bf16, QV><<<(c->T + 8 * combine_tpw<QV>() - 1) /
+                                                                           (8 * combine_tpw<QV>()), 256, 0, s>>>(
         (const bf16*)e_out, row_gate, slot, c->T, c->d, c->E, (bf16*)y), count_launch())
   } else {
-    MOE_QV_DISPATCH(pass_vectors(c->d, 4), combine_kernel<float, QV><<<grid, 256, 0, s>>>(
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), combine_kernel<float, QV><<<(c->T + 8 * combine_tpw<QV>() - 1) /
+                                                                            (8 * combine_tpw<QV>()), 256, 0, s>>>(
         (const float*)e_out, row_gate, slot, c->T, c->d, c->E, (float*)y), count_launch())
   }
   return cudaGetLastError();
