@@ -858,11 +858,20 @@ __global__ void __launch_bounds__(256, 4) ep2_combine_kernel(const __grid_consta
                                                              const float* __restrict__ probs,
                                                              const int* __restrict__ slot, int T_, int d, int E, int El,
                                                              T* __restrict__ y) {
+  constexpr int TPW = combine_tpw<QV>();          // as combine_kernel: both slot rows up front
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int t = blockIdx.x * 8 + warp;
-  if (t >= T_) return;
-  gather_sum_token<T, true, float, QV, PeerRows<T>>(PeerRows<T>{&eo, probs + (long long)t * E, d, El},
-                                                     slot + (long long)t * E, d, E, nullptr, y + (long long)t * d, lane);
+  const int t0 = (blockIdx.x * 8 + warp) * TPW;
+  if (t0 >= T_) return;
+  int sv[TPW][4];
+#pragma unroll
+  for (int j = 0; j < TPW; ++j)
+    if (t0 + j < T_) load_slot_row(slot + (long long)(t0 + j) * E, E, lane, sv[j]);
+#pragma unroll
+  for (int j = 0; j < TPW; ++j)
+    if (t0 + j < T_)
+      gather_sum_token_sv<T, true, float, QV, PeerRows<T>>(PeerRows<T>{&eo, probs + (long long)(t0 + j) * E, d, El},
+                                                           sv[j], d, E, (const float*)nullptr,
+                                                           y + (long long)(t0 + j) * d, lane);
 }
 
 // token side: dx[t] = dxg[t] + sum_{e asc} dx_perm@(e / El)[slot[t,e]]
@@ -1261,12 +1270,13 @@ cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* pr
 cudaError_t launch_ep2_combine(const moe_ctx* c, const PeerTable& eo, const float* probs, const int32_t* slot, void* y,
                                cudaStream_t s) {
   if (c->T == 0) return cudaSuccess;
-  const unsigned grid = (c->T + 7) / 8;
   if (c->dtype == 1) {
-    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_combine_kernel<bf16, QV><<<grid, 256, 0, s>>>(
+    MOE_QV_DISPATCH(pass_vectors(c->d, 8), ep2_combine_kernel<bf16, QV><<<(c->T + 8 * combine_tpw<QV>() - 1) /
+                                                                               (8 * combine_tpw<QV>()), 256, 0, s>>>(
         eo, probs, slot, c->T, c->d, c->E, c->E_local, (bf16*)y), count_launch())
   } else {
-    MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2_combine_kernel<float, QV><<<grid, 256, 0, s>>>(
+    MOE_QV_DISPATCH(pass_vectors(c->d, 4), ep2_combine_kernel<float, QV><<<(c->T + 8 * combine_tpw<QV>() - 1) /
+                                                                                (8 * combine_tpw<QV>()), 256, 0, s>>>(
         eo, probs, slot, c->T, c->d, c->E, c->E_local, (float*)y), count_launch())
   }
   return cudaGetLastError();
