@@ -49,7 +49,7 @@ extern "C" {
 typedef enum {
   MOE_OK = 0,
   MOE_EINVAL = 1,      /* bad scalar argument (tau <= 0 or non-finite, c not in [0,1)), NULL pointer */
-  MOE_ESHAPE = 2,      /* bad dims: E < 1, E % world != 0, d or d_ff not a multiple of 64 (bf16) / 4 (f32) */
+  MOE_ESHAPE = 2,      /* bad dims: E < 1, E % world != 0, d or d_ff not a multiple of 8 (bf16) / 4 (f32) */
   MOE_EDTYPE = 3,      /* unknown dtype */
   MOE_ECUDA = 4,       /* a CUDA runtime call failed (message has the CUDA error string) */
   MOE_ENCCL = 5,       /* an NCCL call failed */
@@ -67,6 +67,9 @@ typedef struct moe_ctx moe_ctx;
 /* Create a layer context.  T = tokens on this rank, E = global number of experts,
  * world = expert-parallel group size (E_local = E / world experts live on `rank`).
  * nccl_comm: an ncclComm_t (borrowed, never destroyed) or NULL when world == 1.
+ * d_model and d_ff: multiples of 8 (bf16; 16-byte rows) or 4 (f32).  bf16 layers whose d_model
+ * and d_ff are both multiples of 64 run the tensor-core GEMMs and gate (64-wide K boxes); other
+ * bf16 shapes run the CUDA-core GEMMs and the warp-per-token gate (same results, slower).
  * Returns MOE_ESHAPE / MOE_EDTYPE / MOE_EINVAL on bad arguments. */
 int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype,
                void* nccl_comm, int rank, int world);

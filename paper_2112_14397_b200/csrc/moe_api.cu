@@ -150,7 +150,10 @@ int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype, vo
   if (!out) return fail(MOE_EINVAL, "moe_create: out is NULL");
   *out = nullptr;
   if (dtype != MOE_F32 && dtype != MOE_BF16) return fail(MOE_EDTYPE, "moe_create: unknown dtype %d", dtype);
-  const int q = dtype == MOE_BF16 ? 64 : 4;
+  // 16-byte rows for the routing vectors and TMA strides: multiples of 8 (bf16) / 4 (fp32); the
+  // tensor-core GEMMs need multiples of 64 (their 64-wide K boxes), other bf16 shapes run the
+  // CUDA-core GEMMs (use_tc below)
+  const int q = dtype == MOE_BF16 ? 8 : 4;
   if (T < 0 || E < 1 || d_model < 1 || d_ff < 1 || world < 1 || rank < 0 || rank >= world)
     return fail(MOE_ESHAPE, "moe_create: bad dims T=%d E=%d d_model=%d d_ff=%d rank=%d world=%d", T, E,
                 d_model, d_ff, rank, world);
@@ -175,7 +178,7 @@ int moe_create(moe_ctx** out, int T, int d_model, int d_ff, int E, int dtype, vo
   c->dwg_splits_max = 64;
   {
     const char* g = getenv("MOE_GEMM");
-    c->use_tc = (dtype == MOE_BF16) && !(g && strcmp(g, "simt") == 0);
+    c->use_tc = (dtype == MOE_BF16) && !(g && strcmp(g, "simt") == 0) && d_model % 64 == 0 && d_ff % 64 == 0;
   }
   *out = c;
   return MOE_OK;

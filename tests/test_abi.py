@@ -65,6 +65,12 @@ def test_create_validation(L):
     ctx = L.moe_create(256, 64, 256, 4, L.MOE_F32)
     assert L.moe_workspace_bytes(ctx) > 0
     L.moe_destroy(ctx)
+    # bf16 dims need only be multiples of 8 (16-byte rows); 4 is refused
+    ctx = L.moe_create(256, 72, 200, 4, L.MOE_BF16)
+    L.moe_destroy(ctx)
+    with pytest.raises(L.MoEError) as e:
+        L.moe_create(128, 68, 256, 4, L.MOE_BF16)
+    assert e.value.code == 2 and "68" in str(e.value)
 
 
 def test_calls_without_workspace_and_bad_scalars(L):

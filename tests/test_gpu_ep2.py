@@ -238,6 +238,11 @@ def test_ep2_fp32_c1_two_ranks():
     _check(configs.C1, 2, 96)
 
 
+def test_ep2_bf16_dims_multiple_of_8_two_ranks():
+    # d = 200, d_ff = 328 (multiples of 8, not 64): the CUDA-core GEMMs under the peer-memory EP path
+    _check(dataclasses.replace(configs.C3, name="C3m8", d_model=200, d_ff=328), 2, 256)
+
+
 def test_ep2_module_lockstep_c2_shape(poison_empty):
     # the same through paper_2112_14397_b200.ep2 (EP2Rank phases + SymmetricBuffers emulation)
     from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers

@@ -312,6 +312,15 @@ def test_bf16_partial_tiles_simt_gate():
     _run(_shape("odd", 300, 192, 320, 80, 0.8, 0.01))
 
 
+def test_bf16_dims_multiple_of_8_not_64():
+    # d = 200, d_ff = 328 (multiples of 8, not of 64): accepted by moe_create (SURVEY §8(b) asks for
+    # multiples of 8); the CUDA-core GEMMs and the SIMT gate run them (the tensor-core GEMMs and
+    # gate need 64-wide K boxes), every value checked against the oracle as usual
+    _run(_shape("m8", 300, 200, 328, 16, 0.7, 0.05))
+    _run(_shape("m8b", 257, 72, 136, 8, 1.0, 0.1))
+    _run(_shape("m8r", 300, 200, 328, 16, 0.7, 0.05), recompute=True)
+
+
 def test_bf16_single_expert_is_dense_ffn():
     # E = 1: every token to the one expert with weight 1 (P:311 special case), dW_g = 0
     rep, g = _run(_shape("E1", 256, 128, 256, 1, 1.0, 0.0))
