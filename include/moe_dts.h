@@ -301,7 +301,8 @@ int moe_ep_allreduce(moe_ctx* ctx, void* buf, int64_t n, int is_int32, void* str
  * the NCCL path's and, for the global token set, the single-rank layer's.  No host sync:
  * R_recv_cap is a static capacity, a multiple of 128 (worst case world*T*E_local + 127*E_local,
  * rounded up); overflow raises
- * MOE_ECAPACITY at moe_check.  d_model <= 1024 (bf16) / 512 (f32) for moe_ep2_combine_bwd.
+ * MOE_ECAPACITY at moe_check.  moe_ep2(d)_combine_bwd fuses the db2 partials into its row pass
+ * up to d_model = 1024 (bf16) / 512 (f32); wider rows take a warp-per-row pass plus a db2 pass.
  * nccl_comm == MOE_COMM_EMULATED (moe_create) runs `world` ranks in ONE process on one device
  * (the tests): moe_ep2_barrier is then a no-op and the caller orders the ranks' launches;
  * the NCCL exchange calls refuse such a ctx. */

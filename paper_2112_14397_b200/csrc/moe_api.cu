@@ -759,7 +759,6 @@ int moe_ep2_combine_bwd(moe_ctx* ctx, void* const* dy_peers, const void* e_out, 
   int rc = ep2_check(ctx, "moe_ep2_combine_bwd");
   if (rc) return rc;
   REQUIRE(e_out); REQUIRE(rgate); REQUIRE(rtok); REQUIRE(rsrc); REQUIRE(offsets_recv); REQUIRE(d_eout); REQUIRE(dG_row);
-  if (!moe::ep2_width_ok(ctx)) return fail(MOE_ESHAPE, "moe_ep2_combine_bwd: d_model=%d too wide (max 1024 bf16 / 512 f32)", ctx->d);
   moe::PeerTable t;
   if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(dy_peers), t, "moe_ep2_combine_bwd"))) return rc;
   return cuda_status(moe::launch_ep2_combine_bwd(ctx, t, e_out, rgate, rtok, rsrc, offsets_recv, R_recv_cap, d_eout,
@@ -863,8 +862,6 @@ int moe_ep2d_combine_bwd(moe_ctx* ctx, const void* dyu, const void* e_out, const
   int rc = ep2_check(ctx, "moe_ep2d_combine_bwd");
   if (rc) return rc;
   REQUIRE(dyu); REQUIRE(e_out); REQUIRE(rgate); REQUIRE(ruid); REQUIRE(offsets_recv); REQUIRE(d_eout); REQUIRE(dG_row);
-  if (!moe::ep2_width_ok(ctx))
-    return fail(MOE_ESHAPE, "moe_ep2d_combine_bwd: d_model=%d too wide (max 1024 bf16 / 512 f32)", ctx->d);
   return cuda_status(moe::launch_ep2d_combine_bwd(ctx, dyu, e_out, rgate, ruid, offsets_recv, R_recv_cap, d_eout,
                                                   dG_row, db2, S(stream)),
                      "moe_ep2d_combine_bwd");

@@ -456,13 +456,17 @@ static inline int pass_vectors(int d, int V) {
 
 // ------------------------------------------------------------------ combine backward
 // One warp per row r < offsets[E]: d_eout[r] = g dy[t]; dG_row[r] = <dy[t], e_out[r]>.
-template <typename T>
+template <typename T, bool PEER = false>
 __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ e_out,
                                                           const float* __restrict__ row_gate,
                                                           const int* __restrict__ row_token,
                                                           const int* __restrict__ offsets, int E, int d,
                                                           long long R_cap, T* __restrict__ d_eout,
-                                                          float* __restrict__ dG_row) {
+                                                          float* __restrict__ dG_row,
+                                                          const int* __restrict__ row_src,
+                                                          const __grid_constant__ PeerTable dyp) {
+  // PEER (peer-memory EP, rows wider than the fused kernel's registers): the row's token lives
+  // on rank row_src[r] and its dy row is read through that rank's peer pointer
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const long long r = (long long)blockIdx.x * 8 + warp;
   const long long R = min((long long)offsets[E], R_cap);
@@ -476,11 +480,12 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const T* __restrict__ 
     if (lane == 0) dG_row[r] = 0.f;
     return;
   }
+  const T* dyt = (PEER ? reinterpret_cast<const T*>(dyp.p[row_src[r]]) : dy) + (long long)t * d;
   const float gw = row_gate[r];
   float dot = 0.f;
   for (int v = lane; v < nvec; v += 32) {
     float a[V], b[V], o[V];
-    unpack16(ld_nc_v4(dy + (long long)t * d + (long long)v * V), a, T());
+    unpack16(ld_nc_v4(dyt + (long long)v * V), a, T());
     unpack16(ld_nc_v4(e_out + r * d + (long long)v * V), b, T());
 #pragma unroll
     for (int k = 0; k < V; ++k) {
@@ -1192,10 +1197,12 @@ cudaError_t launch_combine_bwd(moe_ctx* c, const void* dy, const void* e_out, co
   const unsigned grid = (unsigned)((R_cap + 7) / 8);
   if (c->dtype == 1)
     combine_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dy, (const bf16*)e_out, row_gate, row_token, offsets,
-                                                  c->E, c->d, R_cap, (bf16*)d_eout, dG_row), count_launch();
+                                                  c->E, c->d, R_cap, (bf16*)d_eout, dG_row, nullptr, PeerTable{}),
+        count_launch();
   else
     combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dy, (const float*)e_out, row_gate, row_token,
-                                                   offsets, c->E, c->d, R_cap, (float*)d_eout, dG_row), count_launch();
+                                                   offsets, c->E, c->d, R_cap, (float*)d_eout, dG_row, nullptr,
+                                                   PeerTable{}), count_launch();
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess && db2 ? launch_db2(c, d_eout, offsets, R_cap, db2, s) : e;
 }
@@ -1293,6 +1300,20 @@ cudaError_t launch_ep2_combine_bwd(moe_ctx* c, const PeerTable& dyp, const void*
   if (R_cap == 0) return db2 ? cudaMemsetAsync(db2, 0, sizeof(float) * c->E_local * c->d, s) : cudaSuccess;
   const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
   cudaError_t e;
+  if (!ep2_width_ok(c)) {
+    // rows wider than the fused kernel's register budget: warp per row (dy through the peer
+    // pointers), then db2 from the stored d_eout
+    const unsigned grid = (unsigned)((R_cap + 7) / 8);
+    if (c->dtype == 1)
+      combine_bwd_kernel<bf16, true><<<grid, 256, 0, s>>>(nullptr, (const bf16*)e_out, rgate, rtok, offsets, c->E_local,
+                                                          c->d, R_cap, (bf16*)d_eout, dG_row, rsrc, dyp), count_launch();
+    else
+      combine_bwd_kernel<float, true><<<grid, 256, 0, s>>>(nullptr, (const float*)e_out, rgate, rtok, offsets,
+                                                           c->E_local, c->d, R_cap, (float*)d_eout, dG_row, rsrc, dyp),
+          count_launch();
+    e = cudaGetLastError();
+    return e == cudaSuccess && db2 ? launch_db2(c, d_eout, offsets, R_cap, db2, s) : e;
+  }
   if (c->dtype == 1) {
     if (nvec <= 32) e = launch_cbc<bf16, 1, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
     else if (nvec <= 64) e = launch_cbc<bf16, 2, true, true>(c, nullptr, e_out, rgate, rtok, offsets, R_cap, d_eout, dG_row, s, rsrc, &dyp);
@@ -1416,6 +1437,20 @@ cudaError_t launch_ep2d_combine_bwd(moe_ctx* c, const void* dyu, const void* e_o
   if (R_cap == 0) return db2 ? cudaMemsetAsync(db2, 0, sizeof(float) * c->E_local * c->d, s) : cudaSuccess;
   const int V = c->dtype == 1 ? 8 : 4, nvec = c->d / V;
   cudaError_t e;
+  if (!ep2_width_ok(c)) {
+    // rows wider than the fused kernel's register budget: warp per row, then db2 from d_eout
+    const unsigned grid = (unsigned)((R_cap + 7) / 8);
+    if (c->dtype == 1)
+      combine_bwd_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)dyu, (const bf16*)e_out, rgate, ruid, offsets,
+                                                    c->E_local, c->d, R_cap, (bf16*)d_eout, dG_row, nullptr,
+                                                    PeerTable{}), count_launch();
+    else
+      combine_bwd_kernel<float><<<grid, 256, 0, s>>>((const float*)dyu, (const float*)e_out, rgate, ruid, offsets,
+                                                     c->E_local, c->d, R_cap, (float*)d_eout, dG_row, nullptr,
+                                                     PeerTable{}), count_launch();
+    e = cudaGetLastError();
+    return e == cudaSuccess && db2 ? launch_db2(c, d_eout, offsets, R_cap, db2, s) : e;
+  }
   if (c->dtype == 1) {
     if (nvec <= 32) e = launch_cbc<bf16, 1>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);
     else if (nvec <= 64) e = launch_cbc<bf16, 2>(c, dyu, e_out, rgate, ruid, offsets, R_cap, d_eout, dG_row, s);

@@ -238,6 +238,12 @@ def test_ep2_fp32_c1_two_ranks():
     _check(configs.C1, 2, 96)
 
 
+def test_ep2_wide_rows_two_ranks():
+    # d_model = 1280 > 1024: the expert-side combine backward takes the warp-per-row pass (dy
+    # through the peer pointers) and a separate db2 pass instead of the fused register kernel
+    _check(dataclasses.replace(configs.C3, name="C3w", d_model=1280, d_ff=512), 2, 192)
+
+
 def test_ep2_bf16_dims_multiple_of_8_two_ranks():
     # d = 200, d_ff = 328 (multiples of 8, not 64): the CUDA-core GEMMs under the peer-memory EP path
     _check(dataclasses.replace(configs.C3, name="C3m8", d_model=200, d_ff=328), 2, 256)
@@ -338,6 +344,14 @@ def test_ep2_dedup_matches_single_rank(poison_empty, name, W, T):
         assert _rel(ep["y"][q], y[sl]) < tol, f"rank {q} y {_rel(ep['y'][q], y[sl])}"
         assert _rel(ep["g"][q]["dx"], g["dx"][sl]) < tol, f"rank {q} dx {_rel(ep['g'][q]['dx'], g['dx'][sl])}"
     assert _rel(ep["dWg"], g["dWg"]) < 1e-5
+
+
+def test_ep2d_wide_rows_two_ranks(poison_empty):
+    # the token-dedup path with d_model = 1280 > 1024 (warp-per-row combine backward + db2 pass)
+    cfg = dataclasses.replace(configs.C3, name="C3w", d_model=1280, d_ff=512)
+    ep, ranks_in = _lockstep(cfg, 2, 192, dedup=True)
+    _vs_oracle(cfg, 2, 192, ranks_in, ep["probs"], ep["slot"], ep["y"], [gq["dx"] for gq in ep["g"]],
+               [gq["dlogits"] for gq in ep["g"]], ep["g"], ep["dWg"])
 
 
 def test_ep2_dedup_single_owner_rows_are_exact(poison_empty):
