@@ -736,10 +736,17 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
           make_store_map_pair(&mO1, gp, R_cap, f,
                               (long long)(reinterpret_cast<uintptr_t>(h) - reinterpret_cast<uintptr_t>(gp)));
   const long long up = rows_pairs_upper(R_cap, El);
-  cudaError_t e = gp ? launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p,
-                                                                       up * ((f + BN - 1) / BN), c->sm_count, s)
-                      : launch_tc<TEPI_BIAS_GELU_H, false, false, false>(mA, mB, mO2, mO2, mO2, p,
-                                                                         up * ((f + BN - 1) / BN), c->sm_count, s);
+  // 4 GELU epilogue warps per lane quarter below d = 1024 (the short mainloop leaves the epilogue
+  // exposed: C5 step 0 -4.6% cycles, C2 -1.4%), 3 from d = 1024 up (C4: +2.9% with 4);
+  // profiles/r02/ab_gelu_epq.txt
+  const long long jobs = up * ((f + BN - 1) / BN);
+  cudaError_t e;
+  if (d < 1024)
+    e = gp ? launch_tc<TEPI_BIAS_GELU, false, false, false, 4>(mA, mB, mO1, mO2, mO1, p, jobs, c->sm_count, s)
+           : launch_tc<TEPI_BIAS_GELU_H, false, false, false, 4>(mA, mB, mO2, mO2, mO2, p, jobs, c->sm_count, s);
+  else
+    e = gp ? launch_tc<TEPI_BIAS_GELU, false, false, false>(mA, mB, mO1, mO2, mO1, p, jobs, c->sm_count, s)
+           : launch_tc<TEPI_BIAS_GELU_H, false, false, false>(mA, mB, mO2, mO2, mO2, p, jobs, c->sm_count, s);
   if (e != cudaSuccess) return e;
   if (!W2) return cudaSuccess;          // recompute call: GEMM1 only
   // GEMM2: e_out = h W2^T + b2                     A [R, f] K-major, B = W2 [El*d, f] K-major
