@@ -912,23 +912,84 @@ __global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
     const __grid_constant__ PeerTable rgate, const __grid_constant__ PeerTable ruid,
     const __grid_constant__ PeerTable urows, int* __restrict__ uslot) {
   __shared__ unsigned s_bal[kGateBT / 32][128];
+  __shared__ long long s_base[128];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
-  for (int e0 = 0; e0 < E; e0 += 8) {          // 8 flags in flight, then 8 ballots (as dispatch_rank_kernel)
-    int v[8];
+  if (!DEDUP)   // the block's first row of every expert on its owner (as dispatch_rank_kernel)
+    for (int e = tid; e < E; e += kGateBT) s_base[e] = (long long)base[e] + blk_base[(long long)e * gridDim.x + blockIdx.x];
+  // 16 selection flags per thread in flight (16-byte loads when the rows allow), then 16 ballots
+  const bool vec = (E & 3) == 0;
+  unsigned selm[4] = {0u, 0u, 0u, 0u};              // this thread's selected experts (E <= 128)
+  for (int e0 = 0; e0 < E; e0 += 16) {
+    int v[16];
+    if (vec && e0 + 16 <= E) {
+      int4 q[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
+      for (int i = 0; i < 4; ++i) {
+        q[i] = make_int4(-1, -1, -1, -1);
+        if (valid) q[i] = *reinterpret_cast<const int4*>(slot + (long long)t * E + e0 + 4 * i);
+      }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const unsigned bal = __ballot_sync(0xffffffffu, v[j] >= 0);
+      for (int i = 0; i < 4; ++i) { v[4 * i] = q[i].x; v[4 * i + 1] = q[i].y; v[4 * i + 2] = q[i].z; v[4 * i + 3] = q[i].w; }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = (valid && e0 + j < E) ? slot[(long long)t * E + e0 + j] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const bool sel = v[j] >= 0 && e0 + j < E;
+      const unsigned bal = __ballot_sync(0xffffffffu, sel);
       if (lane == 0 && e0 + j < E) s_bal[warp][e0 + j] = bal;
+      if (sel) selm[(e0 + j) >> 5] |= 1u << ((e0 + j) & 31);
     }
   }
   __syncthreads();
   if (!valid) return;
   const unsigned lower = (1u << lane) - 1u;
   const long long u = (long long)me * T_ + t;
+  if (!DEDUP) {
+    // the selected experts only, ascending, up to 8 per batch with their gate loads in flight
+    int word = 0;
+    unsigned bits = selm[0];
+    while (true) {
+      int es[8], nb = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        while (bits == 0u && word < 3) bits = selm[++word];
+        es[j] = -1;
+        if (bits) {
+          es[j] = word * 32 + __ffs(bits) - 1;
+          bits &= bits - 1u;
+          ++nb;
+        }
+      }
+      if (nb == 0) break;
+      float pg[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) pg[j] = es[j] >= 0 ? probs[(long long)t * E + es[j]] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int e = es[j];
+        if (e < 0) continue;
+        const unsigned mine = s_bal[warp][e];
+        int wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
+        const long long r = s_base[e] + wpre + __popc(mine & lower);
+        int row = -1;
+        if (r < R_cap) {
+          const int p = e / El;
+          row = (int)r;
+          reinterpret_cast<int*>(const_cast<void*>(rtok.p[p]))[r] = t;
+          reinterpret_cast<int*>(const_cast<void*>(rsrc.p[p]))[r] = me;
+          reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[r] = pg[j];
+        }
+        slot[(long long)t * E + e] = row;            // -1: dropped (MOE_ECAPACITY raised by the plan)
+      }
+      if (nb < 8) break;
+    }
+    return;
+  }
   for (int e = 0; e < E; ++e) {
     const unsigned mine = s_bal[warp][e];
     const int p = e / El;
