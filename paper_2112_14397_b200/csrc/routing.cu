@@ -916,8 +916,8 @@ __global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int t = blockIdx.x * kGateBT + tid;
   const bool valid = t < T_;
-  if (!DEDUP)   // the block's first row of every expert on its owner (as dispatch_rank_kernel)
-    for (int e = tid; e < E; e += kGateBT) s_base[e] = (long long)base[e] + blk_base[(long long)e * gridDim.x + blockIdx.x];
+  // the block's first row of every expert on its owner (as dispatch_rank_kernel)
+  for (int e = tid; e < E; e += kGateBT) s_base[e] = (long long)base[e] + blk_base[(long long)e * gridDim.x + blockIdx.x];
   // 16 selection flags per thread in flight (16-byte loads when the rows allow), then 16 ballots
   const bool vec = (E & 3) == 0;
   unsigned selm[4] = {0u, 0u, 0u, 0u};              // this thread's selected experts (E <= 128)
@@ -990,25 +990,39 @@ __global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
     }
     return;
   }
-  for (int e = 0; e < E; ++e) {
-    const unsigned mine = s_bal[warp][e];
-    const int p = e / El;
-    int row = -1;
-    if ((mine >> lane) & 1u) {
-      int wpre = 0;
-      for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
-      const long long r = (long long)base[e] + blk_base[(long long)e * gridDim.x + blockIdx.x] + wpre +
-                          __popc(mine & lower);
-      if (r < R_cap) {
-        row = (int)r;
-        reinterpret_cast<int*>(const_cast<void*>(rtok.p[p]))[r] = t;
-        reinterpret_cast<int*>(const_cast<void*>(rsrc.p[p]))[r] = me;
-        reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[r] = probs[(long long)t * E + e];
-        if (DEDUP) reinterpret_cast<int*>(const_cast<void*>(ruid.p[p]))[r] = (int)u;
+  // dedup: every (token, local expert) entry of urows on every owner is written (the row or -1),
+  // four contiguous entries per 16-byte store when El allows
+  const bool v4 = (El & 3) == 0;
+  for (int p = 0; p < W; ++p) {
+    int* ur = reinterpret_cast<int*>(const_cast<void*>(urows.p[p])) + u * El;
+    for (int j0 = 0; j0 < El; j0 += 4) {
+      int rows4[4] = {-1, -1, -1, -1};
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = j0 + jj, e = p * El + j;
+        if (j >= El) break;
+        const unsigned mine = s_bal[warp][e];
+        if (!((mine >> lane) & 1u)) continue;
+        int wpre = 0;
+        for (int w = 0; w < warp; ++w) wpre += __popc(s_bal[w][e]);
+        const long long r = s_base[e] + wpre + __popc(mine & lower);
+        int row = -1;
+        if (r < R_cap) {
+          row = (int)r;
+          reinterpret_cast<int*>(const_cast<void*>(rtok.p[p]))[r] = t;
+          reinterpret_cast<int*>(const_cast<void*>(rsrc.p[p]))[r] = me;
+          reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[r] = probs[(long long)t * E + e];
+          reinterpret_cast<int*>(const_cast<void*>(ruid.p[p]))[r] = (int)u;
+        }
+        slot[(long long)t * E + e] = row;          // -1: dropped (MOE_ECAPACITY raised by the plan)
+        rows4[jj] = row;
       }
-      slot[(long long)t * E + e] = row;            // -1: dropped (MOE_ECAPACITY raised by the plan)
+      if (v4) {
+        *reinterpret_cast<int4*>(ur + j0) = make_int4(rows4[0], rows4[1], rows4[2], rows4[3]);
+      } else {
+        for (int jj = 0; jj < 4 && j0 + jj < El; ++jj) ur[j0 + jj] = rows4[jj];
+      }
     }
-    if (DEDUP) reinterpret_cast<int*>(const_cast<void*>(urows.p[p]))[u * El + (e - p * El)] = row;
   }
   if (DEDUP) {
     for (int p = 0; p < W; ++p) {
