@@ -225,52 +225,65 @@ __global__ void __launch_bounds__(256) gate_bwd_token_kernel(
     for (int k = 2 * Ep + lane; k < Kp; k += 32) dL2[(long long)t * Kp + k] = __float2bfloat16_rn(0.f);
 }
 
-// The same for E a power of two, 2 <= E <= 64: lane = two adjacent (token, expert) entries of
-// the flat [T, E] arrays (float2 / int2 / bf16x2 accesses, E / 2 lanes per token, 64 / E tokens
-// per warp); <p, dp> is a butterfly over the token's E / 2 lanes.  Half the memory
-// instructions of the lane-per-expert form, no idle lanes at E < 32.
+// The same for E = 16, 32, 64 (E a power of two and Ep == E): lane = four adjacent (token,
+// expert) entries of the flat [T, E] arrays (float4 / int4 loads, one 8-byte store of each bf16
+// half of dL), E / 4 lanes per token; <p, dp> is a butterfly over the token's E / 4 lanes.  A
+// quarter of the threads and memory instructions of the lane-per-expert form (C4: 48 -> 31 us;
+// two entries per lane: 38 us).
 template <bool PEER = false>
-__global__ void __launch_bounds__(256) gate_bwd_pair_kernel(
+__global__ void __launch_bounds__(256) gate_bwd_quad_kernel(
     const float* __restrict__ dG_row, const int* __restrict__ slot, const float* __restrict__ probs,
     int T_, int E, float tau, float alpha, const int* __restrict__ counts, int count_rows, double bal_scale,
     float* __restrict__ dlogits, bf16* __restrict__ dL2, int Ep, int Kp, int El,
     const __grid_constant__ PeerTable dGp) {
   const int lane = threadIdx.x % 32;
-  const long long i0 = 2 * (((long long)blockIdx.x * 8 + threadIdx.x / 32) * 32 + lane);
+  const long long i0 = 4 * (((long long)blockIdx.x * 8 + threadIdx.x / 32) * 32 + lane);
   const long long t = i0 / E;
-  const int e = (int)(i0 % E), G = E / 2;
+  const int e = (int)(i0 % E), G = E / 4;
   const bool ok = t < T_;
-  float2 pp = make_float2(0.f, 0.f);
-  int2 rr = make_int2(-1, -1);
+  float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
+  int4 rr = make_int4(-1, -1, -1, -1);
   if (ok) {
-    pp = *reinterpret_cast<const float2*>(probs + i0);
-    rr = *reinterpret_cast<const int2*>(slot + i0);
+    pp = *reinterpret_cast<const float4*>(probs + i0);
+    rr = *reinterpret_cast<const int4*>(slot + i0);
   }
-  float dp0 = rr.x >= 0 ? (PEER ? reinterpret_cast<const float*>(dGp.p[e / El])[rr.x] : dG_row[rr.x]) : 0.f;
-  float dp1 = rr.y >= 0 ? (PEER ? reinterpret_cast<const float*>(dGp.p[(e + 1) / El])[rr.y] : dG_row[rr.y]) : 0.f;
+  const int r4[4] = {rr.x, rr.y, rr.z, rr.w};
+  const float p4[4] = {pp.x, pp.y, pp.z, pp.w};
+  float dp[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    dp[j] = r4[j] >= 0 ? (PEER ? reinterpret_cast<const float*>(dGp.p[(e + j) / El])[r4[j]] : dG_row[r4[j]]) : 0.f;
   if (alpha > 0.f && ok) {                 // global count of e: the column sum of the count rows
-    int c0 = 0, c1 = 0;
-    for (int q = 0; q < count_rows; ++q) {
-      c0 += counts[(long long)q * E + e];
-      c1 += counts[(long long)q * E + e + 1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int cn = 0;
+      for (int q = 0; q < count_rows; ++q) cn += counts[(long long)q * E + e + j];
+      dp[j] += (float)(bal_scale * (double)cn);
     }
-    dp0 += (float)(bal_scale * (double)c0);
-    dp1 += (float)(bal_scale * (double)c1);
   }
-  float sum = pp.x * dp0 + pp.y * dp1;
+  float sum = (p4[0] * dp[0] + p4[1] * dp[1]) + (p4[2] * dp[2] + p4[3] * dp[3]);
   for (int o = 1; o < G; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   if (!ok) return;
   const float inv_tau = 1.0f / tau;
-  const float v0 = pp.x * (dp0 - sum) * inv_tau, v1 = pp.y * (dp1 - sum) * inv_tau;
-  *reinterpret_cast<float2*>(dlogits + i0) = make_float2(v0, v1);
+  float v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = p4[j] * (dp[j] - sum) * inv_tau;
+  *reinterpret_cast<float4*>(dlogits + i0) = make_float4(v[0], v[1], v[2], v[3]);
   if (dL2) {   // tensor-core operand row [hi | lo | 0] of dlogits (dl_split_kernel's layout)
-    const bf16 h0 = __float2bfloat16_rn(v0), h1 = __float2bfloat16_rn(v1);
+    bf16 h[4], l[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      h[j] = __float2bfloat16_rn(v[j]);
+      l[j] = __float2bfloat16_rn(v[j] - __bfloat162float(h[j]));
+    }
     bf16* row = dL2 + t * Kp;
-    *reinterpret_cast<__nv_bfloat162*>(row + e) = __halves2bfloat162(h0, h1);
-    *reinterpret_cast<__nv_bfloat162*>(row + Ep + e) =
-        __halves2bfloat162(__float2bfloat16_rn(v0 - __bfloat162float(h0)), __float2bfloat16_rn(v1 - __bfloat162float(h1)));
-    for (int k = 2 * Ep + e; k < Kp; k += E)
-      *reinterpret_cast<__nv_bfloat162*>(row + k) = __halves2bfloat162(__float2bfloat16_rn(0.f), __float2bfloat16_rn(0.f));
+    const __nv_bfloat162 h01 = __halves2bfloat162(h[0], h[1]), h23 = __halves2bfloat162(h[2], h[3]);
+    const __nv_bfloat162 l01 = __halves2bfloat162(l[0], l[1]), l23 = __halves2bfloat162(l[2], l[3]);
+    *reinterpret_cast<uint2*>(row + e) = make_uint2(*reinterpret_cast<const unsigned*>(&h01),
+                                                    *reinterpret_cast<const unsigned*>(&h23));
+    *reinterpret_cast<uint2*>(row + Ep + e) = make_uint2(*reinterpret_cast<const unsigned*>(&l01),
+                                                         *reinterpret_cast<const unsigned*>(&l23));
+    for (int k = 2 * Ep + e; k < Kp; k += E) *reinterpret_cast<uint2*>(row + k) = make_uint2(0u, 0u);
   }
 }
 
@@ -349,17 +362,17 @@ static cudaError_t gate_bwd_impl(const moe_ctx* c, const float* dG_row, const Pe
   bf16* dL2 = tc ? reinterpret_cast<bf16*>(gate_dl2_buffer(c)) : nullptr;
   const int Ep = (c->E + 15) / 16 * 16, Kp = (2 * Ep + 63) / 64 * 64;
   PeerTable tab{};
-  const bool pair = c->E >= 2 && c->E <= 64 && (c->E & (c->E - 1)) == 0 && Ep == c->E;
-  if (pair) {
-    // 256 threads = 512 entries of the flat [T, E] arrays per block
-    const unsigned grid = (unsigned)(((long long)c->T * c->E + 511) / 512);
+  const bool quad = c->E >= 16 && c->E <= 64 && (c->E & (c->E - 1)) == 0 && Ep == c->E;
+  if (quad) {
+    // 256 threads = 1024 entries of the flat [T, E] arrays per block
+    const unsigned grid = (unsigned)(((long long)c->T * c->E + 1023) / 1024);
     if (dGp) {
       tab = *dGp;
-      gate_bwd_pair_kernel<true><<<grid, 256, 0, s>>>(nullptr, slot, probs, c->T, c->E, tau, alpha, counts, count_rows,
+      gate_bwd_quad_kernel<true><<<grid, 256, 0, s>>>(nullptr, slot, probs, c->T, c->E, tau, alpha, counts, count_rows,
                                                       bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
           count_launch();
     } else {
-      gate_bwd_pair_kernel<false><<<grid, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts, count_rows,
+      gate_bwd_quad_kernel<false><<<grid, 256, 0, s>>>(dG_row, slot, probs, c->T, c->E, tau, alpha, counts, count_rows,
                                                        bal, dlogits, dL2, Ep, Kp, c->E_local, tab),
           count_launch();
     }

@@ -37,7 +37,7 @@ def algorithmic_bytes(cfg, R, Rp):
         (r"combine_bwd_colsum_kernel", T * d * b + R * d * b + Rp * d * b + Rp * 12,
          "read dy (each token once) + e_out, write d_eout (+ dG, meta)"),
         (r"combine_kernel", R * d * b + T * d * b + T * E * 4 + R * 4, "read e_out rows + slot + gates, write y"),
-        (r"gate_bwd_token_kernel|gate_bwd_pair_kernel", 3 * T * E * 4 + R * 4 + T * Kp * 2, "read probs, slot, dG; write dlogits + bf16 hi|lo"),
+        (r"gate_bwd_token_kernel|gate_bwd_quad_kernel", 3 * T * E * 4 + R * 4 + T * Kp * 2, "read probs, slot, dG; write dlogits + bf16 hi|lo"),
         (r"gate_tc_kernel<2>", T * d * b + T * Kp * 2, "dW_g: read x, dL hi|lo"),
         (r"tc_gemm_kernel<3, false, false, false, 0>|tc_gemm_kernel<3, 0, 0, 0", T * Kp * 2 + T * d * b,
          "dL W_g^T: read dL hi|lo, write dx"),
