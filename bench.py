@@ -795,7 +795,10 @@ def run_ep(args, rank, world):
         "parallelism": f"ep{world}: E/{world}={El} experts per GPU, T={cfg.T} tokens per GPU; " + (
             "NCCL grouped send/recv all-to-all-v (eager, host-planned)" if path == "nccl" else
             "fused NVLink peer-memory dispatch / combine (torch symmetric memory), " +
-            ("one row per (token, owner) each way (moe_ep2d_*)" if path == "p2p-dedup" else "moe_ep2_*")),
+            ("one row per (token, owner) each way (moe_ep2d_*)" if path == "p2p-dedup" else "moe_ep2_*") +
+            ("; exchange / GEMM overlap: no barrier between the x exchange and the expert GEMMs, each "
+             "expert's GEMM1 tiles wait on its arrival counter" if path != "nccl" and getattr(r, "overlap", False)
+             else "")),
         "ep_path": path + (f" ({note})" if note else ""),
         "row_capacity": None if path == "nccl" else {"R_cap": r.R_cap, "grows": r.grows},
         "launch": "cuda-graph replay (static capacity, no host sync)" if graph is not None else "eager",

@@ -55,7 +55,8 @@ typedef enum {
   MOE_ENCCL = 5,       /* an NCCL call failed */
   MOE_ENONFINITE = 6,  /* device: a gate logit was NaN/Inf ("NaN is an error state") */
   MOE_ECAPACITY = 7,   /* device: R_pad > R_cap; rows beyond R_cap were not written */
-  MOE_EWORKSPACE = 8   /* workspace missing or too small */
+  MOE_EWORKSPACE = 8,  /* workspace missing or too small */
+  MOE_EARRIVAL = 9     /* device: overlap mode, an expert's rows did not all arrive (bounded wait timed out) */
 } moe_status;
 
 typedef enum { MOE_F32 = 0, MOE_BF16 = 1 } moe_dtype;
@@ -315,6 +316,35 @@ int moe_ep2_prepare_recv(moe_ctx* ctx, void* x_recv, int32_t* rtok, int32_t* rsr
 int moe_ep2_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, void* const* x_recv_peers,
                      int32_t* const* rtok_peers, int32_t* const* rsrc_peers, float* const* rgate_peers,
                      int64_t R_recv_cap, void* stream);
+/* Exchange / GEMM overlap ("low utilization of network bandwidth"): the x
+ * exchange and the expert GEMMs without a barrier between them.  Sequence per rank:
+ *   moe_ep2_counts -> barrier -> moe_ep2_plan -> moe_ep2_arrival_plan -> moe_ep2_prepare_recv ->
+ *   moe_ep2_dispatch_ordered -> moe_ep2_expert_ffn (no barrier) -> barrier -> moe_ep2_combine.
+ * moe_ep2_arrival_plan: sprefix [E+1] int32 (device, caller-owned) = prefix of THIS rank's counts
+ *   (row `rank` of counts_all) in (local expert j, owner p) order, index j*world + p; arrive_target
+ *   [E_local] int32 (device, caller-owned, zero before the first step, never reset) += the rows all
+ *   sources send to each of this rank's local experts this step (uint32 wrap-around arithmetic).
+ * moe_ep2_dispatch_ordered: as moe_ep2_dispatch, plus the send list send [T*E] int32 (device scratch,
+ *   caller-owned, any contents; entry i = the token of the i-th (token, expert) pair in sprefix
+ *   order) and arrive_peers (world device pointers to every rank's [E_local] int32 arrival counters,
+ *   symmetric memory, zero before the first step, never reset): the copy pass walks the send list
+ *   in order, so every owner's local expert 0 is filled first, and after each chunk of 64 entries
+ *   adds the chunk's per-(owner, expert) entry counts to the owner's counters with a system-scope
+ *   release (dropped rows of an overflowing step count too).
+ * moe_ep2_expert_ffn: moe_expert_ffn on the recv layout whose GEMM1 TMA producer acquire-polls
+ *   arrive[g] (this rank's counters) up to arrive_target[g] before an expert's first tile (the
+ *   CUDA-core path: one wait for all experts before its GEMMs).  The wait ends early when the plan
+ *   raised MOE_ECAPACITY and after a bounded spin raises MOE_EARRIVAL (at moe_check) instead of
+ *   hanging.  Results are those of moe_ep2_dispatch + barrier + moe_expert_ffn, bit for bit. */
+int moe_ep2_arrival_plan(moe_ctx* ctx, const int32_t* counts_all, int32_t* sprefix, int32_t* arrive_target,
+                         void* stream);
+int moe_ep2_dispatch_ordered(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, void* const* x_recv_peers,
+                             int32_t* const* rtok_peers, int32_t* const* rsrc_peers, float* const* rgate_peers,
+                             int64_t R_recv_cap, const int32_t* sprefix, int32_t* send, int32_t* const* arrive_peers,
+                             void* stream);
+int moe_ep2_expert_ffn(moe_ctx* ctx, const void* x_recv, const int32_t* offsets_recv, int64_t R_recv_cap,
+                       const void* W1, const void* b1, const void* W2, const void* b2, void* gp_saved, void* h_saved,
+                       void* e_out, const int32_t* arrive, const int32_t* arrive_target, void* stream);
 int moe_ep2_combine(moe_ctx* ctx, void* const* e_out_peers, const float* probs, const int32_t* slot, void* y,
                     void* stream);
 int moe_ep2_combine_bwd(moe_ctx* ctx, void* const* dy_peers, const void* e_out, const float* rgate,

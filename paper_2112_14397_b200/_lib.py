@@ -15,7 +15,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MOE_DTS_LIB", os.path.join(_PKG, "lib", "libmoe_dts.so"))
 
 STATUS = {0: "MOE_OK", 1: "MOE_EINVAL", 2: "MOE_ESHAPE", 3: "MOE_EDTYPE", 4: "MOE_ECUDA", 5: "MOE_ENCCL",
-          6: "MOE_ENONFINITE", 7: "MOE_ECAPACITY", 8: "MOE_EWORKSPACE"}
+          6: "MOE_ENONFINITE", 7: "MOE_ECAPACITY", 8: "MOE_EWORKSPACE", 9: "MOE_EARRIVAL"}
 MOE_F32, MOE_BF16 = 0, 1
 ROW_ALIGN = 128
 
@@ -61,6 +61,9 @@ SIGNATURES = {
     "moe_ep2_plan": (_I, [_P, _P, _L, _P, _P]),
     "moe_ep2_prepare_recv": (_I, [_P, _P, _P, _P, _P, _L, _P]),
     "moe_ep2_dispatch": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _P]),
+    "moe_ep2_arrival_plan": (_I, [_P, _P, _P, _P, _P]),
+    "moe_ep2_dispatch_ordered": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P]),
+    "moe_ep2_expert_ffn": (_I, [_P, _P, _P, _L, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "moe_ep2_combine": (_I, [_P, _P, _P, _P, _P, _P]),
     "moe_ep2_combine_bwd": (_I, [_P, _P, _P, _P, _P, _P, _P, _L, _P, _P, _P, _P]),
     "moe_ep2_gate_bwd": (_I, [_P, _P, _P, _P, _P, _P, _F, _F, _P, _L, _P, _P, _P, _P]),
@@ -361,6 +364,28 @@ def moe_ep2_dispatch(ctx, x, probs, slot, x_recv_peers, rtok_peers, rsrc_peers, 
     c, kc = _peers(rsrc_peers)
     d, kd = _peers(rgate_peers)
     _call("moe_ep2_dispatch", ctx, _ptr(x), _ptr(probs), _ptr(slot), a, b, c, d, int(R_recv_cap), _stream(stream))
+
+
+def moe_ep2_arrival_plan(ctx, counts_all, sprefix, arrive_target, stream=None):
+    _call("moe_ep2_arrival_plan", ctx, _ptr(counts_all), _ptr(sprefix), _ptr(arrive_target), _stream(stream))
+
+
+def moe_ep2_dispatch_ordered(ctx, x, probs, slot, x_recv_peers, rtok_peers, rsrc_peers, rgate_peers,
+                             R_recv_cap: int, sprefix, send, arrive_peers, stream=None):
+    a, ka = _peers(x_recv_peers)
+    b, kb = _peers(rtok_peers)
+    c, kc = _peers(rsrc_peers)
+    d, kd = _peers(rgate_peers)
+    e, ke = _peers(arrive_peers)
+    _call("moe_ep2_dispatch_ordered", ctx, _ptr(x), _ptr(probs), _ptr(slot), a, b, c, d, int(R_recv_cap),
+          _ptr(sprefix), _ptr(send), e, _stream(stream))
+
+
+def moe_ep2_expert_ffn(ctx, x_recv, offsets_recv, R_recv_cap: int, W1, b1, W2, b2, gp_saved, h_saved, e_out,
+                       arrive, arrive_target, stream=None):
+    _call("moe_ep2_expert_ffn", ctx, _ptr(x_recv), _ptr(offsets_recv), int(R_recv_cap), _ptr(W1), _ptr(b1),
+          _ptr(W2), _ptr(b2), _ptr(gp_saved), _ptr(h_saved), _ptr(e_out), _ptr(arrive), _ptr(arrive_target),
+          _stream(stream))
 
 
 def moe_ep2_combine(ctx, e_out_peers, probs, slot, y, stream=None):

@@ -12,6 +12,7 @@ constexpr int kWarp = 32;
 // device error flag bits (workspace word 0)
 constexpr int kFlagNonFinite = 1;
 constexpr int kFlagCapacity = 2;
+constexpr int kFlagArrival = 4;    // overlap mode: an expert's rows did not all arrive in time
 
 typedef __nv_bfloat16 bf16;
 

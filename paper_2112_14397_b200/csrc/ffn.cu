@@ -17,12 +17,37 @@ static SimtGemm base_rows(const int32_t* offsets, int G, int64_t R_cap) {
   return g;
 }
 
+// overlap mode on the CUDA-core path: one warp waits for every local expert's rows before the
+// GEMMs (the tcgen05 path waits per expert inside the GEMM's TMA producer instead)
+__global__ void ep2_wait_all_kernel(const int* __restrict__ arrive, const int* __restrict__ target, int El,
+                                    int* __restrict__ flags) {
+  for (int g = threadIdx.x; g < El; g += blockDim.x) {
+    const int tgt = target[g];
+    for (int spins = 0;; ++spins) {
+      int v;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(arrive + g) : "memory");
+      if ((int)((unsigned)v - (unsigned)tgt) >= 0) break;
+      if (*reinterpret_cast<volatile int*>(flags) & kFlagCapacity) break;
+      if (spins > (1 << 22)) {
+        atomicOr(flags, kFlagArrival);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+}
+
 cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
                               const void* W1, const void* b1, const void* W2, const void* b2, void* gp, void* h,
-                              void* e_out, cudaStream_t s) {
+                              void* e_out, cudaStream_t s, const int32_t* arrive, const int32_t* arrive_target) {
   const int d = c->d, f = c->f, El = c->E_local, dt = c->dtype;
   cudaError_t e;
-  if (c->use_tc) return tc_expert_ffn(c, x_perm, offsets, R_cap, W1, b1, W2, b2, gp, h, e_out, s);
+  if (c->use_tc)
+    return tc_expert_ffn(c, x_perm, offsets, R_cap, W1, b1, W2, b2, gp, h, e_out, s, arrive, arrive_target);
+  if (arrive) {
+    ep2_wait_all_kernel<<<1, 32, 0, s>>>(arrive, arrive_target, El, c->flags), count_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
   // GEMM1: a = x_perm W1_e^T + b1_e, h = GELU(a)
   SimtGemm g1 = base_rows(offsets, El, R_cap);
   g1.A = x_perm; g1.sAm = d; g1.sAk = 1;

@@ -131,7 +131,31 @@ struct TcParams {
   int o12;                // GEMM1: gp and h are one [2][R_cap][f] buffer, stored with ONE 3D TMA op per chunk
   void* reserved1;        // (unused; keeps the parameter block's layout of the measured builds)
   int a3d, b3d;           // MN-major operand given as a 3D map {64, K rows, MN / 64}: one TMA op per stage
+  // exchange / GEMM overlap (ROWS, peer-memory EP): before the first A load of an expert's tile the
+  // producer waits until arrive[g] reaches arrive_target[g] (wrap-safe), then fences the async proxy
+  const int* arrive;
+  const int* arrive_target;
+  int* flags;
 };
+
+// Acquire-poll of expert g's arrival counter (written by peers' ep2_copy_ordered_kernel with
+// release adds).  Stops early when the plan raised MOE_ECAPACITY (dropped rows are counted anyway,
+// but the step is re-run) and after a bounded spin (kFlagArrival instead of a hang).
+__device__ __forceinline__ void wait_arrival(const TcParams& p, int g) {
+  const int tgt = p.arrive_target[g];
+  for (int spins = 0;; ++spins) {
+    int v;
+    asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p.arrive + g) : "memory");
+    if ((int)((unsigned)v - (unsigned)tgt) >= 0) break;
+    if (*reinterpret_cast<volatile int*>(p.flags) & kFlagCapacity) break;
+    if (spins > (1 << 22)) {
+      atomicOr(p.flags, kFlagArrival);
+      break;
+    }
+    __nanosleep(256);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 
 struct Tile {
   int g, m_own, n0, kb0, nkb, row_end;
@@ -246,9 +270,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<EPI, QOV>::TH
       uint32_t phase = 0;
       const uint32_t smem_base = tc::smem_u32(smem);
       const uint32_t full_leader = tc::mapa(tc::smem_u32(full_bar), 0);
+      int waited_g = -1;
       for (int t = cid; t < total; t += ncl) {
         Tile tl;
         if (!decode_tile<KGRP>(p, s_off, s_pair, t, n_tiles, rank, tl)) continue;
+        if (!KGRP && p.arrive && tl.g != waited_g) {
+          wait_arrival(p, tl.g);
+          waited_g = tl.g;
+        }
         const int n_own = tl.n0 + BNH * (int)rank;
         const int brow = KGRP ? 0 : tl.g * p.b_group_rows;
         for (int kb = 0; kb < tl.nkb; ++kb) {
@@ -708,7 +737,7 @@ cudaError_t tc_dense_store(const moe_ctx* c, const void* A, long long rows, int 
 // ---------------------------------------------------------------- step 5 / B5 on tensor cores
 cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
                           const void* W1, const void* b1, const void* W2, const void* b2, void* gp, void* h,
-                          void* e_out, cudaStream_t s) {
+                          void* e_out, cudaStream_t s, const int32_t* arrive, const int32_t* arrive_target) {
   const int d = c->d, f = c->f, El = c->E_local;
   if (R_cap == 0) return cudaSuccess;
   const int fp = (f + 255) / 256 * 256, dp = (d + 255) / 256 * 256;
@@ -723,6 +752,7 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
   CUtensorMap mA, mB, mO1, mO2;
   TcParams p{};
   p.G = El; p.offsets = offsets; p.rows_cap = (int)R_cap;
+  p.arrive = arrive; p.arrive_target = arrive_target; p.flags = c->flags;   // GEMM1 only (reads x_perm)
   // GEMM1: a = x_perm W1^T + b1, h = GELU(a)      A [R, d] K-major, B = W1 [El*f, d] K-major
   if (!make_map(&mA, x_perm, R_cap, d, d, 64, BM) || !make_map(&mB, W1, (long long)El * f, d, d, 64, BNH) ||
       (gp && !make_store_map(&mO1, gp, R_cap, f)) || !make_store_map(&mO2, h, R_cap, f))
@@ -749,6 +779,7 @@ cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* o
            : launch_tc<TEPI_BIAS_GELU_H, false, false, false>(mA, mB, mO2, mO2, mO2, p, jobs, c->sm_count, s);
   if (e != cudaSuccess) return e;
   if (!W2) return cudaSuccess;          // recompute call: GEMM1 only
+  p.arrive = nullptr;
   // GEMM2: e_out = h W2^T + b2                     A [R, f] K-major, B = W2 [El*d, f] K-major
   if (!make_map(&mA, h, R_cap, f, f, 64, BM) || !make_map(&mB, W2, (long long)El * d, f, f, 64, BNH) ||
       !make_store_map(&mO1, e_out, R_cap, d))

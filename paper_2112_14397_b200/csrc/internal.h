@@ -108,7 +108,8 @@ cudaError_t launch_balance_loss(const moe_ctx* c, const float* probs, const int3
 
 cudaError_t launch_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets,
                               int64_t R_cap, const void* W1, const void* b1, const void* W2,
-                              const void* b2, void* gp, void* h, void* e_out, cudaStream_t s);
+                              const void* b2, void* gp, void* h, void* e_out, cudaStream_t s, const int32_t* arrive = nullptr,
+                              const int32_t* arrive_target = nullptr);
 
 cudaError_t launch_expert_ffn_bwd(moe_ctx* c, const void* d_eout, const void* x_perm,
                                   const void* gp, const void* h, const int32_t* offsets,
@@ -124,7 +125,10 @@ cudaError_t launch_ep2_prepare(const moe_ctx* c, void* x_recv, int32_t* rtok, in
                                int64_t R_cap, cudaStream_t s);
 cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot, const PeerTable& xr,
                                 const PeerTable& rtok, const PeerTable& rsrc, const PeerTable& rgate, int64_t R_cap,
-                                cudaStream_t s);
+                                cudaStream_t s, const int32_t* sprefix = nullptr, int32_t* send = nullptr,
+                                const PeerTable* arrive = nullptr);
+cudaError_t launch_ep2_arrival_plan(const moe_ctx* c, const int32_t* counts_all, int32_t* sprefix, int32_t* target,
+                                    cudaStream_t s);
 cudaError_t launch_ep2_combine(const moe_ctx* c, const PeerTable& eo, const float* probs, const int32_t* slot, void* y,
                                cudaStream_t s);
 bool ep2_width_ok(const moe_ctx* c);
@@ -157,7 +161,8 @@ cudaError_t launch_gate_bwd_peer(const moe_ctx* c, const PeerTable& dGp, const i
 bool tc_available();
 cudaError_t tc_expert_ffn(const moe_ctx* c, const void* x_perm, const int32_t* offsets, int64_t R_cap,
                           const void* W1, const void* b1, const void* W2, const void* b2, void* gp, void* h,
-                          void* e_out, cudaStream_t s);
+                          void* e_out, cudaStream_t s, const int32_t* arrive = nullptr,
+                          const int32_t* arrive_target = nullptr);
 cudaError_t tc_expert_ffn_bwd(const moe_ctx* c, const void* d_eout, const void* x_perm, const void* gp,
                               const void* h, const int32_t* offsets, int64_t R_cap, const void* W1,
                               const void* W2, void* da, void* dx_perm, float* dW1, float* dW2, float* db1,

@@ -222,6 +222,8 @@ int moe_check(moe_ctx* ctx, void* stream) {
     return fail(MOE_ENONFINITE, "moe_check: non-finite gate logit detected (first token %d)", h[1]);
   if (h[0] & moe::kFlagCapacity)
     return fail(MOE_ECAPACITY, "moe_check: R_pad=%d exceeds R_cap; rows beyond R_cap were dropped", h[2]);
+  if (h[0] & moe::kFlagArrival)
+    return fail(MOE_EARRIVAL, "moe_check: an expert's rows did not all arrive (overlap wait timed out)");
   return MOE_OK;
 }
 
@@ -741,6 +743,52 @@ int moe_ep2_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* s
     return rc;
   return cuda_status(moe::launch_ep2_dispatch(ctx, x, probs, slot, xr, rt, rs, rg, R_recv_cap, S(stream)),
                      "moe_ep2_dispatch");
+}
+
+int moe_ep2_arrival_plan(moe_ctx* ctx, const int32_t* counts_all, int32_t* sprefix, int32_t* arrive_target,
+                         void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_arrival_plan");
+  if (rc) return rc;
+  REQUIRE(counts_all); REQUIRE(sprefix); REQUIRE(arrive_target);
+  return cuda_status(moe::launch_ep2_arrival_plan(ctx, counts_all, sprefix, arrive_target, S(stream)),
+                     "moe_ep2_arrival_plan");
+}
+
+int moe_ep2_dispatch_ordered(moe_ctx* ctx, const void* x, const float* probs, int32_t* slot, void* const* x_recv_peers,
+                             int32_t* const* rtok_peers, int32_t* const* rsrc_peers, float* const* rgate_peers,
+                             int64_t R_recv_cap, const int32_t* sprefix, int32_t* send, int32_t* const* arrive_peers,
+                             void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_dispatch_ordered");
+  if (rc) return rc;
+  REQUIRE_T(x); REQUIRE_T(probs); REQUIRE_T(slot); REQUIRE(sprefix);
+  if (ctx->T > 0 && !send) return fail(MOE_EINVAL, "moe_ep2_dispatch_ordered: send is NULL");
+  if ((rc = check_gate_outputs(ctx, probs, slot, "moe_ep2_dispatch_ordered"))) return rc;
+  moe::PeerTable xr, rt, rs, rg, ar;
+  if ((rc = ep2_table(ctx, reinterpret_cast<const void* const*>(x_recv_peers), xr, "moe_ep2_dispatch_ordered")) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rtok_peers), rt, "moe_ep2_dispatch_ordered")) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rsrc_peers), rs, "moe_ep2_dispatch_ordered")) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(rgate_peers), rg, "moe_ep2_dispatch_ordered")) ||
+      (rc = ep2_table(ctx, reinterpret_cast<const void* const*>(arrive_peers), ar, "moe_ep2_dispatch_ordered")))
+    return rc;
+  return cuda_status(moe::launch_ep2_dispatch(ctx, x, probs, slot, xr, rt, rs, rg, R_recv_cap, S(stream), sprefix,
+                                              send, &ar),
+                     "moe_ep2_dispatch_ordered");
+}
+
+int moe_ep2_expert_ffn(moe_ctx* ctx, const void* x_recv, const int32_t* offsets_recv, int64_t R_recv_cap,
+                       const void* W1, const void* b1, const void* W2, const void* b2, void* gp_saved, void* h_saved,
+                       void* e_out, const int32_t* arrive, const int32_t* arrive_target, void* stream) {
+  int rc = ep2_check(ctx, "moe_ep2_expert_ffn");
+  if (rc) return rc;
+  const int64_t R_cap = R_recv_cap;
+  REQUIRE_R(x_recv); REQUIRE(offsets_recv); REQUIRE(W1); REQUIRE(b1); REQUIRE(W2); REQUIRE(b2);
+  REQUIRE_R(h_saved); REQUIRE_R(e_out); REQUIRE(arrive); REQUIRE(arrive_target);
+  if (R_recv_cap < 0 || R_recv_cap % moe::kRowAlign != 0)
+    return fail(MOE_EINVAL, "moe_ep2_expert_ffn: R_recv_cap=%lld must be a non-negative multiple of %d",
+                (long long)R_recv_cap, moe::kRowAlign);
+  return cuda_status(moe::launch_expert_ffn(ctx, x_recv, offsets_recv, R_recv_cap, W1, b1, W2, b2, gp_saved, h_saved,
+                                            e_out, S(stream), arrive, arrive_target),
+                     "moe_ep2_expert_ffn");
 }
 
 int moe_ep2_combine(moe_ctx* ctx, void* const* e_out_peers, const float* probs, const int32_t* slot, void* y,

@@ -857,6 +857,82 @@ __global__ void __launch_bounds__(256) ep2_copy_kernel(const T* __restrict__ x, 
   }
 }
 
+// Exchange / GEMM overlap: arrival plan.  sprefix [E + 1]: prefix of this rank's
+// counts in (local expert j, owner p) order (index j * W + p, global expert p * El + j) -- the
+// order of the ordered send list; target [El] (cumulative over steps, wrap-safe): += the rows
+// every source sends to my local expert j this step.
+__global__ void ep2_arrival_plan_kernel(const int* __restrict__ counts_all, int W, int E, int me,
+                                        int* __restrict__ sprefix, int* __restrict__ target) {
+  const int El = E / W;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < E; ++i) {
+      sprefix[i] = acc;
+      const int j = i / W, p = i - j * W;
+      acc += counts_all[(long long)me * E + p * El + j];
+    }
+    sprefix[E] = acc;
+  }
+  for (int j = threadIdx.x; j < El; j += blockDim.x) {
+    int tot = 0;
+    for (int q = 0; q < W; ++q) tot += counts_all[(long long)q * E + me * El + j];
+    target[j] = (int)((unsigned)target[j] + (unsigned)tot);
+  }
+}
+
+// token side copy pass in send-list order: block-chunks of kSendChunk entries, warp per entry
+// (x_t stored into its row on the owner), then one release add per (owner, local expert) of the
+// chunk into the owner's arrival counters -- entries whose row was dropped (-1) count too, so the
+// counters always reach the plan's targets.
+constexpr int kSendChunk = 64;
+template <typename T>
+__global__ void __launch_bounds__(256) ep2_copy_ordered_kernel(const T* __restrict__ x, const int* __restrict__ slot,
+                                                               const int* __restrict__ send,
+                                                               const int* __restrict__ sprefix, int d, int E, int El,
+                                                               int W, const __grid_constant__ PeerTable xr,
+                                                               const __grid_constant__ PeerTable arrive) {
+  __shared__ int s_pref[129];
+  for (int i = threadIdx.x; i <= E; i += blockDim.x) s_pref[i] = sprefix[i];
+  __syncthreads();
+  const int n = s_pref[E];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  constexpr int V = Vec16<T>::N;
+  const int nvec = d / V;
+  auto idx_of = [&](int i) {          // largest idx with s_pref[idx] <= i
+    int lo = 0, hi = E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pref[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  };
+  for (int c0 = blockIdx.x * kSendChunk; c0 < n; c0 += gridDim.x * kSendChunk) {
+    const int c1 = min(n, c0 + kSendChunk);
+    for (int i = c0 + warp; i < c1; i += 8) {
+      const int idx = idx_of(i);
+      const int j = idx / W, p = idx - j * W, e = p * El + j;
+      const int t = send[i];
+      const int row = slot[(long long)t * E + e];
+      if (row < 0) continue;
+      const T* src = x + (long long)t * d;
+      T* dst = reinterpret_cast<T*>(const_cast<void*>(xr.p[p])) + (long long)row * d;
+      for (int v = lane; v < nvec; v += 32) st_v4(dst + (long long)v * V, ld_nc_v4(src + (long long)v * V));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int idx = idx_of(c0); idx < E && s_pref[idx] < c1; ++idx) {
+        const int cnt = min(c1, s_pref[idx + 1]) - max(c0, s_pref[idx]);
+        if (cnt <= 0) continue;
+        const int j = idx / W, p = idx - j * W;
+        int* a = reinterpret_cast<int*>(const_cast<void*>(arrive.p[p])) + j;
+        asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(a), "r"(cnt) : "memory");
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // token side: y[t] = sum_{e asc} probs[t,e] e_out@(e / El)[slot[t,e]]
 template <typename T, int QV>
 __global__ void __launch_bounds__(256, 4) ep2_combine_kernel(const __grid_constant__ PeerTable eo,
@@ -910,7 +986,8 @@ __global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
     const int* __restrict__ blk_base, const int* __restrict__ base, long long R_cap,
     const __grid_constant__ PeerTable rtok, const __grid_constant__ PeerTable rsrc,
     const __grid_constant__ PeerTable rgate, const __grid_constant__ PeerTable ruid,
-    const __grid_constant__ PeerTable urows, int* __restrict__ uslot) {
+    const __grid_constant__ PeerTable urows, int* __restrict__ uslot, int* __restrict__ send = nullptr,
+    const int* __restrict__ sprefix = nullptr) {
   __shared__ unsigned s_bal[kGateBT / 32][128];
   __shared__ long long s_base[128];
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -985,6 +1062,9 @@ __global__ void __launch_bounds__(kGateBT) ep2_rank_kernel(
           reinterpret_cast<float*>(const_cast<void*>(rgate.p[p]))[r] = pg[j];
         }
         slot[(long long)t * E + e] = row;            // -1: dropped (MOE_ECAPACITY raised by the plan)
+        // ordered send list (overlap mode): entry (e, local position r - base[e]) in (local expert,
+        // owner) order, so the copy pass fills every owner's expert 0 first, then expert 1, ...
+        if (send) send[sprefix[(e % El) * W + e / El] + (int)(r - base[e])] = t;
       }
       if (nb < 8) break;
     }
@@ -1330,16 +1410,32 @@ cudaError_t launch_ep2_prepare(const moe_ctx* c, void* x_recv, int32_t* rtok, in
   return cudaGetLastError();
 }
 
+cudaError_t launch_ep2_arrival_plan(const moe_ctx* c, const int32_t* counts_all, int32_t* sprefix, int32_t* target,
+                                    cudaStream_t s) {
+  ep2_arrival_plan_kernel<<<1, 128, 0, s>>>(counts_all, c->world, c->E, c->rank, sprefix, target), count_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* probs, int32_t* slot, const PeerTable& xr,
                                 const PeerTable& rtok, const PeerTable& rsrc, const PeerTable& rgate, int64_t R_cap,
-                                cudaStream_t s) {
+                                cudaStream_t s, const int32_t* sprefix, int32_t* send, const PeerTable* arrive) {
   // per-block ranks (scan over this rank's token blocks; the local layout itself is not built)
   launch_dispatch_scan(c, c->ep2_scr, c->ep2_scr + c->E + 1, (long long)1 << 62, s);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || c->nblk == 0) return e;
   ep2_rank_kernel<false><<<c->nblk, kGateBT, 0, s>>>(probs, slot, c->T, c->E, c->E_local, c->rank, c->world,
                                                      c->blk_base, c->ep2_base, R_cap, rtok, rsrc, rgate, PeerTable{},
-                                                     PeerTable{}, nullptr), count_launch();
+                                                     PeerTable{}, nullptr, send, sprefix), count_launch();
+  if (send) {   // overlap mode: copy in send-list order with arrival counters
+    const int grid = 8 * c->sm_count;
+    if (c->dtype == 1)
+      ep2_copy_ordered_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)x, slot, send, sprefix, c->d, c->E, c->E_local,
+                                                         c->world, xr, *arrive), count_launch();
+    else
+      ep2_copy_ordered_kernel<float><<<grid, 256, 0, s>>>((const float*)x, slot, send, sprefix, c->d, c->E,
+                                                          c->E_local, c->world, xr, *arrive), count_launch();
+    return cudaGetLastError();
+  }
   if (c->dtype == 1)
     ep2_copy_kernel<bf16><<<(c->T + 7) / 8, 256, 0, s>>>((const bf16*)x, slot, c->T, c->d, c->E, c->E_local, xr),
         count_launch();

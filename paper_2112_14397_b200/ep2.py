@@ -71,8 +71,17 @@ class EP2Rank:
 
     def __init__(self, T: int, d_model: int, d_ff: int, E: int, dtype: torch.dtype, device: torch.device, rank: int,
                  world: int, syms: SymmetricBuffers, comm: Optional[int] = None, dedup: bool = False,
-                 capacity: Optional[int] = None, headroom: float = 1.25):
+                 capacity: Optional[int] = None, headroom: float = 1.25, overlap: Optional[bool] = None):
         self.T, self.d, self.f, self.E, self.El = T, d_model, d_ff, E, E // world
+        # exchange / GEMM overlap (non-dedup path; moe_ep2_dispatch_ordered + moe_ep2_expert_ffn):
+        # no barrier between the x exchange and the expert GEMMs -- each expert's GEMM1 tiles wait
+        # on that expert's arrival counter instead.  Counters (symmetric) and targets (local) are
+        # zero at construction and cumulative over steps (never reset, never re-allocated).
+        self.overlap = (not dedup) if overlap is None else bool(overlap and not dedup)
+        if self.overlap:
+            self.arr_target = torch.zeros(E // world, dtype=torch.int32, device=device)
+            self.sprefix = torch.zeros(E + 1, dtype=torch.int32, device=device)
+            self.send = torch.empty(max(1, T * E), dtype=torch.int32, device=device)
         # dedup (moe_ep2d_*): one row per (token, owner) each way; U = world * T unique slots
         self.dedup, self.U = dedup, world * T
         self.dtype, self.device, self.rank, self.world, self.syms = dtype, device, rank, world, syms
@@ -160,6 +169,8 @@ class EP2Rank:
                                 ("e_out", (R, d), self.dtype), ("dG", (R,), torch.float32),
                                 ("dx_perm", (R, d), self.dtype), ("dy", (self.T, d), self.dtype)):
             self._sym(name, shape, dt)
+        if self.overlap:
+            self._sym("arrive", (self.El,), torch.int32)
         if self.dedup:
             for name, shape, dt in (("ruid", (R,), torch.int32), ("tokbuf", (self.U, d), self.dtype),
                                     ("urows", (self.U, self.El), torch.int32), ("ysum", (self.U, d), self.dtype),
@@ -194,6 +205,8 @@ class EP2Rank:
         ca, _ = self._sym("counts_all", (self.world, self.E), torch.int32)
         s["off"] = torch.empty(self.El + 1, dtype=torch.int32, device=self.device)
         L.moe_ep2_plan(self.ctx, ca, R, s["off"])
+        if self.overlap:
+            L.moe_ep2_arrival_plan(self.ctx, ca, self.sprefix, self.arr_target)
         xr, _ = self._sym("x_recv", (R, d), self.dtype)
         rt, _ = self._sym("rtok", (R,), torch.int32)
         rs, _ = self._sym("rsrc", (R,), torch.int32)
@@ -213,6 +226,13 @@ class EP2Rank:
                                 self._sym("urows", (self.U, self.El), torch.int32)[1],
                                 self._sym("rtok", (R,), torch.int32)[1], self._sym("rsrc", (R,), torch.int32)[1],
                                 self._sym("rgate", (R,), torch.float32)[1], self._sym("ruid", (R,), torch.int32)[1], R)
+            return
+        if self.overlap:
+            L.moe_ep2_dispatch_ordered(self.ctx, s["x"], s["probs"], s["slot"],
+                                       self._sym("x_recv", (R, d), self.dtype)[1],
+                                       self._sym("rtok", (R,), torch.int32)[1], self._sym("rsrc", (R,), torch.int32)[1],
+                                       self._sym("rgate", (R,), torch.float32)[1], R, self.sprefix, self.send,
+                                       self._sym("arrive", (self.El,), torch.int32)[1])
             return
         L.moe_ep2_dispatch(self.ctx, s["x"], s["probs"], s["slot"], self._sym("x_recv", (R, d), self.dtype)[1],
                            self._sym("rtok", (R,), torch.int32)[1], self._sym("rsrc", (R,), torch.int32)[1],
@@ -238,7 +258,11 @@ class EP2Rank:
         s["gp"], s["h"] = gph[0], gph[1]
         xr, eo = self._sym("x_recv", (R, d), self.dtype)[0], self._sym("e_out", (R, d), self.dtype)[0]
         self._mark("experts_fwd", 0)
-        L.moe_expert_ffn(self.ctx, xr, s["off"], R, self.W1, self.b1, self.W2, self.b2, s["gp"], s["h"], eo)
+        if self.overlap:
+            L.moe_ep2_expert_ffn(self.ctx, xr, s["off"], R, self.W1, self.b1, self.W2, self.b2, s["gp"], s["h"], eo,
+                                 self._sym("arrive", (self.El,), torch.int32)[0], self.arr_target)
+        else:
+            L.moe_expert_ffn(self.ctx, xr, s["off"], R, self.W1, self.b1, self.W2, self.b2, s["gp"], s["h"], eo)
         self._mark("experts_fwd", 1)
 
     def fwd_combine(self):
@@ -338,7 +362,8 @@ class EP2Rank:
         self.fwd_plan()
         self.fwd_dispatch()
         st("dispatch", 1)
-        self.barrier()
+        if not self.overlap:          # overlap: the GEMMs wait per expert on the arrival counters
+            self.barrier()
         st("expert_ffn", 0)
         if self.dedup:
             self.fwd_permute()

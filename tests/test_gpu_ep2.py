@@ -453,3 +453,51 @@ def test_ep2_step_captures_as_cuda_graph(poison_empty, dedup):
             for k in ("dx", "dlogits", "dW1", "dW2", "db1", "db2", "dWg"):
                 assert torch.equal(g1[q][k], ref[1][q][k]), (q, k)
         assert torch.equal(dWg1, ref[2])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,W,T", [("C2", 2, 384), ("C4", 4, 256), ("C1", 2, 256)])
+def test_ep2_overlap_matches_barrier_path_and_counters(name, W, T):
+    """Exchange / GEMM overlap (moe_ep2_arrival_plan + moe_ep2_dispatch_ordered + moe_ep2_expert_ffn,
+    DESIGN §8): the ordered copy pass with arrival counters and the per-expert GEMM waits give the
+    barrier path's results bit for bit, and after every step each rank's counters equal its
+    cumulative targets (= the rows all sources sent to its experts, summed over the steps)."""
+    from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
+    from _ep_lockstep import run_lockstep
+    cfg = getattr(configs, name)
+    dev = torch.device("cuda", 0)
+    dt = inputs.TORCH_DTYPE[cfg.dtype]
+    ranks_in = [inputs.make_inputs(cfg, rank=q, T=T) for q in range(W)]
+    li0 = ranks_in[0]
+    args = ([ri.x.to(dev) for ri in ranks_in], [ri.u.to(dev) for ri in ranks_in], [ri.dy.to(dev) for ri in ranks_in],
+            float(np.float32(cfg.tau)), float(np.float32(cfg.threshold)))
+    res = {}
+    for overlap in (False, True):
+        syms = SymmetricBuffers(W, dev)
+        ranks = []
+        for q in range(W):
+            r = EP2Rank(T, cfg.d_model, cfg.d_ff, cfg.E, dt, dev, q, W, syms, overlap=overlap)
+            r.set_gate(li0.Wg.to(dev))
+            r.spawn(*(t.to(dev) for t in (li0.W1s, li0.b1s, li0.W2s, li0.b2s, li0.M1bits, li0.M2bits)))
+            ranks.append(r)
+        assert all(r.overlap == overlap for r in ranks)
+        for step in range(2):
+            ys, grads, dWg = run_lockstep(ranks, *args, top1=cfg.top1)
+            torch.cuda.synchronize()
+            for r in ranks:
+                r.check()
+            if overlap:
+                ca = ranks[0].counts_all_host()
+                El = cfg.E // W
+                for q, r in enumerate(ranks):
+                    arrive = syms.buf("arrive", q, (El,), torch.int32)[0].cpu().numpy()
+                    want = (step + 1) * ca[:, q * El:(q + 1) * El].sum(0)
+                    assert np.array_equal(arrive, want), (q, arrive, want)
+                    assert np.array_equal(r.arr_target.cpu().numpy(), want)
+        res[overlap] = (ys, grads, dWg)
+    (y0, g0, w0), (y1, g1, w1) = res[False], res[True]
+    for q in range(W):
+        assert torch.equal(y0[q], y1[q])
+        for k in ("dx", "dW1", "dW2", "db1", "db2", "dWg"):
+            assert torch.equal(g0[q][k], g1[q][k]), k
+    assert torch.equal(w0, w1)
