@@ -673,7 +673,7 @@ def run_ep(args, rank, world):
             from paper_2112_14397_b200.ep2 import EP2Rank, SymmetricBuffers
             syms = SymmetricBuffers(world, dev, mode="symm_mem", group=dist.group.WORLD)
             r = EP2Rank(cfg.T, cfg.d_model, cfg.d_ff, cfg.E, dt, dev, rank, world, syms, comm=comm,
-                        dedup=path == "p2p-dedup")
+                        dedup=path == "p2p-dedup", overlap=not args.no_overlap)
             r.set_gate(li.Wg.to(dev))
             r.spawn(*(t.to(dev) for t in (li.W1s, li.b1s, li.W2s, li.b2s, li.M1bits, li.M2bits)))
             dyb = r.dy_buffer()
@@ -892,6 +892,9 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=256)
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="peer-memory EP: put the barrier back between the x exchange and the expert GEMMs "
+                         "(token-order copy pass, no arrival counters) -- the A/B of the overlap")
     ap.add_argument("--ep", default=None, choices=["p2p", "p2p-dedup", "nccl"],
                     help="expert-parallel exchange: the fused NVLink peer-memory path (moe_ep2_*, torch symmetric "
                          "memory; the default at N > 1), the same with one row per (token, owner) each way "
