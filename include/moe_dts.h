@@ -328,7 +328,7 @@ int moe_ep2_dispatch(moe_ctx* ctx, const void* x, const float* probs, int32_t* s
  *   caller-owned, any contents; entry i = the token of the i-th (token, expert) pair in sprefix
  *   order) and arrive_peers (world device pointers to every rank's [E_local] int32 arrival counters,
  *   symmetric memory, zero before the first step, never reset): the copy pass walks the send list
- *   in order, so every owner's local expert 0 is filled first, and after each chunk of 64 entries
+ *   in order, so every owner's local expert 0 is filled first, and after each chunk of 256 entries
  *   adds the chunk's per-(owner, expert) entry counts to the owner's counters with a system-scope
  *   release (dropped rows of an overflowing step count too).
  * moe_ep2_expert_ffn: moe_expert_ffn on the recv layout whose GEMM1 TMA producer acquire-polls

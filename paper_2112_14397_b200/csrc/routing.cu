@@ -880,11 +880,11 @@ __global__ void ep2_arrival_plan_kernel(const int* __restrict__ counts_all, int 
   }
 }
 
-// token side copy pass in send-list order: block-chunks of kSendChunk entries, warp per entry
+// token side copy pass in send-list order: block-chunks of kSendChunk entries, 32 per warp
 // (x_t stored into its row on the owner), then one release add per (owner, local expert) of the
 // chunk into the owner's arrival counters -- entries whose row was dropped (-1) count too, so the
 // counters always reach the plan's targets.
-constexpr int kSendChunk = 64;
+constexpr int kSendChunk = 256;     // 8 warps x 32 entries
 template <typename T>
 __global__ void __launch_bounds__(256) ep2_copy_ordered_kernel(const T* __restrict__ x, const int* __restrict__ slot,
                                                                const int* __restrict__ send,
@@ -908,15 +908,37 @@ __global__ void __launch_bounds__(256) ep2_copy_ordered_kernel(const T* __restri
   };
   for (int c0 = blockIdx.x * kSendChunk; c0 < n; c0 += gridDim.x * kSendChunk) {
     const int c1 = min(n, c0 + kSendChunk);
-    for (int i = c0 + warp; i < c1; i += 8) {
+    // lane-parallel entry metadata (token, owner, row) of this warp's 32 entries, then the rows
+    // four at a time with their loads in flight
+    const int i = c0 + warp * 32 + lane;
+    int tl = 0, pl = 0, rl = -1;
+    if (i < c1) {
       const int idx = idx_of(i);
-      const int j = idx / W, p = idx - j * W, e = p * El + j;
-      const int t = send[i];
-      const int row = slot[(long long)t * E + e];
-      if (row < 0) continue;
-      const T* src = x + (long long)t * d;
-      T* dst = reinterpret_cast<T*>(const_cast<void*>(xr.p[p])) + (long long)row * d;
-      for (int v = lane; v < nvec; v += 32) st_v4(dst + (long long)v * V, ld_nc_v4(src + (long long)v * V));
+      const int j = idx / W;
+      pl = idx - j * W;
+      tl = send[i];
+      rl = slot[(long long)tl * E + pl * El + j];
+    }
+    for (int b = 0; b < 32; b += 4) {
+      int tt[4], rr[4], pp[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        tt[k] = __shfl_sync(0xffffffffu, tl, b + k);
+        rr[k] = __shfl_sync(0xffffffffu, rl, b + k);
+        pp[k] = __shfl_sync(0xffffffffu, pl, b + k);
+      }
+      if (rr[0] < 0 && rr[1] < 0 && rr[2] < 0 && rr[3] < 0) continue;
+      for (int v = lane; v < nvec; v += 32) {
+        uint4 buf[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (rr[k] >= 0) buf[k] = ld_nc_v4(x + (long long)tt[k] * d + (long long)v * V);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (rr[k] >= 0)
+            st_v4(reinterpret_cast<T*>(const_cast<void*>(xr.p[pp[k]])) + (long long)rr[k] * d + (long long)v * V,
+                  buf[k]);
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1427,7 +1449,7 @@ cudaError_t launch_ep2_dispatch(const moe_ctx* c, const void* x, const float* pr
                                                      c->blk_base, c->ep2_base, R_cap, rtok, rsrc, rgate, PeerTable{},
                                                      PeerTable{}, nullptr, send, sprefix), count_launch();
   if (send) {   // overlap mode: copy in send-list order with arrival counters
-    const int grid = 8 * c->sm_count;
+    const int grid = 4 * c->sm_count;
     if (c->dtype == 1)
       ep2_copy_ordered_kernel<bf16><<<grid, 256, 0, s>>>((const bf16*)x, slot, send, sprefix, c->d, c->E, c->E_local,
                                                          c->world, xr, *arrive), count_launch();
