@@ -864,12 +864,17 @@ __global__ void __launch_bounds__(256) ep2_copy_kernel(const T* __restrict__ x, 
 __global__ void ep2_arrival_plan_kernel(const int* __restrict__ counts_all, int W, int E, int me,
                                         int* __restrict__ sprefix, int* __restrict__ target) {
   const int El = E / W;
+  __shared__ int s_c[128];              // this rank's counts in (j, p) order
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    const int j = i / W, p = i - j * W;
+    s_c[i] = counts_all[(long long)me * E + p * El + j];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int i = 0; i < E; ++i) {
       sprefix[i] = acc;
-      const int j = i / W, p = i - j * W;
-      acc += counts_all[(long long)me * E + p * El + j];
+      acc += s_c[i];
     }
     sprefix[E] = acc;
   }
